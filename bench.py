@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""Hybrid-step benchmark (BASELINE.json metric) — one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload lm1b] [--impl ours|reference]
+
+N=1 runs in-process; N>1 is launched by the driver with torch.distributed.run
+(one rank per GPU, NCCL). A "step" is one hybrid-communication pass over one
+batch per worker: dense allreduce(+scale/cast) and, per sparse table, dedup ->
+route -> (exchange) -> merge + Adagrad apply -> gather/pull -> stitch.
+
+value : words/s = N * 2560 * K / t, t = max over ranks of the device time of
+        K steps with inputs resident in HBM (rotated over R pre-generated
+        batches whose total exceeds L2, so no step reads warm inputs).
+e2e   : the same metric through HybridRunner with the step's inputs copied
+        from pinned host memory inside the timed region and a result read back.
+roofline : the K4 scatter-apply kernel of the largest table, algorithmic bytes
+         / its CUDA-event duration, against MEASURED_PEAKS.json.
+cpu_baseline : the oracle port (oracle/oracle.py) timed on this host (rank 0, N=1).
+--impl reference : the oracle port on this host for the same config/metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "hybrid-step words/sec"
+UNIT = "words/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="lm1b")
+    ap.add_argument("--partitions", type=int, default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rotations", type=int, default=0, help="distinct resident batches")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "src": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)"}
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(self.gpu), "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            time.sleep(0.25)
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self) -> dict:
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = [r.split(",") for r in Path(self.f.name).read_text().splitlines() if r.strip()]
+        sm = [float(r[1]) for r in rows if len(r) > 8 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) > 8 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) > 8 for i in range(4)
+                          if r[5 + i].strip().lower() == "active"})
+        load = [s for s in sm if mx and s >= 0.3 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ CPU oracle step
+def cpu_oracle_step(wl, batches, states, step):
+    """The oracle's hybrid step for len(batches) simulated workers (one process)."""
+    from oracle import oracle as orc
+
+    n = len(batches)
+    for t in wl.tables:
+        owner = np.zeros(1, np.int32) if n == 1 else orc.owner_table(t.name, wl.partitions, n)
+        P = 1 if n == 1 else wl.partitions
+        orc.sparse_step(states[t.name], wl.optimizer["kind"], wl.optimizer, step,
+                        [b[t.name] for b in batches], t.V, P, owner)
+    for name in wl.dense:
+        orc.dense_allreduce([b[name] for b in batches], 1.0 / n)
+
+
+def lazy_states(wl):
+    st = {}
+    for t in wl.tables:
+        z = lambda: np.zeros((t.V, t.D), np.float32)  # calloc: only touched pages are real
+        kind = wl.optimizer["kind"]
+        st[t.name] = {"w": z()} | ({"acc": z()} if kind == "adagrad" else {}) | (
+            {"m": z(), "v": z()} if kind == "adam" else {})
+    return st
+
+
+def time_cpu(wl, n_workers: int, steps: int, seed: int = 0):
+    from paper_1808_02621_b200.synth import make_batch
+
+    batches = [make_batch(wl, seed, r) for r in range(n_workers)]
+    states = lazy_states(wl)
+    cpu_oracle_step(wl, batches, states, 1)  # warm-up (page faults, caches)
+    t0 = time.perf_counter()
+    for s in range(steps):
+        cpu_oracle_step(wl, batches, states, s + 2)
+    dt = (time.perf_counter() - t0) / steps
+    words = n_workers * wl.words_per_worker
+    return words / dt, dt
+
+
+def run_reference(args, wl):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n = args.gpus
+    for _ in range(max(args.warmup, 0) and 1):
+        pass
+    value, dt = time_cpu(wl, n, max(args.steps, 1), seed=0)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": config(args, wl),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"{args.steps} full oracle steps of {n} simulated worker(s), "
+                                   "numpy single-threaded"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config(args, wl):
+    return {"workload": wl.name, "tables": [f"{t.name}:{t.V}x{t.D},T={t.T + t.sampled}"
+                                            for t in wl.tables],
+            "dense_elems": sum(wl.dense.values()), "optimizer": wl.optimizer["kind"],
+            "partitions": args.partitions or wl.partitions, "words_per_worker": wl.words_per_worker,
+            "parallelism": f"hybrid dp{args.gpus}",
+            "l2_policy": "inputs rotated over distinct resident batches totalling > 2x L2"}
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    args = parse()
+    from paper_1808_02621_b200.synth import WORKLOADS, micro_workload
+
+    wl = WORKLOADS[args.workload] if not args.workload.startswith("micro") else micro_workload(
+        int(args.workload.split("_")[1]))
+    if args.impl == "reference":
+        return run_reference(args, wl)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1808_02621_b200 as hp
+    from paper_1808_02621_b200 import ops
+    from paper_1808_02621_b200.synth import make_batch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        comm = hp.Comm.from_torch_distributed()
+    P = args.partitions or wl.partitions
+    graph = hp.load_graph_spec(json.dumps(wl.graph_json()))
+    cluster = hp.ClusterSpec.b200_box(world)
+    plan = hp.transform_hybrid(graph, cluster, partitions={t.name: P for t in wl.tables})
+    opt = hp.OptimizerConfig(**wl.optimizer)
+    runner = hp.HybridRunner(plan, graph, cluster, rank=rank, world_size=world, comm=comm,
+                             optimizer=opt, device=dev, seed=0)
+
+    # resident batches, rotated so their total exceeds 2x L2 (126 MB)
+    host = [make_batch(wl, seed=1 + i, rank=rank) for i in range(1)]
+    per_batch = sum(v[0].nbytes + v[1].nbytes if isinstance(v, tuple) else v.nbytes
+                    for v in host[0].values())
+    R = args.rotations or max(2, int(np.ceil(2 * 126e6 / max(per_batch, 1))))
+    R = min(R, 16)
+    host += [make_batch(wl, seed=1 + i, rank=rank) for i in range(1, R)]
+
+    def to_dev(b):
+        return {k: ((torch.from_numpy(v[0]).to(dev), torch.from_numpy(v[1]).to(dev))
+                    if isinstance(v, tuple) else torch.from_numpy(v).to(dev))
+                for k, v in b.items()}
+
+    batches = [to_dev(b) for b in host]
+    use_graph = world == 1 and not args.no_graph and opt.kind != "adam"
+    stream = torch.cuda.current_stream()
+
+    for i in range(args.warmup):
+        runner.step(batches[i % R], timed=False)
+    torch.cuda.synchronize()
+    l0 = ops.launch_count()
+    runner.step(batches[0], timed=False)
+    torch.cuda.synchronize()
+    launches_per_step = ops.launch_count() - l0
+    graphs = [runner.capture(b) for b in batches] if use_graph else None
+    torch.cuda.synchronize()
+
+    def run_steps(k):
+        for i in range(k):
+            if graphs:
+                graphs[i % R].replay()
+            else:
+                runner.step(batches[i % R], timed=False)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    run_steps(max(args.warmup, 3))
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run_steps(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+    t_dev = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    words = world * wl.words_per_worker * args.steps
+    value = words / t_dev
+
+    # ---- per-kernel timing (eager steps, events around K4 / K5 launches)
+    kern = {}
+    if world == 1:
+        runner.kernel_events = {}
+        kt = min(args.steps, 20)
+        for i in range(kt):
+            runner.step(batches[i % R], timed=False)
+        torch.cuda.synchronize()
+        for key, evs in runner.kernel_events.items():
+            d = [a.elapsed_time(b) * 1e3 for a, b in zip(evs[0::2], evs[1::2])]
+            kern[key] = float(np.mean(d))
+        runner.kernel_events = None
+    pk = peaks()
+    roof = None
+    big = max(wl.tables, key=lambda t: (t.T + t.sampled) * t.D) if wl.tables else None
+    if big is not None and f"k4:{big.name}" in kern:
+        tab = runner.tables[big.name]
+        T = big.T + big.sampled
+        ops.dedup_plan(batches[0][big.name][0], tab.V, tab.P, None, 1, tab.D, tab.ws,
+                       outputs=False)
+        U = int(tab.ws.buf[:4].view(torch.int32).item())
+        k = 1 + opt.n_state
+        algo = T * (4 + 4 * big.D) + U * (4 + 4 * big.D * 2 * k)
+        us = kern[f"k4:{big.name}"]
+        achieved = algo / (us * 1e-6) / 1e9
+        roof = {"kernel": f"K4 merge+apply ({big.name}, k_reduce+k_combine)", "bound": "hbm",
+                "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                "algorithmic_bytes": algo, "launch_us": us, "peak_src": pk["src"],
+                "unique_rows": U, "T": T,
+                "step_share": us / (t_dev / args.steps * 1e6)}
+        gk = f"k5:{big.name}"
+        if gk in kern:
+            g_algo = T * 8 + U * 4 * big.D + T * 4 * big.D
+            roof["gather"] = {"launch_us": kern[gk], "algorithmic_bytes": g_algo,
+                              "achieved": g_algo / (kern[gk] * 1e-6) / 1e9}
+
+    # ---- e2e through the public API: pinned host inputs -> step -> result to host
+    pinned = []
+    for b in host:
+        pinned.append({k: ((torch.from_numpy(v[0]).pin_memory(), torch.from_numpy(v[1]).pin_memory())
+                           if isinstance(v, tuple) else torch.from_numpy(v).pin_memory())
+                       for k, v in b.items()})
+    static = to_dev(host[0])
+    e2e_graph = runner.capture(static) if use_graph else None
+    res_host = torch.empty(len(wl.tables) or 1, 4, dtype=torch.float32).pin_memory()
+    h2d = sum(x.numel() * x.element_size() for v in pinned[0].values()
+              for x in (v if isinstance(v, tuple) else (v,)))
+    d2h = res_host.numel() * 4
+
+    def e2e_step(i):
+        src = pinned[i % R]
+        for k, v in src.items():
+            if isinstance(v, tuple):
+                static[k][0].copy_(v[0], non_blocking=True)
+                static[k][1].copy_(v[1], non_blocking=True)
+            else:
+                static[k].copy_(v, non_blocking=True)
+        if e2e_graph:
+            e2e_graph.replay()
+        else:
+            runner.step(static, timed=False)
+        if wl.tables:
+            for j, t in enumerate(wl.tables):
+                res_host[j].copy_(runner.outputs[t.name][0, :4], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    for i in range(2):
+        e2e_step(i)
+    barrier()
+    torch.cuda.synchronize()
+    ke = max(5, min(args.steps, 30))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for i in range(ke):
+        e2e_step(i)
+    b.record(stream)
+    torch.cuda.synchronize()
+    t_e2e = max_over_ranks(a.elapsed_time(b) / 1e3)
+    e2e_value = world * wl.words_per_worker * ke / t_e2e
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, dt = time_cpu(wl, 1, args.cpu_steps)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"{args.cpu_steps} full oracle steps (1 worker, numpy), {dt*1e3:.1f} ms/step"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_dev / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (Zipf(1.1) ids, normal grads, hash-initialised tables)",
+            "config": config(args, wl) | {"rotations": R, "cuda_graph": bool(graphs)},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": ke},
+            "gpu_launches": launches_per_step * args.steps,
+            "launches_per_step": launches_per_step,
+            "roofline": roof, "kernels_us": kern, "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

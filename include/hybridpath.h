@@ -1,0 +1,182 @@
+/*
+ * hybridpath.h — C ABI of the B200-native hybrid-communication hot path.
+ *
+ * The reference (`sparseplan`, /root/reference/pkg/src/sparseplan) has no FFI:
+ * its boundary is the Python API re-exported in `sparseplan/__init__.py:4-55`,
+ * and the hot path it only *models* lives in `simulate.py`. Each entry point
+ * below replaces one modelled operation of that path (file:line cited per
+ * function); the Python package `paper_1808_02621_b200` binds them with ctypes
+ * behind the reference's own names.
+ *
+ * Conventions
+ *   - Every function returns 0 on success, a negative HP_E* code on failure;
+ *     hp_last_error() gives the thread-local message. No exceptions, no exit().
+ *   - All device buffers are allocated and owned by the caller (PyTorch).
+ *     The library never allocates in a hot call; workspace is caller-provided
+ *     and sized by the matching *_ws_bytes() query.
+ *   - All work is enqueued on the caller's stream (cudaStream_t passed as
+ *     void*). No host synchronisation unless the name says so.
+ *   - Row ids are int64 at the boundary; a table holds V < 2^31 rows of D fp32
+ *     (D % 4 == 0, D <= 2048).
+ */
+#ifndef HYBRIDPATH_H
+#define HYBRIDPATH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HP_OK 0
+#define HP_EINVAL (-1)   /* bad argument / unsupported shape */
+#define HP_ECUDA (-2)    /* CUDA runtime error */
+#define HP_ENCCL (-3)    /* NCCL error */
+#define HP_EWS (-4)      /* workspace too small */
+
+#define HP_OPT_SGD 0
+#define HP_OPT_ADAGRAD 1
+#define HP_OPT_ADAM 2
+
+#define HP_DTYPE_F32 0
+#define HP_DTYPE_BF16 1
+#define HP_DTYPE_F16 2
+
+/* Optimizer hyper-parameters for one step. lr_t / one_minus_beta* are
+ * precomputed by the host in float64 and rounded to fp32. */
+typedef struct hp_optim {
+  int32_t kind;           /* HP_OPT_* */
+  float lr;               /* SGD / Adagrad step size */
+  float beta1, beta2;     /* Adam */
+  float one_minus_beta1, one_minus_beta2;
+  float eps;              /* Adam epsilon */
+  float lr_t;             /* Adam bias-corrected step size for this step */
+  float agg_scale;        /* 1/n ('mean') or 1 ('sum') applied to the merged gradient */
+} hp_optim;
+
+/* Sharded table slab owned by one rank: the rows of every partition it owns,
+ * concatenated in ascending partition order. part_base[p] = first slab row of
+ * partition p if owned here, else -1 (device int64[P]). */
+typedef struct hp_slab {
+  float* w;               /* [rows, D] */
+  float* s0;              /* Adagrad accumulator or Adam m (NULL for SGD) */
+  float* s1;              /* Adam v (NULL otherwise) */
+  const int64_t* part_base; /* device int64[P] */
+  int64_t V;              /* global rows of the table */
+  int32_t P;              /* partition count */
+  int32_t D;              /* row width (floats) */
+} hp_slab;
+
+int hp_version(void);
+const char* hp_last_error(void);
+int hp_device_sm_count(void);
+/* Cumulative number of kernels this library has launched in the process. */
+int64_t hp_launch_count(void);
+
+/* ---------------------------------------------------------------- K1 + K2
+ * Sort + dedup + route of one worker's IndexedSlices.
+ * Replaces: local aggregation (`placement.py:155-161`, `simulate.py:202-208`)
+ *           and partition routing (`model.py:36-44,192-204`,
+ *           `placement.py:95-97,185-193`).
+ * Outputs (device): send_ids int64[U], send_rows f32[U,D] in send order
+ * (ascending (owner[p(id)], id)), counts int32[U] multiplicity,
+ * inv int32[T] send slot per position, dest_counts int32[nranks],
+ * n_uniq int32[1]. Capacity: U <= T.
+ */
+size_t hp_dedup_ws_bytes(int64_t T, int32_t D, int32_t P, int32_t nranks);
+int hp_sort_dedup_route(const int64_t* ids, const float* vals, int64_t T, int32_t D,
+                        int64_t V, int32_t P, const int32_t* owner, int32_t nranks,
+                        int64_t* send_ids, float* send_rows, int32_t* counts, int32_t* inv,
+                        int32_t* dest_counts, int32_t* n_uniq,
+                        void* ws, size_t ws_bytes, void* stream);
+
+/* Index-only half of hp_sort_dedup_route (no value rows): the dedup plan is
+ * left in ws for hp_reduce_local_apply. */
+int hp_dedup_plan(const int64_t* ids, int64_t T, int32_t D, int64_t V, int32_t P,
+                  const int32_t* owner, int32_t nranks, int64_t* send_ids, int32_t* counts,
+                  int32_t* inv, int32_t* dest_counts, int32_t* n_uniq,
+                  void* ws, size_t ws_bytes, void* stream);
+
+/* Error word of the last plan built in ws (bit 0: an id was outside [0, V),
+ * bit 1: a row was not homed on this rank). Synchronises the stream. */
+int hp_plan_status(const void* ws, int32_t* out_err, void* stream);
+
+/* ---------------------------------------------------------------- K4
+ * Fused merge + scatter-apply on the owner.
+ * Replaces: server aggregation + update (`simulate.py:294-323,358-367`),
+ *           colocated update chain (`placement.py:151-154`).
+ * rows [R, D] / ids [R] are what the owner received, concatenated in source
+ * rank order; equal ids are summed in that order, scaled by agg_scale and
+ * applied once to the slab (touched rows only).
+ */
+int hp_merge_apply(const int64_t* ids, const float* rows, int64_t R, hp_slab slab,
+                   hp_optim opt, void* ws, size_t ws_bytes, void* stream);
+
+/* Single-rank fused step (n == 1: every partition local, no exchange):
+ * dedup the worker's slices and apply directly to the slab.
+ * Equivalent to hp_sort_dedup_route followed by hp_merge_apply, without
+ * materialising the summed rows. */
+int hp_local_apply(const int64_t* ids, const float* vals, int64_t T, hp_slab slab,
+                   hp_optim opt, void* ws, size_t ws_bytes, void* stream);
+
+/* Value half of hp_local_apply / hp_merge_apply: reduce + apply using the plan
+ * a preceding hp_dedup_plan(ids, R, slab.D, slab.V, slab.P, NULL, 1, ...) left
+ * in ws (same stream). Lets a caller time K4 on its own. */
+int hp_apply_plan(const float* rows, int64_t R, hp_slab slab, hp_optim opt, void* ws,
+                  size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- K5 / K6
+ * Gather: out[i] = slab row of global id ids[i], i < n (coalesced row copy).
+ * Replaces: PS pull (`simulate.py:195-199`).
+ * n_dev (nullable) = device count bounding i (rows i >= *n_dev are skipped). */
+int hp_gather_rows(hp_slab slab, const int64_t* ids, int64_t n, const int32_t* n_dev,
+                   float* out, void* stream);
+
+/* Stitch: out[t] = rows[inv[t]] (t < T). Replaces the partition stitch
+ * (`PAPER.md:473`, `simulate.py:317-323` "stitch" term). */
+int hp_stitch(const float* rows, const int32_t* inv, int64_t T, int32_t D, float* out,
+              void* stream);
+
+/* Deterministic table init: rows [row_lo, row_lo+nrows) of a D-wide table,
+ * uniform[-scale, scale) from a counter hash of (seed, row, col). */
+int hp_init_rows(float* w, int64_t row_lo, int64_t nrows, int32_t D, uint64_t seed,
+                 float scale, void* stream);
+int hp_fill(float* x, int64_t n, float value, void* stream);
+
+/* ---------------------------------------------------------------- K7
+ * Dense gradient allreduce fused with scale + cast.
+ * Replaces: ring / hierarchical AllReduce (`simulate.py:97-135,243-261`).
+ * comm may be NULL when nranks == 1 (then only scale + cast run).
+ * in is fp32 [count]; out is out_dtype [count] (may alias in when fp32). */
+typedef struct hp_comm_s* hp_comm_t;
+int hp_dense_allreduce_scale_cast(hp_comm_t comm, float* in, void* out, int64_t count,
+                                  int32_t out_dtype, float scale, void* stream);
+
+/* ---------------------------------------------------------------- comm / K3
+ * One communicator per process/GPU over NCCL (NVLink 5 / NVSwitch).
+ * Replaces: the modelled PS pull/push messages (`simulate.py:183-240`). */
+int hp_nccl_unique_id_bytes(void);
+int hp_nccl_get_unique_id(void* out /* hp_nccl_unique_id_bytes() bytes */);
+int hp_comm_init(hp_comm_t* out, int32_t nranks, int32_t rank, const void* unique_id);
+int hp_comm_destroy(hp_comm_t comm);
+int hp_comm_size(hp_comm_t comm);
+
+/* all-to-all of one int32 per peer (device counts), graph-capturable. */
+int hp_alltoall_counts(hp_comm_t comm, const int32_t* send, int32_t* recv, void* stream);
+
+/* Push: (id, row) all-to-all-v with HOST counts (rows); send buffers are in
+ * send order (dest-major), receive buffers are filled in source-rank order. */
+int hp_exchange_push(hp_comm_t comm, const int64_t* send_ids, const float* send_rows,
+                     const int32_t* send_counts, int64_t* recv_ids, float* recv_rows,
+                     const int32_t* recv_counts, int32_t D, void* stream);
+
+/* Pull: rows back along the reverse routes (owner -> worker), HOST counts. */
+int hp_exchange_pull(hp_comm_t comm, const float* owner_rows, const int32_t* owner_counts,
+                     float* worker_rows, const int32_t* worker_counts, int32_t D,
+                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HYBRIDPATH_H */

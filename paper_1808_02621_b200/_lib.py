@@ -1,0 +1,98 @@
+"""ctypes binding of ``libhybridpath.so`` (the C ABI in ``include/hybridpath.h``).
+
+There is no CPU fallback: if the library is missing the import of any device
+op raises. ``symbols()`` lists every exported entry point so the CPU test suite
+can check the ABI without a GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libhybridpath.so"
+
+HP_OPT = {"sgd": 0, "adagrad": 1, "adam": 2}
+HP_DTYPE = {"float32": 0, "bfloat16": 1, "float16": 2}
+
+vp = C.c_void_p
+i32, i64, u64, f32, sz = C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_size_t
+
+
+class Optim(C.Structure):
+    _fields_ = [("kind", i32), ("lr", f32), ("beta1", f32), ("beta2", f32),
+                ("one_minus_beta1", f32), ("one_minus_beta2", f32), ("eps", f32),
+                ("lr_t", f32), ("agg_scale", f32)]
+
+
+class Slab(C.Structure):
+    _fields_ = [("w", vp), ("s0", vp), ("s1", vp), ("part_base", vp), ("V", i64), ("P", i32),
+                ("D", i32)]
+
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "hp_version": (C.c_int, []),
+    "hp_last_error": (C.c_char_p, []),
+    "hp_device_sm_count": (C.c_int, []),
+    "hp_launch_count": (i64, []),
+    "hp_apply_plan": (C.c_int, [vp, i64, Slab, Optim, vp, sz, vp]),
+    "hp_dedup_ws_bytes": (sz, [i64, i32, i32, i32]),
+    "hp_sort_dedup_route": (C.c_int, [vp, vp, i64, i32, i64, i32, vp, i32, vp, vp, vp, vp, vp, vp,
+                                      vp, sz, vp]),
+    "hp_dedup_plan": (C.c_int, [vp, i64, i32, i64, i32, vp, i32, vp, vp, vp, vp, vp, vp, sz, vp]),
+    "hp_plan_status": (C.c_int, [vp, vp, vp]),
+    "hp_merge_apply": (C.c_int, [vp, vp, i64, Slab, Optim, vp, sz, vp]),
+    "hp_local_apply": (C.c_int, [vp, vp, i64, Slab, Optim, vp, sz, vp]),
+    "hp_gather_rows": (C.c_int, [Slab, vp, i64, vp, vp, vp]),
+    "hp_stitch": (C.c_int, [vp, vp, i64, i32, vp, vp]),
+    "hp_init_rows": (C.c_int, [vp, i64, i64, i32, u64, f32, vp]),
+    "hp_fill": (C.c_int, [vp, i64, f32, vp]),
+    "hp_dense_allreduce_scale_cast": (C.c_int, [vp, vp, vp, i64, i32, f32, vp]),
+    "hp_nccl_unique_id_bytes": (C.c_int, []),
+    "hp_nccl_get_unique_id": (C.c_int, [vp]),
+    "hp_comm_init": (C.c_int, [C.POINTER(vp), i32, i32, vp]),
+    "hp_comm_destroy": (C.c_int, [vp]),
+    "hp_comm_size": (C.c_int, [vp]),
+    "hp_alltoall_counts": (C.c_int, [vp, vp, vp, vp]),
+    "hp_exchange_push": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, i32, vp]),
+    "hp_exchange_pull": (C.c_int, [vp, vp, vp, vp, vp, i32, vp]),
+}
+
+_lib = None
+
+
+class HybridPathError(RuntimeError):
+    pass
+
+
+def load() -> C.CDLL:
+    """Load (once) and type the library; raises if it was never built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise HybridPathError(
+            f"{LIB_PATH} not found: build it with `python -m paper_1808_02621_b200._build` "
+            "(there is no CPU fallback)")
+    lib = C.CDLL(str(LIB_PATH))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load().hp_last_error().decode(errors="replace")
+        raise HybridPathError(f"{what} failed ({rc}): {msg}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)
+
+
+def symbols() -> list:
+    return sorted(SIGNATURES)

@@ -1,0 +1,47 @@
+// Error reporting, version and device queries for the C ABI.
+#include <atomic>
+#include <string>
+
+#include "hp_common.cuh"
+
+namespace hp {
+
+static thread_local std::string g_err;
+
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+int cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return HP_ECUDA;
+}
+
+int sm_count() {
+  static int cached = 0;
+  if (cached == 0) {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
+      cached = n;
+    else
+      return 148;
+  }
+  return cached;
+}
+
+}  // namespace hp
+
+extern "C" {
+
+int hp_version(void) { return 100; /* 0.1.0 */ }
+
+const char* hp_last_error(void) { return hp::g_err.c_str(); }
+
+int hp_device_sm_count(void) { return hp::sm_count(); }
+
+int64_t hp_launch_count(void) { return hp::g_launches.load(std::memory_order_relaxed); }
+
+}  // extern "C"

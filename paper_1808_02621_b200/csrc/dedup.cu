@@ -1,0 +1,642 @@
+// K1 + K2: on-device radix sort of row ids, segment (dedup) metadata and
+// partition routing. Produces the DedupPlan the reduce/apply kernels consume.
+//
+// Reference semantics replaced: local aggregation ("iterating through nonzero
+// indices one by one to accumulate values with the same index", PAPER.md:471;
+// placement.py:155-161) and routing (model.py:36-44, 192-204; placement.py:95-97,
+// 185-193). Output order and the summation tree are specified in oracle/oracle.py.
+//
+// Two paths:
+//  * T <= HP_SMALL_MAX: ONE CTA sorts in shared memory (warp-striped items,
+//    __match_any_sync multisplit ranking, 8-bit digits) and derives every index
+//    structure in the same launch (LM/NMT shapes: 2.5k-11k ids per table).
+//  * larger T: LSD radix sort over 4096-key tiles (tile histogram -> per-digit
+//    column scan -> stable in-tile rank + smem-staged coalesced scatter), then
+//    grid-wide metadata kernels with a reduce-then-scan device scan.
+#include "hp_dedup.cuh"
+
+namespace hp {
+
+namespace {
+
+constexpr int HS = HP_RADIX + 1;  // padded histogram row (bank spread)
+
+__device__ __forceinline__ uint32_t load_key(const int64_t* ids, int64_t i, int64_t V, int* err) {
+  int64_t id = ids[i];
+  if (id < 0 || id >= V) {
+    if (err) atomicOr(err, 1);
+    id = id < 0 ? 0 : V - 1;
+  }
+  return (uint32_t)id;
+}
+
+// Stable rank of NT*IPT warp-striped items by an 8-bit digit.
+// Item (warp w, round r, lane l) has tile index w*32*IPT + r*32 + l; ranks
+// preserve that order within a digit. s_hist: NW*HS ints, s_scan: 33 ints.
+// On return s_hist[d] (warp 0 row) = first rank of digit d in the tile.
+template <int NT, int IPT>
+__device__ __forceinline__ void block_rank(const uint32_t (&key)[IPT], int shift, int (&rank)[IPT],
+                                           int* s_hist, int* s_scan) {
+  constexpr int NW = NT / 32;
+  constexpr int E = NW * HP_RADIX;
+  constexpr int PER = E / NT;
+  static_assert(E % NT == 0, "histogram must split evenly");
+  const int w = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < NW * HS; i += NT) s_hist[i] = 0;
+  __syncthreads();
+  int* my = s_hist + w * HS;
+  const unsigned lt = lanemask_lt();
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    const unsigned d = (key[r] >> shift) & (HP_RADIX - 1);
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const int before = __popc(peers & lt);
+    const int cnt = my[d];
+    rank[r] = cnt + before;
+    __syncwarp();
+    if (before == 0) my[d] = cnt + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // Exclusive scan over (digit, warp) in digit-major order.
+  int v[PER];
+  int sum = 0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int e = threadIdx.x * PER + k;
+    v[k] = s_hist[(e % NW) * HS + e / NW];
+    sum += v[k];
+  }
+  int total;
+  int base = block_excl_scan<NT>(sum, s_scan, &total);
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int e = threadIdx.x * PER + k;
+    s_hist[(e % NW) * HS + e / NW] = base;
+    base += v[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) rank[r] += my[(key[r] >> shift) & (HP_RADIX - 1)];
+}
+
+// Owner-grouped send-slot bases: part_base[p] = dest_off[owner[p]] +
+// sum_{p'<p, owner[p']==owner[p]} cnt[p']. Runs inside ONE block of NT threads.
+template <int NT>
+__device__ void partition_bases(const int32_t* first_u, const int32_t* owner, int P, int nranks,
+                                int32_t* part_base, int32_t* dest_counts, int* s_dest) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int o = w; o < nranks; o += NW) {
+    int carry = 0;
+    for (int pb = 0; pb < P; pb += 32) {
+      const int p = pb + lane;
+      const bool mine = p < P && (owner ? owner[p] : 0) == o;
+      const int c = mine ? first_u[p + 1] - first_u[p] : 0;
+      const int incl = warp_incl_scan(c);
+      if (mine) part_base[p] = carry + incl - c;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) {
+      s_dest[o] = carry;
+      if (dest_counts) dest_counts[o] = carry;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int o = 0; o < nranks; ++o) {
+      const int c = s_dest[o];
+      s_dest[o] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < P; p += NT) part_base[p] += s_dest[owner ? owner[p] : 0];
+  __syncthreads();
+}
+
+__device__ __forceinline__ int lower_bound_u32(const uint32_t* a, int n, uint32_t x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+constexpr int MAX_RANKS = 1024;
+
+// ------------------------------------------------------------------ small path
+template <int NT, int IPT>
+__global__ void __launch_bounds__(NT, 1)
+k_dedup_small(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __restrict__ owner,
+              int64_t* send_ids, int32_t* counts, int32_t* inv, int32_t* dest_counts,
+              int32_t* n_uniq) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int N = NT * IPT;
+  constexpr int NW = NT / 32;
+  uint32_t* s_key = reinterpret_cast<uint32_t*>(smem);
+  int32_t* s_pos = reinterpret_cast<int32_t*>(s_key + N);
+  int* s_hist = s_pos + N;
+  int* s_scan = s_hist + NW * HS;       // 33 (+pad)
+  int* s_dest = s_scan + 40;            // MAX_RANKS
+  const int T = (int)pl.T;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const Router route(pl.V, pl.P);
+
+  uint32_t key[IPT];
+  int32_t pos[IPT];
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    const int i = w * 32 * IPT + r * 32 + lane;
+    key[r] = i < T ? load_key(ids, i, pl.V, &pl.counters[C_ERR]) : 0xffffffffu;
+    pos[r] = i;
+  }
+  const int passes = (pl.key_bits + HP_RADIX_BITS - 1) / HP_RADIX_BITS;
+  for (int ps = 0; ps < passes; ++ps) {
+    int rank[IPT];
+    block_rank<NT, IPT>(key, ps * HP_RADIX_BITS, rank, s_hist, s_scan);
+#pragma unroll
+    for (int r = 0; r < IPT; ++r) {
+      s_key[rank[r]] = key[r];
+      s_pos[rank[r]] = pos[r];
+    }
+    __syncthreads();
+    if (ps + 1 < passes) {
+#pragma unroll
+      for (int r = 0; r < IPT; ++r) {
+        const int i = w * 32 * IPT + r * 32 + lane;
+        key[r] = s_key[i];
+        pos[r] = s_pos[i];
+      }
+    }
+  }
+  // ---- segments (blocked: thread t owns sorted items [t*IPT, t*IPT+IPT))
+  int myseg[IPT];
+  int heads = 0;
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const int i = threadIdx.x * IPT + k;
+    const bool h = i < T && (i == 0 || s_key[i] != s_key[i - 1]);
+    heads += h;
+  }
+  int U;
+  int segbase = block_excl_scan<NT>(heads, s_scan, &U);
+  {
+    int c = 0;
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      const int i = threadIdx.x * IPT + k;
+      const bool h = i < T && (i == 0 || s_key[i] != s_key[i - 1]);
+      if (h) {
+        pl.seg_start[segbase + c] = i;
+        pl.uniq_key[segbase + c] = s_key[i];
+        ++c;
+      }
+      myseg[k] = segbase + c - 1;
+      if (i < T) pl.sorted_pos[i] = s_pos[i];
+    }
+  }
+  if (threadIdx.x == 0) {
+    pl.seg_start[U] = T;
+    pl.counters[C_UNIQ] = U;
+    if (n_uniq) *n_uniq = U;
+  }
+  __syncthreads();
+  // ---- partition boundaries in the (ascending) unique ids
+  for (int p = threadIdx.x; p <= pl.P; p += NT)
+    pl.first_u[p] = p == pl.P ? U : lower_bound_u32(pl.uniq_key, U, (uint32_t)route.lo(p));
+  __syncthreads();
+  partition_bases<NT>(pl.first_u, owner, pl.P, pl.nranks, pl.part_base, dest_counts, s_dest);
+  // ---- per-segment slots, reduce items, long segments (blocked over u)
+  const int ku = (U + NT - 1) / NT;
+  const int u0 = min(U, (int)threadIdx.x * ku), u1 = min(U, u0 + ku);
+  int ni = 0, np = 0, nl = 0;
+  for (int u = u0; u < u1; ++u) {
+    const int L = pl.seg_start[u + 1] - pl.seg_start[u];
+    const int n0 = (L + HP_CHUNK - 1) / HP_CHUNK;
+    ni += n0;
+    if (L > HP_CHUNK) { np += n0; ++nl; }
+  }
+  int tot_i, tot_p, tot_l;
+  int bi = block_excl_scan<NT>(ni, s_scan, &tot_i);
+  int bp = block_excl_scan<NT>(np, s_scan, &tot_p);
+  int bl = block_excl_scan<NT>(nl, s_scan, &tot_l);
+  for (int u = u0; u < u1; ++u) {
+    const int L = pl.seg_start[u + 1] - pl.seg_start[u];
+    const int n0 = (L + HP_CHUNK - 1) / HP_CHUNK;
+    const uint32_t id = pl.uniq_key[u];
+    const int p = route.part(id);
+    const int slot = pl.part_base[p] + (u - pl.first_u[p]);
+    pl.sigma[u] = slot;
+    if (send_ids) send_ids[slot] = id;
+    if (counts) counts[slot] = L;
+    pl.item_off[u] = bi;
+    for (int k = 0; k < n0; ++k) pl.item_seg[bi + k] = u;
+    bi += n0;
+    if (L > HP_CHUNK) {
+      pl.part_off[u] = bp;
+      bp += n0;
+      pl.long_list[bl++] = u;
+    }
+  }
+  if (threadIdx.x == 0) {
+    pl.item_off[U] = tot_i;
+    pl.counters[C_ITEMS] = tot_i;
+    pl.counters[C_PARTIALS] = tot_p;
+    pl.counters[C_LONG] = tot_l;
+  }
+  __syncthreads();
+  if (inv) {
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      const int i = threadIdx.x * IPT + k;
+      if (i < T) inv[s_pos[i]] = pl.sigma[myseg[k]];
+    }
+  }
+}
+
+constexpr size_t tile_smem_bytes() {
+  return (size_t)HP_TILE * 8 + (size_t)(HP_TILE_THREADS / 32) * HS * 4 + 40 * 4 + HP_RADIX * 4;
+}
+
+constexpr size_t small_smem_bytes() {
+  return (size_t)HP_SMALL_MAX * 8 + (size_t)(HP_SMALL_THREADS / 32) * HS * 4 + 40 * 4 +
+         MAX_RANKS * 4;
+}
+
+// ------------------------------------------------------------------ large path
+__global__ void __launch_bounds__(HP_TILE_THREADS)
+k_tile_hist(DedupPlan pl, const int64_t* __restrict__ ids, int src, int shift) {
+  __shared__ int s_h[HP_RADIX];
+  for (int i = threadIdx.x; i < HP_RADIX; i += blockDim.x) s_h[i] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * HP_TILE;
+  for (int k = 0; k < HP_TILE_IPT; ++k) {
+    const int64_t i = base + k * HP_TILE_THREADS + threadIdx.x;
+    if (i < pl.T) {
+      const uint32_t key = ids ? load_key(ids, i, pl.V, &pl.counters[C_ERR]) : pl.key[src][i];
+      const unsigned d = (key >> shift) & (HP_RADIX - 1);
+      const unsigned peers = __match_any_sync(__activemask(), d);
+      if ((peers & lanemask_lt()) == 0) atomicAdd(&s_h[d], __popc(peers));
+    }
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < HP_RADIX; d += blockDim.x)
+    pl.tile_hist[(int64_t)d * pl.ntiles + blockIdx.x] = s_h[d];
+}
+
+// One CTA per digit: exclusive scan of that digit's per-tile counts.
+__global__ void __launch_bounds__(1024) k_digit_scan(DedupPlan pl) {
+  __shared__ int s_scan[40];
+  int* row = pl.tile_hist + (int64_t)blockIdx.x * pl.ntiles;
+  int carry = 0;
+  for (int b = 0; b < pl.ntiles; b += 1024) {
+    const int i = b + threadIdx.x;
+    const int v = i < pl.ntiles ? row[i] : 0;
+    int tot;
+    const int ex = block_excl_scan<1024>(v, s_scan, &tot);
+    if (i < pl.ntiles) row[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) pl.digit_tot[blockIdx.x] = carry;
+}
+
+__global__ void __launch_bounds__(HP_TILE_THREADS, 2)
+k_tile_scatter(DedupPlan pl, const int64_t* __restrict__ ids, int src, int shift) {
+  constexpr int NT = HP_TILE_THREADS, IPT = HP_TILE_IPT, NW = NT / 32;
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* s_key = reinterpret_cast<uint32_t*>(smem);
+  int32_t* s_pos = reinterpret_cast<int32_t*>(s_key + HP_TILE);
+  int* s_hist = s_pos + HP_TILE;
+  int* s_scan = s_hist + NW * HS;
+  int* s_gbase = s_scan + 40;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t base = (int64_t)blockIdx.x * HP_TILE;
+  const int valid = (int)min((int64_t)HP_TILE, pl.T - base);
+  uint32_t key[IPT];
+  int32_t pos[IPT];
+  int rank[IPT];
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    const int li = w * 32 * IPT + r * 32 + lane;
+    const int64_t i = base + li;
+    if (li < valid) {
+      if (ids) {
+        key[r] = load_key(ids, i, pl.V, nullptr);  // errors already flagged by k_tile_hist
+        pos[r] = (int32_t)i;
+      } else {
+        key[r] = pl.key[src][i];
+        pos[r] = pl.pos[src][i];
+      }
+    } else {
+      key[r] = 0xffffffffu;
+      pos[r] = -1;
+    }
+  }
+  // digit bases: exclusive scan of digit totals + this tile's column offset
+  if (threadIdx.x < HP_RADIX) s_gbase[threadIdx.x] = pl.digit_tot[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int carry = 0;
+    for (int d0 = 0; d0 < HP_RADIX; d0 += 32) {
+      const int v = s_gbase[d0 + lane];
+      const int incl = warp_incl_scan(v);
+      s_gbase[d0 + lane] = carry + incl - v;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < HP_RADIX)
+    s_gbase[threadIdx.x] += pl.tile_hist[(int64_t)threadIdx.x * pl.ntiles + blockIdx.x];
+  block_rank<NT, IPT>(key, shift, rank, s_hist, s_scan);
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    s_key[rank[r]] = key[r];
+    s_pos[rank[r]] = pos[r];
+  }
+  __syncthreads();
+  const int dst = src ^ 1;
+  for (int idx = threadIdx.x; idx < valid; idx += NT) {
+    const uint32_t k = s_key[idx];
+    const int d = (k >> shift) & (HP_RADIX - 1);
+    const int64_t o = s_gbase[d] + (idx - s_hist[d]);
+    pl.key[dst][o] = k;
+    pl.pos[dst][o] = s_pos[idx];
+  }
+}
+
+// ---- device-wide exclusive scan (reduce-then-scan), n from host or device
+__global__ void __launch_bounds__(HP_SCAN_BLOCK)
+k_scan_reduce(const int32_t* __restrict__ a, int64_t n_host, const int32_t* n_dev, int32_t* bsum) {
+  __shared__ int s_scan[40];
+  const int64_t n = n_dev ? *n_dev : n_host;
+  const int64_t base = (int64_t)blockIdx.x * HP_SCAN_TILE;
+  int s = 0;
+  for (int k = 0; k < HP_SCAN_IPT; ++k) {
+    const int64_t i = base + (int64_t)threadIdx.x * HP_SCAN_IPT + k;
+    if (i < n) s += a[i];
+  }
+  int tot;
+  block_excl_scan<HP_SCAN_BLOCK>(s, s_scan, &tot);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_top(int32_t* bsum, int nb, int32_t* total) {
+  __shared__ int s_scan[40];
+  int carry = 0;
+  for (int b = 0; b < nb; b += 1024) {
+    const int i = b + threadIdx.x;
+    const int v = i < nb ? bsum[i] : 0;
+    int tot;
+    const int ex = block_excl_scan<1024>(v, s_scan, &tot);
+    if (i < nb) bsum[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0 && total) *total = carry;
+}
+
+__global__ void __launch_bounds__(HP_SCAN_BLOCK)
+k_scan_down(int32_t* a, int64_t n_host, const int32_t* n_dev, const int32_t* __restrict__ bsum) {
+  __shared__ int s_scan[40];
+  const int64_t n = n_dev ? *n_dev : n_host;
+  const int64_t base = (int64_t)blockIdx.x * HP_SCAN_TILE + (int64_t)threadIdx.x * HP_SCAN_IPT;
+  int v[HP_SCAN_IPT];
+  int s = 0;
+  for (int k = 0; k < HP_SCAN_IPT; ++k) {
+    v[k] = base + k < n ? a[base + k] : 0;
+    s += v[k];
+  }
+  int tot;
+  int run = block_excl_scan<HP_SCAN_BLOCK>(s, s_scan, &tot) + bsum[blockIdx.x];
+  for (int k = 0; k < HP_SCAN_IPT; ++k) {
+    if (base + k < n) a[base + k] = run;
+    run += v[k];
+  }
+}
+
+int device_scan(int32_t* a, int64_t n_host, const int32_t* n_dev, int32_t* bsum, int32_t* total,
+                cudaStream_t st) {
+  const int nb = (int)((n_host + HP_SCAN_TILE - 1) / HP_SCAN_TILE);
+  if (nb == 0) return HP_OK;
+  k_scan_reduce<<<nb, HP_SCAN_BLOCK, 0, st>>>(a, n_host, n_dev, bsum);
+  k_scan_top<<<1, 1024, 0, st>>>(bsum, nb, total);
+  k_scan_down<<<nb, HP_SCAN_BLOCK, 0, st>>>(a, n_host, n_dev, bsum);
+  HP_LAUNCHED(3, "device_scan");
+  return HP_OK;
+}
+
+// ---- large-path metadata kernels
+__global__ void k_heads(DedupPlan pl, const uint32_t* __restrict__ skey) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pl.T;
+       i += (int64_t)gridDim.x * blockDim.x)
+    pl.segidx[i] = (i == 0 || skey[i] != skey[i - 1]) ? 1 : 0;
+}
+
+__global__ void k_heads_write(DedupPlan pl, const uint32_t* __restrict__ skey, int32_t* n_uniq) {
+  const int U = pl.counters[C_UNIQ];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pl.T;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool h = i == 0 || skey[i] != skey[i - 1];
+    const int ex = pl.segidx[i];
+    if (h) {
+      pl.seg_start[ex] = (int)i;
+      pl.uniq_key[ex] = skey[i];
+    }
+    pl.segidx[i] = ex + (h ? 1 : 0) - 1;
+    if (i == 0) {
+      pl.seg_start[U] = (int)pl.T;
+      if (n_uniq) *n_uniq = U;
+    }
+  }
+}
+
+__global__ void k_first_u(DedupPlan pl) {
+  const Router route(pl.V, pl.P);
+  const int U = pl.counters[C_UNIQ];
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p <= pl.P; p += gridDim.x * blockDim.x)
+    pl.first_u[p] = p == pl.P ? U : lower_bound_u32(pl.uniq_key, U, (uint32_t)route.lo(p));
+}
+
+__global__ void __launch_bounds__(1024)
+k_part_base(DedupPlan pl, const int32_t* __restrict__ owner, int32_t* dest_counts) {
+  __shared__ int s_dest[MAX_RANKS];
+  partition_bases<1024>(pl.first_u, owner, pl.P, pl.nranks, pl.part_base, dest_counts, s_dest);
+}
+
+// Per segment: send slot, outputs, and the three count arrays to be scanned.
+__global__ void k_seg_counts(DedupPlan pl, int64_t* send_ids, int32_t* counts, int32_t* long_tmp) {
+  const Router route(pl.V, pl.P);
+  const int U = pl.counters[C_UNIQ];
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x) {
+    const int L = pl.seg_start[u + 1] - pl.seg_start[u];
+    const int n0 = (L + HP_CHUNK - 1) / HP_CHUNK;
+    const uint32_t id = pl.uniq_key[u];
+    const int p = route.part(id);
+    const int slot = pl.part_base[p] + (u - pl.first_u[p]);
+    pl.sigma[u] = slot;
+    if (send_ids) send_ids[slot] = id;
+    if (counts) counts[slot] = L;
+    pl.item_off[u] = n0;
+    pl.part_off[u] = L > HP_CHUNK ? n0 : 0;
+    long_tmp[u] = L > HP_CHUNK ? 1 : 0;
+  }
+}
+
+__global__ void k_items(DedupPlan pl, const int32_t* __restrict__ long_tmp) {
+  const int U = pl.counters[C_UNIQ];
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x) {
+    const int L = pl.seg_start[u + 1] - pl.seg_start[u];
+    const int n0 = (L + HP_CHUNK - 1) / HP_CHUNK;
+    const int b = pl.item_off[u];
+    for (int k = 0; k < n0; ++k) pl.item_seg[b + k] = u;
+    if (L > HP_CHUNK) pl.long_list[long_tmp[u]] = u;
+    if (u == 0) pl.item_off[U] = pl.counters[C_ITEMS];
+  }
+}
+
+__global__ void k_inv(DedupPlan pl, int32_t* inv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pl.T;
+       i += (int64_t)gridDim.x * blockDim.x)
+    inv[pl.sorted_pos[i]] = pl.sigma[pl.segidx[i]];
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+}  // namespace
+
+size_t dedup_ws_bytes(int64_t T, int32_t D, int32_t P) {
+  const int64_t Tc = T < 1 ? 1 : T;
+  const int64_t ntiles = (Tc + HP_TILE - 1) / HP_TILE;
+  const int64_t nscan = (Tc + HP_SCAN_TILE - 1) / HP_SCAN_TILE + 2;
+  const int64_t prow = 2 * Tc / HP_CHUNK + 2;
+  size_t s = align256(4 * C_NCOUNTERS);
+  s += 4 * align256(4 * Tc);          // key[2], pos[2]
+  s += 3 * align256(4 * (Tc + 1));    // uniq_key, seg_start, item_off
+  s += 6 * align256(4 * Tc);          // segidx, sigma, item_seg, part_off, long_list, (spare)
+  s += align256(4 * ((size_t)P + 1)) + 2 * align256(4 * (size_t)P);
+  s += align256(4 * HP_RADIX * ntiles) + align256(4 * HP_RADIX);
+  s += align256(4 * nscan);
+  s += align256(4 * (size_t)D * prow);
+  return s;
+}
+
+int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, int64_t V,
+               int32_t P, int32_t nranks) {
+  HP_REQUIRE(ws != nullptr, "workspace is NULL");
+  HP_REQUIRE(V >= 1 && V < (int64_t(1) << 31), "table rows V must be in [1, 2^31)");
+  HP_REQUIRE(P >= 1 && P <= V, "partition count P must be in [1, V]");
+  HP_REQUIRE(nranks >= 1 && nranks <= MAX_RANKS, "nranks out of range");
+  HP_REQUIRE(T >= 0 && T < (int64_t(1) << 31), "T out of range");
+  HP_REQUIRE(D >= 1, "D must be >= 1");
+  if (ws_bytes < dedup_ws_bytes(T, D, P)) {
+    set_error("workspace too small for dedup plan");
+    return HP_EWS;
+  }
+  const int64_t Tc = T < 1 ? 1 : T;
+  char* p = static_cast<char*>(ws);
+  auto take = [&](size_t bytes) { void* r = p; p += align256(bytes); return r; };
+  pl->counters = (int32_t*)take(4 * C_NCOUNTERS);  // first: fixed offset (hp_plan_status)
+  pl->T = T;
+  pl->D = D;
+  pl->P = P;
+  pl->nranks = nranks;
+  pl->V = V;
+  int bits = 0;
+  while (bits < 31 && (int64_t(1) << bits) < V) ++bits;
+  pl->key_bits = bits < 1 ? 1 : bits;
+  pl->ntiles = (int32_t)((Tc + HP_TILE - 1) / HP_TILE);
+  pl->key[0] = (uint32_t*)take(4 * Tc);
+  pl->key[1] = (uint32_t*)take(4 * Tc);
+  pl->pos[0] = (int32_t*)take(4 * Tc);
+  pl->pos[1] = (int32_t*)take(4 * Tc);
+  pl->uniq_key = (uint32_t*)take(4 * (Tc + 1));
+  pl->seg_start = (int32_t*)take(4 * (Tc + 1));
+  pl->item_off = (int32_t*)take(4 * (Tc + 1));
+  pl->segidx = (int32_t*)take(4 * Tc);
+  pl->sigma = (int32_t*)take(4 * Tc);
+  pl->item_seg = (int32_t*)take(4 * Tc);
+  pl->part_off = (int32_t*)take(4 * Tc);
+  pl->long_list = (int32_t*)take(4 * Tc);
+  take(4 * Tc);
+  pl->first_u = (int32_t*)take(4 * ((size_t)P + 1));
+  pl->part_base = (int32_t*)take(4 * (size_t)P);
+  pl->zero_owner = (int32_t*)take(4 * (size_t)P);
+  pl->tile_hist = (int32_t*)take(4 * HP_RADIX * (size_t)pl->ntiles);
+  pl->digit_tot = (int32_t*)take(4 * HP_RADIX);
+  pl->scan_bsum = (int32_t*)take(4 * ((Tc + HP_SCAN_TILE - 1) / HP_SCAN_TILE + 2));
+  pl->partial_rows = 2 * Tc / HP_CHUNK + 2;
+  pl->partials = (float*)take(4 * (size_t)D * pl->partial_rows);
+  pl->sorted_pos = pl->pos[0];
+  return HP_OK;
+}
+
+int build_plan(DedupPlan& pl, const int64_t* ids, const int32_t* owner, int64_t* send_ids,
+               int32_t* counts, int32_t* inv, int32_t* dest_counts, int32_t* n_uniq,
+               cudaStream_t st) {
+  HP_CUDA(cudaMemsetAsync(pl.counters, 0, 4 * C_NCOUNTERS, st));
+  if (pl.T == 0) {
+    if (dest_counts) HP_CUDA(cudaMemsetAsync(dest_counts, 0, 4 * (size_t)pl.nranks, st));
+    if (n_uniq) HP_CUDA(cudaMemsetAsync(n_uniq, 0, 4, st));
+    HP_CUDA(cudaMemsetAsync(pl.item_off, 0, 4, st));
+    HP_CUDA(cudaMemsetAsync(pl.seg_start, 0, 4, st));
+    return HP_OK;
+  }
+  if (pl.T <= HP_SMALL_MAX) {
+    // The small kernel leaves the sorted positions in s_pos and copies them to
+    // pos[0]; sorted_pos already aliases pos[0].
+    constexpr size_t smem = small_smem_bytes();
+    static bool configured = false;
+    if (!configured) {
+      HP_CUDA(cudaFuncSetAttribute(k_dedup_small<HP_SMALL_THREADS, HP_SMALL_IPT>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      configured = true;
+    }
+    pl.sorted_pos = pl.pos[0];
+    k_dedup_small<HP_SMALL_THREADS, HP_SMALL_IPT><<<1, HP_SMALL_THREADS, smem, st>>>(
+        pl, ids, owner, send_ids, counts, inv, dest_counts, n_uniq);
+    HP_LAUNCHED(1, "k_dedup_small");
+    return HP_OK;
+  }
+  // ---- large path: LSD radix sort, 8-bit digits
+  static bool tile_configured = false;
+  if (!tile_configured) {
+    HP_CUDA(cudaFuncSetAttribute(k_tile_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tile_smem_bytes()));
+    tile_configured = true;
+  }
+  const int passes = (pl.key_bits + HP_RADIX_BITS - 1) / HP_RADIX_BITS;
+  int src = 0;
+  for (int ps = 0; ps < passes; ++ps) {
+    const int shift = ps * HP_RADIX_BITS;
+    const int64_t* in_ids = ps == 0 ? ids : nullptr;
+    k_tile_hist<<<pl.ntiles, HP_TILE_THREADS, 0, st>>>(pl, in_ids, src, shift);
+    k_digit_scan<<<HP_RADIX, 1024, 0, st>>>(pl);
+    k_tile_scatter<<<pl.ntiles, HP_TILE_THREADS, tile_smem_bytes(), st>>>(pl, in_ids, src, shift);
+    HP_LAUNCHED(3, "radix pass");
+    src ^= 1;
+  }
+  pl.sorted_pos = pl.pos[src];
+  const uint32_t* skey = pl.key[src];
+  int32_t* long_tmp = reinterpret_cast<int32_t*>(pl.key[src ^ 1]);
+  const int g = grid_for(pl.T, 256, sm_count() * 8);
+  k_heads<<<g, 256, 0, st>>>(pl, skey);
+  int rc = device_scan(pl.segidx, pl.T, nullptr, pl.scan_bsum, &pl.counters[C_UNIQ], st);
+  if (rc) return rc;
+  k_heads_write<<<g, 256, 0, st>>>(pl, skey, n_uniq);
+  k_first_u<<<grid_for(pl.P + 1, 256, 1024), 256, 0, st>>>(pl);
+  k_part_base<<<1, 1024, 0, st>>>(pl, owner, dest_counts);
+  k_seg_counts<<<g, 256, 0, st>>>(pl, send_ids, counts, long_tmp);
+  HP_LAUNCHED(5, "dedup metadata");
+  const int32_t* U = &pl.counters[C_UNIQ];
+  if ((rc = device_scan(pl.item_off, pl.T, U, pl.scan_bsum, &pl.counters[C_ITEMS], st))) return rc;
+  if ((rc = device_scan(pl.part_off, pl.T, U, pl.scan_bsum, &pl.counters[C_PARTIALS], st))) return rc;
+  if ((rc = device_scan(long_tmp, pl.T, U, pl.scan_bsum, &pl.counters[C_LONG], st))) return rc;
+  k_items<<<g, 256, 0, st>>>(pl, long_tmp);
+  if (inv) k_inv<<<g, 256, 0, st>>>(pl, inv);
+  HP_LAUNCHED(inv ? 2 : 1, "dedup items");
+  return HP_OK;
+}
+
+}  // namespace hp

@@ -1,0 +1,123 @@
+// Shared helpers for the hybrid-path kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/hybridpath.h"
+
+#define HP_CHUNK 128          // rows per sequential group of the summation tree (oracle CHUNK)
+#define HP_SMALL_THREADS 1024 // single-CTA sort path
+#define HP_SMALL_IPT 16
+#define HP_SMALL_MAX (HP_SMALL_THREADS * HP_SMALL_IPT)  // 16384 items
+#define HP_RADIX_BITS 8
+#define HP_RADIX 256
+#define HP_TILE_THREADS 512   // multi-CTA sort tile
+#define HP_TILE_IPT 8
+#define HP_TILE (HP_TILE_THREADS * HP_TILE_IPT)          // 4096 keys per tile
+#define HP_SCAN_BLOCK 1024
+#define HP_SCAN_IPT 4
+#define HP_SCAN_TILE (HP_SCAN_BLOCK * HP_SCAN_IPT)
+
+namespace hp {
+
+void set_error(const std::string& msg);
+void count_launches(int n);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define HP_CUDA(call)                                        \
+  do {                                                       \
+    cudaError_t _e = (call);                                 \
+    if (_e != cudaSuccess) return ::hp::cuda_fail(_e, #call); \
+  } while (0)
+// Check the launch(es) just issued and add them to the library's kernel-launch
+// counter (hp_launch_count(): the bench's "gpu_launches" evidence).
+#define HP_LAUNCHED(n, name)      \
+  do {                            \
+    HP_CUDA(cudaGetLastError());  \
+    ::hp::count_launches(n);      \
+  } while (0)
+#define HP_REQUIRE(cond, msg)          \
+  do {                                 \
+    if (!(cond)) {                     \
+      ::hp::set_error(msg);            \
+      return HP_EINVAL;                \
+    }                                  \
+  } while (0)
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ int warp_incl_scan(int v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan of one int per thread. s_warp needs 33 ints.
+// Returns the exclusive prefix; *total receives the block sum.
+template <int NT>
+__device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int* total) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int incl = warp_incl_scan(v);
+  if (lane == 31) s_warp[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    int x = lane < NW ? s_warp[lane] : 0;
+    int xi = warp_incl_scan(x);
+    if (lane < NW) s_warp[lane] = xi - x;
+    if (lane == NW - 1) s_warp[32] = xi;
+  }
+  __syncthreads();
+  int r = s_warp[wid] + incl - v;
+  *total = s_warp[32];
+  __syncthreads();
+  return r;
+}
+
+// Row id -> partition of the contiguous even split of V rows into P parts
+// (reference model.py:36-44): first e = V % P parts hold q+1 rows.
+struct Router {
+  int64_t q, e, split;  // split = e * (q + 1)
+  __host__ __device__ Router(int64_t V, int32_t P) : q(V / P), e(V % P), split((V % P) * (V / P + 1)) {}
+  __device__ __forceinline__ int part(int64_t r) const {
+    return r < split ? (int)(r / (q + 1)) : (int)(e + (r - split) / q);
+  }
+  __device__ __forceinline__ int64_t lo(int p) const {
+    return p < e ? (int64_t)p * (q + 1) : split + (int64_t)(p - e) * q;
+  }
+};
+
+__device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
+                     __fadd_rn(a.w, b.w));
+}
+
+__device__ __forceinline__ float4 ldg_stream(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+
+inline int grid_for(int64_t work, int per_block, int max_blocks) {
+  int64_t b = (work + per_block - 1) / per_block;
+  if (b < 1) b = 1;
+  if (b > max_blocks) b = max_blocks;
+  return (int)b;
+}
+
+int sm_count();
+
+}  // namespace hp

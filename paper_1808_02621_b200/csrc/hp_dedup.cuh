@@ -1,0 +1,51 @@
+// Dedup plan: the index-side result of K1+K2, shared by the reduce/apply kernels.
+#pragma once
+
+#include "hp_common.cuh"
+
+namespace hp {
+
+// Counter slots in DedupPlan::counters (device int32).
+enum { C_UNIQ = 0, C_ITEMS = 1, C_LONG = 2, C_PARTIALS = 3, C_ERR = 4, C_NCOUNTERS = 8 };
+
+// Views into the caller's workspace (all device pointers).
+struct DedupPlan {
+  int64_t T;            // items
+  int32_t D;            // row width (floats) the partial buffer was sized for
+  int32_t P, nranks;
+  int64_t V;
+  int32_t key_bits;     // bits of the sort key (ceil(log2 V))
+  int32_t ntiles;       // large path tiles
+  uint32_t* key[2];     // ping-pong sort keys [T]
+  int32_t* pos[2];      // ping-pong original positions [T]
+  int32_t* sorted_pos;  // alias of the final pos buffer
+  uint32_t* uniq_key;   // [T] unique ids ascending (u order)
+  int32_t* seg_start;   // [T+1]
+  int32_t* segidx;      // [T] segment of each sorted item
+  int32_t* sigma;       // [T] send slot of segment u
+  int32_t* item_off;    // [T+1] first reduce item of segment u
+  int32_t* item_seg;    // [T] segment of reduce item
+  int32_t* part_off;    // [T] partial-buffer slot of segment u (long segments)
+  int32_t* long_list;   // [T] long segments (L > HP_CHUNK)
+  int32_t* first_u;     // [P+1] first unique index of partition p
+  int32_t* part_base;   // [P] send-slot base of partition p
+  int32_t* zero_owner;  // [P] zeros (owner table when all partitions are local)
+  int32_t* tile_hist;   // [256 * ntiles]
+  int32_t* digit_tot;   // [256]
+  int32_t* scan_bsum;   // [scan blocks + 1]
+  int32_t* counters;    // [C_NCOUNTERS]
+  float* partials;      // [(2T/C + 2) * D]
+  int64_t partial_rows;
+};
+
+size_t dedup_ws_bytes(int64_t T, int32_t D, int32_t P);
+int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, int64_t V,
+               int32_t P, int32_t nranks);
+
+// Build the plan on `stream`. owner == nullptr means every partition is on rank 0.
+// Optional outputs (nullable): send_ids, counts, inv, dest_counts, n_uniq.
+int build_plan(DedupPlan& pl, const int64_t* ids, const int32_t* owner, int64_t* send_ids,
+               int32_t* counts, int32_t* inv, int32_t* dest_counts, int32_t* n_uniq,
+               cudaStream_t stream);
+
+}  // namespace hp

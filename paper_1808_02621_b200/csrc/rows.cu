@@ -1,0 +1,235 @@
+// K5 gather, K6 stitch, table init, dense scale+cast epilogue.
+//
+// K5 (PS pull, sparseplan/simulate.py:195-199): out[i] = slab row of ids[i].
+// K6 (stitch):                     out[t] = rows[inv[t]].
+// Both are warp-per-row copies with several rows in flight per warp and
+// 128-bit loads/stores; bytes moved = rows * D * 4 read + written.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "hp_common.cuh"
+
+namespace hp {
+namespace {
+
+struct SrcSlab {  // row of a global id in this rank's slab (nullptr if not homed)
+  const float4* w;
+  const int64_t* part_base;
+  const int64_t* ids;
+  Router route;
+  int D4;
+  __device__ __forceinline__ const float4* operator()(int64_t i) const {
+    const int64_t id = ids[i];
+    const int p = route.part(id);
+    const int64_t b = part_base[p];
+    return b < 0 ? nullptr : w + (b + (id - route.lo(p))) * D4;
+  }
+};
+
+struct SrcInv {
+  const float4* rows;
+  const int32_t* inv;
+  int D4;
+  __device__ __forceinline__ const float4* operator()(int64_t t) const {
+    return rows + (int64_t)inv[t] * D4;
+  }
+};
+
+template <int VPL, int RPW, class Src>
+__global__ void __launch_bounds__(256)
+k_copy_rows(Src src, int64_t n, const int32_t* n_dev, float4* __restrict__ out, int D4) {
+  const int lane = threadIdx.x & 31;
+  const int64_t lim = n_dev ? min(n, (int64_t)*n_dev) : n;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * RPW; r0 < lim;
+       r0 += nw * RPW) {
+    float4 x[RPW][VPL];
+#pragma unroll
+    for (int e = 0; e < RPW; ++e) {
+      const int64_t r = r0 + e;
+      const float4* s = r < lim ? src(r) : nullptr;
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        const int c4 = lane + 32 * v;
+        x[e][v] = (s && c4 < D4) ? s[c4] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < RPW; ++e) {
+      const int64_t r = r0 + e;
+      if (r >= lim) break;
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        const int c4 = lane + 32 * v;
+        if (c4 < D4) out[r * D4 + c4] = x[e][v];
+      }
+    }
+  }
+}
+
+template <class Src>
+int launch_copy(const Src& src, int64_t n, const int32_t* n_dev, float* out, int D,
+                cudaStream_t st) {
+  if (n <= 0) return HP_OK;
+  const int D4 = D >> 2;
+  const int sms = sm_count();
+  float4* o = reinterpret_cast<float4*>(out);
+  if (D4 <= 32) {
+    k_copy_rows<1, 8, Src><<<grid_for(n, 64, sms * 8), 256, 0, st>>>(src, n, n_dev, o, D4);
+  } else if (D4 <= 64) {
+    k_copy_rows<2, 4, Src><<<grid_for(n, 32, sms * 8), 256, 0, st>>>(src, n, n_dev, o, D4);
+  } else if (D4 <= 128) {
+    k_copy_rows<4, 2, Src><<<grid_for(n, 16, sms * 8), 256, 0, st>>>(src, n, n_dev, o, D4);
+  } else if (D4 <= 256) {
+    k_copy_rows<8, 1, Src><<<grid_for(n, 8, sms * 8), 256, 0, st>>>(src, n, n_dev, o, D4);
+  } else {
+    k_copy_rows<16, 1, Src><<<grid_for(n, 8, sms * 8), 256, 0, st>>>(src, n, n_dev, o, D4);
+  }
+  HP_LAUNCHED(1, "k_copy_rows");
+  return HP_OK;
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_init_rows(float* w, int64_t row_lo, int64_t nrows, int D, uint64_t seed,
+                            float two_scale, float scale) {
+  const int64_t n = nrows * D;
+  const uint64_t mix = seed * 0xD1B54A32D192ED03ull;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t g = (uint64_t)(row_lo * D) + (uint64_t)i;  // global element index
+    const float u = (float)(splitmix64(g ^ mix) >> 40) * (1.0f / 16777216.0f);
+    w[i] = __fsub_rn(__fmul_rn(u, two_scale), scale);
+  }
+}
+
+__global__ void k_fill(float4* x, int64_t n4, float v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = make_float4(v, v, v, v);
+}
+
+template <typename OutT>
+__device__ __forceinline__ void store4(OutT* out, int64_t i4, float4 v);
+template <>
+__device__ __forceinline__ void store4<float>(float* out, int64_t i4, float4 v) {
+  reinterpret_cast<float4*>(out)[i4] = v;
+}
+template <>
+__device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* out, int64_t i4, float4 v) {
+  __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&a);
+  u.y = *reinterpret_cast<uint32_t*>(&b);
+  reinterpret_cast<uint2*>(out)[i4] = u;
+}
+template <>
+__device__ __forceinline__ void store4<__half>(__half* out, int64_t i4, float4 v) {
+  __half2 a = __floats2half2_rn(v.x, v.y), b = __floats2half2_rn(v.z, v.w);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&a);
+  u.y = *reinterpret_cast<uint32_t*>(&b);
+  reinterpret_cast<uint2*>(out)[i4] = u;
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(256)
+k_scale_cast(const float* __restrict__ in, OutT* __restrict__ out, int64_t n, float scale) {
+  const int64_t n4 = n >> 2;
+  const float4* in4 = reinterpret_cast<const float4*>(in);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 v = ldg_stream(in4 + i);
+    v.x = __fmul_rn(v.x, scale);
+    v.y = __fmul_rn(v.y, scale);
+    v.z = __fmul_rn(v.z, scale);
+    v.w = __fmul_rn(v.w, scale);
+    store4<OutT>(out, i, v);
+  }
+  for (int64_t i = (n4 << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float v = __fmul_rn(in[i], scale);
+    if constexpr (sizeof(OutT) == 4) out[i] = v;
+    else if constexpr (std::is_same<OutT, __nv_bfloat16>::value) out[i] = __float2bfloat16_rn(v);
+    else out[i] = __float2half_rn(v);
+  }
+}
+
+}  // namespace
+
+int scale_cast(const float* in, void* out, int64_t count, int32_t out_dtype, float scale,
+               cudaStream_t st) {
+  if (count <= 0) return HP_OK;
+  HP_REQUIRE(((uintptr_t)in & 15) == 0 && ((uintptr_t)out & 15) == 0,
+             "dense buffers must be 16-byte aligned");
+  const int g = grid_for((count >> 2) + 1, 256, sm_count() * 8);
+  switch (out_dtype) {
+    case HP_DTYPE_F32:
+      if (scale == 1.0f && out == in) return HP_OK;
+      k_scale_cast<float><<<g, 256, 0, st>>>(in, static_cast<float*>(out), count, scale);
+      break;
+    case HP_DTYPE_BF16:
+      k_scale_cast<__nv_bfloat16><<<g, 256, 0, st>>>(in, static_cast<__nv_bfloat16*>(out), count,
+                                                     scale);
+      break;
+    case HP_DTYPE_F16:
+      k_scale_cast<__half><<<g, 256, 0, st>>>(in, static_cast<__half*>(out), count, scale);
+      break;
+    default:
+      set_error("unknown out_dtype");
+      return HP_EINVAL;
+  }
+  HP_LAUNCHED(1, "k_scale_cast");
+  return HP_OK;
+}
+
+}  // namespace hp
+
+using namespace hp;
+
+extern "C" {
+
+int hp_gather_rows(hp_slab slab, const int64_t* ids, int64_t n, const int32_t* n_dev, float* out,
+                   void* stream) {
+  HP_REQUIRE(slab.D >= 4 && slab.D % 4 == 0 && slab.D <= 2048, "D must be a multiple of 4");
+  HP_REQUIRE(n == 0 || (ids && out && slab.w && slab.part_base), "NULL argument");
+  SrcSlab src{reinterpret_cast<const float4*>(slab.w), slab.part_base, ids, Router(slab.V, slab.P),
+              slab.D >> 2};
+  return launch_copy(src, n, n_dev, out, slab.D, static_cast<cudaStream_t>(stream));
+}
+
+int hp_stitch(const float* rows, const int32_t* inv, int64_t T, int32_t D, float* out,
+              void* stream) {
+  HP_REQUIRE(D >= 4 && D % 4 == 0 && D <= 2048, "D must be a multiple of 4");
+  HP_REQUIRE(T == 0 || (rows && inv && out), "NULL argument");
+  SrcInv src{reinterpret_cast<const float4*>(rows), inv, D >> 2};
+  return launch_copy(src, T, nullptr, out, D, static_cast<cudaStream_t>(stream));
+}
+
+int hp_init_rows(float* w, int64_t row_lo, int64_t nrows, int32_t D, uint64_t seed, float scale,
+                 void* stream) {
+  if (nrows <= 0) return HP_OK;
+  HP_REQUIRE(w != nullptr && D >= 1, "bad init arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  k_init_rows<<<grid_for(nrows * D, 256, sm_count() * 8), 256, 0, st>>>(w, row_lo, nrows, D, seed,
+                                                                         2.0f * scale, scale);
+  HP_LAUNCHED(1, "k_init_rows");
+  return HP_OK;
+}
+
+int hp_fill(float* x, int64_t n, float value, void* stream) {
+  if (n <= 0) return HP_OK;
+  HP_REQUIRE(x != nullptr && n % 4 == 0 && ((uintptr_t)x & 15) == 0,
+             "fill needs a 16-byte aligned buffer of 4k floats");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  k_fill<<<grid_for(n / 4, 256, sm_count() * 8), 256, 0, st>>>(reinterpret_cast<float4*>(x), n / 4,
+                                                               value);
+  HP_LAUNCHED(1, "k_fill");
+  return HP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,221 @@
+"""Typed PyTorch wrappers over the C ABI (one call = one C entry point).
+
+Every function checks dtype / device / contiguity, marshals ``data_ptr()`` and
+the current CUDA stream, and raises :class:`HybridPathError` on a non-zero
+return. No op has a CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import Optim, Slab, call, load
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def _need(t: torch.Tensor, dtype, name: str, dim: int | None = None) -> None:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if dim is not None and t.dim() != dim:
+        raise ValueError(f"{name} must be {dim}-D, got shape {tuple(t.shape)}")
+
+
+class Workspace:
+    """Grow-only device scratch buffer shared by consecutive calls on one stream."""
+
+    def __init__(self, device):
+        self.device = torch.device(device)
+        self.buf = torch.empty(0, dtype=torch.uint8, device=self.device)
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        if self.buf.numel() < nbytes:
+            self.buf = torch.empty(int(nbytes * 1.25) + 4096, dtype=torch.uint8, device=self.device)
+        return self.buf
+
+    @property
+    def ptr(self) -> int:
+        return self.buf.data_ptr()
+
+    @property
+    def nbytes(self) -> int:
+        return self.buf.numel()
+
+
+def dedup_ws_bytes(T: int, D: int, P: int, nranks: int = 1) -> int:
+    return int(load().hp_dedup_ws_bytes(T, D, P, nranks))
+
+
+@dataclass
+class OptimizerConfig:
+    """Sparse row optimizer: sgd | adagrad | adam."""
+
+    kind: str = "adagrad"
+    lr: float = 0.2
+    init_acc: float = 0.1
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+
+    def __post_init__(self):
+        if self.kind not in _lib.HP_OPT:
+            raise ValueError(f"unknown optimizer {self.kind!r}")
+
+    def c_struct(self, step: int, agg_scale: float) -> Optim:
+        lr_t = 0.0
+        if self.kind == "adam":
+            lr_t = self.lr * np.sqrt(1.0 - self.beta2 ** step) / (1.0 - self.beta1 ** step)
+        return Optim(_lib.HP_OPT[self.kind], self.lr, self.beta1, self.beta2, 1.0 - self.beta1,
+                     1.0 - self.beta2, self.eps, float(np.float32(lr_t)), agg_scale)
+
+    @property
+    def n_state(self) -> int:
+        return {"sgd": 0, "adagrad": 1, "adam": 2}[self.kind]
+
+
+def sort_dedup_route(ids: torch.Tensor, vals: torch.Tensor, V: int, P: int, owner: torch.Tensor,
+                     nranks: int, ws: Workspace, out: dict | None = None, stream=None) -> dict:
+    """K1+K2: dedup + route one worker's IndexedSlices into send order."""
+    _need(ids, torch.int64, "ids", 1)
+    _need(vals, torch.float32, "vals", 2)
+    _need(owner, torch.int32, "owner", 1)
+    T, D = vals.shape
+    if ids.numel() != T:
+        raise ValueError("ids and vals disagree on T")
+    dev = ids.device
+    o = out if out is not None else {}
+    if "send_rows" in o and (o["send_rows"].shape[0] < max(T, 1) or o["send_rows"].shape[1] != D
+                             or o["dest_counts"].numel() != nranks):
+        o.clear()
+    o.setdefault("send_ids", torch.empty(max(T, 1), dtype=torch.int64, device=dev))
+    o.setdefault("send_rows", torch.empty(max(T, 1), D, dtype=torch.float32, device=dev))
+    o.setdefault("counts", torch.empty(max(T, 1), dtype=torch.int32, device=dev))
+    o.setdefault("inv", torch.empty(max(T, 1), dtype=torch.int32, device=dev))
+    o.setdefault("dest_counts", torch.empty(nranks, dtype=torch.int32, device=dev))
+    o.setdefault("n_uniq", torch.empty(1, dtype=torch.int32, device=dev))
+    need = dedup_ws_bytes(T, D, P, nranks)
+    ws.get(need)
+    call("hp_sort_dedup_route", _p(ids), _p(vals), T, D, V, P, _p(owner), nranks,
+         _p(o["send_ids"]), _p(o["send_rows"]), _p(o["counts"]), _p(o["inv"]),
+         _p(o["dest_counts"]), _p(o["n_uniq"]), ws.ptr, ws.nbytes, _stream(stream))
+    return o
+
+
+def dedup_plan(ids: torch.Tensor, V: int, P: int, owner: torch.Tensor | None, nranks: int, D: int,
+               ws: Workspace, outputs: bool = True, stream=None) -> dict:
+    """Index-only K1+K2 (no rows): send ids, counts, inverse map, dest counts.
+
+    With ``outputs=False`` only the plan in ``ws`` is built (for apply_plan)."""
+    _need(ids, torch.int64, "ids", 1)
+    T = ids.numel()
+    dev = ids.device
+    if outputs:
+        o = {"send_ids": torch.empty(max(T, 1), dtype=torch.int64, device=dev),
+             "counts": torch.empty(max(T, 1), dtype=torch.int32, device=dev),
+             "inv": torch.empty(max(T, 1), dtype=torch.int32, device=dev),
+             "dest_counts": torch.empty(nranks, dtype=torch.int32, device=dev),
+             "n_uniq": torch.empty(1, dtype=torch.int32, device=dev)}
+    else:
+        o = {k: None for k in ("send_ids", "counts", "inv", "dest_counts", "n_uniq")}
+    ws.get(dedup_ws_bytes(T, D, P, nranks))
+    call("hp_dedup_plan", _p(ids), T, D, V, P, _p(owner), nranks, _p(o["send_ids"]),
+         _p(o["counts"]), _p(o["inv"]), _p(o["dest_counts"]), _p(o["n_uniq"]), ws.ptr, ws.nbytes,
+         _stream(stream))
+    return o
+
+
+def plan_status(ws: Workspace, stream=None) -> int:
+    err = C.c_int32(0)
+    call("hp_plan_status", ws.ptr, C.addressof(err), _stream(stream))
+    return err.value
+
+
+def merge_apply(ids: torch.Tensor, rows: torch.Tensor, n: int, slab: Slab, opt: Optim,
+                ws: Workspace, stream=None) -> None:
+    """K4: merge received (id, row) pairs and apply the optimizer on the owner slab."""
+    _need(ids, torch.int64, "ids", 1)
+    _need(rows, torch.float32, "rows", 2)
+    ws.get(dedup_ws_bytes(n, slab.D, slab.P))
+    call("hp_merge_apply", _p(ids), _p(rows), n, slab, opt, ws.ptr, ws.nbytes, _stream(stream))
+
+
+def local_apply(ids: torch.Tensor, vals: torch.Tensor, slab: Slab, opt: Optim, ws: Workspace,
+                stream=None) -> None:
+    """n == 1 fused K1+K4: dedup the worker's slices and apply straight to the slab."""
+    _need(ids, torch.int64, "ids", 1)
+    _need(vals, torch.float32, "vals", 2)
+    T = ids.numel()
+    ws.get(dedup_ws_bytes(T, slab.D, slab.P))
+    call("hp_local_apply", _p(ids), _p(vals), T, slab, opt, ws.ptr, ws.nbytes, _stream(stream))
+
+
+def apply_plan(rows: torch.Tensor, n: int, slab: Slab, opt: Optim, ws: Workspace,
+               stream=None) -> None:
+    """K4 only: reduce + apply with the plan a preceding dedup_plan left in ``ws``."""
+    _need(rows, torch.float32, "rows", 2)
+    call("hp_apply_plan", _p(rows), n, slab, opt, ws.ptr, ws.nbytes, _stream(stream))
+
+
+def launch_count() -> int:
+    """Kernels this library has launched so far in the process."""
+    return int(load().hp_launch_count())
+
+
+def gather_rows(slab: Slab, ids: torch.Tensor, out: torch.Tensor, n: int | None = None,
+                n_dev: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """K5: out[i] = row ids[i] of this rank's slab."""
+    _need(ids, torch.int64, "ids", 1)
+    _need(out, torch.float32, "out", 2)
+    n = ids.numel() if n is None else n
+    call("hp_gather_rows", slab, _p(ids), n, _p(n_dev), _p(out), _stream(stream))
+    return out
+
+
+def stitch(rows: torch.Tensor, inv: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
+    """K6: out[t] = rows[inv[t]]."""
+    _need(rows, torch.float32, "rows", 2)
+    _need(inv, torch.int32, "inv", 1)
+    _need(out, torch.float32, "out", 2)
+    T, D = out.shape
+    call("hp_stitch", _p(rows), _p(inv), T, D, _p(out), _stream(stream))
+    return out
+
+
+def init_rows(w: torch.Tensor, row_lo: int, seed: int, scale: float = 0.05, stream=None) -> None:
+    _need(w, torch.float32, "w", 2)
+    call("hp_init_rows", _p(w), row_lo, w.shape[0], w.shape[1], seed, scale, _stream(stream))
+
+
+def fill(x: torch.Tensor, value: float, stream=None) -> None:
+    _need(x, torch.float32, "x")
+    call("hp_fill", _p(x), x.numel(), value, _stream(stream))
+
+
+def dense_allreduce_scale_cast(comm, grad: torch.Tensor, out: torch.Tensor, scale: float,
+                               stream=None) -> torch.Tensor:
+    """K7: out = cast(scale * sum over ranks of grad); grad is reduced in place."""
+    _need(grad, torch.float32, "grad")
+    if out.dtype not in (torch.float32, torch.bfloat16, torch.float16) or not out.is_contiguous():
+        raise TypeError("out must be a contiguous float32/bfloat16/float16 tensor")
+    if out.numel() != grad.numel():
+        raise ValueError("grad and out sizes differ")
+    code = _lib.HP_DTYPE[str(out.dtype).split(".")[1]]
+    call("hp_dense_allreduce_scale_cast", comm, _p(grad), _p(out), grad.numel(), code, scale,
+         _stream(stream))
+    return out

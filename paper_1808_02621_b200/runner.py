@@ -1,0 +1,361 @@
+"""HybridRunner: one synchronous hybrid-communication step on real devices.
+
+The device counterpart of the reference's ``simulate_iteration`` /
+``simulate_training`` (`sparseplan/simulate.py:326-402`): it consumes an
+unchanged :class:`DistributedPlan` (from :func:`transform_hybrid`) and runs
+
+* dense (AR) Weights  -> K7 allreduce fused with the 1/n scale + cast;
+* sparse (PS) Weights -> K1+K2 sort/dedup/route, K3 push all-to-all,
+  K4 owner merge + scatter-apply, K5 owner gather, K3 pull, K6 stitch.
+  With one GPU every partition is local (the reference marks every Weight AR
+  at one machine, `placement.py:111`) and the step is the fused local apply
+  followed by a gather.
+
+Tables live as row slabs: rank r holds the partitions p with owner[p] == r,
+concatenated in ascending p (each partition is a separate view,
+:meth:`ShardedTable.partition`). ``step()`` returns an ``IterationStats`` with
+measured phase times (CUDA events) and measured exchange bytes.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import ops
+from ._lib import Slab
+from .model import ClusterSpec, GraphSpec, SpecError, VariableSpec, partition_bounds
+from .ops import OptimizerConfig, Workspace
+from .placement import DistributedPlan, Mechanism, transform_hybrid
+from .stats import IterationStats, Message, TransferReport
+
+
+class ShardedTable:
+    """This rank's partitions of one sparse Weight plus optimizer state."""
+
+    def __init__(self, var: VariableSpec, partitions: int, owner: np.ndarray, rank: int,
+                 optimizer: OptimizerConfig, device, seed: int = 0, init_scale: float = 0.05):
+        if var.elem_bytes % 16:
+            raise SpecError(f"table {var.name!r}: row bytes must be a multiple of 16 (D % 4 == 0)")
+        self.var = var
+        self.name = var.name
+        self.V = var.elements
+        self.D = var.elem_bytes // 4
+        self.P = partitions
+        self.rank = rank
+        self.optimizer = optimizer
+        self.device = torch.device(device)
+        self.owner = np.asarray(owner, dtype=np.int32)
+        self.bounds = partition_bounds(self.V, self.P)
+        self.owned = [p for p in range(self.P) if self.owner[p] == rank]
+        base = np.full(self.P, -1, dtype=np.int64)
+        rows = 0
+        for p in self.owned:
+            base[p] = rows
+            rows += int(self.bounds[p + 1] - self.bounds[p])
+        self.rows = rows
+        self.part_base_host = base
+        self.part_base = torch.from_numpy(base).to(self.device)
+        self.owner_dev = torch.from_numpy(self.owner).to(self.device)
+        self.w = torch.empty(max(rows, 1), self.D, dtype=torch.float32, device=self.device)
+        self.state = [torch.empty_like(self.w) for _ in range(optimizer.n_state)]
+        for p in self.owned:
+            lo, hi = int(self.bounds[p]), int(self.bounds[p + 1])
+            ops.init_rows(self.partition(p), lo, seed, init_scale)
+        if optimizer.kind == "adagrad":
+            ops.fill(self.state[0], optimizer.init_acc)
+        elif optimizer.kind == "adam":
+            for s in self.state:
+                s.zero_()
+        self.ws = Workspace(self.device)
+        self.step_count = 0
+
+    def partition(self, p: int) -> torch.Tensor:
+        """Partition p as its own [rows_p, D] array (view into the slab)."""
+        b = int(self.part_base_host[p])
+        if b < 0:
+            raise KeyError(f"partition {p} of {self.name!r} is not homed on rank {self.rank}")
+        n = int(self.bounds[p + 1] - self.bounds[p])
+        return self.w[b:b + n]
+
+    def slab(self) -> Slab:
+        s0 = self.state[0].data_ptr() if self.state else None
+        s1 = self.state[1].data_ptr() if len(self.state) > 1 else None
+        return Slab(self.w.data_ptr(), s0, s1, self.part_base.data_ptr(), self.V, self.P, self.D)
+
+    def state_dict(self) -> dict:
+        out = {"w": self.w[:self.rows]}
+        for k, s in zip(("acc",) if self.optimizer.kind == "adagrad" else ("m", "v"), self.state):
+            out[k] = s[:self.rows]
+        return out
+
+
+@dataclass
+class _Scratch:
+    """Grow-only per-table exchange buffers."""
+
+    cap: int = 0
+    tensors: dict = field(default_factory=dict)
+
+
+class HybridRunner:
+    """Run hybrid-communication steps for ``plan`` on this process's GPU.
+
+    Parameters mirror the reference planner inputs: ``plan`` / ``graph`` /
+    ``cluster`` (a one-box cluster is ``ClusterSpec.b200_box(n)``), plus the
+    runtime choices the reference leaves to the framework: the sparse row
+    optimizer, ``aggregation`` ('mean' divides by n as Horovod/Parallax
+    averaging does, 'sum' does not; `PAPER.md:542`) and the dense output dtype.
+    """
+
+    def __init__(self, plan: DistributedPlan, graph: GraphSpec, cluster: ClusterSpec, *,
+                 rank: int = 0, world_size: int = 1, comm=None,
+                 optimizer: OptimizerConfig | None = None, aggregation: str = "mean",
+                 dense_dtype: torch.dtype = torch.float32, device=None, seed: int = 0):
+        if aggregation not in ("mean", "sum"):
+            raise ValueError("aggregation must be 'mean' or 'sum'")
+        if cluster.total_gpus != world_size:
+            raise SpecError(f"cluster has {cluster.total_gpus} GPUs but world_size={world_size}")
+        if world_size > 1 and cluster.gpus_per_machine != 1:
+            raise SpecError("one B200 box is ClusterSpec(machines=n_gpus, gpus_per_machine=1)")
+        if world_size > 1 and comm is None:
+            raise ValueError("world_size > 1 needs a Comm (Comm.from_torch_distributed())")
+        self.plan, self.graph, self.cluster = plan, graph, cluster
+        self.rank, self.world_size, self.comm = rank, world_size, comm
+        self.optimizer = optimizer or OptimizerConfig()
+        self.aggregation = aggregation
+        self.scale = 1.0 / world_size if aggregation == "mean" else 1.0
+        self.dense_dtype = dense_dtype
+        self.device = torch.device(device if device is not None else torch.cuda.current_device())
+        self.seed = seed
+        self.tables: dict[str, ShardedTable] = {}
+        self.dense: list[VariableSpec] = []
+        for i, var in enumerate(graph.variables):
+            mech = plan.mech_of[var.name]
+            if var.kind == "dense":
+                self.dense.append(var)
+                continue
+            if mech is Mechanism.PS:
+                P = plan.partitions_of[var.name]
+                owner = plan.owner_table(var.name)
+            elif world_size == 1:
+                P, owner = 1, np.zeros(1, dtype=np.int32)  # AR over one replica: local apply
+            else:
+                raise NotImplementedError(
+                    f"sparse Weight {var.name!r} resolved to AR at n={world_size}: the "
+                    "AllGatherv baseline is SURVEY §8(f) 'next', not built yet")
+            self.tables[var.name] = ShardedTable(var, P, owner, rank, self.optimizer,
+                                                 self.device, seed=seed * 1000 + i)
+        self._scratch: dict[str, _Scratch] = {n: _Scratch() for n in self.tables}
+        self.dense_out: dict[str, torch.Tensor] = {}
+        self.outputs: dict[str, torch.Tensor] = {}
+        self.step_count = 0
+        self.last_counts: dict = {}
+        self.kernel_events: dict | None = None
+
+    # ------------------------------------------------------------------ step
+    def _buf(self, name: str, key: str, shape, dtype) -> torch.Tensor:
+        sc = self._scratch[name]
+        t = sc.tensors.get(key)
+        numel = int(np.prod(shape))
+        if t is None or t.numel() < numel or t.dtype != dtype:
+            t = torch.empty(max(numel, 1), dtype=dtype, device=self.device)
+            sc.tensors[key] = t
+        return t[:numel].view(*shape) if len(shape) > 0 else t
+
+    def _kev(self, key: str, begin: bool) -> None:
+        """Per-kernel CUDA events (bench roofline); off unless kernel_events is a dict."""
+        if self.kernel_events is None:
+            return
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(torch.cuda.current_stream())
+        self.kernel_events.setdefault(key, []).append(e)
+
+    def _sparse_local(self, tab: ShardedTable, ids, vals, opt) -> torch.Tensor:
+        T = ids.numel()
+        slab = tab.slab()
+        ops.dedup_plan(ids, tab.V, tab.P, None, 1, tab.D, tab.ws, outputs=False)
+        self._kev(f"k4:{tab.name}", True)
+        ops.apply_plan(vals, T, slab, opt, tab.ws)
+        self._kev(f"k4:{tab.name}", False)
+        out = self._buf(tab.name, "out", (T, tab.D), torch.float32)
+        self._kev(f"k5:{tab.name}", True)
+        ops.gather_rows(slab, ids, out)
+        self._kev(f"k5:{tab.name}", False)
+        return out
+
+    def _sparse_exchange(self, tab: ShardedTable, ids, vals, opt, ev) -> torch.Tensor:
+        n, D, T = self.world_size, tab.D, ids.numel()
+        name = tab.name
+        r = ops.sort_dedup_route(ids, vals, tab.V, tab.P, tab.owner_dev, n, tab.ws,
+                                 out=self._scratch[name].tensors.setdefault("k1", {}))
+        recv_counts = self._buf(name, "recv_counts", (n,), torch.int32)
+        self.comm.alltoall_counts(r["dest_counts"], recv_counts)
+        both = torch.cat([r["dest_counts"], recv_counts]).cpu()  # host counts for NCCL a2a-v
+        send_c = both[:n].tolist()
+        recv_c = both[n:].tolist()
+        R = int(sum(recv_c))
+        ev("intra")
+        recv_ids = self._buf(name, "recv_ids", (max(R, 1),), torch.int64)
+        recv_rows = self._buf(name, "recv_rows", (max(R, 1), D), torch.float32)
+        self.comm.push(r["send_ids"], r["send_rows"], send_c, recv_ids, recv_rows, recv_c, D)
+        ev("network")
+        ops.merge_apply(recv_ids, recv_rows, R, tab.slab(), opt, tab.ws)
+        resp = self._buf(name, "resp", (max(R, 1), D), torch.float32)
+        ops.gather_rows(tab.slab(), recv_ids, resp, n=R)
+        ev("update")
+        pulled = self._buf(name, "pulled", (max(int(sum(send_c)), 1), D), torch.float32)
+        self.comm.pull(resp, recv_c, pulled, send_c, D)
+        ev("network")
+        out = self._buf(name, "out", (T, D), torch.float32)
+        ops.stitch(pulled, r["inv"], out)
+        ev("update")
+        self.last_counts[name] = {"send": send_c, "recv": recv_c}
+        return out
+
+    def step(self, batch: dict, timed: bool = True) -> IterationStats:
+        """One synchronous hybrid step.
+
+        ``batch[name]`` is ``(ids int64[T], vals f32[T, D])`` for a sparse Weight
+        and an fp32 gradient tensor for a dense one (all on this GPU). Pulled
+        rows land in ``self.outputs[name]``; averaged dense gradients in
+        ``self.dense_out[name]``.
+        """
+        self.step_count += 1
+        stream = torch.cuda.current_stream()
+        phases = {"compute": 0.0, "network": 0.0, "intra": 0.0, "update": 0.0}
+        marks = []
+
+        def ev(phase):
+            if timed:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                marks.append((phase, e))
+
+        ev("start")
+        t0 = time.perf_counter()
+        for var in self.dense:
+            g = batch[var.name]
+            out = self.dense_out.get(var.name)
+            if out is None or out.numel() != g.numel() or out.dtype != self.dense_dtype:
+                out = g if self.dense_dtype == torch.float32 else torch.empty(
+                    g.shape, dtype=self.dense_dtype, device=self.device)
+            self.dense_out[var.name] = ops.dense_allreduce_scale_cast(
+                self.comm.ptr if self.comm else None, g, out, self.scale)
+            ev("network")
+        for name, tab in self.tables.items():
+            ids, vals = batch[name]
+            tab.step_count += 1
+            opt = self.optimizer.c_struct(tab.step_count, self.scale)
+            if self.world_size == 1:
+                self.outputs[name] = self._sparse_local(tab, ids, vals, opt)
+                ev("update")
+            else:
+                self.outputs[name] = self._sparse_exchange(tab, ids, vals, opt, ev)
+        if timed:
+            stream.synchronize()
+            for (_, a), (ph, b) in zip(marks, marks[1:]):
+                phases[ph] += a.elapsed_time(b) * 1e3
+            iter_us = marks[0][1].elapsed_time(marks[-1][1]) * 1e3
+        else:
+            iter_us = (time.perf_counter() - t0) * 1e6
+        return IterationStats(iter_us, self._bytes_report(), phases, self._trace(),
+                              {"step": self.step_count})
+
+    def _bytes_report(self) -> TransferReport:
+        n = self.world_size
+        rows = [[0.0, 0.0] for _ in range(n)]
+        for name, c in self.last_counts.items():
+            D = self.tables[name].D
+            for o in range(n):
+                if o == self.rank:
+                    continue
+                rows[self.rank][0] += c["send"][o] * (8 + 4 * D) + c["recv"][o] * 4 * D
+                rows[self.rank][1] += c["recv"][o] * (8 + 4 * D) + c["send"][o] * 4 * D
+        for var in self.dense:
+            if n > 1:
+                per_dir = 2.0 * var.payload_bytes * (n - 1) / n
+                rows[self.rank][0] += per_dir
+                rows[self.rank][1] += per_dir
+        return TransferReport(tuple(tuple(r) for r in rows))
+
+    def _trace(self) -> tuple:
+        out = []
+        me = (self.rank, "gpu0")
+        for name, c in self.last_counts.items():
+            D = self.tables[name].D
+            for o in range(self.world_size):
+                if c["send"][o]:
+                    out.append(Message(me, (o, "server"), c["send"][o] * (8 + 4 * D), name, -1, "push"))
+                if c["recv"][o]:
+                    out.append(Message((self.rank, "server"), (o, "gpu0"), c["recv"][o] * 4 * D,
+                                       name, -1, "pull"))
+        return tuple(out)
+
+    def capture(self, batch: dict, warmup: int = 2) -> torch.cuda.CUDAGraph:
+        """Capture one full step on ``batch``'s (static) tensors as a CUDA graph.
+
+        Single-GPU steps have no host synchronisation, so the whole step
+        (dedup, apply, gather, dense epilogue) replays with one launch. The
+        optimizer struct is baked in at capture: use it for step-independent
+        optimizers (SGD / Adagrad); Adam's bias correction would freeze.
+        """
+        if self.world_size > 1:
+            raise NotImplementedError("the NCCL a2a-v path reads counts on the host")
+        cur = torch.cuda.current_stream()
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                self.step(batch, timed=False)
+        cur.wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step(batch, timed=False)
+        return g
+
+    # ------------------------------------------------------------------ timing / P search
+    def measure(self, make_batch, iterations: int = 100) -> float:
+        """Mean device step time (us) with the first half discarded
+        (reference `simulate.py:380-402`, `PAPER.md:485`)."""
+        if iterations < 2:
+            raise SpecError(f"iterations must be >= 2, got {iterations}")
+        times = []
+        for i in range(iterations):
+            stats = self.step(make_batch(i), timed=True)
+            times.append(stats.iter_time_us)
+        kept = times[iterations // 2:]
+        t = float(np.mean(kept))
+        if self.world_size > 1:
+            import torch.distributed as dist
+
+            x = torch.tensor([t], dtype=torch.float64, device=self.device)
+            dist.all_reduce(x, op=dist.ReduceOp.MAX)
+            t = float(x.item())
+        return t
+
+
+def device_evaluator(graph: GraphSpec, cluster: ClusterSpec, make_batch, *, rank: int = 0,
+                     world_size: int = 1, comm=None, optimizer: OptimizerConfig | None = None,
+                     iterations: int = 100, names: list | None = None, **kw):
+    """evaluator(P) -> mean step us, for :func:`tuning.tune_evaluator`.
+
+    Rebuilds the hybrid plan with every partitionable sparse Weight split into P
+    (the reference CLI's shared-P rule, `cli.py:93-102`) and times real steps.
+    """
+    cands = names or [v.name for v in graph.variables if v.kind == "sparse" and v.partitionable]
+
+    def evaluator(P: int) -> float:
+        parts = {n: min(P, graph.variable(n).elements) for n in cands}
+        plan = transform_hybrid(graph, cluster, partitions=parts)
+        runner = HybridRunner(plan, graph, cluster, rank=rank, world_size=world_size, comm=comm,
+                              optimizer=optimizer, **kw)
+        t = runner.measure(make_batch, iterations)
+        del runner
+        torch.cuda.empty_cache()
+        return t
+
+    return evaluator

@@ -1,0 +1,48 @@
+import os
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+REF_SRC = Path("/root/reference/pkg/src")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (run on the GPU box)")
+    config.addinivalue_line("markers", "slow: long-running")
+
+
+@pytest.fixture(scope="session")
+def reference():
+    """The reference package imported read-only (build container only)."""
+    if not REF_SRC.exists():
+        pytest.skip("reference not present (GPU box): golden vectors cover this")
+    sys.dont_write_bytecode = True
+    if str(REF_SRC) not in sys.path:
+        sys.path.append(str(REF_SRC))
+    import sparseplan
+
+    return sparseplan
+
+
+@pytest.fixture(scope="session")
+def golden():
+    import json
+
+    return json.loads((ROOT / "tests" / "golden" / "planner_golden.json").read_text())
+
+
+@pytest.fixture(scope="session")
+def cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1808_02621_b200 import _lib
+
+    _lib.load()
+    return torch.device("cuda:0")
