@@ -289,8 +289,7 @@ def main():
     if big is not None and f"k4:{big.name}" in kern:
         tab = runner.tables[big.name]
         T = big.T + big.sampled
-        ops.dedup_plan(batches[0][big.name][0], tab.V, tab.P, None, 1, tab.D, tab.ws,
-                       outputs=False)
+        ops.apply_plan_build(batches[0][big.name][0], tab.slab(), tab.ws)
         U = int(tab.ws.buf[:4].view(torch.int32).item())
         k = 1 + opt.n_state
         algo = T * (4 + 4 * big.D) + U * (4 + 4 * big.D * 2 * k)

@@ -120,9 +120,12 @@ int hp_merge_apply(const int64_t* ids, const float* rows, int64_t R, hp_slab sla
 int hp_local_apply(const int64_t* ids, const float* vals, int64_t T, hp_slab slab,
                    hp_optim opt, void* ws, size_t ws_bytes, void* stream);
 
-/* Value half of hp_local_apply / hp_merge_apply: reduce + apply using the plan
- * a preceding hp_dedup_plan(ids, R, slab.D, slab.V, slab.P, NULL, 1, ...) left
- * in ws (same stream). Lets a caller time K4 on its own. */
+/* hp_merge_apply split in two so a caller can time K4 alone:
+ * hp_apply_plan_build dedups ids[R] into a plan (in ws) whose destinations are
+ * slab rows; hp_apply_plan then reduces rows[R, D] and applies the optimizer
+ * with that plan (same stream, same R / slab). */
+int hp_apply_plan_build(const int64_t* ids, int64_t R, hp_slab slab, void* ws, size_t ws_bytes,
+                        void* stream);
 int hp_apply_plan(const float* rows, int64_t R, hp_slab slab, hp_optim opt, void* ws,
                   size_t ws_bytes, void* stream);
 

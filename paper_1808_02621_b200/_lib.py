@@ -37,6 +37,7 @@ SIGNATURES = {
     "hp_device_sm_count": (C.c_int, []),
     "hp_launch_count": (i64, []),
     "hp_apply_plan": (C.c_int, [vp, i64, Slab, Optim, vp, sz, vp]),
+    "hp_apply_plan_build": (C.c_int, [vp, i64, Slab, vp, sz, vp]),
     "hp_dedup_ws_bytes": (sz, [i64, i32, i32, i32]),
     "hp_sort_dedup_route": (C.c_int, [vp, vp, i64, i32, i64, i32, vp, i32, vp, vp, vp, vp, vp, vp,
                                       vp, sz, vp]),

@@ -13,6 +13,8 @@
 //  * larger T: LSD radix sort over 4096-key tiles (tile histogram -> per-digit
 //    column scan -> stable in-tile rank + smem-staged coalesced scatter), then
 //    grid-wide metadata kernels with a reduce-then-scan device scan.
+#include <cooperative_groups.h>
+
 #include "hp_dedup.cuh"
 
 namespace hp {
@@ -127,91 +129,163 @@ __device__ __forceinline__ int lower_bound_u32(const uint32_t* a, int n, uint32_
 
 constexpr int MAX_RANKS = 1024;
 
-// ------------------------------------------------------------------ small path
-template <int NT, int IPT>
-__global__ void __launch_bounds__(NT, 1)
-k_dedup_small(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __restrict__ owner,
-              int64_t* send_ids, int32_t* counts, int32_t* inv, int32_t* dest_counts,
-              int32_t* n_uniq) {
+// Destination row of a segment: its send slot (send plans) or its row in the
+// caller's slab (apply plans; -1 + error bit if the row is not homed here).
+__device__ __forceinline__ int seg_dst(uint32_t id, int p, int slot, const int64_t* dst_pb,
+                                       const Router& route, int* err) {
+  if (!dst_pb) return slot;
+  const int64_t b = dst_pb[p];
+  if (b < 0) {
+    atomicOr(err, 2);
+    return -1;
+  }
+  return (int)(b + ((int64_t)id - route.lo(p)));
+}
+
+// Reduce items of segment u: chunks of HP_CHUNK sorted rows. Short segments
+// (one chunk) are final and write straight to dst; long ones write partial
+// slots bp.. and get a long descriptor for k_combine.
+__device__ __forceinline__ void emit_items(const DedupPlan& pl, int u, int j0, int L, int dst,
+                                           int bi, int bp, int bl) {
+  const int n0 = (L + HP_CHUNK - 1) / HP_CHUNK;
+  const bool lg = L > HP_CHUNK;
+  for (int k = 0; k < n0; ++k)
+    pl.items[bi + k] = make_int4(j0 + k * HP_CHUNK, min(HP_CHUNK, L - k * HP_CHUNK),
+                                 lg ? bp + k : dst, lg ? 0 : 1);
+  if (lg) pl.longs[bl] = make_int4(bp, n0, dst, u);
+}
+
+// ------------------------------------------------------------------ cluster path
+// T <= HP_SMALL_MAX: one thread-block cluster of CS CTAs sorts the ids in
+// distributed shared memory. CTA c owns sorted slice [c*S, (c+1)*S); each LSD
+// pass ranks the slice locally (warp multisplit), publishes its digit counts,
+// and after a cluster barrier scatters every (key, pos) straight into the
+// owning CTA's shared memory (DSMEM stores). The index metadata is derived in
+// the same launch with cluster-wide prefix sums.
+template <int NT, int IPT, int CS>
+__global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(NT, 1)
+k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __restrict__ owner,
+                const int64_t* __restrict__ dst_pb, int64_t* send_ids, int32_t* counts,
+                int32_t* inv, int32_t* dest_counts, int32_t* n_uniq) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  constexpr int S = NT * IPT, NW = NT / 32;
   extern __shared__ __align__(16) unsigned char smem[];
-  constexpr int N = NT * IPT;
-  constexpr int NW = NT / 32;
-  uint32_t* s_key = reinterpret_cast<uint32_t*>(smem);
-  int32_t* s_pos = reinterpret_cast<int32_t*>(s_key + N);
-  int* s_hist = s_pos + N;
-  int* s_scan = s_hist + NW * HS;       // 33 (+pad)
-  int* s_dest = s_scan + 40;            // MAX_RANKS
+  uint2* s_buf = reinterpret_cast<uint2*>(smem);  // sorted slice (key, pos)
+  int* s_hist = reinterpret_cast<int*>(s_buf + S);
+  int* s_scan = s_hist + NW * HS;
+  int* s_cnt = s_scan + 40;       // published digit counts
+  int* s_base = s_cnt + HP_RADIX;
+  int* s_pub = s_base + HP_RADIX; // published scalars
+  int* s_dest = s_pub + 8;
+  const int c = (int)cl.block_rank();
   const int T = (int)pl.T;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const Router route(pl.V, pl.P);
 
   uint32_t key[IPT];
   int32_t pos[IPT];
 #pragma unroll
   for (int r = 0; r < IPT; ++r) {
-    const int i = w * 32 * IPT + r * 32 + lane;
+    const int i = c * S + w * 32 * IPT + r * 32 + lane;
     key[r] = i < T ? load_key(ids, i, pl.V, &pl.counters[C_ERR]) : 0xffffffffu;
     pos[r] = i;
   }
   const int passes = (pl.key_bits + HP_RADIX_BITS - 1) / HP_RADIX_BITS;
   for (int ps = 0; ps < passes; ++ps) {
+    const int shift = ps * HP_RADIX_BITS;
     int rank[IPT];
-    block_rank<NT, IPT>(key, ps * HP_RADIX_BITS, rank, s_hist, s_scan);
+    block_rank<NT, IPT>(key, shift, rank, s_hist, s_scan);
+    if (tid < HP_RADIX) s_cnt[tid] = (tid + 1 < HP_RADIX ? s_hist[tid + 1] : S) - s_hist[tid];
+    cl.sync();
+    int tot = 0, pre = 0;
+    if (tid < HP_RADIX) {
+#pragma unroll
+      for (int cc = 0; cc < CS; ++cc) {
+        const int v = cl.map_shared_rank(s_cnt, cc)[tid];
+        tot += v;
+        pre += cc < c ? v : 0;
+      }
+    }
+    int all;
+    const int ex = block_excl_scan<NT>(tid < HP_RADIX ? tot : 0, s_scan, &all);
+    if (tid < HP_RADIX) s_base[tid] = ex + pre - s_hist[tid];
+    __syncthreads();
 #pragma unroll
     for (int r = 0; r < IPT; ++r) {
-      s_key[rank[r]] = key[r];
-      s_pos[rank[r]] = pos[r];
+      const int g = s_base[(key[r] >> shift) & (HP_RADIX - 1)] + rank[r];
+      const int dc = g / S;
+      cl.map_shared_rank(s_buf, dc)[g - dc * S] = make_uint2(key[r], (uint32_t)pos[r]);
     }
-    __syncthreads();
+    cl.sync();
     if (ps + 1 < passes) {
 #pragma unroll
       for (int r = 0; r < IPT; ++r) {
-        const int i = w * 32 * IPT + r * 32 + lane;
-        key[r] = s_key[i];
-        pos[r] = s_pos[i];
+        const uint2 v = s_buf[w * 32 * IPT + r * 32 + lane];
+        key[r] = v.x;
+        pos[r] = (int32_t)v.y;
       }
     }
   }
-  // ---- segments (blocked: thread t owns sorted items [t*IPT, t*IPT+IPT))
-  int myseg[IPT];
+  // ---- segment heads (blocked: thread t owns slice items [t*IPT, t*IPT+IPT))
+  const uint32_t prev_last = c > 0 ? cl.map_shared_rank(s_buf, c - 1)[S - 1].x : 0u;
   int heads = 0;
 #pragma unroll
   for (int k = 0; k < IPT; ++k) {
-    const int i = threadIdx.x * IPT + k;
-    const bool h = i < T && (i == 0 || s_key[i] != s_key[i - 1]);
-    heads += h;
+    const int li = tid * IPT + k, gi = c * S + li;
+    const uint32_t prev = li > 0 ? s_buf[li - 1].x : prev_last;
+    heads += gi < T && (gi == 0 || s_buf[li].x != prev);
   }
-  int U;
-  int segbase = block_excl_scan<NT>(heads, s_scan, &U);
+  int cta_heads;
+  const int lbase = block_excl_scan<NT>(heads, s_scan, &cta_heads);
+  if (tid == 0) s_pub[0] = cta_heads;
+  cl.sync();
+  int seg_base = 0, U = 0;
+#pragma unroll
+  for (int cc = 0; cc < CS; ++cc) {
+    const int v = cl.map_shared_rank(s_pub, cc)[0];
+    U += v;
+    seg_base += cc < c ? v : 0;
+  }
+  int myseg[IPT];
   {
-    int c = 0;
+    int cnt = 0;
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
-      const int i = threadIdx.x * IPT + k;
-      const bool h = i < T && (i == 0 || s_key[i] != s_key[i - 1]);
+      const int li = tid * IPT + k, gi = c * S + li;
+      const uint32_t prev = li > 0 ? s_buf[li - 1].x : prev_last;
+      const bool h = gi < T && (gi == 0 || s_buf[li].x != prev);
       if (h) {
-        pl.seg_start[segbase + c] = i;
-        pl.uniq_key[segbase + c] = s_key[i];
-        ++c;
+        const int seg = seg_base + lbase + cnt;
+        pl.seg_start[seg] = gi;
+        pl.uniq_key[seg] = s_buf[li].x;
+        ++cnt;
       }
-      myseg[k] = segbase + c - 1;
-      if (i < T) pl.sorted_pos[i] = s_pos[i];
+      myseg[k] = seg_base + lbase + cnt - 1;
+      if (gi < T) pl.sorted_pos[gi] = (int32_t)s_buf[li].y;
     }
   }
-  if (threadIdx.x == 0) {
+  if (c == CS - 1 && tid == 0) {
     pl.seg_start[U] = T;
     pl.counters[C_UNIQ] = U;
     if (n_uniq) *n_uniq = U;
   }
-  __syncthreads();
-  // ---- partition boundaries in the (ascending) unique ids
-  for (int p = threadIdx.x; p <= pl.P; p += NT)
-    pl.first_u[p] = p == pl.P ? U : lower_bound_u32(pl.uniq_key, U, (uint32_t)route.lo(p));
-  __syncthreads();
-  partition_bases<NT>(pl.first_u, owner, pl.P, pl.nranks, pl.part_base, dest_counts, s_dest);
-  // ---- per-segment slots, reduce items, long segments (blocked over u)
-  const int ku = (U + NT - 1) / NT;
-  const int u0 = min(U, (int)threadIdx.x * ku), u1 = min(U, u0 + ku);
+  __threadfence();
+  cl.sync();
+  // ---- partition boundaries / send-slot bases (CTA 0, global)
+  if (c == 0) {
+    for (int p = tid; p <= pl.P; p += NT)
+      pl.first_u[p] = p == pl.P ? U : lower_bound_u32(pl.uniq_key, U, (uint32_t)route.lo(p));
+    __syncthreads();
+    partition_bases<NT>(pl.first_u, owner, pl.P, pl.nranks, pl.part_base, dest_counts, s_dest);
+    __threadfence();
+  }
+  cl.sync();
+  // ---- per-segment slots and reduce items (CTA c: segments [ua, ub), blocked per thread)
+  const int cu = (U + CS - 1) / CS;
+  const int ua = min(U, c * cu), ub = min(U, ua + cu);
+  const int ku = (ub - ua + NT - 1) / NT;
+  const int u0 = min(ub, ua + tid * ku), u1 = min(ub, u0 + ku);
   int ni = 0, np = 0, nl = 0;
   for (int u = u0; u < u1; ++u) {
     const int L = pl.seg_start[u + 1] - pl.seg_start[u];
@@ -219,40 +293,51 @@ k_dedup_small(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __re
     ni += n0;
     if (L > HP_CHUNK) { np += n0; ++nl; }
   }
-  int tot_i, tot_p, tot_l;
-  int bi = block_excl_scan<NT>(ni, s_scan, &tot_i);
-  int bp = block_excl_scan<NT>(np, s_scan, &tot_p);
-  int bl = block_excl_scan<NT>(nl, s_scan, &tot_l);
+  int ti, tp, tl;
+  int bi = block_excl_scan<NT>(ni, s_scan, &ti);
+  int bp = block_excl_scan<NT>(np, s_scan, &tp);
+  int bl = block_excl_scan<NT>(nl, s_scan, &tl);
+  if (tid == 0) {
+    s_pub[1] = ti;
+    s_pub[2] = tp;
+    s_pub[3] = tl;
+  }
+  cl.sync();
+  int all_i = 0, all_p = 0, all_l = 0;
+#pragma unroll
+  for (int cc = 0; cc < CS; ++cc) {
+    const int* q = cl.map_shared_rank(s_pub, cc);
+    const int a = q[1], b = q[2], d = q[3];
+    if (cc < c) { bi += a; bp += b; bl += d; }
+    all_i += a; all_p += b; all_l += d;
+  }
   for (int u = u0; u < u1; ++u) {
-    const int L = pl.seg_start[u + 1] - pl.seg_start[u];
-    const int n0 = (L + HP_CHUNK - 1) / HP_CHUNK;
+    const int j0 = pl.seg_start[u];
+    const int L = pl.seg_start[u + 1] - j0;
     const uint32_t id = pl.uniq_key[u];
     const int p = route.part(id);
     const int slot = pl.part_base[p] + (u - pl.first_u[p]);
     pl.sigma[u] = slot;
     if (send_ids) send_ids[slot] = id;
     if (counts) counts[slot] = L;
-    pl.item_off[u] = bi;
-    for (int k = 0; k < n0; ++k) pl.item_seg[bi + k] = u;
+    const int dst = seg_dst(id, p, slot, dst_pb, route, &pl.counters[C_ERR]);
+    emit_items(pl, u, j0, L, dst, bi, bp, bl);
+    const int n0 = (L + HP_CHUNK - 1) / HP_CHUNK;
     bi += n0;
-    if (L > HP_CHUNK) {
-      pl.part_off[u] = bp;
-      bp += n0;
-      pl.long_list[bl++] = u;
-    }
+    if (L > HP_CHUNK) { bp += n0; ++bl; }
   }
-  if (threadIdx.x == 0) {
-    pl.item_off[U] = tot_i;
-    pl.counters[C_ITEMS] = tot_i;
-    pl.counters[C_PARTIALS] = tot_p;
-    pl.counters[C_LONG] = tot_l;
+  if (c == CS - 1 && tid == 0) {
+    pl.counters[C_ITEMS] = all_i;
+    pl.counters[C_PARTIALS] = all_p;
+    pl.counters[C_LONG] = all_l;
   }
-  __syncthreads();
+  __threadfence();
+  cl.sync();  // sigma visible; no DSMEM access after this point
   if (inv) {
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
-      const int i = threadIdx.x * IPT + k;
-      if (i < T) inv[s_pos[i]] = pl.sigma[myseg[k]];
+      const int li = tid * IPT + k, gi = c * S + li;
+      if (gi < T) inv[s_buf[li].y] = pl.sigma[myseg[k]];
     }
   }
 }
@@ -261,9 +346,9 @@ constexpr size_t tile_smem_bytes() {
   return (size_t)HP_TILE * 8 + (size_t)(HP_TILE_THREADS / 32) * HS * 4 + 40 * 4 + HP_RADIX * 4;
 }
 
-constexpr size_t small_smem_bytes() {
-  return (size_t)HP_SMALL_MAX * 8 + (size_t)(HP_SMALL_THREADS / 32) * HS * 4 + 40 * 4 +
-         MAX_RANKS * 4;
+constexpr size_t cluster_smem_bytes() {
+  return (size_t)HP_CL_SLICE * 8 + (size_t)(HP_CL_THREADS / 32) * HS * 4 + 40 * 4 +
+         2 * HP_RADIX * 4 + 8 * 4 + MAX_RANKS * 4;
 }
 
 // ------------------------------------------------------------------ large path
@@ -465,8 +550,10 @@ k_part_base(DedupPlan pl, const int32_t* __restrict__ owner, int32_t* dest_count
   partition_bases<1024>(pl.first_u, owner, pl.P, pl.nranks, pl.part_base, dest_counts, s_dest);
 }
 
-// Per segment: send slot, outputs, and the three count arrays to be scanned.
-__global__ void k_seg_counts(DedupPlan pl, int64_t* send_ids, int32_t* counts, int32_t* long_tmp) {
+// Per segment: send slot, destination row, outputs, and the three count
+// arrays (items, partial slots, long flag) to be scanned.
+__global__ void k_seg_counts(DedupPlan pl, const int64_t* __restrict__ dst_pb, int64_t* send_ids,
+                             int32_t* counts) {
   const Router route(pl.V, pl.P);
   const int U = pl.counters[C_UNIQ];
   for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x) {
@@ -478,21 +565,19 @@ __global__ void k_seg_counts(DedupPlan pl, int64_t* send_ids, int32_t* counts, i
     pl.sigma[u] = slot;
     if (send_ids) send_ids[slot] = id;
     if (counts) counts[slot] = L;
+    pl.dst[u] = seg_dst(id, p, slot, dst_pb, route, &pl.counters[C_ERR]);
     pl.item_off[u] = n0;
     pl.part_off[u] = L > HP_CHUNK ? n0 : 0;
-    long_tmp[u] = L > HP_CHUNK ? 1 : 0;
+    pl.long_tmp[u] = L > HP_CHUNK ? 1 : 0;
   }
 }
 
-__global__ void k_items(DedupPlan pl, const int32_t* __restrict__ long_tmp) {
+__global__ void k_items(DedupPlan pl) {
   const int U = pl.counters[C_UNIQ];
   for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x) {
-    const int L = pl.seg_start[u + 1] - pl.seg_start[u];
-    const int n0 = (L + HP_CHUNK - 1) / HP_CHUNK;
-    const int b = pl.item_off[u];
-    for (int k = 0; k < n0; ++k) pl.item_seg[b + k] = u;
-    if (L > HP_CHUNK) pl.long_list[long_tmp[u]] = u;
-    if (u == 0) pl.item_off[U] = pl.counters[C_ITEMS];
+    const int j0 = pl.seg_start[u];
+    emit_items(pl, u, j0, pl.seg_start[u + 1] - j0, pl.dst[u], pl.item_off[u], pl.part_off[u],
+               pl.long_tmp[u]);
   }
 }
 
@@ -514,7 +599,8 @@ size_t dedup_ws_bytes(int64_t T, int32_t D, int32_t P) {
   size_t s = align256(4 * C_NCOUNTERS);
   s += 4 * align256(4 * Tc);          // key[2], pos[2]
   s += 3 * align256(4 * (Tc + 1));    // uniq_key, seg_start, item_off
-  s += 6 * align256(4 * Tc);          // segidx, sigma, item_seg, part_off, long_list, (spare)
+  s += 5 * align256(4 * Tc);          // segidx, sigma, part_off, dst, long_tmp
+  s += align256(16 * Tc) + align256(16 * (Tc / HP_CHUNK + 2));  // items, longs
   s += align256(4 * ((size_t)P + 1)) + 2 * align256(4 * (size_t)P);
   s += align256(4 * HP_RADIX * ntiles) + align256(4 * HP_RADIX);
   s += align256(4 * nscan);
@@ -556,10 +642,11 @@ int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, i
   pl->item_off = (int32_t*)take(4 * (Tc + 1));
   pl->segidx = (int32_t*)take(4 * Tc);
   pl->sigma = (int32_t*)take(4 * Tc);
-  pl->item_seg = (int32_t*)take(4 * Tc);
   pl->part_off = (int32_t*)take(4 * Tc);
-  pl->long_list = (int32_t*)take(4 * Tc);
-  take(4 * Tc);
+  pl->dst = (int32_t*)take(4 * Tc);
+  pl->long_tmp = (int32_t*)take(4 * Tc);
+  pl->items = (int4*)take(16 * Tc);
+  pl->longs = (int4*)take(16 * (Tc / HP_CHUNK + 2));
   pl->first_u = (int32_t*)take(4 * ((size_t)P + 1));
   pl->part_base = (int32_t*)take(4 * (size_t)P);
   pl->zero_owner = (int32_t*)take(4 * (size_t)P);
@@ -572,31 +659,27 @@ int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, i
   return HP_OK;
 }
 
-int build_plan(DedupPlan& pl, const int64_t* ids, const int32_t* owner, int64_t* send_ids,
-               int32_t* counts, int32_t* inv, int32_t* dest_counts, int32_t* n_uniq,
-               cudaStream_t st) {
+int build_plan(DedupPlan& pl, const int64_t* ids, const int32_t* owner,
+               const int64_t* dst_pb, int64_t* send_ids, int32_t* counts, int32_t* inv,
+               int32_t* dest_counts, int32_t* n_uniq, cudaStream_t st) {
   HP_CUDA(cudaMemsetAsync(pl.counters, 0, 4 * C_NCOUNTERS, st));
   if (pl.T == 0) {
     if (dest_counts) HP_CUDA(cudaMemsetAsync(dest_counts, 0, 4 * (size_t)pl.nranks, st));
     if (n_uniq) HP_CUDA(cudaMemsetAsync(n_uniq, 0, 4, st));
-    HP_CUDA(cudaMemsetAsync(pl.item_off, 0, 4, st));
-    HP_CUDA(cudaMemsetAsync(pl.seg_start, 0, 4, st));
     return HP_OK;
   }
   if (pl.T <= HP_SMALL_MAX) {
-    // The small kernel leaves the sorted positions in s_pos and copies them to
-    // pos[0]; sorted_pos already aliases pos[0].
-    constexpr size_t smem = small_smem_bytes();
+    constexpr size_t smem = cluster_smem_bytes();
+    auto kern = k_dedup_cluster<HP_CL_THREADS, HP_CL_IPT, HP_CL_CTAS>;
     static bool configured = false;
     if (!configured) {
-      HP_CUDA(cudaFuncSetAttribute(k_dedup_small<HP_SMALL_THREADS, HP_SMALL_IPT>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       configured = true;
     }
     pl.sorted_pos = pl.pos[0];
-    k_dedup_small<HP_SMALL_THREADS, HP_SMALL_IPT><<<1, HP_SMALL_THREADS, smem, st>>>(
-        pl, ids, owner, send_ids, counts, inv, dest_counts, n_uniq);
-    HP_LAUNCHED(1, "k_dedup_small");
+    kern<<<HP_CL_CTAS, HP_CL_THREADS, smem, st>>>(pl, ids, owner, dst_pb, send_ids, counts, inv,
+                                                  dest_counts, n_uniq);
+    HP_LAUNCHED(1, "k_dedup_cluster");
     return HP_OK;
   }
   // ---- large path: LSD radix sort, 8-bit digits
@@ -619,7 +702,6 @@ int build_plan(DedupPlan& pl, const int64_t* ids, const int32_t* owner, int64_t*
   }
   pl.sorted_pos = pl.pos[src];
   const uint32_t* skey = pl.key[src];
-  int32_t* long_tmp = reinterpret_cast<int32_t*>(pl.key[src ^ 1]);
   const int g = grid_for(pl.T, 256, sm_count() * 8);
   k_heads<<<g, 256, 0, st>>>(pl, skey);
   int rc = device_scan(pl.segidx, pl.T, nullptr, pl.scan_bsum, &pl.counters[C_UNIQ], st);
@@ -627,13 +709,13 @@ int build_plan(DedupPlan& pl, const int64_t* ids, const int32_t* owner, int64_t*
   k_heads_write<<<g, 256, 0, st>>>(pl, skey, n_uniq);
   k_first_u<<<grid_for(pl.P + 1, 256, 1024), 256, 0, st>>>(pl);
   k_part_base<<<1, 1024, 0, st>>>(pl, owner, dest_counts);
-  k_seg_counts<<<g, 256, 0, st>>>(pl, send_ids, counts, long_tmp);
+  k_seg_counts<<<g, 256, 0, st>>>(pl, dst_pb, send_ids, counts);
   HP_LAUNCHED(5, "dedup metadata");
   const int32_t* U = &pl.counters[C_UNIQ];
   if ((rc = device_scan(pl.item_off, pl.T, U, pl.scan_bsum, &pl.counters[C_ITEMS], st))) return rc;
   if ((rc = device_scan(pl.part_off, pl.T, U, pl.scan_bsum, &pl.counters[C_PARTIALS], st))) return rc;
-  if ((rc = device_scan(long_tmp, pl.T, U, pl.scan_bsum, &pl.counters[C_LONG], st))) return rc;
-  k_items<<<g, 256, 0, st>>>(pl, long_tmp);
+  if ((rc = device_scan(pl.long_tmp, pl.T, U, pl.scan_bsum, &pl.counters[C_LONG], st))) return rc;
+  k_items<<<g, 256, 0, st>>>(pl);
   if (inv) k_inv<<<g, 256, 0, st>>>(pl, inv);
   HP_LAUNCHED(inv ? 2 : 1, "dedup items");
   return HP_OK;

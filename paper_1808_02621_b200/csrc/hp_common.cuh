@@ -8,10 +8,12 @@
 
 #include "../../include/hybridpath.h"
 
-#define HP_CHUNK 128          // rows per sequential group of the summation tree (oracle CHUNK)
-#define HP_SMALL_THREADS 1024 // single-CTA sort path
-#define HP_SMALL_IPT 16
-#define HP_SMALL_MAX (HP_SMALL_THREADS * HP_SMALL_IPT)  // 16384 items
+#define HP_CHUNK 32           // rows per sequential group of the summation tree (oracle CHUNK)
+#define HP_CL_CTAS 8          // cluster sort path: CTAs per cluster (portable maximum)
+#define HP_CL_THREADS 1024
+#define HP_CL_IPT 2
+#define HP_CL_SLICE (HP_CL_THREADS * HP_CL_IPT)           // items per CTA
+#define HP_SMALL_MAX (HP_CL_CTAS * HP_CL_SLICE)           // 16384 items
 #define HP_RADIX_BITS 8
 #define HP_RADIX 256
 #define HP_TILE_THREADS 512   // multi-CTA sort tile

@@ -23,10 +23,12 @@ struct DedupPlan {
   int32_t* seg_start;   // [T+1]
   int32_t* segidx;      // [T] segment of each sorted item
   int32_t* sigma;       // [T] send slot of segment u
-  int32_t* item_off;    // [T+1] first reduce item of segment u
-  int32_t* item_seg;    // [T] segment of reduce item
-  int32_t* part_off;    // [T] partial-buffer slot of segment u (long segments)
-  int32_t* long_list;   // [T] long segments (L > HP_CHUNK)
+  int32_t* item_off;    // [T+1] first reduce item of segment u (large-path scratch)
+  int4* items;          // [T] reduce items {j0, n, dst, final}: rows sorted[j0, j0+n)
+  int32_t* part_off;    // [T] partial-buffer slot of segment u (large-path scratch)
+  int4* longs;          // [T/C+1] long segments {partial slot, n0, dst, u}
+  int32_t* dst;         // [T] destination row of segment u (send slot or slab row)
+  int32_t* long_tmp;    // [T] large-path scratch
   int32_t* first_u;     // [P+1] first unique index of partition p
   int32_t* part_base;   // [P] send-slot base of partition p
   int32_t* zero_owner;  // [P] zeros (owner table when all partitions are local)
@@ -43,9 +45,11 @@ int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, i
                int32_t P, int32_t nranks);
 
 // Build the plan on `stream`. owner == nullptr means every partition is on rank 0.
+// dst_part_base (nullable): when given, a segment's destination row is its row in
+// that slab (apply plans); otherwise it is the segment's send slot (send plans).
 // Optional outputs (nullable): send_ids, counts, inv, dest_counts, n_uniq.
-int build_plan(DedupPlan& pl, const int64_t* ids, const int32_t* owner, int64_t* send_ids,
-               int32_t* counts, int32_t* inv, int32_t* dest_counts, int32_t* n_uniq,
-               cudaStream_t stream);
+int build_plan(DedupPlan& pl, const int64_t* ids, const int32_t* owner,
+               const int64_t* dst_part_base, int64_t* send_ids, int32_t* counts, int32_t* inv,
+               int32_t* dest_counts, int32_t* n_uniq, cudaStream_t stream);
 
 }  // namespace hp

@@ -17,12 +17,15 @@
 namespace hp {
 namespace {
 
+// Epilogue interface: Pre load(dst, c4) is issued BEFORE the row loads (it
+// only depends on the item), store(dst, c4, g, pre) consumes the summed float4.
 struct EpiSend {
   float4* rows;
-  const int32_t* sigma;
   int D4;
-  __device__ __forceinline__ void operator()(int u, int c4, float4 g) const {
-    rows[(int64_t)sigma[u] * D4 + c4] = g;
+  struct Pre {};
+  __device__ __forceinline__ Pre load(int, int) const { return {}; }
+  __device__ __forceinline__ void store(int dst, int c4, float4 g, Pre) const {
+    rows[(int64_t)dst * D4 + c4] = g;
   }
 };
 
@@ -31,14 +34,23 @@ struct EpiApply {
   float4* w;
   float4* s0;
   float4* s1;
-  const int64_t* part_base;
-  const uint32_t* uniq_key;
-  Router route;
   hp_optim o;
   int D4;
-  int* err;
+  struct Pre {
+    float4 w, a, b;
+  };
 
-  __device__ __forceinline__ float upd(float& wv, float& a, float& b, float g) const {
+  __device__ __forceinline__ Pre load(int dst, int c4) const {
+    Pre p;
+    const int64_t off = (int64_t)dst * D4 + c4;
+    p.w = w[off];
+    p.a = p.b = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (OPT != HP_OPT_SGD) p.a = s0[off];
+    if (OPT == HP_OPT_ADAM) p.b = s1[off];
+    return p;
+  }
+
+  __device__ __forceinline__ void upd(float& wv, float& a, float& b, float g) const {
     g = __fmul_rn(g, o.agg_scale);
     if (OPT == HP_OPT_SGD) {
       wv = __fsub_rn(wv, __fmul_rn(o.lr, g));
@@ -50,109 +62,91 @@ struct EpiApply {
       b = __fadd_rn(__fmul_rn(o.beta2, b), __fmul_rn(o.one_minus_beta2, __fmul_rn(g, g)));
       wv = __fsub_rn(wv, __fdiv_rn(__fmul_rn(o.lr_t, a), __fadd_rn(__fsqrt_rn(b), o.eps)));
     }
-    return wv;
   }
 
-  __device__ __forceinline__ void operator()(int u, int c4, float4 g) const {
-    const int64_t id = uniq_key[u];
-    const int p = route.part(id);
-    const int64_t base = part_base[p];
-    if (base < 0) {  // row not homed on this rank: routing bug or bad ids
-      atomicOr(err, 2);
-      return;
-    }
-    const int64_t off = (base + (id - route.lo(p))) * D4 + c4;
-    float4 wv = w[off];
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-    if (OPT != HP_OPT_SGD) a = s0[off];
-    if (OPT == HP_OPT_ADAM) b = s1[off];
-    upd(wv.x, a.x, b.x, g.x);
-    upd(wv.y, a.y, b.y, g.y);
-    upd(wv.z, a.z, b.z, g.z);
-    upd(wv.w, a.w, b.w, g.w);
-    w[off] = wv;
-    if (OPT != HP_OPT_SGD) s0[off] = a;
-    if (OPT == HP_OPT_ADAM) s1[off] = b;
+  __device__ __forceinline__ void store(int dst, int c4, float4 g, Pre p) const {
+    upd(p.w.x, p.a.x, p.b.x, g.x);
+    upd(p.w.y, p.a.y, p.b.y, g.y);
+    upd(p.w.z, p.a.z, p.b.z, g.z);
+    upd(p.w.w, p.a.w, p.b.w, g.w);
+    const int64_t off = (int64_t)dst * D4 + c4;
+    w[off] = p.w;
+    if (OPT != HP_OPT_SGD) s0[off] = p.a;
+    if (OPT == HP_OPT_ADAM) s1[off] = p.b;
   }
 };
 
-// Level 0: one warp per (segment, chunk) item.
-template <int VPL, class Epi>
-__global__ void __launch_bounds__(256)
+// Level 0 of the summation tree. A group of TPI threads (one float4 column
+// each) owns an item {j0, n <= HP_CHUNK, dst, final}: its row positions are
+// loaded once per warp and broadcast by shuffle, then all n row loads are in
+// flight together (batches of B) before the in-order fp32 adds. Final items run
+// the epilogue (whose table-row loads were issued with the item); long-segment
+// chunks write a partial row for k_combine.
+template <int TPI, int B, class Epi>
+__global__ void __launch_bounds__(TPI > 256 ? TPI : 256)
 k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
-  constexpr int UNR = VPL >= 8 ? 1 : 8 / VPL;
   const float4* __restrict__ vals = reinterpret_cast<const float4*>(vals_f);
   float4* partials = reinterpret_cast<float4*>(pl.partials);
   const int D4 = pl.D >> 2;
+  const int gpb = blockDim.x / TPI;
+  const int c4 = threadIdx.x % TPI;
   const int lane = threadIdx.x & 31;
+  const bool col = c4 < D4;
   const int n_items = pl.counters[C_ITEMS];
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < n_items; it += nw) {
-    const int u = pl.item_seg[it];
-    const int k = it - pl.item_off[u];
-    const int s0 = pl.seg_start[u], s1 = pl.seg_start[u + 1];
-    const int j0 = s0 + k * HP_CHUNK, j1 = min(j0 + HP_CHUNK, s1);
-    float4 acc[VPL];
+  for (int it = blockIdx.x * gpb + threadIdx.x / TPI; it < n_items; it += gridDim.x * gpb) {
+    const int4 item = pl.items[it];
+    const int j0 = item.x, n = item.y, dst = item.z;
+    const bool fin = item.w != 0;
+    typename Epi::Pre pre{};
+    if (fin && col && dst >= 0) pre = epi.load(dst, c4);
+    const int myp = lane < n ? pl.sorted_pos[j0 + lane] : 0;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int jb = 0; jb < n; jb += B) {
+      float4 x[B];
 #pragma unroll
-    for (int v = 0; v < VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int jb = j0; jb < j1; jb += 32) {
-      const int nb = min(32, j1 - jb);
-      const int myp = lane < nb ? pl.sorted_pos[jb + lane] : 0;
-      int q = 0;
-      for (; q + UNR <= nb; q += UNR) {
-        float4 x[UNR][VPL];
-#pragma unroll
-        for (int e = 0; e < UNR; ++e) {
-          const int64_t rb = (int64_t)__shfl_sync(0xffffffffu, myp, q + e) * D4;
-#pragma unroll
-          for (int v = 0; v < VPL; ++v) {
-            const int c4 = lane + 32 * v;
-            if (c4 < D4) x[e][v] = ldg_stream(vals + rb + c4);
-          }
-        }
-#pragma unroll
-        for (int e = 0; e < UNR; ++e)
-#pragma unroll
-          for (int v = 0; v < VPL; ++v) acc[v] = f4_add(acc[v], x[e][v]);
+      for (int e = 0; e < B; ++e) {
+        const int p = __shfl_sync(0xffffffffu, myp, jb + e);
+        if (jb + e < n && col) x[e] = ldg_stream(vals + (int64_t)p * D4 + c4);
       }
-      for (; q < nb; ++q) {
-        const int64_t rb = (int64_t)__shfl_sync(0xffffffffu, myp, q) * D4;
 #pragma unroll
-        for (int v = 0; v < VPL; ++v) {
-          const int c4 = lane + 32 * v;
-          if (c4 < D4) acc[v] = f4_add(acc[v], ldg_stream(vals + rb + c4));
-        }
-      }
+      for (int e = 0; e < B; ++e)
+        if (jb + e < n) acc = f4_add(acc, x[e]);
     }
-    if (s1 - s0 <= HP_CHUNK) {
-#pragma unroll
-      for (int v = 0; v < VPL; ++v) {
-        const int c4 = lane + 32 * v;
-        if (c4 < D4) epi(u, c4, acc[v]);
-      }
+    if (!col) continue;
+    if (fin) {
+      if (dst >= 0) epi.store(dst, c4, acc, pre);
     } else {
-      float4* dst = partials + (int64_t)(pl.part_off[u] + k) * D4;
-#pragma unroll
-      for (int v = 0; v < VPL; ++v) {
-        const int c4 = lane + 32 * v;
-        if (c4 < D4) dst[c4] = acc[v];
-      }
+      partials[(int64_t)dst * D4 + c4] = acc;
     }
   }
 }
 
-// Upper levels for segments longer than HP_CHUNK: one CTA per segment,
-// in-place over the segment's partial rows.
+// ((0 + r0) + r1) + ... over n <= HP_CHUNK rows of stride D4, 8 loads in flight.
+__device__ __forceinline__ float4 seq_sum_rows(const float4* src, int n, int D4) {
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int j0 = 0; j0 < n; j0 += 8) {
+    float4 x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j0 + j < n) x[j] = src[(int64_t)(j0 + j) * D4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j0 + j < n) acc = f4_add(acc, x[j]);
+  }
+  return acc;
+}
+
+// Upper levels for segments longer than HP_CHUNK: one CTA per long segment
+// {partial slot, n0, dst, u}, in place over its partial rows.
 template <class Epi>
 __global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
   const int D4 = pl.D >> 2;
   const int n_long = pl.counters[C_LONG];
   float4* partials = reinterpret_cast<float4*>(pl.partials);
   for (int li = blockIdx.x; li < n_long; li += gridDim.x) {
-    const int u = pl.long_list[li];
-    const int L = pl.seg_start[u + 1] - pl.seg_start[u];
-    int n = (L + HP_CHUNK - 1) / HP_CHUNK;
-    float4* Pp = partials + (int64_t)pl.part_off[u] * D4;
+    const int4 d = pl.longs[li];
+    int n = d.y;
+    float4* Pp = partials + (int64_t)d.x * D4;
     while (n > HP_CHUNK) {
       const int ng = (n + HP_CHUNK - 1) / HP_CHUNK;
       const int units = ng * D4;
@@ -164,8 +158,7 @@ __global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
           g = unit / D4;
           c4 = unit - g * D4;
           const int e = min(HP_CHUNK, n - g * HP_CHUNK);
-          const float4* src = Pp + (int64_t)g * HP_CHUNK * D4 + c4;
-          for (int j = 0; j < e; ++j) acc = f4_add(acc, src[(int64_t)j * D4]);
+          acc = seq_sum_rows(Pp + (int64_t)g * HP_CHUNK * D4 + c4, e, D4);
         }
         __syncthreads();
         if (unit < units) Pp[(int64_t)g * D4 + c4] = acc;
@@ -174,32 +167,35 @@ __global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
       n = ng;
     }
     for (int c4 = threadIdx.x; c4 < D4; c4 += blockDim.x) {
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int j = 0; j < n; ++j) acc = f4_add(acc, Pp[(int64_t)j * D4 + c4]);
-      epi(u, c4, acc);
+      typename Epi::Pre pre{};
+      if (d.z >= 0) pre = epi.load(d.z, c4);
+      const float4 acc = seq_sum_rows(Pp + c4, n, D4);
+      if (d.z >= 0) epi.store(d.z, c4, acc, pre);
     }
     __syncthreads();
   }
+}
+
+template <int TPI, class Epi>
+void launch_k_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaStream_t st) {
+  constexpr int BT = TPI > 256 ? TPI : 256;
+  constexpr int B = 16;
+  const int gpb = BT / TPI;
+  const int blocks = grid_for(pl.T, gpb, sm_count() * 16);  // <= one group per item
+  k_reduce<TPI, B, Epi><<<blocks, BT, 0, st>>>(pl, vals, epi);
 }
 
 template <class Epi>
 int launch_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaStream_t st) {
   if (pl.T == 0) return HP_OK;
   const int D4 = pl.D >> 2;
-  const int sms = sm_count();
-  const int blocks = grid_for(pl.T, 8, sms * 8);  // <= one warp per item
-  if (D4 <= 32)
-    k_reduce<1, Epi><<<blocks, 256, 0, st>>>(pl, vals, epi);
-  else if (D4 <= 64)
-    k_reduce<2, Epi><<<blocks, 256, 0, st>>>(pl, vals, epi);
-  else if (D4 <= 128)
-    k_reduce<4, Epi><<<blocks, 256, 0, st>>>(pl, vals, epi);
-  else if (D4 <= 256)
-    k_reduce<8, Epi><<<blocks, 256, 0, st>>>(pl, vals, epi);
-  else
-    k_reduce<16, Epi><<<blocks, 256, 0, st>>>(pl, vals, epi);
+  if (D4 <= 32) launch_k_reduce<32>(pl, vals, epi, st);
+  else if (D4 <= 64) launch_k_reduce<64>(pl, vals, epi, st);
+  else if (D4 <= 128) launch_k_reduce<128>(pl, vals, epi, st);
+  else if (D4 <= 256) launch_k_reduce<256>(pl, vals, epi, st);
+  else launch_k_reduce<512>(pl, vals, epi, st);
   HP_LAUNCHED(1, "k_reduce");
-  const int cblocks = grid_for(pl.T / HP_CHUNK + 1, 1, sms * 2);
+  const int cblocks = grid_for(pl.T / HP_CHUNK + 1, 1, sm_count() * 2);
   k_combine<Epi><<<cblocks, 256, 0, st>>>(pl, epi);
   HP_LAUNCHED(1, "k_combine");
   return HP_OK;
@@ -215,19 +211,18 @@ int check_slab(const hp_slab& s, int opt) {
 }
 
 template <int OPT>
-EpiApply<OPT> make_apply(const DedupPlan& pl, const hp_slab& s, const hp_optim& o) {
+EpiApply<OPT> make_apply(const hp_slab& s, const hp_optim& o) {
   EpiApply<OPT> e{reinterpret_cast<float4*>(s.w), reinterpret_cast<float4*>(s.s0),
-                  reinterpret_cast<float4*>(s.s1), s.part_base, pl.uniq_key,
-                  Router(s.V, s.P), o, s.D >> 2, &pl.counters[C_ERR]};
+                  reinterpret_cast<float4*>(s.s1), o, s.D >> 2};
   return e;
 }
 
 int apply_plan(const DedupPlan& pl, const float* vals, const hp_slab& s, const hp_optim& o,
                cudaStream_t st) {
   switch (o.kind) {
-    case HP_OPT_SGD: return launch_reduce(pl, vals, make_apply<HP_OPT_SGD>(pl, s, o), st);
-    case HP_OPT_ADAGRAD: return launch_reduce(pl, vals, make_apply<HP_OPT_ADAGRAD>(pl, s, o), st);
-    default: return launch_reduce(pl, vals, make_apply<HP_OPT_ADAM>(pl, s, o), st);
+    case HP_OPT_SGD: return launch_reduce(pl, vals, make_apply<HP_OPT_SGD>(s, o), st);
+    case HP_OPT_ADAGRAD: return launch_reduce(pl, vals, make_apply<HP_OPT_ADAGRAD>(s, o), st);
+    default: return launch_reduce(pl, vals, make_apply<HP_OPT_ADAM>(s, o), st);
   }
 }
 
@@ -252,7 +247,7 @@ int hp_dedup_plan(const int64_t* ids, int64_t T, int32_t D, int64_t V, int32_t P
   if (rc) return rc;
   HP_REQUIRE(T == 0 || ids != nullptr, "ids is NULL");
   HP_REQUIRE(owner != nullptr || nranks == 1, "owner table required when nranks > 1");
-  return build_plan(pl, ids, owner, send_ids, counts, inv, dest_counts, n_uniq,
+  return build_plan(pl, ids, owner, nullptr, send_ids, counts, inv, dest_counts, n_uniq,
                     static_cast<cudaStream_t>(stream));
 }
 
@@ -268,9 +263,9 @@ int hp_sort_dedup_route(const int64_t* ids, const float* vals, int64_t T, int32_
   HP_REQUIRE(T == 0 || ids != nullptr, "ids is NULL");
   HP_REQUIRE(owner != nullptr || nranks == 1, "owner table required when nranks > 1");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  rc = build_plan(pl, ids, owner, send_ids, counts, inv, dest_counts, n_uniq, st);
+  rc = build_plan(pl, ids, owner, nullptr, send_ids, counts, inv, dest_counts, n_uniq, st);
   if (rc) return rc;
-  EpiSend epi{reinterpret_cast<float4*>(send_rows), pl.sigma, D >> 2};
+  EpiSend epi{reinterpret_cast<float4*>(send_rows), D >> 2};
   return launch_reduce(pl, vals, epi, st);
 }
 
@@ -281,9 +276,21 @@ int hp_merge_apply(const int64_t* ids, const float* rows, int64_t R, hp_slab sla
   DedupPlan pl;
   if ((rc = carve_plan(&pl, ws, ws_bytes, R, slab.D, slab.V, slab.P, 1))) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if ((rc = build_plan(pl, ids, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, st)))
+  if ((rc = build_plan(pl, ids, nullptr, slab.part_base, nullptr, nullptr, nullptr, nullptr,
+                       nullptr, st)))
     return rc;
   return apply_plan(pl, rows, slab, opt, st);
+}
+
+int hp_apply_plan_build(const int64_t* ids, int64_t R, hp_slab slab, void* ws, size_t ws_bytes,
+                        void* stream) {
+  HP_REQUIRE(slab.part_base != nullptr, "slab.part_base is NULL");
+  HP_REQUIRE(R == 0 || ids != nullptr, "ids is NULL");
+  DedupPlan pl;
+  int rc = carve_plan(&pl, ws, ws_bytes, R, slab.D, slab.V, slab.P, 1);
+  if (rc) return rc;
+  return build_plan(pl, ids, nullptr, slab.part_base, nullptr, nullptr, nullptr, nullptr,
+                    nullptr, static_cast<cudaStream_t>(stream));
 }
 
 int hp_local_apply(const int64_t* ids, const float* vals, int64_t T, hp_slab slab, hp_optim opt,

@@ -165,9 +165,18 @@ def local_apply(ids: torch.Tensor, vals: torch.Tensor, slab: Slab, opt: Optim, w
     call("hp_local_apply", _p(ids), _p(vals), T, slab, opt, ws.ptr, ws.nbytes, _stream(stream))
 
 
+def apply_plan_build(ids: torch.Tensor, slab: Slab, ws: Workspace, n: int | None = None,
+                     stream=None) -> None:
+    """Index half of K4: dedup ids into a plan whose destinations are slab rows."""
+    _need(ids, torch.int64, "ids", 1)
+    n = ids.numel() if n is None else n
+    ws.get(dedup_ws_bytes(n, slab.D, slab.P))
+    call("hp_apply_plan_build", _p(ids), n, slab, ws.ptr, ws.nbytes, _stream(stream))
+
+
 def apply_plan(rows: torch.Tensor, n: int, slab: Slab, opt: Optim, ws: Workspace,
                stream=None) -> None:
-    """K4 only: reduce + apply with the plan a preceding dedup_plan left in ``ws``."""
+    """K4 only: reduce + apply with the plan apply_plan_build left in ``ws``."""
     _need(rows, torch.float32, "rows", 2)
     call("hp_apply_plan", _p(rows), n, slab, opt, ws.ptr, ws.nbytes, _stream(stream))
 

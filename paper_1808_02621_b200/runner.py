@@ -177,7 +177,7 @@ class HybridRunner:
     def _sparse_local(self, tab: ShardedTable, ids, vals, opt) -> torch.Tensor:
         T = ids.numel()
         slab = tab.slab()
-        ops.dedup_plan(ids, tab.V, tab.P, None, 1, tab.D, tab.ws, outputs=False)
+        ops.apply_plan_build(ids, slab, tab.ws)
         self._kev(f"k4:{tab.name}", True)
         ops.apply_plan(vals, T, slab, opt, tab.ws)
         self._kev(f"k4:{tab.name}", False)
