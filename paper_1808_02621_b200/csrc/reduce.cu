@@ -76,47 +76,61 @@ struct EpiApply {
   }
 };
 
-// Level 0 of the summation tree. A group of TPI threads (one float4 column
-// each) owns an item {j0, n <= HP_CHUNK, dst, final}: its row positions are
-// loaded once per warp and broadcast by shuffle, then all n row loads are in
-// flight together (batches of B) before the in-order fp32 adds. Final items run
-// the epilogue (whose table-row loads were issued with the item); long-segment
-// chunks write a partial row for k_combine.
-template <int TPI, int B, class Epi>
-__global__ void __launch_bounds__(TPI > 256 ? TPI : 256)
+// Level 0 of the summation tree. A group of TPI threads owns an item
+// {j0, n <= HP_CHUNK, dst, final}; each thread owns VPT float4 columns
+// (c4 = lane-in-group + k*TPI). Row positions are loaded once per warp and
+// broadcast by shuffle; B rows x VPT columns are in flight per thread before
+// the in-order fp32 adds. Final items run the epilogue (its table-row loads
+// are issued together with the positions); long-segment chunks write a
+// partial row for k_combine. Small groups + <= 64 registers keep many items
+// in flight per SM: the kernel is latency-bound on the item chain
+// (descriptor -> positions/table rows -> gradient rows).
+template <int TPI, int VPT, int B, class Epi>
+__global__ void __launch_bounds__(256, 3)
 k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
   const float4* __restrict__ vals = reinterpret_cast<const float4*>(vals_f);
   float4* partials = reinterpret_cast<float4*>(pl.partials);
   const int D4 = pl.D >> 2;
-  const int gpb = blockDim.x / TPI;
-  const int c4 = threadIdx.x % TPI;
+  constexpr int GPB = 256 / TPI;
+  const int q = threadIdx.x % TPI;
   const int lane = threadIdx.x & 31;
-  const bool col = c4 < D4;
   const int n_items = pl.counters[C_ITEMS];
-  for (int it = blockIdx.x * gpb + threadIdx.x / TPI; it < n_items; it += gridDim.x * gpb) {
+  for (int it = blockIdx.x * GPB + threadIdx.x / TPI; it < n_items; it += gridDim.x * GPB) {
     const int4 item = pl.items[it];
     const int j0 = item.x, n = item.y, dst = item.z;
     const bool fin = item.w != 0;
-    typename Epi::Pre pre{};
-    if (fin && col && dst >= 0) pre = epi.load(dst, c4);
+    typename Epi::Pre pre[VPT];
+#pragma unroll
+    for (int v = 0; v < VPT; ++v)
+      if (fin && dst >= 0 && q + v * TPI < D4) pre[v] = epi.load(dst, q + v * TPI);
     const int myp = lane < n ? pl.sorted_pos[j0 + lane] : 0;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 acc[VPT];
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int jb = 0; jb < n; jb += B) {
-      float4 x[B];
+      float4 x[B][VPT];
 #pragma unroll
       for (int e = 0; e < B; ++e) {
-        const int p = __shfl_sync(0xffffffffu, myp, jb + e);
-        if (jb + e < n && col) x[e] = ldg_stream(vals + (int64_t)p * D4 + c4);
+        const int64_t rb = (int64_t)__shfl_sync(0xffffffffu, myp, jb + e) * D4;
+#pragma unroll
+        for (int v = 0; v < VPT; ++v)
+          if (jb + e < n && q + v * TPI < D4) x[e][v] = ldg_stream(vals + rb + q + v * TPI);
       }
 #pragma unroll
       for (int e = 0; e < B; ++e)
-        if (jb + e < n) acc = f4_add(acc, x[e]);
+#pragma unroll
+        for (int v = 0; v < VPT; ++v)
+          if (jb + e < n) acc[v] = f4_add(acc[v], x[e][v]);
     }
-    if (!col) continue;
-    if (fin) {
-      if (dst >= 0) epi.store(dst, c4, acc, pre);
-    } else {
-      partials[(int64_t)dst * D4 + c4] = acc;
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) {
+      const int c4 = q + v * TPI;
+      if (c4 >= D4) continue;
+      if (fin) {
+        if (dst >= 0) epi.store(dst, c4, acc[v], pre[v]);
+      } else {
+        partials[(int64_t)dst * D4 + c4] = acc[v];
+      }
     }
   }
 }
@@ -176,24 +190,22 @@ __global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
   }
 }
 
-template <int TPI, class Epi>
+template <int TPI, int VPT, class Epi>
 void launch_k_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaStream_t st) {
-  constexpr int BT = TPI > 256 ? TPI : 256;
-  constexpr int B = 16;
-  const int gpb = BT / TPI;
-  const int blocks = grid_for(pl.T, gpb, sm_count() * 16);  // <= one group per item
-  k_reduce<TPI, B, Epi><<<blocks, BT, 0, st>>>(pl, vals, epi);
+  constexpr int B = VPT >= 8 ? 1 : 8 / VPT;
+  const int blocks = grid_for(pl.T, 256 / TPI, sm_count() * 16);  // <= one group per item
+  k_reduce<TPI, VPT, B, Epi><<<blocks, 256, 0, st>>>(pl, vals, epi);
 }
 
 template <class Epi>
 int launch_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaStream_t st) {
   if (pl.T == 0) return HP_OK;
   const int D4 = pl.D >> 2;
-  if (D4 <= 32) launch_k_reduce<32>(pl, vals, epi, st);
-  else if (D4 <= 64) launch_k_reduce<64>(pl, vals, epi, st);
-  else if (D4 <= 128) launch_k_reduce<128>(pl, vals, epi, st);
-  else if (D4 <= 256) launch_k_reduce<256>(pl, vals, epi, st);
-  else launch_k_reduce<512>(pl, vals, epi, st);
+  if (D4 <= 32) launch_k_reduce<32, 1>(pl, vals, epi, st);
+  else if (D4 <= 64) launch_k_reduce<32, 2>(pl, vals, epi, st);
+  else if (D4 <= 128) launch_k_reduce<64, 2>(pl, vals, epi, st);
+  else if (D4 <= 256) launch_k_reduce<64, 4>(pl, vals, epi, st);
+  else launch_k_reduce<128, 4>(pl, vals, epi, st);
   HP_LAUNCHED(1, "k_reduce");
   const int cblocks = grid_for(pl.T / HP_CHUNK + 1, 1, sm_count() * 2);
   k_combine<Epi><<<cblocks, 256, 0, st>>>(pl, epi);
