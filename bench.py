@@ -274,11 +274,16 @@ def main():
     # ---- per-kernel timing (eager steps, events around K4 / K5 launches)
     kern = {}
     if world == 1:
+        # Eager steps, tables one after another, each step queued behind a GPU
+        # sleep so the CPU enqueue cost never shows up between an event pair.
         runner.kernel_events = {}
+        runner.concurrent_tables = False
         kt = min(args.steps, 20)
         for i in range(kt):
+            torch.cuda._sleep(20_000_000)
             runner.step(batches[i % R], timed=False)
         torch.cuda.synchronize()
+        runner.concurrent_tables = True
         for key, evs in runner.kernel_events.items():
             d = [a.elapsed_time(b) * 1e3 for a, b in zip(evs[0::2], evs[1::2])]
             kern[key] = float(np.mean(d))

@@ -160,8 +160,19 @@ __device__ __forceinline__ void emit_items(const DedupPlan& pl, int u, int j0, i
 // distributed shared memory. CTA c owns sorted slice [c*S, (c+1)*S); each LSD
 // pass ranks the slice locally (warp multisplit), publishes its digit counts,
 // and after a cluster barrier scatters every (key, pos) straight into the
-// owning CTA's shared memory (DSMEM stores). The index metadata is derived in
-// the same launch with cluster-wide prefix sums.
+// owning CTA's shared memory (DSMEM stores).
+// Metadata needs ONE more barrier: each CTA analyses the segments whose head
+// lies in its slice (lengths, reduce items, per-partition unique counts) from
+// shared memory, publishes a few scalars and its partition histogram, and after
+// the barrier derives every global offset it needs (segment / item / partial
+// prefixes, partition bases) from the other CTAs' published state.
+constexpr int CL_PMAX = 2048;  // partitions handled by the cluster path
+
+// Published per-CTA scalars (s_pub).
+enum { PB_HEADS = 0, PB_FIRST, PB_LAST, PB_ITEMS, PB_PARTS, PB_LONGS, PB_N };
+
+__device__ __forceinline__ int pack3(int a, int b, int c) { return a | (b << 12) | (c << 22); }
+
 template <int NT, int IPT, int CS>
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(NT, 1)
 k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __restrict__ owner,
@@ -170,18 +181,24 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   constexpr int S = NT * IPT, NW = NT / 32;
+  static_assert(S < 4096, "packed scan fields are 12/10/10 bits");
   extern __shared__ __align__(16) unsigned char smem[];
   uint2* s_buf = reinterpret_cast<uint2*>(smem);  // sorted slice (key, pos)
   int* s_hist = reinterpret_cast<int*>(s_buf + S);
+  int* s_hpos = s_hist;          // after the sort: local head positions [S]
+  int* s_sig = s_hist + S;       //                 send slot of local segment [S]
   int* s_scan = s_hist + NW * HS;
-  int* s_cnt = s_scan + 40;       // published digit counts
+  int* s_cnt = s_scan + 40;      // published digit counts
   int* s_base = s_cnt + HP_RADIX;
-  int* s_pub = s_base + HP_RADIX; // published scalars
-  int* s_dest = s_pub + 8;
+  int* s_pub = s_base + HP_RADIX;  // published scalars
+  int* s_dest = s_pub + 16;
+  int* s_pcnt = s_dest + MAX_RANKS;  // published unique counts per partition
+  int* s_first = s_pcnt + CL_PMAX;   // first unique index of partition p (P+1)
+  int* s_pbase = s_first + CL_PMAX + 1;
   const int c = (int)cl.block_rank();
-  const int T = (int)pl.T;
+  const int T = (int)pl.T, P = pl.P;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const Router route(pl.V, pl.P);
+  const Router route(pl.V, P);
 
   uint32_t key[IPT];
   int32_t pos[IPT];
@@ -191,6 +208,7 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
     key[r] = i < T ? load_key(ids, i, pl.V, &pl.counters[C_ERR]) : 0xffffffffu;
     pos[r] = i;
   }
+  for (int p = tid; p < P; p += NT) s_pcnt[p] = 0;
   const int passes = (pl.key_bits + HP_RADIX_BITS - 1) / HP_RADIX_BITS;
   for (int ps = 0; ps < passes; ++ps) {
     const int shift = ps * HP_RADIX_BITS;
@@ -227,119 +245,143 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
       }
     }
   }
-  // ---- segment heads (blocked: thread t owns slice items [t*IPT, t*IPT+IPT))
+  // ---- local segment analysis (thread t owns slice items [t*IPT, t*IPT+IPT))
+  const int nvalid = min(S, max(0, T - c * S));
   const uint32_t prev_last = c > 0 ? cl.map_shared_rank(s_buf, c - 1)[S - 1].x : 0u;
+  bool h[IPT];
   int heads = 0;
 #pragma unroll
   for (int k = 0; k < IPT; ++k) {
-    const int li = tid * IPT + k, gi = c * S + li;
+    const int li = tid * IPT + k;
     const uint32_t prev = li > 0 ? s_buf[li - 1].x : prev_last;
-    heads += gi < T && (gi == 0 || s_buf[li].x != prev);
+    h[k] = li < nvalid && ((c == 0 && li == 0) || s_buf[li].x != prev);
+    heads += h[k];
+    if (li < nvalid) pl.sorted_pos[c * S + li] = (int32_t)s_buf[li].y;
   }
   int cta_heads;
-  const int lbase = block_excl_scan<NT>(heads, s_scan, &cta_heads);
-  if (tid == 0) s_pub[0] = cta_heads;
-  cl.sync();
-  int seg_base = 0, U = 0;
-#pragma unroll
-  for (int cc = 0; cc < CS; ++cc) {
-    const int v = cl.map_shared_rank(s_pub, cc)[0];
-    U += v;
-    seg_base += cc < c ? v : 0;
-  }
-  int myseg[IPT];
+  const int hb = block_excl_scan<NT>(heads, s_scan, &cta_heads);
   {
     int cnt = 0;
 #pragma unroll
-    for (int k = 0; k < IPT; ++k) {
-      const int li = tid * IPT + k, gi = c * S + li;
-      const uint32_t prev = li > 0 ? s_buf[li - 1].x : prev_last;
-      const bool h = gi < T && (gi == 0 || s_buf[li].x != prev);
-      if (h) {
-        const int seg = seg_base + lbase + cnt;
-        pl.seg_start[seg] = gi;
-        pl.uniq_key[seg] = s_buf[li].x;
-        ++cnt;
+    for (int k = 0; k < IPT; ++k)
+      if (h[k]) {
+        const int li = tid * IPT + k;
+        s_hpos[hb + cnt++] = li;
+        atomicAdd(&s_pcnt[route.part(s_buf[li].x)], 1);
       }
-      myseg[k] = seg_base + lbase + cnt - 1;
-      if (gi < T) pl.sorted_pos[gi] = (int32_t)s_buf[li].y;
-    }
   }
-  if (c == CS - 1 && tid == 0) {
-    pl.seg_start[U] = T;
-    pl.counters[C_UNIQ] = U;
-    if (n_uniq) *n_uniq = U;
-  }
-  __threadfence();
-  cl.sync();
-  // ---- partition boundaries / send-slot bases (CTA 0, global)
-  if (c == 0) {
-    for (int p = tid; p <= pl.P; p += NT)
-      pl.first_u[p] = p == pl.P ? U : lower_bound_u32(pl.uniq_key, U, (uint32_t)route.lo(p));
-    __syncthreads();
-    partition_bases<NT>(pl.first_u, owner, pl.P, pl.nranks, pl.part_base, dest_counts, s_dest);
-    __threadfence();
-  }
-  cl.sync();
-  // ---- per-segment slots and reduce items (CTA c: segments [ua, ub), blocked per thread)
-  const int cu = (U + CS - 1) / CS;
-  const int ua = min(U, c * cu), ub = min(U, ua + cu);
-  const int ku = (ub - ua + NT - 1) / NT;
-  const int u0 = min(ub, ua + tid * ku), u1 = min(ub, u0 + ku);
+  __syncthreads();
+  // lengths of every local segment except the last one (its end lies in a later CTA)
   int ni = 0, np = 0, nl = 0;
-  for (int u = u0; u < u1; ++u) {
-    const int L = pl.seg_start[u + 1] - pl.seg_start[u];
+  for (int sidx = hb; sidx < hb + heads; ++sidx) {
+    if (sidx + 1 >= cta_heads) break;
+    const int L = s_hpos[sidx + 1] - s_hpos[sidx];
     const int n0 = (L + HP_CHUNK - 1) / HP_CHUNK;
     ni += n0;
     if (L > HP_CHUNK) { np += n0; ++nl; }
   }
-  int ti, tp, tl;
-  int bi = block_excl_scan<NT>(ni, s_scan, &ti);
-  int bp = block_excl_scan<NT>(np, s_scan, &tp);
-  int bl = block_excl_scan<NT>(nl, s_scan, &tl);
+  int packed_tot;
+  const int packed = block_excl_scan<NT>(pack3(ni, np, nl), s_scan, &packed_tot);
   if (tid == 0) {
-    s_pub[1] = ti;
-    s_pub[2] = tp;
-    s_pub[3] = tl;
+    s_pub[PB_HEADS] = cta_heads;
+    s_pub[PB_FIRST] = cta_heads ? c * S + s_hpos[0] : INT_MAX;
+    s_pub[PB_LAST] = cta_heads ? c * S + s_hpos[cta_heads - 1] : -1;
+    s_pub[PB_ITEMS] = packed_tot & 0xfff;
+    s_pub[PB_PARTS] = (packed_tot >> 12) & 0x3ff;
+    s_pub[PB_LONGS] = (packed_tot >> 22) & 0x3ff;
   }
-  cl.sync();
-  int all_i = 0, all_p = 0, all_l = 0;
+  cl.sync();  // ---- the one metadata barrier
+  // global prefixes from the published state of every CTA
+  int seg_base = 0, U = 0, bi = packed & 0xfff, bp = (packed >> 12) & 0x3ff, bl = packed >> 22;
+  int tot_i = 0, tot_p = 0, tot_l = 0, my_last_len = 0;
+  {
+    int pub[CS][PB_N];
 #pragma unroll
-  for (int cc = 0; cc < CS; ++cc) {
-    const int* q = cl.map_shared_rank(s_pub, cc);
-    const int a = q[1], b = q[2], d = q[3];
-    if (cc < c) { bi += a; bp += b; bl += d; }
-    all_i += a; all_p += b; all_l += d;
+    for (int cc = 0; cc < CS; ++cc) {
+      const int* q = cl.map_shared_rank(s_pub, cc);
+#pragma unroll
+      for (int f = 0; f < PB_N; ++f) pub[cc][f] = q[f];
+    }
+    int next_head = T;
+#pragma unroll
+    for (int cc = CS - 1; cc >= 0; --cc) {
+      int ci = pub[cc][PB_ITEMS], cp = pub[cc][PB_PARTS], cl_ = pub[cc][PB_LONGS];
+      if (pub[cc][PB_HEADS]) {
+        const int L = next_head - pub[cc][PB_LAST];
+        const int n0 = (L + HP_CHUNK - 1) / HP_CHUNK;
+        ci += n0;
+        if (L > HP_CHUNK) { cp += n0; ++cl_; }
+        if (cc == c) my_last_len = L;
+        next_head = pub[cc][PB_FIRST];
+      }
+      U += pub[cc][PB_HEADS];
+      tot_i += ci; tot_p += cp; tot_l += cl_;
+      if (cc < c) { seg_base += pub[cc][PB_HEADS]; bi += ci; bp += cp; bl += cl_; }
+    }
   }
-  for (int u = u0; u < u1; ++u) {
-    const int j0 = pl.seg_start[u];
-    const int L = pl.seg_start[u + 1] - j0;
-    const uint32_t id = pl.uniq_key[u];
+  // partition totals -> first unique index and owner-grouped send-slot bases
+  {
+    int carry = 0;
+    for (int p0 = 0; p0 <= P; p0 += NT) {
+      const int p = p0 + tid;
+      int v = 0;
+      if (p < P)
+#pragma unroll
+        for (int cc = 0; cc < CS; ++cc) v += cl.map_shared_rank(s_pcnt, cc)[p];
+      int t;
+      const int ex = block_excl_scan<NT>(v, s_scan, &t);
+      if (p <= P) s_first[p] = carry + ex;
+      carry += t;
+    }
+  }
+  __syncthreads();
+  partition_bases<NT>(s_first, owner, P, pl.nranks, s_pbase, c == 0 ? dest_counts : nullptr,
+                      s_dest);
+  // ---- per-segment outputs (thread t: segments whose head is in its items)
+  auto seg_out = [&](int sidx, int L, int& bi_, int& bp_, int& bl_) {
+    const int u = seg_base + sidx;
+    const int li = s_hpos[sidx];
+    const uint32_t id = s_buf[li].x;
     const int p = route.part(id);
-    const int slot = pl.part_base[p] + (u - pl.first_u[p]);
-    pl.sigma[u] = slot;
+    const int slot = s_pbase[p] + (u - s_first[p]);
+    s_sig[sidx] = slot;
     if (send_ids) send_ids[slot] = id;
     if (counts) counts[slot] = L;
     const int dst = seg_dst(id, p, slot, dst_pb, route, &pl.counters[C_ERR]);
-    emit_items(pl, u, j0, L, dst, bi, bp, bl);
+    emit_items(pl, u, c * S + li, L, dst, bi_, bp_, bl_);
     const int n0 = (L + HP_CHUNK - 1) / HP_CHUNK;
-    bi += n0;
-    if (L > HP_CHUNK) { bp += n0; ++bl; }
+    bi_ += n0;
+    if (L > HP_CHUNK) { bp_ += n0; ++bl_; }
+  };
+  for (int sidx = hb; sidx < hb + heads; ++sidx) {
+    const int L = sidx + 1 < cta_heads ? s_hpos[sidx + 1] - s_hpos[sidx] : my_last_len;
+    seg_out(sidx, L, bi, bp, bl);
   }
   if (c == CS - 1 && tid == 0) {
-    pl.counters[C_ITEMS] = all_i;
-    pl.counters[C_PARTIALS] = all_p;
-    pl.counters[C_LONG] = all_l;
+    pl.counters[C_UNIQ] = U;
+    pl.counters[C_ITEMS] = tot_i;
+    pl.counters[C_PARTIALS] = tot_p;
+    pl.counters[C_LONG] = tot_l;
+    if (n_uniq) *n_uniq = U;
   }
-  __threadfence();
-  cl.sync();  // sigma visible; no DSMEM access after this point
+  __syncthreads();
   if (inv) {
+    // items before the first local head belong to the previous CTA's last segment
+    int spill_slot = 0;
+    if (c > 0 && (cta_heads == 0 || s_hpos[0] > 0) && nvalid > 0) {
+      const uint32_t id = s_buf[0].x;
+      const int p = route.part(id);
+      spill_slot = s_pbase[p] + (seg_base - 1 - s_first[p]);
+    }
+    int hcount = hb;
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
-      const int li = tid * IPT + k, gi = c * S + li;
-      if (gi < T) inv[s_buf[li].y] = pl.sigma[myseg[k]];
+      const int li = tid * IPT + k;
+      hcount += h[k];
+      if (li < nvalid) inv[s_buf[li].y] = hcount > 0 ? s_sig[hcount - 1] : spill_slot;
     }
   }
+  cl.sync();  // no CTA may exit while others still read its shared memory
 }
 
 constexpr size_t tile_smem_bytes() {
@@ -348,7 +390,7 @@ constexpr size_t tile_smem_bytes() {
 
 constexpr size_t cluster_smem_bytes() {
   return (size_t)HP_CL_SLICE * 8 + (size_t)(HP_CL_THREADS / 32) * HS * 4 + 40 * 4 +
-         2 * HP_RADIX * 4 + 8 * 4 + MAX_RANKS * 4;
+         2 * HP_RADIX * 4 + 16 * 4 + MAX_RANKS * 4 + (3 * CL_PMAX + 1) * 4;
 }
 
 // ------------------------------------------------------------------ large path
@@ -659,6 +701,23 @@ int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, i
   return HP_OK;
 }
 
+template <int CS>
+int launch_cluster(const DedupPlan& pl, const int64_t* ids, const int32_t* owner,
+                   const int64_t* dst_pb, int64_t* send_ids, int32_t* counts, int32_t* inv,
+                   int32_t* dest_counts, int32_t* n_uniq, cudaStream_t st) {
+  constexpr size_t smem = cluster_smem_bytes();
+  auto kern = k_dedup_cluster<HP_CL_THREADS, HP_CL_IPT, CS>;
+  static bool configured = false;
+  if (!configured) {
+    HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  kern<<<CS, HP_CL_THREADS, smem, st>>>(pl, ids, owner, dst_pb, send_ids, counts, inv,
+                                        dest_counts, n_uniq);
+  HP_LAUNCHED(1, "k_dedup_cluster");
+  return HP_OK;
+}
+
 int build_plan(DedupPlan& pl, const int64_t* ids, const int32_t* owner,
                const int64_t* dst_pb, int64_t* send_ids, int32_t* counts, int32_t* inv,
                int32_t* dest_counts, int32_t* n_uniq, cudaStream_t st) {
@@ -668,19 +727,17 @@ int build_plan(DedupPlan& pl, const int64_t* ids, const int32_t* owner,
     if (n_uniq) HP_CUDA(cudaMemsetAsync(n_uniq, 0, 4, st));
     return HP_OK;
   }
-  if (pl.T <= HP_SMALL_MAX) {
-    constexpr size_t smem = cluster_smem_bytes();
-    auto kern = k_dedup_cluster<HP_CL_THREADS, HP_CL_IPT, HP_CL_CTAS>;
-    static bool configured = false;
-    if (!configured) {
-      HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      configured = true;
-    }
+  if (pl.T <= HP_SMALL_MAX && pl.P <= CL_PMAX) {
     pl.sorted_pos = pl.pos[0];
-    kern<<<HP_CL_CTAS, HP_CL_THREADS, smem, st>>>(pl, ids, owner, dst_pb, send_ids, counts, inv,
-                                                  dest_counts, n_uniq);
-    HP_LAUNCHED(1, "k_dedup_cluster");
-    return HP_OK;
+    // smallest cluster that holds T (fewer CTAs -> cheaper cluster barriers)
+    int rc;
+    if (pl.T <= 2 * HP_CL_SLICE)
+      rc = launch_cluster<2>(pl, ids, owner, dst_pb, send_ids, counts, inv, dest_counts, n_uniq, st);
+    else if (pl.T <= 4 * HP_CL_SLICE)
+      rc = launch_cluster<4>(pl, ids, owner, dst_pb, send_ids, counts, inv, dest_counts, n_uniq, st);
+    else
+      rc = launch_cluster<8>(pl, ids, owner, dst_pb, send_ids, counts, inv, dest_counts, n_uniq, st);
+    return rc;
   }
   // ---- large path: LSD radix sort, 8-bit digits
   static bool tile_configured = false;

@@ -155,6 +155,8 @@ class HybridRunner:
         self.step_count = 0
         self.last_counts: dict = {}
         self.kernel_events: dict | None = None
+        self._streams = {n: torch.cuda.Stream(device=self.device) for n in self.tables}
+        self.concurrent_tables = True
 
     # ------------------------------------------------------------------ step
     def _buf(self, name: str, key: str, shape, dtype) -> torch.Tensor:
@@ -246,15 +248,33 @@ class HybridRunner:
             self.dense_out[var.name] = ops.dense_allreduce_scale_cast(
                 self.comm.ptr if self.comm else None, g, out, self.scale)
             ev("network")
-        for name, tab in self.tables.items():
-            ids, vals = batch[name]
-            tab.step_count += 1
-            opt = self.optimizer.c_struct(tab.step_count, self.scale)
-            if self.world_size == 1:
-                self.outputs[name] = self._sparse_local(tab, ids, vals, opt)
+        if self.world_size == 1 and self.concurrent_tables:
+            # Tables are independent: each runs on its own stream (parallel
+            # branches when the step is captured as a CUDA graph).
+            joins = []
+            for name, tab in self.tables.items():
+                ids, vals = batch[name]
+                tab.step_count += 1
+                opt = self.optimizer.c_struct(tab.step_count, self.scale)
+                side = self._streams[name]
+                side.wait_stream(stream)
+                with torch.cuda.stream(side):
+                    self.outputs[name] = self._sparse_local(tab, ids, vals, opt)
+                joins.append(side)
+            for side in joins:
+                stream.wait_stream(side)
+            if self.tables:
                 ev("update")
-            else:
-                self.outputs[name] = self._sparse_exchange(tab, ids, vals, opt, ev)
+        else:
+            for name, tab in self.tables.items():
+                ids, vals = batch[name]
+                tab.step_count += 1
+                opt = self.optimizer.c_struct(tab.step_count, self.scale)
+                if self.world_size == 1:
+                    self.outputs[name] = self._sparse_local(tab, ids, vals, opt)
+                    ev("update")
+                else:
+                    self.outputs[name] = self._sparse_exchange(tab, ids, vals, opt, ev)
         if timed:
             stream.synchronize()
             for (_, a), (ph, b) in zip(marks, marks[1:]):

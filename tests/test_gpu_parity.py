@@ -46,6 +46,10 @@ K1_CASES = [
     (20000, 999, 36, 4, 2, "few"),            # large path, 3 hot segments
     (200_000, 10_000_000, 128, 128, 8, "zipf"),
     (300_000, 1 << 20, 8, 33, 7, "uniform"),
+    (3000, 100_000, 16, 4096, 8, "uniform"),   # P beyond the cluster path -> large path
+    (2560, 800_000, 512, 2048, 8, "zipf"),     # cluster path, maximum P
+    (4097, 65_536, 8, 3, 3, "zipf"),           # 3-CTA data in a 4-CTA cluster
+    (8193, 1 << 24, 4, 2, 2, "uniform"),       # 3 radix passes, 8-CTA cluster
 ]
 
 
