@@ -73,6 +73,11 @@ const char* hp_last_error(void);
 int hp_device_sm_count(void);
 /* Cumulative number of kernels this library has launched in the process. */
 int64_t hp_launch_count(void);
+/* Instrumentation: device buffer (>= 16 x 16 int64) that the dedup kernels fill
+ * with per-phase clock64 stamps; NULL (default) disables it. */
+void hp_debug_set_profile(long long* dev_buf);
+/* Tuning: CTA size (256 | 512 | 1024) of the cluster dedup path. */
+void hp_debug_set_cluster_threads(int nt);
 
 /* ---------------------------------------------------------------- K1 + K2
  * Sort + dedup + route of one worker's IndexedSlices.

@@ -6,6 +6,9 @@
 
 namespace hp {
 
+extern long long* g_prof;
+void set_cluster_threads(int nt);
+
 static thread_local std::string g_err;
 
 static std::atomic<int64_t> g_launches{0};
@@ -43,5 +46,11 @@ const char* hp_last_error(void) { return hp::g_err.c_str(); }
 int hp_device_sm_count(void) { return hp::sm_count(); }
 
 int64_t hp_launch_count(void) { return hp::g_launches.load(std::memory_order_relaxed); }
+
+// Instrumentation only: device buffer for per-phase clock64 stamps of the dedup kernels.
+void hp_debug_set_profile(long long* dev_buf) { hp::g_prof = dev_buf; }
+
+// Tuning only: CTA size (256 | 512 | 1024) of the cluster dedup path.
+void hp_debug_set_cluster_threads(int nt) { hp::set_cluster_threads(nt); }
 
 }  // extern "C"

@@ -185,9 +185,9 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
   extern __shared__ __align__(16) unsigned char smem[];
   uint2* s_buf = reinterpret_cast<uint2*>(smem);  // sorted slice (key, pos)
   int* s_hist = reinterpret_cast<int*>(s_buf + S);
-  int* s_hpos = s_hist;          // after the sort: local head positions [S]
-  int* s_sig = s_hist + S;       //                 send slot of local segment [S]
-  int* s_scan = s_hist + NW * HS;
+  int* s_hpos = s_hist + NW * HS;  // local head positions [S]
+  int* s_sig = s_hpos + S;         // send slot of local segment [S]
+  int* s_scan = s_sig + S;
   int* s_cnt = s_scan + 40;      // published digit counts
   int* s_base = s_cnt + HP_RADIX;
   int* s_pub = s_base + HP_RADIX;  // published scalars
@@ -199,6 +199,13 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
   const int T = (int)pl.T, P = pl.P;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const Router route(pl.V, P);
+  int nprof = 0;
+#define HP_PROF()                                                     \
+  do {                                                                \
+    if (pl.prof && tid == 0) pl.prof[c * 16 + nprof] = clock64();     \
+    ++nprof;                                                          \
+  } while (0)
+  HP_PROF();
 
   uint32_t key[IPT];
   int32_t pos[IPT];
@@ -208,13 +215,14 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
     key[r] = i < T ? load_key(ids, i, pl.V, &pl.counters[C_ERR]) : 0xffffffffu;
     pos[r] = i;
   }
-  for (int p = tid; p < P; p += NT) s_pcnt[p] = 0;
+  HP_PROF();
   const int passes = (pl.key_bits + HP_RADIX_BITS - 1) / HP_RADIX_BITS;
   for (int ps = 0; ps < passes; ++ps) {
     const int shift = ps * HP_RADIX_BITS;
     int rank[IPT];
     block_rank<NT, IPT>(key, shift, rank, s_hist, s_scan);
     if (tid < HP_RADIX) s_cnt[tid] = (tid + 1 < HP_RADIX ? s_hist[tid + 1] : S) - s_hist[tid];
+    HP_PROF();
     cl.sync();
     int tot = 0, pre = 0;
     if (tid < HP_RADIX) {
@@ -235,6 +243,7 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
       const int dc = g / S;
       cl.map_shared_rank(s_buf, dc)[g - dc * S] = make_uint2(key[r], (uint32_t)pos[r]);
     }
+    HP_PROF();
     cl.sync();
     if (ps + 1 < passes) {
 #pragma unroll
@@ -247,7 +256,9 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
   }
   // ---- local segment analysis (thread t owns slice items [t*IPT, t*IPT+IPT))
   const int nvalid = min(S, max(0, T - c * S));
-  const uint32_t prev_last = c > 0 ? cl.map_shared_rank(s_buf, c - 1)[S - 1].x : 0u;
+  if (tid == 0) s_pub[15] = c > 0 ? (int)cl.map_shared_rank(s_buf, c - 1)[S - 1].x : 0;
+  __syncthreads();
+  const uint32_t prev_last = (uint32_t)s_pub[15];
   bool h[IPT];
   int heads = 0;
 #pragma unroll
@@ -256,21 +267,30 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
     const uint32_t prev = li > 0 ? s_buf[li - 1].x : prev_last;
     h[k] = li < nvalid && ((c == 0 && li == 0) || s_buf[li].x != prev);
     heads += h[k];
-    if (li < nvalid) pl.sorted_pos[c * S + li] = (int32_t)s_buf[li].y;
   }
+  for (int li = tid; li < nvalid; li += NT) pl.sorted_pos[c * S + li] = (int32_t)s_buf[li].y;
   int cta_heads;
   const int hb = block_excl_scan<NT>(heads, s_scan, &cta_heads);
   {
     int cnt = 0;
 #pragma unroll
     for (int k = 0; k < IPT; ++k)
-      if (h[k]) {
-        const int li = tid * IPT + k;
-        s_hpos[hb + cnt++] = li;
-        atomicAdd(&s_pcnt[route.part(s_buf[li].x)], 1);
-      }
+      if (h[k]) s_hpos[hb + cnt++] = tid * IPT + k;
   }
   __syncthreads();
+  // unique ids of this slice per partition: heads are in ascending id order, so
+  // count(p) = #heads with id < lo(p+1) - #heads with id < lo(p)
+  for (int p = tid; p < P; p += NT) {
+    auto below = [&](int64_t x) {
+      int lo = 0, hi = cta_heads;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((int64_t)s_buf[s_hpos[mid]].x < x) lo = mid + 1; else hi = mid;
+      }
+      return lo;
+    };
+    s_pcnt[p] = below(p + 1 < P ? route.lo(p + 1) : pl.V) - below(route.lo(p));
+  }
   // lengths of every local segment except the last one (its end lies in a later CTA)
   int ni = 0, np = 0, nl = 0;
   for (int sidx = hb; sidx < hb + heads; ++sidx) {
@@ -290,18 +310,22 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
     s_pub[PB_PARTS] = (packed_tot >> 12) & 0x3ff;
     s_pub[PB_LONGS] = (packed_tot >> 22) & 0x3ff;
   }
+  HP_PROF();
   cl.sync();  // ---- the one metadata barrier
+  HP_PROF();
   // global prefixes from the published state of every CTA
   int seg_base = 0, U = 0, bi = packed & 0xfff, bp = (packed >> 12) & 0x3ff, bl = packed >> 22;
   int tot_i = 0, tot_p = 0, tot_l = 0, my_last_len = 0;
   {
+    // one DSMEM read per published value, then every thread reads local smem
+    int* s_all = s_base;  // CS * PB_N <= 256 ints, free after the sort
+    if (tid < CS * PB_N) s_all[tid] = cl.map_shared_rank(s_pub, tid / PB_N)[tid % PB_N];
+    __syncthreads();
     int pub[CS][PB_N];
 #pragma unroll
-    for (int cc = 0; cc < CS; ++cc) {
-      const int* q = cl.map_shared_rank(s_pub, cc);
+    for (int cc = 0; cc < CS; ++cc)
 #pragma unroll
-      for (int f = 0; f < PB_N; ++f) pub[cc][f] = q[f];
-    }
+      for (int f = 0; f < PB_N; ++f) pub[cc][f] = s_all[cc * PB_N + f];
     int next_head = T;
 #pragma unroll
     for (int cc = CS - 1; cc >= 0; --cc) {
@@ -337,6 +361,7 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
   __syncthreads();
   partition_bases<NT>(s_first, owner, P, pl.nranks, s_pbase, c == 0 ? dest_counts : nullptr,
                       s_dest);
+  HP_PROF();
   // ---- per-segment outputs (thread t: segments whose head is in its items)
   auto seg_out = [&](int sidx, int L, int& bi_, int& bp_, int& bl_) {
     const int u = seg_base + sidx;
@@ -365,6 +390,7 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
     if (n_uniq) *n_uniq = U;
   }
   __syncthreads();
+  HP_PROF();
   if (inv) {
     // items before the first local head belong to the previous CTA's last segment
     int spill_slot = 0;
@@ -381,15 +407,19 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
       if (li < nvalid) inv[s_buf[li].y] = hcount > 0 ? s_sig[hcount - 1] : spill_slot;
     }
   }
+  HP_PROF();
   cl.sync();  // no CTA may exit while others still read its shared memory
+  HP_PROF();
+#undef HP_PROF
 }
 
 constexpr size_t tile_smem_bytes() {
   return (size_t)HP_TILE * 8 + (size_t)(HP_TILE_THREADS / 32) * HS * 4 + 40 * 4 + HP_RADIX * 4;
 }
 
+template <int NT>
 constexpr size_t cluster_smem_bytes() {
-  return (size_t)HP_CL_SLICE * 8 + (size_t)(HP_CL_THREADS / 32) * HS * 4 + 40 * 4 +
+  return (size_t)HP_CL_SLICE * 16 + (size_t)(NT / 32) * HS * 4 + 40 * 4 +
          2 * HP_RADIX * 4 + 16 * 4 + MAX_RANKS * 4 + (3 * CL_PMAX + 1) * 4;
 }
 
@@ -633,6 +663,8 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 }  // namespace
 
+long long* g_prof = nullptr;  // set by hp_debug_set_profile (instrumentation only)
+
 size_t dedup_ws_bytes(int64_t T, int32_t D, int32_t P) {
   const int64_t Tc = T < 1 ? 1 : T;
   const int64_t ntiles = (Tc + HP_TILE - 1) / HP_TILE;
@@ -698,24 +730,46 @@ int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, i
   pl->partial_rows = 2 * Tc / HP_CHUNK + 2;
   pl->partials = (float*)take(4 * (size_t)D * pl->partial_rows);
   pl->sorted_pos = pl->pos[0];
+  pl->prof = g_prof;
   return HP_OK;
 }
 
-template <int CS>
-int launch_cluster(const DedupPlan& pl, const int64_t* ids, const int32_t* owner,
-                   const int64_t* dst_pb, int64_t* send_ids, int32_t* counts, int32_t* inv,
-                   int32_t* dest_counts, int32_t* n_uniq, cudaStream_t st) {
-  constexpr size_t smem = cluster_smem_bytes();
-  auto kern = k_dedup_cluster<HP_CL_THREADS, HP_CL_IPT, CS>;
+template <int NT, int CS>
+int launch_cluster_nt(const DedupPlan& pl, const int64_t* ids, const int32_t* owner,
+                      const int64_t* dst_pb, int64_t* send_ids, int32_t* counts, int32_t* inv,
+                      int32_t* dest_counts, int32_t* n_uniq, cudaStream_t st) {
+  constexpr int IPT = HP_CL_SLICE / NT;
+  constexpr size_t smem = cluster_smem_bytes<NT>();
+  auto kern = k_dedup_cluster<NT, IPT, CS>;
   static bool configured = false;
   if (!configured) {
     HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
-  kern<<<CS, HP_CL_THREADS, smem, st>>>(pl, ids, owner, dst_pb, send_ids, counts, inv,
-                                        dest_counts, n_uniq);
+  kern<<<CS, NT, smem, st>>>(pl, ids, owner, dst_pb, send_ids, counts, inv, dest_counts, n_uniq);
   HP_LAUNCHED(1, "k_dedup_cluster");
   return HP_OK;
+}
+
+int g_cl_threads = HP_CL_THREADS;  // CTA shape of the cluster path (hp_debug_set_cluster_threads)
+
+void set_cluster_threads(int nt) { g_cl_threads = nt; }
+
+template <int CS>
+int launch_cluster(const DedupPlan& pl, const int64_t* ids, const int32_t* owner,
+                   const int64_t* dst_pb, int64_t* send_ids, int32_t* counts, int32_t* inv,
+                   int32_t* dest_counts, int32_t* n_uniq, cudaStream_t st) {
+  switch (g_cl_threads) {
+    case 256:
+      return launch_cluster_nt<256, CS>(pl, ids, owner, dst_pb, send_ids, counts, inv,
+                                        dest_counts, n_uniq, st);
+    case 512:
+      return launch_cluster_nt<512, CS>(pl, ids, owner, dst_pb, send_ids, counts, inv,
+                                        dest_counts, n_uniq, st);
+    default:
+      return launch_cluster_nt<1024, CS>(pl, ids, owner, dst_pb, send_ids, counts, inv,
+                                         dest_counts, n_uniq, st);
+  }
 }
 
 int build_plan(DedupPlan& pl, const int64_t* ids, const int32_t* owner,

@@ -10,9 +10,8 @@
 
 #define HP_CHUNK 32           // rows per sequential group of the summation tree (oracle CHUNK)
 #define HP_CL_CTAS 8          // cluster sort path: CTAs per cluster (portable maximum)
-#define HP_CL_THREADS 1024
-#define HP_CL_IPT 2
-#define HP_CL_SLICE (HP_CL_THREADS * HP_CL_IPT)           // items per CTA
+#define HP_CL_THREADS 1024    // default CTA size (256 / 512 selectable for tuning)
+#define HP_CL_SLICE 2048      // items per CTA
 #define HP_SMALL_MAX (HP_CL_CTAS * HP_CL_SLICE)           // 16384 items
 #define HP_RADIX_BITS 8
 #define HP_RADIX 256

@@ -38,6 +38,7 @@ struct DedupPlan {
   int32_t* counters;    // [C_NCOUNTERS]
   float* partials;      // [(2T/C + 2) * D]
   int64_t partial_rows;
+  long long* prof;      // optional per-phase clock64 stamps (HP_PROFILE_PTR), else nullptr
 };
 
 size_t dedup_ws_bytes(int64_t T, int32_t D, int32_t P);
