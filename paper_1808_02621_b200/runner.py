@@ -30,6 +30,7 @@ from ._lib import Slab
 from .model import ClusterSpec, GraphSpec, SpecError, VariableSpec, partition_bounds
 from .ops import OptimizerConfig, Workspace
 from .placement import DistributedPlan, Mechanism, transform_hybrid
+from .protocol import slab_layout, wire_bytes
 from .stats import IterationStats, Message, TransferReport
 
 
@@ -50,12 +51,7 @@ class ShardedTable:
         self.device = torch.device(device)
         self.owner = np.asarray(owner, dtype=np.int32)
         self.bounds = partition_bounds(self.V, self.P)
-        self.owned = [p for p in range(self.P) if self.owner[p] == rank]
-        base = np.full(self.P, -1, dtype=np.int64)
-        rows = 0
-        for p in self.owned:
-            base[p] = rows
-            rows += int(self.bounds[p + 1] - self.bounds[p])
+        self.owned, base, rows = slab_layout(self.bounds, self.owner, rank)
         self.rows = rows
         self.part_base_host = base
         self.part_base = torch.from_numpy(base).to(self.device)
@@ -289,12 +285,9 @@ class HybridRunner:
         n = self.world_size
         rows = [[0.0, 0.0] for _ in range(n)]
         for name, c in self.last_counts.items():
-            D = self.tables[name].D
-            for o in range(n):
-                if o == self.rank:
-                    continue
-                rows[self.rank][0] += c["send"][o] * (8 + 4 * D) + c["recv"][o] * 4 * D
-                rows[self.rank][1] += c["recv"][o] * (8 + 4 * D) + c["send"][o] * 4 * D
+            eg, ing = wire_bytes(c["send"], c["recv"], self.rank, self.tables[name].D)
+            rows[self.rank][0] += eg
+            rows[self.rank][1] += ing
         for var in self.dense:
             if n > 1:
                 per_dir = 2.0 * var.payload_bytes * (n - 1) / n

@@ -1,0 +1,91 @@
+"""Multi-GPU parity check of HybridRunner (NCCL path), one rank per GPU.
+
+    python -m torch.distributed.run --standalone --nproc-per-node N tests/dist_gpu_check.py
+
+Every rank recomputes the single-process oracle of the same step for all
+ranks' (seeded) batches and checks, bit-exactly, its pulled rows and the
+partitions it homes; the dense allreduce is checked within 1e-5 rel + 1e-6 abs.
+Prints one "DIST_CHECK rank r: PASS/FAIL ..." line per rank; exit 1 on failure.
+"""
+
+import json
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import paper_1808_02621_b200 as hp  # noqa: E402
+from oracle import oracle as orc  # noqa: E402
+from paper_1808_02621_b200.synth import TableShape, Workload, make_batch  # noqa: E402
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    comm = hp.Comm.from_torch_distributed()
+    opt_kind = os.environ.get("HP_CHECK_OPT", "adagrad")
+    wl = Workload("check", [TableShape("embedding", 60_000, 128, 2560),
+                            TableShape("softmax", 60_000, 256, 2560, sampled=3000)],
+                  {"lstm": 50_001}, {"kind": opt_kind, "lr": 0.1, "init_acc": 0.1}, 2560,
+                  partitions=8)
+    graph = hp.load_graph_spec(json.dumps(wl.graph_json()))
+    cluster = hp.ClusterSpec.b200_box(world)
+    plan = hp.transform_hybrid(graph, cluster, partitions={"embedding": 8, "softmax": 12})
+    runner = hp.HybridRunner(plan, graph, cluster, rank=rank, world_size=world, comm=comm,
+                             optimizer=hp.OptimizerConfig(kind=opt_kind, lr=0.1), device=dev,
+                             seed=5)
+    hpar = {"lr": 0.1, "beta1": 0.9, "beta2": 0.999, "eps": 1e-8}
+    states = {t.name: orc.init_state(opt_kind, t.V, t.D, 5 * 1000 + i + 1, 0.1)
+              for i, t in enumerate(wl.tables)}
+    ok, why = True, []
+    for step in (1, 2, 3):
+        batches = [make_batch(wl, seed=step, rank=r) for r in range(world)]
+        mine = batches[rank]
+        batch = {k: ((torch.from_numpy(v[0]).to(dev), torch.from_numpy(v[1]).to(dev))
+                     if isinstance(v, tuple) else torch.from_numpy(v).to(dev))
+                 for k, v in mine.items()}
+        stats = runner.step(batch)
+        for t in wl.tables:
+            owner = plan.owner_table(t.name)
+            orc.sparse_step(states[t.name], opt_kind, hpar, step, [b[t.name] for b in batches],
+                            t.V, plan.partitions_of[t.name], owner)
+            got = runner.outputs[t.name].cpu().numpy()
+            if not np.array_equal(got, states[t.name]["w"][mine[t.name][0]]):
+                ok = False
+                why.append(f"step {step} {t.name}: pulled rows differ")
+            tab = runner.tables[t.name]
+            w = tab.w.cpu().numpy()
+            for p in tab.owned:
+                lo, hi = int(tab.bounds[p]), int(tab.bounds[p + 1])
+                b = int(tab.part_base_host[p])
+                if not np.array_equal(w[b:b + hi - lo], states[t.name]["w"][lo:hi]):
+                    ok = False
+                    why.append(f"step {step} {t.name} partition {p} differs")
+        ref = orc.dense_allreduce([b["lstm"] for b in batches], 1.0 / world)
+        got = runner.dense_out["lstm"].cpu().numpy()
+        if not np.allclose(got, ref, rtol=1e-5, atol=1e-6):
+            ok = False
+            why.append(f"step {step} dense differs (max {np.abs(got - ref).max():.3g})")
+        eg, ing = stats.per_machine_bytes.per_machine[rank]
+        if world > 1 and not (eg > 0 and ing > 0):
+            ok = False
+            why.append("no exchange bytes recorded")
+    print(f"DIST_CHECK rank {rank}/{world} opt={opt_kind}: {'PASS' if ok else 'FAIL'} {why[:4]}",
+          flush=True)
+    flag = torch.tensor([0 if ok else 1], device=dev)
+    dist.all_reduce(flag)
+    comm.close()
+    dist.destroy_process_group()
+    sys.exit(int(flag.item() > 0))
+
+
+if __name__ == "__main__":
+    main()

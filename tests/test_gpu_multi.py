@@ -1,0 +1,32 @@
+"""Multi-GPU parity (NCCL path) — runs tests/dist_gpu_check.py under torchrun
+when the box has >= 2 GPUs (skipped on a 1-GPU box)."""
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _ngpu():
+    import torch
+
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.parametrize("opt", ["adagrad", "adam"])
+def test_multi_gpu_step_matches_oracle(opt):
+    n = min(_ngpu(), 8)
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    env = dict(os.environ, HP_CHECK_OPT=opt)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nproc-per-node",
+           str(n), str(ROOT / "tests" / "dist_gpu_check.py")]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("DIST_CHECK")]
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    assert len(lines) == n and all("PASS" in ln for ln in lines), lines
