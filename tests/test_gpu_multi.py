@@ -24,8 +24,14 @@ def test_multi_gpu_step_matches_oracle(opt):
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     env = dict(os.environ, HP_CHECK_OPT=opt)
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nproc-per-node",
-           str(n), str(ROOT / "tests" / "dist_gpu_check.py")]
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node",
+           str(n), "--master-addr", "127.0.0.1", "--master-port", str(port),
+           str(ROOT / "tests" / "dist_gpu_check.py")]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     lines = [ln for ln in res.stdout.splitlines() if ln.startswith("DIST_CHECK")]
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
