@@ -184,6 +184,36 @@ int hp_exchange_pull(hp_comm_t comm, const float* owner_rows, const int32_t* own
                      float* worker_rows, const int32_t* worker_counts, int32_t D,
                      void* stream);
 
+/* ---------------------------------------------------------------- K3/K4/K5 over NVLink
+ * Device-initiated exchange through symmetric IPC windows (one per table per
+ * rank): NVLink stores into owners' inboxes + epoch flags, sort-free owner
+ * merge + apply, peer reads for the pull. No host synchronisation: a full
+ * multi-GPU step can be captured in a CUDA graph.
+ * Replaces: PS push/pull (`simulate.py:183-240`) and server aggregation +
+ * update (`simulate.py:294-323`). */
+typedef struct hp_xchg_s* hp_xchg_t;
+size_t hp_xchg_window_bytes(int32_t n, int32_t D, int64_t cap, int64_t rows_cap);
+/* Allocates this rank's window (slab of rows_cap x D fp32 + inboxes for n
+ * sources x cap rows); returns the 64-byte cudaIpc handle and the slab pointer. */
+int hp_xchg_create(hp_xchg_t* out, int32_t n, int32_t me, int32_t D, int64_t cap,
+                   int64_t rows_cap, void* ipc_handle_out, void** w_out);
+int hp_xchg_open_peer(hp_xchg_t x, int32_t rank, const void* ipc_handle);
+int hp_xchg_destroy(hp_xchg_t x);
+/* Worker: send blocks (send order, dest-major; from hp_sort_dedup_route) -> owners. */
+int hp_xchg_push(hp_xchg_t x, const int64_t* send_ids, const float* send_rows,
+                 const int32_t* dest_counts, int64_t T_bound, void* stream);
+/* Owner: wait for all pushes, merge in source order, apply to the slab, signal. */
+int hp_xchg_merge_apply(hp_xchg_t x, hp_slab slab, hp_optim opt, void* stream);
+/* Worker: wait for all applies, pulled[k] = updated row of send slot k
+ * (glob_base[p] = slab row of partition p on its owner, device int64[P]). */
+int hp_xchg_pull(hp_xchg_t x, const int64_t* send_ids, const int32_t* n_uniq, int64_t T_bound,
+                 const int32_t* owner, const int64_t* glob_base, int64_t V, int32_t P,
+                 float* pulled, void* stream);
+/* Rows received from each source in the last push -> device int32[n] (async). */
+int hp_xchg_recv_counts(hp_xchg_t x, int32_t* out_dev, void* stream);
+/* Error bits (4/8: a wait timed out, 16: a received id is not homed here). */
+int hp_xchg_status(hp_xchg_t x, int32_t* out_err, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

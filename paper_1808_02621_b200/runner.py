@@ -38,7 +38,8 @@ class ShardedTable:
     """This rank's partitions of one sparse Weight plus optimizer state."""
 
     def __init__(self, var: VariableSpec, partitions: int, owner: np.ndarray, rank: int,
-                 optimizer: OptimizerConfig, device, seed: int = 0, init_scale: float = 0.05):
+                 optimizer: OptimizerConfig, device, seed: int = 0, init_scale: float = 0.05,
+                 w_storage=None):
         if var.elem_bytes % 16:
             raise SpecError(f"table {var.name!r}: row bytes must be a multiple of 16 (D % 4 == 0)")
         self.var = var
@@ -56,7 +57,10 @@ class ShardedTable:
         self.part_base_host = base
         self.part_base = torch.from_numpy(base).to(self.device)
         self.owner_dev = torch.from_numpy(self.owner).to(self.device)
-        self.w = torch.empty(max(rows, 1), self.D, dtype=torch.float32, device=self.device)
+        if w_storage is not None:  # the slab lives in a peer-readable window
+            self.w = w_storage(max(rows, 1))
+        else:
+            self.w = torch.empty(max(rows, 1), self.D, dtype=torch.float32, device=self.device)
         self.state = [torch.empty_like(self.w) for _ in range(optimizer.n_state)]
         for p in self.owned:
             lo, hi = int(self.bounds[p]), int(self.bounds[p + 1])
@@ -110,7 +114,8 @@ class HybridRunner:
     def __init__(self, plan: DistributedPlan, graph: GraphSpec, cluster: ClusterSpec, *,
                  rank: int = 0, world_size: int = 1, comm=None,
                  optimizer: OptimizerConfig | None = None, aggregation: str = "mean",
-                 dense_dtype: torch.dtype = torch.float32, device=None, seed: int = 0):
+                 dense_dtype: torch.dtype = torch.float32, device=None, seed: int = 0,
+                 exchange: str = "p2p", max_ids: dict | None = None):
         if aggregation not in ("mean", "sum"):
             raise ValueError("aggregation must be 'mean' or 'sum'")
         if cluster.total_gpus != world_size:
@@ -119,6 +124,11 @@ class HybridRunner:
             raise SpecError("one B200 box is ClusterSpec(machines=n_gpus, gpus_per_machine=1)")
         if world_size > 1 and comm is None:
             raise ValueError("world_size > 1 needs a Comm (Comm.from_torch_distributed())")
+        if exchange not in ("p2p", "nccl"):
+            raise ValueError("exchange must be 'p2p' (NVLink peer memory) or 'nccl'")
+        self.exchange = exchange if world_size > 1 else "local"
+        self.xchg: dict = {}
+        self.glob_base: dict = {}
         self.plan, self.graph, self.cluster = plan, graph, cluster
         self.rank, self.world_size, self.comm = rank, world_size, comm
         self.optimizer = optimizer or OptimizerConfig()
@@ -143,8 +153,12 @@ class HybridRunner:
                 raise NotImplementedError(
                     f"sparse Weight {var.name!r} resolved to AR at n={world_size}: the "
                     "AllGatherv baseline is SURVEY §8(f) 'next', not built yet")
+            storage = None
+            if self.exchange == "p2p":
+                storage = self._make_window(var, P, owner, (max_ids or {}).get(var.name))
             self.tables[var.name] = ShardedTable(var, P, owner, rank, self.optimizer,
-                                                 self.device, seed=seed * 1000 + i)
+                                                 self.device, seed=seed * 1000 + i,
+                                                 w_storage=storage)
         self._scratch: dict[str, _Scratch] = {n: _Scratch() for n in self.tables}
         self.dense_out: dict[str, torch.Tensor] = {}
         self.outputs: dict[str, torch.Tensor] = {}
@@ -152,7 +166,61 @@ class HybridRunner:
         self.last_counts: dict = {}
         self.kernel_events: dict | None = None
         self._streams = {n: torch.cuda.Stream(device=self.device) for n in self.tables}
+        self._pending_counts: dict = {}
         self.concurrent_tables = True
+
+    def _make_window(self, var: VariableSpec, P: int, owner: np.ndarray, max_ids):
+        """Create the table's peer window; returns the slab allocator for ShardedTable.
+
+        Inbox capacity per source = the most unique rows one worker can send to
+        one owner: bounded by the ids per worker per step, i.e. the Weight's
+        touched rows ceil(alpha * V) (reference `model.py:27-33,73-81`) unless
+        ``max_ids`` overrides it.
+        """
+        from .xchg import PeerExchange
+
+        D = var.elem_bytes // 4
+        bounds = partition_bounds(var.elements, P)
+        _, _, rows = slab_layout(bounds, owner, self.rank)
+        cap = int(max_ids or var.touched_elements)
+        x = PeerExchange(self.world_size, self.rank, D, cap, max(rows, 1), self.device)
+        self.xchg[var.name] = x
+        gb = np.zeros(P, dtype=np.int64)
+        for r in range(self.world_size):
+            _, base, _ = slab_layout(bounds, owner, r)
+            gb[base >= 0] = base[base >= 0]
+        self.glob_base[var.name] = torch.from_numpy(gb).to(self.device)
+        return lambda nrows: x.w[:nrows]
+
+    def _sparse_p2p(self, tab: ShardedTable, ids, vals, opt) -> torch.Tensor:
+        n, D, T = self.world_size, tab.D, ids.numel()
+        name = tab.name
+        x = self.xchg[name]
+        if T > x.cap:
+            raise SpecError(f"table {name!r}: {T} ids exceed the inbox capacity {x.cap} "
+                            "(raise max_ids)")
+        r = ops.sort_dedup_route(ids, vals, tab.V, tab.P, tab.owner_dev, n, tab.ws,
+                                 out=self._scratch[name].tensors.setdefault("k1", {}))
+        x.push(r["send_ids"], r["send_rows"], r["dest_counts"], T)
+        x.merge_apply(tab.slab(), opt)
+        rc = self._buf(name, "recv_counts", (n,), torch.int32)
+        x.recv_counts(rc)
+        pulled = self._buf(name, "pulled", (max(T, 1), D), torch.float32)
+        x.pull(r["send_ids"], r["n_uniq"], T, tab.owner_dev, self.glob_base[name], tab.V, tab.P,
+               pulled)
+        out = self._buf(name, "out", (T, D), torch.float32)
+        ops.stitch(pulled, r["inv"], out)
+        self._pending_counts[name] = (r["dest_counts"], rc)
+        return out
+
+    def exchange_status(self) -> dict:
+        """Error bits of every table's peer exchange (synchronises)."""
+        return {k: x.status() for k, x in self.xchg.items()}
+
+    def close(self) -> None:
+        for x in self.xchg.values():
+            x.close()
+        self.xchg.clear()
 
     # ------------------------------------------------------------------ step
     def _buf(self, name: str, key: str, shape, dtype) -> torch.Tensor:
@@ -269,10 +337,15 @@ class HybridRunner:
                 if self.world_size == 1:
                     self.outputs[name] = self._sparse_local(tab, ids, vals, opt)
                     ev("update")
+                elif self.exchange == "p2p":
+                    self.outputs[name] = self._sparse_p2p(tab, ids, vals, opt)
+                    ev("network")
                 else:
                     self.outputs[name] = self._sparse_exchange(tab, ids, vals, opt, ev)
         if timed:
             stream.synchronize()
+            for name, (sc, rc) in self._pending_counts.items():
+                self.last_counts[name] = {"send": sc.tolist(), "recv": rc.tolist()}
             for (_, a), (ph, b) in zip(marks, marks[1:]):
                 phases[ph] += a.elapsed_time(b) * 1e3
             iter_us = marks[0][1].elapsed_time(marks[-1][1]) * 1e3
@@ -316,7 +389,7 @@ class HybridRunner:
         optimizer struct is baked in at capture: use it for step-independent
         optimizers (SGD / Adagrad); Adam's bias correction would freeze.
         """
-        if self.world_size > 1:
+        if self.world_size > 1 and self.exchange != "p2p":
             raise NotImplementedError("the NCCL a2a-v path reads counts on the host")
         cur = torch.cuda.current_stream()
         side = torch.cuda.Stream(device=self.device)

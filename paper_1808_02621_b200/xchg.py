@@ -1,0 +1,70 @@
+"""Python side of the NVLink peer-memory exchange (``hp_xchg_*`` in the C ABI).
+
+One :class:`PeerExchange` per sparse table per rank: it owns the rank's
+symmetric window (the table slab + inboxes + flags), swaps cudaIpc handles
+with the other ranks over ``torch.distributed`` (plumbing only) and exposes
+the three device-initiated phases push / merge_apply / pull.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from ._lib import call, load
+
+
+class _DevPtr:
+    """Zero-copy tensor view of library-owned device memory."""
+
+    def __init__(self, ptr: int, shape, typestr: str = "<f4"):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+class PeerExchange:
+    def __init__(self, n: int, rank: int, D: int, cap: int, rows_cap: int, device, group=None):
+        import torch.distributed as dist
+
+        load()
+        self.n, self.rank, self.D, self.cap = n, rank, D, cap
+        self.handle = C.c_void_p()
+        ipc = (C.c_ubyte * 64)()
+        wptr = C.c_void_p()
+        call("hp_xchg_create", C.byref(self.handle), n, rank, D, cap, rows_cap, C.addressof(ipc),
+             C.byref(wptr))
+        handles = [None] * n
+        dist.all_gather_object(handles, bytes(ipc), group=group)
+        for r, h in enumerate(handles):
+            if r != rank:
+                buf = (C.c_ubyte * 64).from_buffer_copy(h)
+                call("hp_xchg_open_peer", self.handle, r, C.addressof(buf))
+        self.w = torch.as_tensor(_DevPtr(wptr.value, (rows_cap, D)), device=device)
+
+    def push(self, send_ids, send_rows, dest_counts, T_bound: int) -> None:
+        call("hp_xchg_push", self.handle, send_ids.data_ptr(), send_rows.data_ptr(),
+             dest_counts.data_ptr(), T_bound, torch.cuda.current_stream().cuda_stream)
+
+    def merge_apply(self, slab, opt) -> None:
+        call("hp_xchg_merge_apply", self.handle, slab, opt, torch.cuda.current_stream().cuda_stream)
+
+    def pull(self, send_ids, n_uniq, T_bound: int, owner, glob_base, V: int, P: int, pulled) -> None:
+        call("hp_xchg_pull", self.handle, send_ids.data_ptr(), n_uniq.data_ptr(), T_bound,
+             owner.data_ptr(), glob_base.data_ptr(), V, P, pulled.data_ptr(),
+             torch.cuda.current_stream().cuda_stream)
+
+    def recv_counts(self, out) -> None:
+        call("hp_xchg_recv_counts", self.handle, out.data_ptr(),
+             torch.cuda.current_stream().cuda_stream)
+
+    def status(self) -> int:
+        err = C.c_int32(0)
+        call("hp_xchg_status", self.handle, C.addressof(err), torch.cuda.current_stream().cuda_stream)
+        return err.value
+
+    def close(self) -> None:
+        if self.handle:
+            torch.cuda.synchronize()
+            call("hp_xchg_destroy", self.handle)
+            self.handle = None

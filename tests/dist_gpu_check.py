@@ -32,6 +32,7 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     comm = hp.Comm.from_torch_distributed()
     opt_kind = os.environ.get("HP_CHECK_OPT", "adagrad")
+    xmode = os.environ.get("HP_CHECK_XCHG", "p2p")
     wl = Workload("check", [TableShape("embedding", 60_000, 128, 2560),
                             TableShape("softmax", 60_000, 256, 2560, sampled=3000)],
                   {"lstm": 50_001}, {"kind": opt_kind, "lr": 0.1, "init_acc": 0.1}, 2560,
@@ -41,7 +42,7 @@ def main():
     plan = hp.transform_hybrid(graph, cluster, partitions={"embedding": 8, "softmax": 12})
     runner = hp.HybridRunner(plan, graph, cluster, rank=rank, world_size=world, comm=comm,
                              optimizer=hp.OptimizerConfig(kind=opt_kind, lr=0.1), device=dev,
-                             seed=5)
+                             seed=5, exchange=xmode)
     hpar = {"lr": 0.1, "beta1": 0.9, "beta2": 0.999, "eps": 1e-8}
     states = {t.name: orc.init_state(opt_kind, t.V, t.D, 5 * 1000 + i + 1, 0.1)
               for i, t in enumerate(wl.tables)}
@@ -78,8 +79,35 @@ def main():
         if world > 1 and not (eg > 0 and ing > 0):
             ok = False
             why.append("no exchange bytes recorded")
-    print(f"DIST_CHECK rank {rank}/{world} opt={opt_kind}: {'PASS' if ok else 'FAIL'} {why[:4]}",
-          flush=True)
+    if xmode == "p2p":
+        errs = runner.exchange_status()
+        if any(errs.values()):
+            ok = False
+            why.append(f"exchange error bits {errs}")
+        # the same step replayed from a CUDA graph must give the same bytes
+        if ok:
+            step = 4
+            batches = [make_batch(wl, seed=step, rank=r) for r in range(world)]
+            mine = batches[rank]
+            static = {k: ((torch.from_numpy(v[0]).to(dev), torch.from_numpy(v[1]).to(dev))
+                          if isinstance(v, tuple) else torch.from_numpy(v).to(dev))
+                      for k, v in mine.items()}
+            g = runner.capture(static, warmup=1)  # runs step 4 eagerly, records one step
+            g.replay()                            # executes step 5
+            for st_ in (4, 5):
+                for t in wl.tables:
+                    orc.sparse_step(states[t.name], opt_kind, hpar, st_, [b[t.name] for b in batches],
+                                    t.V, plan.partitions_of[t.name], plan.owner_table(t.name))
+            torch.cuda.synchronize()
+            if opt_kind != "adam":  # Adam's bias correction is frozen in a graph
+                for t in wl.tables:
+                    got = runner.outputs[t.name].cpu().numpy()
+                    if not np.array_equal(got, states[t.name]["w"][mine[t.name][0]]):
+                        ok = False
+                        why.append(f"graph replay {t.name}: pulled rows differ")
+        runner.close()
+    print(f"DIST_CHECK rank {rank}/{world} opt={opt_kind} xchg={xmode}: "
+          f"{'PASS' if ok else 'FAIL'} {why[:4]}", flush=True)
     flag = torch.tensor([0 if ok else 1], device=dev)
     dist.all_reduce(flag)
     comm.close()

@@ -18,12 +18,12 @@ def _ngpu():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("opt", ["adagrad", "adam"])
-def test_multi_gpu_step_matches_oracle(opt):
+@pytest.mark.parametrize("opt,xchg", [("adagrad", "p2p"), ("adam", "p2p"), ("sgd", "nccl")])
+def test_multi_gpu_step_matches_oracle(opt, xchg):
     n = min(_ngpu(), 8)
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
-    env = dict(os.environ, HP_CHECK_OPT=opt)
+    env = dict(os.environ, HP_CHECK_OPT=opt, HP_CHECK_XCHG=xchg)
     import socket
 
     with socket.socket() as sk:
