@@ -209,6 +209,8 @@ int hp_xchg_merge_apply(hp_xchg_t x, hp_slab slab, hp_optim opt, void* stream);
 int hp_xchg_pull(hp_xchg_t x, const int64_t* send_ids, const int32_t* n_uniq, int64_t T_bound,
                  const int32_t* owner, const int64_t* glob_base, int64_t V, int32_t P,
                  float* pulled, void* stream);
+/* Debug: the window's signal words (>= 200 int32) to host memory (syncs). */
+int hp_xchg_debug_sig(hp_xchg_t x, int32_t* host_out, void* stream);
 /* Rows received from each source in the last push -> device int32[n] (async). */
 int hp_xchg_recv_counts(hp_xchg_t x, int32_t* out_dev, void* stream);
 /* Error bits (4/8: a wait timed out, 16: a received id is not homed here). */

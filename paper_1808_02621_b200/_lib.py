@@ -69,6 +69,7 @@ SIGNATURES = {
     "hp_xchg_pull": (C.c_int, [vp, vp, vp, i64, vp, vp, i64, i32, vp, vp]),
     "hp_xchg_status": (C.c_int, [vp, vp, vp]),
     "hp_xchg_recv_counts": (C.c_int, [vp, vp, vp]),
+    "hp_xchg_debug_sig": (C.c_int, [vp, vp, vp]),
 }
 
 _lib = None

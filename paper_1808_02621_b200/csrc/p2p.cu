@@ -21,6 +21,7 @@
 // Spin-waits run in ONE small block (k_wait) and give up after a bounded time,
 // raising an error bit instead of hanging the GPU.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "hp_common.cuh"
@@ -259,6 +260,15 @@ k_pull(PeerTable peers, int64_t w_off, int D4, const int64_t* __restrict__ send_
 
 using namespace hp;
 
+// Spin-wait budget (cycles) before a wait gives up and raises an error bit.
+static long long wait_budget() {
+  static long long v = [] {
+    const char* e = getenv("HP_WAIT_TIMEOUT_CYCLES");
+    return e ? atoll(e) : 4000000000LL;  // ~2 s at 1.9 GHz
+  }();
+  return v;
+}
+
 // Opaque exchange state for one table (declared in include/hybridpath.h).
 struct hp_xchg_s {
   int n, me, D;
@@ -359,7 +369,7 @@ int hp_xchg_merge_apply(hp_xchg_t x, hp_slab slab, hp_optim opt, void* stream) {
   HP_REQUIRE(x && slab.part_base, "NULL argument");
   HP_REQUIRE(slab.D == x->D, "slab width differs from the exchange");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  k_wait<<<1, 64, 0, st>>>(x->win, 0, x->n, 20000000000LL);
+  k_wait<<<1, 64, 0, st>>>(x->win, 0, x->n, wait_budget());
   const int64_t total = (int64_t)x->n * x->cap;
   k_owner_scatter<<<grid_for(total, 256, sm_count() * 8), 256, 0, st>>>(
       x->win, x->n, x->ids_off, x->cap, slab.part_base, Router(slab.V, slab.P), x->slot, x->touch,
@@ -397,7 +407,7 @@ int hp_xchg_pull(hp_xchg_t x, const int64_t* send_ids, const int32_t* n_uniq, in
                  float* pulled, void* stream) {
   HP_REQUIRE(x && send_ids && n_uniq && owner && glob_base && pulled, "NULL argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  k_wait<<<1, 64, 0, st>>>(x->win, 1, x->n, 20000000000LL);
+  k_wait<<<1, 64, 0, st>>>(x->win, 1, x->n, wait_budget());
   k_pull<<<grid_for(T_bound, 8, sm_count() * 4), 256, 0, st>>>(
       x->peers, x->w_off, x->D / 4, send_ids, n_uniq, owner, glob_base, Router(V, P),
       reinterpret_cast<float4*>(pulled));
@@ -406,6 +416,16 @@ int hp_xchg_pull(hp_xchg_t x, const int64_t* send_ids, const int32_t* n_uniq, in
 }
 
 // Rows received from each source in the last push (device copy, stream-ordered).
+// Debug: copy the window's signal words (push_flag[64], push_count[64],
+// applied_flag[64], epoch, err, ...) to a host buffer of >= 200 ints (syncs).
+int hp_xchg_debug_sig(hp_xchg_t x, int32_t* host_out, void* stream) {
+  HP_REQUIRE(x && host_out, "NULL argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  HP_CUDA(cudaMemcpyAsync(host_out, x->win, 200 * 4, cudaMemcpyDeviceToHost, st));
+  HP_CUDA(cudaStreamSynchronize(st));
+  return HP_OK;
+}
+
 int hp_xchg_recv_counts(hp_xchg_t x, int32_t* out_dev, void* stream) {
   HP_REQUIRE(x && out_dev, "NULL argument");
   SigView sig(x->win);

@@ -58,6 +58,15 @@ class PeerExchange:
         call("hp_xchg_recv_counts", self.handle, out.data_ptr(),
              torch.cuda.current_stream().cuda_stream)
 
+    def debug_sig(self) -> dict:
+        buf = (C.c_int32 * 200)()
+        call("hp_xchg_debug_sig", self.handle, C.addressof(buf),
+             torch.cuda.current_stream().cuda_stream)
+        v = list(buf)
+        return {"push_flag": v[:self.n], "push_count": v[64:64 + self.n],
+                "applied_flag": v[128:128 + self.n], "epoch": v[192], "err": v[193],
+                "done": v[196:200]}
+
     def status(self) -> int:
         err = C.c_int32(0)
         call("hp_xchg_status", self.handle, C.addressof(err), torch.cuda.current_stream().cuda_stream)
