@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"])
     return ap.parse_args()
 
 
@@ -208,7 +209,7 @@ def main():
     plan = hp.transform_hybrid(graph, cluster, partitions={t.name: P for t in wl.tables})
     opt = hp.OptimizerConfig(**wl.optimizer)
     runner = hp.HybridRunner(plan, graph, cluster, rank=rank, world_size=world, comm=comm,
-                             optimizer=opt, device=dev, seed=0)
+                             optimizer=opt, device=dev, seed=0, exchange=args.exchange)
 
     # resident batches, rotated so their total exceeds 2x L2 (126 MB)
     host = [make_batch(wl, seed=1 + i, rank=rank) for i in range(1)]
@@ -224,7 +225,7 @@ def main():
                 for k, v in b.items()}
 
     batches = [to_dev(b) for b in host]
-    use_graph = world == 1 and not args.no_graph and opt.kind != "adam"
+    use_graph = (world == 1 or args.exchange == "p2p") and not args.no_graph and opt.kind != "adam"
     stream = torch.cuda.current_stream()
 
     for i in range(args.warmup):
@@ -369,7 +370,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": t_dev / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (Zipf(1.1) ids, normal grads, hash-initialised tables)",
-            "config": config(args, wl) | {"rotations": R, "cuda_graph": bool(graphs)},
+            "config": config(args, wl) | {"rotations": R, "cuda_graph": bool(graphs),
+                                          "exchange": runner.exchange},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": ke},
             "gpu_launches": launches_per_step * args.steps,
@@ -378,9 +380,16 @@ def main():
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    if comm is not None:
-        comm.close()
+    # release captured graphs (they reference NCCL and peer windows) before teardown
+    graphs = e2e_graph = None
+    torch.cuda.synchronize()
     if world > 1:
+        errs = runner.exchange_status()
+        if any(errs.values()):
+            print(f"rank {rank}: exchange error bits {errs}", file=sys.stderr, flush=True)
+        barrier()
+        runner.close()
+        comm.close()
         dist.destroy_process_group()
 
 

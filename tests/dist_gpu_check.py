@@ -94,6 +94,8 @@ def main():
                       for k, v in mine.items()}
             g = runner.capture(static, warmup=1)  # runs step 4 eagerly, records one step
             g.replay()                            # executes step 5
+            torch.cuda.synchronize()
+            del g  # release the captured NCCL/peer work before tearing the comms down
             for st_ in (4, 5):
                 for t in wl.tables:
                     orc.sparse_step(states[t.name], opt_kind, hpar, st_, [b[t.name] for b in batches],
@@ -110,9 +112,12 @@ def main():
           f"{'PASS' if ok else 'FAIL'} {why[:4]}", flush=True)
     flag = torch.tensor([0 if ok else 1], device=dev)
     dist.all_reduce(flag)
-    comm.close()
-    dist.destroy_process_group()
-    sys.exit(int(flag.item() > 0))
+    failed = int(flag.item() > 0)
+    if os.environ.get("HP_CHECK_TEARDOWN", "1") == "1":
+        comm.close()
+        dist.destroy_process_group()
+    print(f"DIST_CHECK rank {rank} exiting", flush=True)
+    sys.exit(failed)
 
 
 if __name__ == "__main__":
