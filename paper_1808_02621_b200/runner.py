@@ -199,17 +199,28 @@ class HybridRunner:
         if T > x.cap:
             raise SpecError(f"table {name!r}: {T} ids exceed the inbox capacity {x.cap} "
                             "(raise max_ids)")
+        k = self._kev
+        k(f"k1:{name}", True)
         r = ops.sort_dedup_route(ids, vals, tab.V, tab.P, tab.owner_dev, n, tab.ws,
                                  out=self._scratch[name].tensors.setdefault("k1", {}))
+        k(f"k1:{name}", False)
+        k(f"push:{name}", True)
         x.push(r["send_ids"], r["send_rows"], r["dest_counts"], T)
+        k(f"push:{name}", False)
+        k(f"apply:{name}", True)
         x.merge_apply(tab.slab(), opt)
+        k(f"apply:{name}", False)
         rc = self._buf(name, "recv_counts", (n,), torch.int32)
         x.recv_counts(rc)
         pulled = self._buf(name, "pulled", (max(T, 1), D), torch.float32)
+        k(f"pull:{name}", True)
         x.pull(r["send_ids"], r["n_uniq"], T, tab.owner_dev, self.glob_base[name], tab.V, tab.P,
                pulled)
+        k(f"pull:{name}", False)
         out = self._buf(name, "out", (T, D), torch.float32)
+        k(f"stitch:{name}", True)
         ops.stitch(pulled, r["inv"], out)
+        k(f"stitch:{name}", False)
         self._pending_counts[name] = (r["dest_counts"], rc)
         return out
 
@@ -309,8 +320,10 @@ class HybridRunner:
             if out is None or out.numel() != g.numel() or out.dtype != self.dense_dtype:
                 out = g if self.dense_dtype == torch.float32 else torch.empty(
                     g.shape, dtype=self.dense_dtype, device=self.device)
+            self._kev(f"k7:{var.name}", True)
             self.dense_out[var.name] = ops.dense_allreduce_scale_cast(
                 self.comm.ptr if self.comm else None, g, out, self.scale)
+            self._kev(f"k7:{var.name}", False)
             ev("network")
         if self.world_size == 1 and self.concurrent_tables:
             # Tables are independent: each runs on its own stream (parallel
