@@ -199,17 +199,19 @@ int hp_xchg_create(hp_xchg_t* out, int32_t n, int32_t me, int32_t D, int64_t cap
                    int64_t rows_cap, void* ipc_handle_out, void** w_out);
 int hp_xchg_open_peer(hp_xchg_t x, int32_t rank, const void* ipc_handle);
 int hp_xchg_destroy(hp_xchg_t x);
-/* Worker: send blocks (send order, dest-major; from hp_sort_dedup_route) -> owners. */
-int hp_xchg_push(hp_xchg_t x, const int64_t* send_ids, const float* send_rows,
-                 const int32_t* dest_counts, int64_t T_bound, void* stream);
-/* Owner: wait for all pushes, merge in source order, apply to the slab, signal. */
+/* Worker, fused K1+K2+K3: dedup + route ids[T]/vals[T,D] and store every summed
+ * row straight into its owner's inbox (NVLink stores); publishes counts,
+ * offsets and the step epoch at every owner. Outputs: send_ids[U], inv[T],
+ * dest_counts[n], n_uniq[1] (device). ws sized by hp_dedup_ws_bytes. */
+int hp_xchg_push(hp_xchg_t x, const int64_t* ids, const float* vals, int64_t T, int64_t V,
+                 int32_t P, const int32_t* owner, int64_t* send_ids, int32_t* inv,
+                 int32_t* dest_counts, int32_t* n_uniq, void* ws, size_t ws_bytes, void* stream);
+/* Owner, fused K4+K5: wait for all pushes, merge in source order, apply to the
+ * slab, store each updated row back into its contributors' return buffers. */
 int hp_xchg_merge_apply(hp_xchg_t x, hp_slab slab, hp_optim opt, void* stream);
-/* Worker: wait for all applies, pulled[k] = updated row of send slot k
- * (glob_base[p] = slab row of partition p on its owner, device int64[P]). */
-int hp_xchg_pull(hp_xchg_t x, const int64_t* send_ids, const int32_t* n_uniq, int64_t T_bound,
-                 const int32_t* owner, const int64_t* glob_base, int64_t V, int32_t P,
-                 float* pulled, void* stream);
-/* Debug: the window's signal words (>= 200 int32) to host memory (syncs). */
+/* Worker K6: wait for all applies, out[t] = returned row of send slot inv[t]. */
+int hp_xchg_stitch(hp_xchg_t x, const int32_t* inv, int64_t T, float* out, void* stream);
+/* Debug: the window's signal words (320 int32) to host memory (syncs). */
 int hp_xchg_debug_sig(hp_xchg_t x, int32_t* host_out, void* stream);
 /* Rows received from each source in the last push -> device int32[n] (async). */
 int hp_xchg_recv_counts(hp_xchg_t x, int32_t* out_dev, void* stream);

@@ -1,0 +1,226 @@
+// Segmented row reduction kernels shared by the local (reduce.cu) and the
+// peer-memory (p2p.cu) paths; see reduce.cu for the summation tree.
+#pragma once
+
+#include "hp_dedup.cuh"
+
+namespace hp {
+
+// Epilogue contract:
+//   Pre load(dst, c4)            issued before the row loads (depends on the item only)
+//   void store(dst, c4, g, pre)  consumes the summed float4
+//   kRemote                      stores go to peer memory: every block fences at
+//                                system scope before exit and the last k_combine
+//                                block calls grid_done() (publication hook)
+
+// Epilogue interface: Pre load(dst, c4) is issued BEFORE the row loads (it
+// only depends on the item), store(dst, c4, g, pre) consumes the summed float4.
+struct EpiSend {
+  static constexpr bool kRemote = false;
+  float4* rows;
+  int D4;
+  struct Pre {};
+  __device__ __forceinline__ Pre load(int, int) const { return {}; }
+  __device__ __forceinline__ void store(int dst, int c4, float4 g, Pre) const {
+    rows[(int64_t)dst * D4 + c4] = g;
+  }
+};
+
+template <int OPT>
+struct EpiApply {
+  static constexpr bool kRemote = false;
+  float4* w;
+  float4* s0;
+  float4* s1;
+  hp_optim o;
+  int D4;
+  struct Pre {
+    float4 w, a, b;
+  };
+
+  __device__ __forceinline__ Pre load(int dst, int c4) const {
+    Pre p;
+    const int64_t off = (int64_t)dst * D4 + c4;
+    p.w = w[off];
+    p.a = p.b = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (OPT != HP_OPT_SGD) p.a = s0[off];
+    if (OPT == HP_OPT_ADAM) p.b = s1[off];
+    return p;
+  }
+
+  __device__ __forceinline__ void upd(float& wv, float& a, float& b, float g) const {
+    g = __fmul_rn(g, o.agg_scale);
+    if (OPT == HP_OPT_SGD) {
+      wv = __fsub_rn(wv, __fmul_rn(o.lr, g));
+    } else if (OPT == HP_OPT_ADAGRAD) {
+      a = __fadd_rn(a, __fmul_rn(g, g));
+      wv = __fsub_rn(wv, __fdiv_rn(__fmul_rn(o.lr, g), __fsqrt_rn(a)));
+    } else {
+      a = __fadd_rn(__fmul_rn(o.beta1, a), __fmul_rn(o.one_minus_beta1, g));
+      b = __fadd_rn(__fmul_rn(o.beta2, b), __fmul_rn(o.one_minus_beta2, __fmul_rn(g, g)));
+      wv = __fsub_rn(wv, __fdiv_rn(__fmul_rn(o.lr_t, a), __fadd_rn(__fsqrt_rn(b), o.eps)));
+    }
+  }
+
+  __device__ __forceinline__ void store(int dst, int c4, float4 g, Pre p) const {
+    upd(p.w.x, p.a.x, p.b.x, g.x);
+    upd(p.w.y, p.a.y, p.b.y, g.y);
+    upd(p.w.z, p.a.z, p.b.z, g.z);
+    upd(p.w.w, p.a.w, p.b.w, g.w);
+    const int64_t off = (int64_t)dst * D4 + c4;
+    w[off] = p.w;
+    if (OPT != HP_OPT_SGD) s0[off] = p.a;
+    if (OPT == HP_OPT_ADAM) s1[off] = p.b;
+  }
+};
+
+// Level 0 of the summation tree. A group of TPI threads owns an item
+// {j0, n <= HP_CHUNK, dst, final}; each thread owns VPT float4 columns
+// (c4 = lane-in-group + k*TPI). Row positions are loaded once per warp and
+// broadcast by shuffle; B rows x VPT columns are in flight per thread before
+// the in-order fp32 adds. Final items run the epilogue (its table-row loads
+// are issued together with the positions); long-segment chunks write a
+// partial row for k_combine. Small groups + <= 64 registers keep many items
+// in flight per SM: the kernel is latency-bound on the item chain
+// (descriptor -> positions/table rows -> gradient rows).
+template <int TPI, int VPT, int B, class Epi>
+__global__ void __launch_bounds__(256, 3)
+k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
+  const float4* __restrict__ vals = reinterpret_cast<const float4*>(vals_f);
+  float4* partials = reinterpret_cast<float4*>(pl.partials);
+  const int D4 = pl.D >> 2;
+  constexpr int GPB = 256 / TPI;
+  const int q = threadIdx.x % TPI;
+  const int lane = threadIdx.x & 31;
+  const int n_items = pl.counters[C_ITEMS];
+  for (int it = blockIdx.x * GPB + threadIdx.x / TPI; it < n_items; it += gridDim.x * GPB) {
+    const int4 item = pl.items[it];
+    const int j0 = item.x, n = item.y, dst = item.z;
+    const bool fin = item.w != 0;
+    typename Epi::Pre pre[VPT];
+#pragma unroll
+    for (int v = 0; v < VPT; ++v)
+      if (fin && dst >= 0 && q + v * TPI < D4) pre[v] = epi.load(dst, q + v * TPI);
+    const int myp = lane < n ? pl.sorted_pos[j0 + lane] : 0;
+    float4 acc[VPT];
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int jb = 0; jb < n; jb += B) {
+      float4 x[B][VPT];
+#pragma unroll
+      for (int e = 0; e < B; ++e) {
+        const int64_t rb = (int64_t)__shfl_sync(0xffffffffu, myp, jb + e) * D4;
+#pragma unroll
+        for (int v = 0; v < VPT; ++v)
+          if (jb + e < n && q + v * TPI < D4) x[e][v] = ldg_stream(vals + rb + q + v * TPI);
+      }
+#pragma unroll
+      for (int e = 0; e < B; ++e)
+#pragma unroll
+        for (int v = 0; v < VPT; ++v)
+          if (jb + e < n) acc[v] = f4_add(acc[v], x[e][v]);
+    }
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) {
+      const int c4 = q + v * TPI;
+      if (c4 >= D4) continue;
+      if (fin) {
+        if (dst >= 0) epi.store(dst, c4, acc[v], pre[v]);
+      } else {
+        partials[(int64_t)dst * D4 + c4] = acc[v];
+      }
+    }
+  }
+  if constexpr (Epi::kRemote) __threadfence_system();
+}
+
+// ((0 + r0) + r1) + ... over n <= HP_CHUNK rows of stride D4, 8 loads in flight.
+__device__ __forceinline__ float4 seq_sum_rows(const float4* src, int n, int D4) {
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int j0 = 0; j0 < n; j0 += 8) {
+    float4 x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j0 + j < n) x[j] = src[(int64_t)(j0 + j) * D4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j0 + j < n) acc = f4_add(acc, x[j]);
+  }
+  return acc;
+}
+
+// Upper levels for segments longer than HP_CHUNK: one CTA per long segment
+// {partial slot, n0, dst, u}, in place over its partial rows.
+template <class Epi>
+__global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
+  const int D4 = pl.D >> 2;
+  const int n_long = pl.counters[C_LONG];
+  float4* partials = reinterpret_cast<float4*>(pl.partials);
+  for (int li = blockIdx.x; li < n_long; li += gridDim.x) {
+    const int4 d = pl.longs[li];
+    int n = d.y;
+    float4* Pp = partials + (int64_t)d.x * D4;
+    while (n > HP_CHUNK) {
+      const int ng = (n + HP_CHUNK - 1) / HP_CHUNK;
+      const int units = ng * D4;
+      for (int ub = 0; ub < units; ub += blockDim.x) {
+        const int unit = ub + threadIdx.x;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        int g = 0, c4 = 0;
+        if (unit < units) {
+          g = unit / D4;
+          c4 = unit - g * D4;
+          const int e = min(HP_CHUNK, n - g * HP_CHUNK);
+          acc = seq_sum_rows(Pp + (int64_t)g * HP_CHUNK * D4 + c4, e, D4);
+        }
+        __syncthreads();
+        if (unit < units) Pp[(int64_t)g * D4 + c4] = acc;
+        __syncthreads();
+      }
+      n = ng;
+    }
+    for (int c4 = threadIdx.x; c4 < D4; c4 += blockDim.x) {
+      typename Epi::Pre pre{};
+      if (d.z >= 0) pre = epi.load(d.z, c4);
+      const float4 acc = seq_sum_rows(Pp + c4, n, D4);
+      if (d.z >= 0) epi.store(d.z, c4, acc, pre);
+    }
+    __syncthreads();
+  }
+  if constexpr (Epi::kRemote) {
+    __shared__ bool s_last;
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(epi.done, 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (s_last) {
+      __threadfence_system();
+      epi.grid_done();
+    }
+  }
+}
+
+template <int TPI, int VPT, class Epi>
+void launch_k_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaStream_t st) {
+  constexpr int B = VPT >= 8 ? 1 : 8 / VPT;
+  const int blocks = grid_for(pl.T, 256 / TPI, sm_count() * 16);  // <= one group per item
+  k_reduce<TPI, VPT, B, Epi><<<blocks, 256, 0, st>>>(pl, vals, epi);
+}
+
+template <class Epi>
+int launch_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaStream_t st) {
+  if (pl.T == 0) return HP_OK;
+  const int D4 = pl.D >> 2;
+  if (D4 <= 32) launch_k_reduce<32, 1>(pl, vals, epi, st);
+  else if (D4 <= 64) launch_k_reduce<32, 2>(pl, vals, epi, st);
+  else if (D4 <= 128) launch_k_reduce<64, 2>(pl, vals, epi, st);
+  else if (D4 <= 256) launch_k_reduce<64, 4>(pl, vals, epi, st);
+  else launch_k_reduce<128, 4>(pl, vals, epi, st);
+  HP_LAUNCHED(1, "k_reduce");
+  const int cblocks = grid_for(pl.T / HP_CHUNK + 1, 1, sm_count() * 2);
+  k_combine<Epi><<<cblocks, 256, 0, st>>>(pl, epi);
+  HP_LAUNCHED(1, "k_combine");
+  return HP_OK;
+}
+
+}  // namespace hp

@@ -166,6 +166,7 @@ class HybridRunner:
         self.last_counts: dict = {}
         self.kernel_events: dict | None = None
         self._streams = {n: torch.cuda.Stream(device=self.device) for n in self.tables}
+        self._dense_stream = torch.cuda.Stream(device=self.device)
         self._pending_counts: dict = {}
         self.concurrent_tables = True
 
@@ -200,26 +201,24 @@ class HybridRunner:
             raise SpecError(f"table {name!r}: {T} ids exceed the inbox capacity {x.cap} "
                             "(raise max_ids)")
         k = self._kev
-        k(f"k1:{name}", True)
-        r = ops.sort_dedup_route(ids, vals, tab.V, tab.P, tab.owner_dev, n, tab.ws,
-                                 out=self._scratch[name].tensors.setdefault("k1", {}))
-        k(f"k1:{name}", False)
+        bufs = self._scratch[name].tensors
+        if "p2p" not in bufs:
+            bufs["p2p"] = {"send_ids": torch.empty(x.cap, dtype=torch.int64, device=self.device),
+                           "inv": torch.empty(x.cap, dtype=torch.int32, device=self.device),
+                           "dest_counts": torch.empty(n, dtype=torch.int32, device=self.device),
+                           "n_uniq": torch.empty(1, dtype=torch.int32, device=self.device)}
+        r = bufs["p2p"]
         k(f"push:{name}", True)
-        x.push(r["send_ids"], r["send_rows"], r["dest_counts"], T)
+        x.push(ids, vals, tab.V, tab.P, tab.owner_dev, r, tab.ws)
         k(f"push:{name}", False)
         k(f"apply:{name}", True)
         x.merge_apply(tab.slab(), opt)
         k(f"apply:{name}", False)
         rc = self._buf(name, "recv_counts", (n,), torch.int32)
         x.recv_counts(rc)
-        pulled = self._buf(name, "pulled", (max(T, 1), D), torch.float32)
-        k(f"pull:{name}", True)
-        x.pull(r["send_ids"], r["n_uniq"], T, tab.owner_dev, self.glob_base[name], tab.V, tab.P,
-               pulled)
-        k(f"pull:{name}", False)
         out = self._buf(name, "out", (T, D), torch.float32)
         k(f"stitch:{name}", True)
-        ops.stitch(pulled, r["inv"], out)
+        x.stitch(r["inv"][:T], out)
         k(f"stitch:{name}", False)
         self._pending_counts[name] = (r["dest_counts"], rc)
         return out
@@ -314,47 +313,33 @@ class HybridRunner:
 
         ev("start")
         t0 = time.perf_counter()
-        for var in self.dense:
-            g = batch[var.name]
-            out = self.dense_out.get(var.name)
-            if out is None or out.numel() != g.numel() or out.dtype != self.dense_dtype:
-                out = g if self.dense_dtype == torch.float32 else torch.empty(
-                    g.shape, dtype=self.dense_dtype, device=self.device)
-            self._kev(f"k7:{var.name}", True)
-            self.dense_out[var.name] = ops.dense_allreduce_scale_cast(
-                self.comm.ptr if self.comm else None, g, out, self.scale)
-            self._kev(f"k7:{var.name}", False)
-            ev("network")
-        if self.world_size == 1 and self.concurrent_tables:
-            # Tables are independent: each runs on its own stream (parallel
-            # branches when the step is captured as a CUDA graph).
+        concurrent = self.concurrent_tables and (self.world_size == 1 or self.exchange == "p2p")
+        if concurrent:
+            # The dense allreduce and every table are independent: each runs on
+            # its own stream (parallel branches when captured as a CUDA graph).
+            # The reference serialises these phases; overlap
+            # is its named extension point.
             joins = []
+            if self.dense:
+                self._dense_stream.wait_stream(stream)
+                with torch.cuda.stream(self._dense_stream):
+                    self._dense(batch)
+                joins.append(self._dense_stream)
             for name, tab in self.tables.items():
-                ids, vals = batch[name]
-                tab.step_count += 1
-                opt = self.optimizer.c_struct(tab.step_count, self.scale)
                 side = self._streams[name]
                 side.wait_stream(stream)
                 with torch.cuda.stream(side):
-                    self.outputs[name] = self._sparse_local(tab, ids, vals, opt)
+                    self.outputs[name] = self._sparse(tab, batch[name])
                 joins.append(side)
             for side in joins:
                 stream.wait_stream(side)
-            if self.tables:
-                ev("update")
+            ev("network" if self.world_size > 1 else "update")
         else:
+            if self.dense:
+                self._dense(batch)
+                ev("network")
             for name, tab in self.tables.items():
-                ids, vals = batch[name]
-                tab.step_count += 1
-                opt = self.optimizer.c_struct(tab.step_count, self.scale)
-                if self.world_size == 1:
-                    self.outputs[name] = self._sparse_local(tab, ids, vals, opt)
-                    ev("update")
-                elif self.exchange == "p2p":
-                    self.outputs[name] = self._sparse_p2p(tab, ids, vals, opt)
-                    ev("network")
-                else:
-                    self.outputs[name] = self._sparse_exchange(tab, ids, vals, opt, ev)
+                self.outputs[name] = self._sparse(tab, batch[name], ev)
         if timed:
             stream.synchronize()
             for name, (sc, rc) in self._pending_counts.items():
@@ -366,6 +351,34 @@ class HybridRunner:
             iter_us = (time.perf_counter() - t0) * 1e6
         return IterationStats(iter_us, self._bytes_report(), phases, self._trace(),
                               {"step": self.step_count})
+
+    def _dense(self, batch: dict) -> None:
+        for var in self.dense:
+            g = batch[var.name]
+            out = self.dense_out.get(var.name)
+            if out is None or out.numel() != g.numel() or out.dtype != self.dense_dtype:
+                out = g if self.dense_dtype == torch.float32 else torch.empty(
+                    g.shape, dtype=self.dense_dtype, device=self.device)
+            self._kev(f"k7:{var.name}", True)
+            self.dense_out[var.name] = ops.dense_allreduce_scale_cast(
+                self.comm.ptr if self.comm else None, g, out, self.scale)
+            self._kev(f"k7:{var.name}", False)
+
+    def _sparse(self, tab: ShardedTable, ids_vals, ev=None) -> torch.Tensor:
+        ids, vals = ids_vals
+        tab.step_count += 1
+        opt = self.optimizer.c_struct(tab.step_count, self.scale)
+        if self.world_size == 1:
+            out = self._sparse_local(tab, ids, vals, opt)
+            if ev:
+                ev("update")
+        elif self.exchange == "p2p":
+            out = self._sparse_p2p(tab, ids, vals, opt)
+            if ev:
+                ev("network")
+        else:
+            out = self._sparse_exchange(tab, ids, vals, opt, ev or (lambda _p: None))
+        return out
 
     def _bytes_report(self) -> TransferReport:
         n = self.world_size

@@ -42,16 +42,23 @@ class PeerExchange:
                 call("hp_xchg_open_peer", self.handle, r, C.addressof(buf))
         self.w = torch.as_tensor(_DevPtr(wptr.value, (rows_cap, D)), device=device)
 
-    def push(self, send_ids, send_rows, dest_counts, T_bound: int) -> None:
-        call("hp_xchg_push", self.handle, send_ids.data_ptr(), send_rows.data_ptr(),
-             dest_counts.data_ptr(), T_bound, torch.cuda.current_stream().cuda_stream)
+    def push(self, ids, vals, V: int, P: int, owner, out: dict, ws) -> dict:
+        """Fused dedup + route + NVLink push; fills out[send_ids, inv, dest_counts, n_uniq]."""
+        from .ops import dedup_ws_bytes
+
+        T = ids.numel()
+        ws.get(dedup_ws_bytes(T, self.D, P, self.n))
+        call("hp_xchg_push", self.handle, ids.data_ptr(), vals.data_ptr(), T, V, P,
+             owner.data_ptr(), out["send_ids"].data_ptr(), out["inv"].data_ptr(),
+             out["dest_counts"].data_ptr(), out["n_uniq"].data_ptr(), ws.ptr, ws.nbytes,
+             torch.cuda.current_stream().cuda_stream)
+        return out
 
     def merge_apply(self, slab, opt) -> None:
         call("hp_xchg_merge_apply", self.handle, slab, opt, torch.cuda.current_stream().cuda_stream)
 
-    def pull(self, send_ids, n_uniq, T_bound: int, owner, glob_base, V: int, P: int, pulled) -> None:
-        call("hp_xchg_pull", self.handle, send_ids.data_ptr(), n_uniq.data_ptr(), T_bound,
-             owner.data_ptr(), glob_base.data_ptr(), V, P, pulled.data_ptr(),
+    def stitch(self, inv, out) -> None:
+        call("hp_xchg_stitch", self.handle, inv.data_ptr(), out.shape[0], out.data_ptr(),
              torch.cuda.current_stream().cuda_stream)
 
     def recv_counts(self, out) -> None:
@@ -59,13 +66,13 @@ class PeerExchange:
              torch.cuda.current_stream().cuda_stream)
 
     def debug_sig(self) -> dict:
-        buf = (C.c_int32 * 200)()
+        buf = (C.c_int32 * 320)()
         call("hp_xchg_debug_sig", self.handle, C.addressof(buf),
              torch.cuda.current_stream().cuda_stream)
         v = list(buf)
         return {"push_flag": v[:self.n], "push_count": v[64:64 + self.n],
                 "applied_flag": v[128:128 + self.n], "epoch": v[192], "err": v[193],
-                "done": v[196:200]}
+                "done": v[196:200], "push_off": v[256:256 + self.n]}
 
     def status(self) -> int:
         err = C.c_int32(0)
