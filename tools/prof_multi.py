@@ -30,6 +30,7 @@ for _ in range(3):
     runner.step(batch, timed=False)
 torch.cuda.synchronize()
 runner.kernel_events = {}
+runner.concurrent_tables = os.environ.get("HP_PROF_CONCURRENT", "0") == "1"
 for _ in range(10):
     torch.cuda._sleep(50_000_000)
     runner.step(batch, timed=False)
@@ -38,6 +39,9 @@ res = {}
 for key, evs in runner.kernel_events.items():
     d = [a.elapsed_time(c) * 1e3 for a, c in zip(evs[0::2], evs[1::2])]
     res[key] = round(float(np.median(d)), 1)
+runner.concurrent_tables = True
+for _ in range(3):
+    runner.step(batch, timed=False)
 stats = runner.step(batch, timed=True)
 out = [None] * world
 dist.all_gather_object(out, {"rank": rank, "us": res, "phases": stats.phase_times,
