@@ -206,6 +206,15 @@ int hp_xchg_destroy(hp_xchg_t x);
 int hp_xchg_push(hp_xchg_t x, const int64_t* ids, const float* vals, int64_t T, int64_t V,
                  int32_t P, const int32_t* owner, int64_t* send_ids, int32_t* inv,
                  int32_t* dest_counts, int32_t* n_uniq, void* ws, size_t ws_bytes, void* stream);
+/* The two halves of hp_xchg_push (so a plan can be built ahead of its step):
+ * hp_xchg_plan dedups/routes ids into a send plan in ws; hp_xchg_push_plan
+ * reduces vals with that plan and pushes (same T / V / P / ws). */
+int hp_xchg_plan(hp_xchg_t x, const int64_t* ids, int64_t T, int64_t V, int32_t P,
+                 const int32_t* owner, int64_t* send_ids, int32_t* inv, int32_t* dest_counts,
+                 int32_t* n_uniq, void* ws, size_t ws_bytes, void* stream);
+int hp_xchg_push_plan(hp_xchg_t x, const float* vals, int64_t T, int64_t V, int32_t P,
+                      const int64_t* send_ids, const int32_t* dest_counts, void* ws,
+                      size_t ws_bytes, void* stream);
 /* Owner, fused K4+K5: wait for all pushes, merge in source order, apply to the
  * slab, store each updated row back into its contributors' return buffers. */
 int hp_xchg_merge_apply(hp_xchg_t x, hp_slab slab, hp_optim opt, void* stream);

@@ -772,6 +772,18 @@ int launch_cluster(const DedupPlan& pl, const int64_t* ids, const int32_t* owner
   }
 }
 
+// Which ping-pong buffer holds the sorted positions of a plan built by
+// build_plan with the same (T, P, V): the cluster path writes pos[0]; the
+// multi-kernel path leaves them in pos[passes & 1].
+void restore_sorted_pos(DedupPlan& pl) {
+  if (pl.T <= HP_SMALL_MAX && pl.P <= CL_PMAX) {
+    pl.sorted_pos = pl.pos[0];
+  } else {
+    const int passes = (pl.key_bits + HP_RADIX_BITS - 1) / HP_RADIX_BITS;
+    pl.sorted_pos = pl.pos[passes & 1];
+  }
+}
+
 int build_plan(DedupPlan& pl, const int64_t* ids, const int32_t* owner,
                const int64_t* dst_pb, int64_t* send_ids, int32_t* counts, int32_t* inv,
                int32_t* dest_counts, int32_t* n_uniq, cudaStream_t st) {

@@ -53,4 +53,7 @@ int build_plan(DedupPlan& pl, const int64_t* ids, const int32_t* owner,
                const int64_t* dst_part_base, int64_t* send_ids, int32_t* counts, int32_t* inv,
                int32_t* dest_counts, int32_t* n_uniq, cudaStream_t stream);
 
+// Re-point pl.sorted_pos at the buffer a previous build_plan (same T, P, V) left it in.
+void restore_sorted_pos(DedupPlan& pl);
+
 }  // namespace hp

@@ -348,27 +348,47 @@ int hp_xchg_destroy(hp_xchg_t x) {
   return HP_OK;
 }
 
-// Worker, fused K1+K2+K3: dedup + route the IndexedSlices and store every summed
-// row straight into its owner's inbox; publishes counts / offsets / epoch.
-// send_ids[U], inv[T] (send slot per position), dest_counts[n], n_uniq are
-// device outputs.
-int hp_xchg_push(hp_xchg_t x, const int64_t* ids, const float* vals, int64_t T, int64_t V,
-                 int32_t P, const int32_t* owner, int64_t* send_ids, int32_t* inv,
-                 int32_t* dest_counts, int32_t* n_uniq, void* ws, size_t ws_bytes, void* stream) {
+// Worker K1+K2 (index half of hp_xchg_push): dedup + route ids[T] into a send
+// plan left in ws; outputs send_ids[U], inv[T], dest_counts[n], n_uniq.
+int hp_xchg_plan(hp_xchg_t x, const int64_t* ids, int64_t T, int64_t V, int32_t P,
+                 const int32_t* owner, int64_t* send_ids, int32_t* inv, int32_t* dest_counts,
+                 int32_t* n_uniq, void* ws, size_t ws_bytes, void* stream) {
   HP_REQUIRE(x && owner && send_ids && inv && dest_counts && n_uniq, "NULL argument");
   HP_REQUIRE(T <= x->L.cap, "more ids than the inbox capacity");
-  HP_REQUIRE(T == 0 || (ids && vals), "NULL ids / vals");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  HP_REQUIRE(T == 0 || ids, "NULL ids");
   DedupPlan pl;
   int rc = carve_plan(&pl, ws, ws_bytes, T, x->L.D4 * 4, V, P, x->L.n);
   if (rc) return rc;
-  if ((rc = build_plan(pl, ids, owner, nullptr, send_ids, nullptr, inv, dest_counts, n_uniq, st)))
-    return rc;
+  return build_plan(pl, ids, owner, nullptr, send_ids, nullptr, inv, dest_counts, n_uniq,
+                    static_cast<cudaStream_t>(stream));
+}
+
+// Worker K1 values + K3, fused: with the plan in ws (hp_xchg_plan, same T / V / P),
+// reduce vals[T, D] and store every summed row straight into its owner's inbox
+// over NVLink; the last block publishes counts / offsets / epoch at every owner.
+int hp_xchg_push_plan(hp_xchg_t x, const float* vals, int64_t T, int64_t V, int32_t P,
+                      const int64_t* send_ids, const int32_t* dest_counts, void* ws,
+                      size_t ws_bytes, void* stream) {
+  HP_REQUIRE(x && send_ids && dest_counts, "NULL argument");
+  HP_REQUIRE(T == 0 || vals, "NULL vals");
+  DedupPlan pl;
+  int rc = carve_plan(&pl, ws, ws_bytes, T, x->L.D4 * 4, V, P, x->L.n);
+  if (rc) return rc;
+  restore_sorted_pos(pl);
   SigView me(x->win);
   EpiPush epi{x->peers, x->L, dest_counts, send_ids, me.done + 0, x->win};
-  DedupPlan p2 = pl;
-  p2.T = std::max<int64_t>(T, 1);  // k_combine must run: it carries the publication
-  return launch_reduce(p2, vals, epi, st);
+  pl.T = std::max<int64_t>(T, 1);  // k_combine must run: it carries the publication
+  return launch_reduce(pl, vals, epi, static_cast<cudaStream_t>(stream));
+}
+
+// Worker, fused K1+K2+K3 = hp_xchg_plan + hp_xchg_push_plan.
+int hp_xchg_push(hp_xchg_t x, const int64_t* ids, const float* vals, int64_t T, int64_t V,
+                 int32_t P, const int32_t* owner, int64_t* send_ids, int32_t* inv,
+                 int32_t* dest_counts, int32_t* n_uniq, void* ws, size_t ws_bytes, void* stream) {
+  int rc = hp_xchg_plan(x, ids, T, V, P, owner, send_ids, inv, dest_counts, n_uniq, ws, ws_bytes,
+                        stream);
+  if (rc) return rc;
+  return hp_xchg_push_plan(x, vals, T, V, P, send_ids, dest_counts, ws, ws_bytes, stream);
 }
 
 // Owner: wait for every source's push, merge in source order, apply to the

@@ -122,11 +122,7 @@ int hp_apply_plan(const float* rows, int64_t R, hp_slab slab, hp_optim opt, void
   DedupPlan pl;
   if ((rc = carve_plan(&pl, ws, ws_bytes, R, slab.D, slab.V, slab.P, 1))) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  // the radix sort leaves the positions in pos[passes & 1] on the large path
-  if (R > HP_SMALL_MAX) {
-    const int passes = (pl.key_bits + HP_RADIX_BITS - 1) / HP_RADIX_BITS;
-    pl.sorted_pos = pl.pos[passes & 1];
-  }
+  restore_sorted_pos(pl);
   return apply_plan(pl, rows, slab, opt, st);
 }
 

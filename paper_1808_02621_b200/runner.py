@@ -70,8 +70,15 @@ class ShardedTable:
         elif optimizer.kind == "adam":
             for s in self.state:
                 s.zero_()
-        self.ws = Workspace(self.device)
+        # two plan workspaces: the plan of step i+1 is built while step i applies
+        self.wss = [Workspace(self.device), Workspace(self.device)]
+        self.ready = None       # slot holding a prefetched plan, or None
+        self.ready_ids = None   # the ids tensor that plan was built from
         self.step_count = 0
+
+    @property
+    def ws(self) -> Workspace:
+        return self.wss[0]
 
     def partition(self, p: int) -> torch.Tensor:
         """Partition p as its own [rows_p, D] array (view into the slab)."""
@@ -167,6 +174,7 @@ class HybridRunner:
         self.kernel_events: dict | None = None
         self._streams = {n: torch.cuda.Stream(device=self.device) for n in self.tables}
         self._dense_stream = torch.cuda.Stream(device=self.device)
+        self._plan_streams = {n: torch.cuda.Stream(device=self.device) for n in self.tables}
         self._pending_counts: dict = {}
         self.concurrent_tables = True
 
@@ -193,7 +201,8 @@ class HybridRunner:
         self.glob_base[var.name] = torch.from_numpy(gb).to(self.device)
         return lambda nrows: x.w[:nrows]
 
-    def _sparse_p2p(self, tab: ShardedTable, ids, vals, opt) -> torch.Tensor:
+    def _sparse_p2p(self, tab: ShardedTable, ids, vals, opt, slot: int = 0,
+                    planned: bool = False) -> torch.Tensor:
         n, D, T = self.world_size, tab.D, ids.numel()
         name = tab.name
         x = self.xchg[name]
@@ -201,15 +210,11 @@ class HybridRunner:
             raise SpecError(f"table {name!r}: {T} ids exceed the inbox capacity {x.cap} "
                             "(raise max_ids)")
         k = self._kev
-        bufs = self._scratch[name].tensors
-        if "p2p" not in bufs:
-            bufs["p2p"] = {"send_ids": torch.empty(x.cap, dtype=torch.int64, device=self.device),
-                           "inv": torch.empty(x.cap, dtype=torch.int32, device=self.device),
-                           "dest_counts": torch.empty(n, dtype=torch.int32, device=self.device),
-                           "n_uniq": torch.empty(1, dtype=torch.int32, device=self.device)}
-        r = bufs["p2p"]
+        r = self._p2p_bufs(tab, slot)
+        if not planned:
+            self._plan(tab, ids, slot)
         k(f"push:{name}", True)
-        x.push(ids, vals, tab.V, tab.P, tab.owner_dev, r, tab.ws)
+        x.push_plan(vals, tab.V, tab.P, r, tab.wss[slot])
         k(f"push:{name}", False)
         k(f"apply:{name}", True)
         x.merge_apply(tab.slab(), opt)
@@ -250,12 +255,33 @@ class HybridRunner:
         e.record(torch.cuda.current_stream())
         self.kernel_events.setdefault(key, []).append(e)
 
-    def _sparse_local(self, tab: ShardedTable, ids, vals, opt) -> torch.Tensor:
+    def _plan(self, tab: ShardedTable, ids, slot: int) -> None:
+        """Index half of the step (dedup + route) into plan slot ``slot``."""
+        if self.world_size == 1:
+            ops.apply_plan_build(ids, tab.slab(), tab.wss[slot])
+        else:
+            self.xchg[tab.name].plan(ids, tab.V, tab.P, tab.owner_dev,
+                                     self._p2p_bufs(tab, slot), tab.wss[slot])
+
+    def _p2p_bufs(self, tab: ShardedTable, slot: int) -> dict:
+        bufs = self._scratch[tab.name].tensors
+        key = f"p2p{slot}"
+        if key not in bufs:
+            cap, n = self.xchg[tab.name].cap, self.world_size
+            bufs[key] = {"send_ids": torch.empty(cap, dtype=torch.int64, device=self.device),
+                         "inv": torch.empty(cap, dtype=torch.int32, device=self.device),
+                         "dest_counts": torch.empty(n, dtype=torch.int32, device=self.device),
+                         "n_uniq": torch.empty(1, dtype=torch.int32, device=self.device)}
+        return bufs[key]
+
+    def _sparse_local(self, tab: ShardedTable, ids, vals, opt, slot: int = 0,
+                      planned: bool = False) -> torch.Tensor:
         T = ids.numel()
         slab = tab.slab()
-        ops.apply_plan_build(ids, slab, tab.ws)
+        if not planned:
+            self._plan(tab, ids, slot)
         self._kev(f"k4:{tab.name}", True)
-        ops.apply_plan(vals, T, slab, opt, tab.ws)
+        ops.apply_plan(vals, T, slab, opt, tab.wss[slot])
         self._kev(f"k4:{tab.name}", False)
         out = self._buf(tab.name, "out", (T, tab.D), torch.float32)
         self._kev(f"k5:{tab.name}", True)
@@ -292,13 +318,18 @@ class HybridRunner:
         self.last_counts[name] = {"send": send_c, "recv": recv_c}
         return out
 
-    def step(self, batch: dict, timed: bool = True) -> IterationStats:
+    def step(self, batch: dict, timed: bool = True, next_batch: dict | None = None) -> IterationStats:
         """One synchronous hybrid step.
 
         ``batch[name]`` is ``(ids int64[T], vals f32[T, D])`` for a sparse Weight
         and an fp32 gradient tensor for a dense one (all on this GPU). Pulled
         rows land in ``self.outputs[name]``; averaged dense gradients in
         ``self.dense_out[name]``.
+
+        ``next_batch`` (optional): the batch of the following step. Its dedup /
+        routing plan (which depends only on its ids) is built on a side stream
+        while this step applies, into the other plan slot; the following
+        ``step(next_batch)`` then skips its dedup. Results are identical.
         """
         self.step_count += 1
         stream = torch.cuda.current_stream()
@@ -328,9 +359,22 @@ class HybridRunner:
             for name, tab in self.tables.items():
                 side = self._streams[name]
                 side.wait_stream(stream)
+                free = None
                 with torch.cuda.stream(side):
+                    if next_batch is not None and self.pipelined:
+                        free = torch.cuda.Event()
+                        free.record(side)  # the other plan slot is no longer read
                     self.outputs[name] = self._sparse(tab, batch[name])
                 joins.append(side)
+                if free is not None:
+                    ps = self._plan_streams[name]
+                    ps.wait_stream(stream)
+                    ps.wait_event(free)
+                    nxt = tab.last_slot ^ 1
+                    with torch.cuda.stream(ps):
+                        self._plan(tab, next_batch[name][0], nxt)
+                    tab.ready, tab.ready_ids = nxt, next_batch[name][0]
+                    joins.append(ps)
             for side in joins:
                 stream.wait_stream(side)
             ev("network" if self.world_size > 1 else "update")
@@ -368,17 +412,34 @@ class HybridRunner:
         ids, vals = ids_vals
         tab.step_count += 1
         opt = self.optimizer.c_struct(tab.step_count, self.scale)
+        planned = tab.ready is not None and tab.ready_ids is ids
+        slot = tab.ready if planned else 0
+        tab.ready = tab.ready_ids = None
         if self.world_size == 1:
-            out = self._sparse_local(tab, ids, vals, opt)
+            out = self._sparse_local(tab, ids, vals, opt, slot, planned)
             if ev:
                 ev("update")
         elif self.exchange == "p2p":
-            out = self._sparse_p2p(tab, ids, vals, opt)
+            out = self._sparse_p2p(tab, ids, vals, opt, slot, planned)
             if ev:
                 ev("network")
         else:
             out = self._sparse_exchange(tab, ids, vals, opt, ev or (lambda _p: None))
+        tab.last_slot = slot
         return out
+
+    @property
+    def pipelined(self) -> bool:
+        return self.world_size == 1 or self.exchange == "p2p"
+
+    def prefetch(self, batch: dict) -> None:
+        """Build the plans of ``batch`` now (stream-ordered) so its step skips dedup."""
+        if not self.pipelined:
+            return
+        for name, tab in self.tables.items():
+            ids = batch[name][0]
+            self._plan(tab, ids, 0)
+            tab.ready, tab.ready_ids = 0, ids
 
     def _bytes_report(self) -> TransferReport:
         n = self.world_size
@@ -417,6 +478,8 @@ class HybridRunner:
         """
         if self.world_size > 1 and self.exchange != "p2p":
             raise NotImplementedError("the NCCL a2a-v path reads counts on the host")
+        for tab in self.tables.values():
+            tab.ready = tab.ready_ids = None
         cur = torch.cuda.current_stream()
         side = torch.cuda.Stream(device=self.device)
         side.wait_stream(cur)
@@ -428,6 +491,30 @@ class HybridRunner:
         with torch.cuda.graph(g):
             self.step(batch, timed=False)
         return g
+
+    def capture_pipelined(self, batches: list) -> list:
+        """One CUDA graph per batch of a rotation: graph r applies batches[r]
+        with the plan built by graph r-1 and builds the plan of batches[r+1].
+
+        Replay them in order, repeatedly. ``len(batches)`` must be even (the
+        plan slots alternate). The first plan is built eagerly here.
+        """
+        R = len(batches)
+        if R < 2 or R % 2:
+            raise ValueError("capture_pipelined needs an even number (>= 2) of batches")
+        if not self.pipelined:
+            raise NotImplementedError("the NCCL a2a-v path reads counts on the host")
+        self.prefetch(batches[0])
+        for r in range(R):  # eager warm-up rotation (sizes every buffer)
+            self.step(batches[r], timed=False, next_batch=batches[(r + 1) % R])
+        torch.cuda.synchronize()
+        graphs = []
+        for r in range(R):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.step(batches[r], timed=False, next_batch=batches[(r + 1) % R])
+            graphs.append(g)
+        return graphs
 
     # ------------------------------------------------------------------ timing / P search
     def measure(self, make_batch, iterations: int = 100) -> float:

@@ -54,6 +54,23 @@ class PeerExchange:
              torch.cuda.current_stream().cuda_stream)
         return out
 
+    def plan(self, ids, V: int, P: int, owner, out: dict, ws) -> dict:
+        """Index half of push: dedup + route into a send plan in ``ws``."""
+        from .ops import dedup_ws_bytes
+
+        T = ids.numel()
+        ws.get(dedup_ws_bytes(T, self.D, P, self.n))
+        call("hp_xchg_plan", self.handle, ids.data_ptr(), T, V, P, owner.data_ptr(),
+             out["send_ids"].data_ptr(), out["inv"].data_ptr(), out["dest_counts"].data_ptr(),
+             out["n_uniq"].data_ptr(), ws.ptr, ws.nbytes, torch.cuda.current_stream().cuda_stream)
+        return out
+
+    def push_plan(self, vals, V: int, P: int, out: dict, ws) -> None:
+        """Value half of push: reduce with the plan in ``ws`` and store into owners' inboxes."""
+        call("hp_xchg_push_plan", self.handle, vals.data_ptr(), vals.shape[0], V, P,
+             out["send_ids"].data_ptr(), out["dest_counts"].data_ptr(), ws.ptr, ws.nbytes,
+             torch.cuda.current_stream().cuda_stream)
+
     def merge_apply(self, slab, opt) -> None:
         call("hp_xchg_merge_apply", self.handle, slab, opt, torch.cuda.current_stream().cuda_stream)
 

@@ -47,13 +47,18 @@ def main():
     states = {t.name: orc.init_state(opt_kind, t.V, t.D, 5 * 1000 + i + 1, 0.1)
               for i, t in enumerate(wl.tables)}
     ok, why = True, []
+    def to_dev(b):
+        return {k: ((torch.from_numpy(v[0]).to(dev), torch.from_numpy(v[1]).to(dev))
+                    if isinstance(v, tuple) else torch.from_numpy(v).to(dev)) for k, v in b.items()}
+
+    staged = {s: to_dev(make_batch(wl, seed=s, rank=rank)) for s in (1, 2, 3)}
+    if xmode == "p2p":
+        runner.prefetch(staged[1])  # steps 1-3 run pipelined (plan of step s+1 built during s)
     for step in (1, 2, 3):
         batches = [make_batch(wl, seed=step, rank=r) for r in range(world)]
         mine = batches[rank]
-        batch = {k: ((torch.from_numpy(v[0]).to(dev), torch.from_numpy(v[1]).to(dev))
-                     if isinstance(v, tuple) else torch.from_numpy(v).to(dev))
-                 for k, v in mine.items()}
-        stats = runner.step(batch)
+        batch = staged[step]
+        stats = runner.step(batch, next_batch=staged.get(step + 1) if xmode == "p2p" else None)
         for t in wl.tables:
             owner = plan.owner_table(t.name)
             orc.sparse_step(states[t.name], opt_kind, hpar, step, [b[t.name] for b in batches],
