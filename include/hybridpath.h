@@ -215,11 +215,15 @@ int hp_xchg_plan(hp_xchg_t x, const int64_t* ids, int64_t T, int64_t V, int32_t 
 int hp_xchg_push_plan(hp_xchg_t x, const float* vals, int64_t T, int64_t V, int32_t P,
                       const int64_t* send_ids, const int32_t* dest_counts, void* ws,
                       size_t ws_bytes, void* stream);
-/* Owner, fused K4+K5: wait for all pushes, merge in source order, apply to the
+/* Wait (one spinning block, bounded) until every source pushed (which = 0) or
+ * every owner applied (which = 1) for this rank's current epoch. */
+int hp_xchg_wait(hp_xchg_t x, int32_t which, void* stream);
+/* Owner, fused K4+K5: (wait for all pushes,) merge in source order, apply to the
  * slab, store each updated row back into its contributors' return buffers. */
-int hp_xchg_merge_apply(hp_xchg_t x, hp_slab slab, hp_optim opt, void* stream);
-/* Worker K6: wait for all applies, out[t] = returned row of send slot inv[t]. */
-int hp_xchg_stitch(hp_xchg_t x, const int32_t* inv, int64_t T, float* out, void* stream);
+int hp_xchg_merge_apply(hp_xchg_t x, hp_slab slab, hp_optim opt, int32_t wait, void* stream);
+/* Worker K6: (wait for all applies,) out[t] = returned row of send slot inv[t]. */
+int hp_xchg_stitch(hp_xchg_t x, const int32_t* inv, int64_t T, float* out, int32_t wait,
+                   void* stream);
 /* Debug: the window's signal words (320 int32) to host memory (syncs). */
 int hp_xchg_debug_sig(hp_xchg_t x, int32_t* host_out, void* stream);
 /* Rows received from each source in the last push -> device int32[n] (async). */

@@ -393,11 +393,21 @@ int hp_xchg_push(hp_xchg_t x, const int64_t* ids, const float* vals, int64_t T, 
 
 // Owner: wait for every source's push, merge in source order, apply to the
 // slab, return the updated rows to the contributors, signal "applied".
-int hp_xchg_merge_apply(hp_xchg_t x, hp_slab slab, hp_optim opt, void* stream) {
+int hp_xchg_wait(hp_xchg_t x, int32_t which, void* stream) {
+  HP_REQUIRE(x && (which == 0 || which == 1), "bad wait arguments");
+  k_wait<<<1, 64, 0, static_cast<cudaStream_t>(stream)>>>(x->win, which, x->L.n, wait_budget());
+  HP_LAUNCHED(1, "k_wait");
+  return HP_OK;
+}
+
+int hp_xchg_merge_apply(hp_xchg_t x, hp_slab slab, hp_optim opt, int32_t wait, void* stream) {
   HP_REQUIRE(x && slab.part_base, "NULL argument");
   HP_REQUIRE(slab.D == x->L.D4 * 4, "slab width differs from the exchange");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  k_wait<<<1, 64, 0, st>>>(x->win, 0, x->L.n, wait_budget());
+  if (wait) {
+    int rc = hp_xchg_wait(x, 0, stream);
+    if (rc) return rc;
+  }
   const int64_t total = (int64_t)x->L.n * x->L.cap;
   k_owner_scatter<<<grid_for(total, 256, sm_count() * 8), 256, 0, st>>>(
       x->win, x->L, slab.part_base, Router(slab.V, slab.P), x->slot, x->touch, x->list, x->nlist,
@@ -419,16 +429,18 @@ int hp_xchg_merge_apply(hp_xchg_t x, hp_slab slab, hp_optim opt, void* stream) {
       k_owner_apply<HP_OPT_ADAM><<<blocks, 256, 0, st>>>(x->peers, x->win, x->L, s0, s1, opt,
                                                         x->slot, x->touch, x->list, x->nlist);
   }
-  HP_LAUNCHED(3, "owner merge/apply");
+  HP_LAUNCHED(2, "owner merge/apply");
   return HP_OK;
 }
 
 // Worker: wait for every owner's apply, then out[t] = returned row of send slot inv[t].
-int hp_xchg_stitch(hp_xchg_t x, const int32_t* inv, int64_t T, float* out, void* stream) {
+int hp_xchg_stitch(hp_xchg_t x, const int32_t* inv, int64_t T, float* out, int32_t wait,
+                   void* stream) {
   HP_REQUIRE(x && inv && out, "NULL argument");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  k_wait<<<1, 64, 0, st>>>(x->win, 1, x->L.n, wait_budget());
-  HP_LAUNCHED(1, "k_wait");
+  if (wait) {
+    int rc = hp_xchg_wait(x, 1, stream);
+    if (rc) return rc;
+  }
   const float* ret = reinterpret_cast<const float*>(static_cast<char*>(x->win) + x->L.ret_off);
   return hp_stitch(ret, inv, T, x->L.D4 * 4, out, stream);
 }

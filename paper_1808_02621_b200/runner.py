@@ -216,14 +216,20 @@ class HybridRunner:
         k(f"push:{name}", True)
         x.push_plan(vals, tab.V, tab.P, r, tab.wss[slot])
         k(f"push:{name}", False)
+        k(f"wait_push:{name}", True)
+        x.wait(0)
+        k(f"wait_push:{name}", False)
         k(f"apply:{name}", True)
-        x.merge_apply(tab.slab(), opt)
+        x.merge_apply(tab.slab(), opt, wait=False)
         k(f"apply:{name}", False)
         rc = self._buf(name, "recv_counts", (n,), torch.int32)
         x.recv_counts(rc)
         out = self._buf(name, "out", (T, D), torch.float32)
+        k(f"wait_applied:{name}", True)
+        x.wait(1)
+        k(f"wait_applied:{name}", False)
         k(f"stitch:{name}", True)
-        x.stitch(r["inv"][:T], out)
+        x.stitch(r["inv"][:T], out, wait=False)
         k(f"stitch:{name}", False)
         self._pending_counts[name] = (r["dest_counts"], rc)
         return out

@@ -71,12 +71,17 @@ class PeerExchange:
              out["send_ids"].data_ptr(), out["dest_counts"].data_ptr(), ws.ptr, ws.nbytes,
              torch.cuda.current_stream().cuda_stream)
 
-    def merge_apply(self, slab, opt) -> None:
-        call("hp_xchg_merge_apply", self.handle, slab, opt, torch.cuda.current_stream().cuda_stream)
+    def wait(self, which: int) -> None:
+        """0: until every source pushed; 1: until every owner applied."""
+        call("hp_xchg_wait", self.handle, which, torch.cuda.current_stream().cuda_stream)
 
-    def stitch(self, inv, out) -> None:
-        call("hp_xchg_stitch", self.handle, inv.data_ptr(), out.shape[0], out.data_ptr(),
+    def merge_apply(self, slab, opt, wait: bool = True) -> None:
+        call("hp_xchg_merge_apply", self.handle, slab, opt, int(wait),
              torch.cuda.current_stream().cuda_stream)
+
+    def stitch(self, inv, out, wait: bool = True) -> None:
+        call("hp_xchg_stitch", self.handle, inv.data_ptr(), out.shape[0], out.data_ptr(),
+             int(wait), torch.cuda.current_stream().cuda_stream)
 
     def recv_counts(self, out) -> None:
         call("hp_xchg_recv_counts", self.handle, out.data_ptr(),

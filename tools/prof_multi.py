@@ -26,13 +26,17 @@ runner = hp.HybridRunner(plan, graph, cluster, rank=rank, world_size=world, comm
 b = make_batch(wl, seed=1, rank=rank)
 batch = {k: ((torch.from_numpy(v[0]).to(dev), torch.from_numpy(v[1]).to(dev))
              if isinstance(v, tuple) else torch.from_numpy(v).to(dev)) for k, v in b.items()}
+b2 = make_batch(wl, seed=2, rank=rank)
+batch2 = {k: ((torch.from_numpy(v[0]).to(dev), torch.from_numpy(v[1]).to(dev))
+              if isinstance(v, tuple) else torch.from_numpy(v).to(dev)) for k, v in b2.items()}
 for _ in range(3):
     runner.step(batch, timed=False)
 torch.cuda.synchronize()
 runner.kernel_events = {}
 runner.concurrent_tables = os.environ.get("HP_PROF_CONCURRENT", "0") == "1"
-for _ in range(10):
+for i in range(10):
     torch.cuda._sleep(50_000_000)
+    dist.barrier()
     runner.step(batch, timed=False)
 torch.cuda.synchronize()
 res = {}
