@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"])
+    ap.add_argument("--dense-exchange", default=None, choices=["p2p", "nccl"])
     return ap.parse_args()
 
 
@@ -209,7 +210,8 @@ def main():
     plan = hp.transform_hybrid(graph, cluster, partitions={t.name: P for t in wl.tables})
     opt = hp.OptimizerConfig(**wl.optimizer)
     runner = hp.HybridRunner(plan, graph, cluster, rank=rank, world_size=world, comm=comm,
-                             optimizer=opt, device=dev, seed=0, exchange=args.exchange)
+                             optimizer=opt, device=dev, seed=0, exchange=args.exchange,
+                             dense_exchange=args.dense_exchange)
 
     # resident batches, rotated so their total exceeds 2x L2 (126 MB)
     host = [make_batch(wl, seed=1 + i, rank=rank) for i in range(1)]
@@ -373,7 +375,8 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (Zipf(1.1) ids, normal grads, hash-initialised tables)",
             "config": config(args, wl) | {"rotations": R, "cuda_graph": bool(graphs),
-                                          "exchange": runner.exchange},
+                                          "exchange": runner.exchange,
+                                          "dense_exchange": runner.dense_exchange},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": ke},
             "gpu_launches": launches_per_step * args.steps,

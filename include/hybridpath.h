@@ -231,6 +231,20 @@ int hp_xchg_recv_counts(hp_xchg_t x, int32_t* out_dev, void* stream);
 /* Error bits (4/8: a wait timed out, 16: a received id is not homed here). */
 int hp_xchg_status(hp_xchg_t x, int32_t* out_err, void* stream);
 
+/* ---------------------------------------------------------------- K7 over NVLink
+ * Dense allreduce fused with scale + cast, over peer memory: every rank stores
+ * its chunks into the owners' reduce slots; each owner sums its chunk in
+ * source-rank order (deterministic), scales, casts and stores the result into
+ * every rank's output. Replaces: ring / hierarchical AllReduce
+ * (`simulate.py:97-135,243-261`); the NCCL path stays as the baseline. */
+typedef struct hp_dar_s* hp_dar_t;
+int hp_dar_create(hp_dar_t* out, int32_t n, int32_t me, int64_t S, int32_t out_dtype,
+                  void* ipc_handle_out, void** out_ptr);
+int hp_dar_open_peer(hp_dar_t d, int32_t rank, const void* ipc_handle);
+int hp_dar_destroy(hp_dar_t d);
+int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream);
+int hp_dar_status(hp_dar_t d, int32_t* out_err, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -72,6 +72,11 @@ SIGNATURES = {
     "hp_xchg_stitch": (C.c_int, [vp, vp, i64, vp, i32, vp]),
     "hp_xchg_status": (C.c_int, [vp, vp, vp]),
     "hp_xchg_recv_counts": (C.c_int, [vp, vp, vp]),
+    "hp_dar_create": (C.c_int, [C.POINTER(vp), i32, i32, i64, i32, vp, C.POINTER(vp)]),
+    "hp_dar_open_peer": (C.c_int, [vp, i32, vp]),
+    "hp_dar_destroy": (C.c_int, [vp]),
+    "hp_dar_allreduce": (C.c_int, [vp, vp, f32, vp]),
+    "hp_dar_status": (C.c_int, [vp, vp, vp]),
     "hp_xchg_debug_sig": (C.c_int, [vp, vp, vp]),
 }
 

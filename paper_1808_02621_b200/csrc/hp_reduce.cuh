@@ -203,7 +203,9 @@ __global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
 template <int TPI, int VPT, class Epi>
 void launch_k_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaStream_t st) {
   constexpr int B = VPT >= 8 ? 1 : 8 / VPT;
-  const int blocks = grid_for(pl.T, 256 / TPI, sm_count() * 16);  // <= one group per item
+  // <= one group per item; peer-store epilogues stay in one resident wave so
+  // each block pays its system-scope fence once
+  const int blocks = grid_for(pl.T, 256 / TPI, sm_count() * (Epi::kRemote ? 3 : 16));
   k_reduce<TPI, VPT, B, Epi><<<blocks, 256, 0, st>>>(pl, vals, epi);
 }
 

@@ -29,6 +29,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cuda_bf16.h>
+
 #include "hp_reduce.cuh"
 
 namespace hp {
@@ -198,15 +200,22 @@ k_owner_apply(PeerTable peers, void* my_win, WinLayout L, float4* s0, float4* s1
   const int nw = gridDim.x * (blockDim.x >> 5);
   for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nl; k += nw) {
     const int64_t row = list[k];
-    // contributions in source order (lane s holds source s's inbox index)
+    // contributions in source order: lane j (< cnt) holds the j-th contributor's
+    // inbox index, taken from the slot-table lane of that source
     const int mine = lane < n ? slot[row * n + lane] : -1;
     const unsigned have = __ballot_sync(0xffffffffu, mine >= 0);
-    int idx[32];
-    int cnt = 0;
-    for (unsigned m = have; m; m &= m - 1) idx[cnt++] = __shfl_sync(0xffffffffu, mine, __ffs(m) - 1);
-    for (int c = lane; c < D4; c += 32) {
+    const int cnt = __popc(have);
+    const int from = lane < cnt ? (int)__fns(have, 0, lane + 1) : lane;
+    const int cidx = __shfl_sync(0xffffffffu, mine, from);
+    for (int c0 = 0; c0 < D4; c0 += 32) {
+      const int c = c0 + lane;
+      const bool act = c < D4;
       float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int j = 0; j < cnt; ++j) g = f4_add(g, inbox[(int64_t)idx[j] * D4 + c]);
+      for (int j = 0; j < cnt; ++j) {
+        const int idx = __shfl_sync(0xffffffffu, cidx, j);
+        if (act) g = f4_add(g, inbox[(int64_t)idx * D4 + c]);
+      }
+      if (!act) continue;
       const int64_t off = row * D4 + c;
       float4 wv = w[off];
       float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
@@ -219,13 +228,15 @@ k_owner_apply(PeerTable peers, void* my_win, WinLayout L, float4* s0, float4* s1
       w[off] = wv;
       if (OPT != HP_OPT_SGD) s0[off] = a;
       if (OPT == HP_OPT_ADAM) s1[off] = b;
-      // pull, fused: the updated row goes back to each contributor's send slot
-      for (int j = 0; j < cnt; ++j) {
-        const int s = (int)(idx[j] / L.cap);
-        const int64_t ret_row = sig.push_off[s] + (idx[j] - (int64_t)s * L.cap);
-        reinterpret_cast<float4*>(static_cast<char*>(peers.base[s]) + L.ret_off)[ret_row * D4 + c] =
-            wv;
-      }
+    }
+    // pull, fused: the updated row goes back to each contributor's send slot
+    for (int j = 0; j < cnt; ++j) {
+      const int idx = __shfl_sync(0xffffffffu, cidx, j);
+      const int s = (int)(idx / L.cap);
+      const int64_t ret_row = sig.push_off[s] + (idx - (int64_t)s * L.cap);
+      float4* dst = reinterpret_cast<float4*>(static_cast<char*>(peers.base[s]) + L.ret_off) +
+                    ret_row * D4;
+      for (int c = lane; c < D4; c += 32) dst[c] = w[row * D4 + c];
     }
     __syncwarp();
     if (lane < n) slot[row * n + lane] = -1;
@@ -469,6 +480,204 @@ int hp_xchg_status(hp_xchg_t x, int32_t* out_err, void* stream) {
   HP_REQUIRE(x && out_err, "NULL argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   SigView sig(x->win);
+  HP_CUDA(cudaMemcpyAsync(out_err, sig.err, 4, cudaMemcpyDeviceToHost, st));
+  HP_CUDA(cudaStreamSynchronize(st));
+  return HP_OK;
+}
+
+}  // extern "C"
+
+// ============================================================================
+// K7 over peer memory: dense gradient allreduce fused with scale + cast.
+//
+// Rank r owns chunk r of the S elements. Phase 1 (k_ar_scatter): every rank
+// stores chunk c of its own gradient into rank c's reduce slot [me][*] (NVLink
+// stores; the gradient is read locally, in place, no staging copy). Phase 2
+// (k_ar_reduce_gather): rank c sums the n slots of its chunk in source-rank
+// order (deterministic, bit-reproducible), multiplies by scale, casts, and
+// stores the result into every rank's output. Each phase ends with a
+// last-block epoch flag; one-block k_wait kernels order the phases across GPUs.
+// Per rank NVLink bytes: (n-1)/n * S * (4 + out_bytes).
+// ============================================================================
+namespace hp {
+namespace {
+
+struct ArLayout {
+  int64_t S, S_real, chunk, slots_off, out_off;  // S = S_real padded to a multiple of 4n
+  int n, me, out_bytes;
+};
+
+__global__ void __launch_bounds__(256)
+k_ar_scatter(PeerTable peers, void* my_win, ArLayout A, const float4* __restrict__ grad) {
+  __shared__ bool s_last;
+  const int64_t n4 = A.S >> 2, c4 = A.chunk >> 2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i / c4);
+    const int64_t j = i - (int64_t)c * c4;
+    float4* dst = reinterpret_cast<float4*>(static_cast<char*>(peers.base[c]) + A.slots_off) +
+                  (int64_t)A.me * c4 + j;
+    *dst = i * 4 < A.S_real ? ldg_stream(grad + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __threadfence_system();
+  __syncthreads();
+  SigView sig(my_win);
+  if (threadIdx.x == 0) s_last = atomicAdd(&sig.done[2], 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (s_last) {
+    __threadfence_system();
+    const int e = *sig.epoch + 1;
+    for (int r = threadIdx.x; r < A.n; r += blockDim.x)
+      st_release_sys(&SigView(peers.base[r]).push_flag[A.me], e);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      *sig.epoch = e;
+      sig.done[2] = 0;
+    }
+  }
+}
+
+template <typename OutT>
+__device__ __forceinline__ void put4(void* base, int64_t i4, float4 v);
+template <>
+__device__ __forceinline__ void put4<float>(void* base, int64_t i4, float4 v) {
+  reinterpret_cast<float4*>(base)[i4] = v;
+}
+template <>
+__device__ __forceinline__ void put4<__nv_bfloat16>(void* base, int64_t i4, float4 v) {
+  __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&a);
+  u.y = *reinterpret_cast<uint32_t*>(&b);
+  reinterpret_cast<uint2*>(base)[i4] = u;
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(256)
+k_ar_reduce_gather(PeerTable peers, void* my_win, ArLayout A, float scale) {
+  __shared__ bool s_last;
+  const int64_t c4 = A.chunk >> 2;
+  const float4* slots =
+      reinterpret_cast<const float4*>(static_cast<char*>(my_win) + A.slots_off);
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < c4;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < A.n; ++s) acc = f4_add(acc, slots[(int64_t)s * c4 + j]);
+    acc.x = __fmul_rn(acc.x, scale);
+    acc.y = __fmul_rn(acc.y, scale);
+    acc.z = __fmul_rn(acc.z, scale);
+    acc.w = __fmul_rn(acc.w, scale);
+    const int64_t o4 = (int64_t)A.me * c4 + j;
+    for (int r = 0; r < A.n; ++r)
+      put4<OutT>(static_cast<char*>(peers.base[r]) + A.out_off, o4, acc);
+  }
+  __threadfence_system();
+  __syncthreads();
+  SigView sig(my_win);
+  if (threadIdx.x == 0) s_last = atomicAdd(&sig.done[3], 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (s_last) {
+    __threadfence_system();
+    const int e = *sig.epoch;
+    for (int r = threadIdx.x; r < A.n; r += blockDim.x)
+      st_release_sys(&SigView(peers.base[r]).applied_flag[A.me], e);
+    if (threadIdx.x == 0) sig.done[3] = 0;
+  }
+}
+
+}  // namespace
+}  // namespace hp
+
+struct hp_dar_s {
+  ArLayout A;
+  void* win;
+  PeerTable peers;
+};
+
+extern "C" {
+
+// Symmetric window of one dense Weight: [sig][slots n x chunk fp32][out S].
+// S (elements, a multiple of 4) is padded internally to a multiple of 4 * n.
+// Returns the cudaIpc handle and the output pointer (out_dtype = HP_DTYPE_F32
+// or HP_DTYPE_BF16; the first S elements are the result).
+int hp_dar_create(hp_dar_t* out, int32_t n, int32_t me, int64_t S_real, int32_t out_dtype,
+                  void* ipc_handle_out, void** out_ptr) {
+  HP_REQUIRE(out && ipc_handle_out && out_ptr && n >= 1 && n <= 32 && me >= 0 && me < n,
+             "bad dense allreduce args");
+  HP_REQUIRE(S_real > 0 && S_real % 4 == 0, "S must be a positive multiple of 4");
+  const int64_t S = (S_real + 4 * n - 1) / (4 * n) * (4 * n);
+  HP_REQUIRE(out_dtype == HP_DTYPE_F32 || out_dtype == HP_DTYPE_BF16, "out dtype f32 | bf16");
+  auto* d = new hp_dar_s{};
+  auto al = [](int64_t v) { return (v + 255) & ~(int64_t)255; };
+  d->A.S = S;
+  d->A.S_real = S_real;
+  d->A.n = n;
+  d->A.me = me;
+  d->A.chunk = S / n;
+  d->A.out_bytes = out_dtype == HP_DTYPE_F32 ? 4 : 2;
+  d->A.slots_off = al(SIG_INTS * 4);
+  d->A.out_off = d->A.slots_off + al(S * 4);
+  const int64_t bytes = d->A.out_off + al(S * d->A.out_bytes);
+  cudaError_t e = cudaMalloc(&d->win, bytes);
+  if (e != cudaSuccess) {
+    delete d;
+    return cuda_fail(e, "cudaMalloc(dense window)");
+  }
+  HP_CUDA(cudaMemset(d->win, 0, SIG_INTS * 4));
+  cudaIpcMemHandle_t h;
+  HP_CUDA(cudaIpcGetMemHandle(&h, d->win));
+  memcpy(ipc_handle_out, &h, sizeof(h));
+  for (int r = 0; r < 64; ++r) d->peers.base[r] = nullptr;
+  d->peers.base[me] = d->win;
+  *out_ptr = static_cast<char*>(d->win) + d->A.out_off;
+  *out = d;
+  return HP_OK;
+}
+
+int hp_dar_open_peer(hp_dar_t d, int32_t rank, const void* ipc_handle) {
+  HP_REQUIRE(d && rank >= 0 && rank < d->A.n && ipc_handle, "bad peer args");
+  if (rank == d->A.me) return HP_OK;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, ipc_handle, sizeof(h));
+  void* p = nullptr;
+  HP_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  d->peers.base[rank] = p;
+  return HP_OK;
+}
+
+int hp_dar_destroy(hp_dar_t d) {
+  if (!d) return HP_OK;
+  for (int r = 0; r < d->A.n; ++r)
+    if (r != d->A.me && d->peers.base[r]) cudaIpcCloseMemHandle(d->peers.base[r]);
+  cudaFree(d->win);
+  delete d;
+  return HP_OK;
+}
+
+// out (the window's output, every rank) = cast(scale * sum_r grad_r), summed in
+// rank order. grad is this rank's fp32 gradient [S] (any device buffer).
+int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream) {
+  HP_REQUIRE(d && grad && ((uintptr_t)grad & 15) == 0, "grad must be a 16-byte aligned buffer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int sms = sm_count();
+  k_ar_scatter<<<grid_for(d->A.S / 4, 256, sms * 4), 256, 0, st>>>(
+      d->peers, d->win, d->A, reinterpret_cast<const float4*>(grad));
+  k_wait<<<1, 64, 0, st>>>(d->win, 0, d->A.n, wait_budget());
+  if (d->A.out_bytes == 4)
+    k_ar_reduce_gather<float><<<grid_for(d->A.chunk / 4, 256, sms * 4), 256, 0, st>>>(
+        d->peers, d->win, d->A, scale);
+  else
+    k_ar_reduce_gather<__nv_bfloat16><<<grid_for(d->A.chunk / 4, 256, sms * 4), 256, 0, st>>>(
+        d->peers, d->win, d->A, scale);
+  k_wait<<<1, 64, 0, st>>>(d->win, 1, d->A.n, wait_budget());
+  HP_LAUNCHED(4, "dense p2p allreduce");
+  return HP_OK;
+}
+
+int hp_dar_status(hp_dar_t d, int32_t* out_err, void* stream) {
+  HP_REQUIRE(d && out_err, "NULL argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SigView sig(d->win);
   HP_CUDA(cudaMemcpyAsync(out_err, sig.err, 4, cudaMemcpyDeviceToHost, st));
   HP_CUDA(cudaStreamSynchronize(st));
   return HP_OK;

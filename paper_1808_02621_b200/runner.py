@@ -122,7 +122,8 @@ class HybridRunner:
                  rank: int = 0, world_size: int = 1, comm=None,
                  optimizer: OptimizerConfig | None = None, aggregation: str = "mean",
                  dense_dtype: torch.dtype = torch.float32, device=None, seed: int = 0,
-                 exchange: str = "p2p", max_ids: dict | None = None):
+                 exchange: str = "p2p", max_ids: dict | None = None,
+                 dense_exchange: str | None = None):
         if aggregation not in ("mean", "sum"):
             raise ValueError("aggregation must be 'mean' or 'sum'")
         if cluster.total_gpus != world_size:
@@ -134,6 +135,11 @@ class HybridRunner:
         if exchange not in ("p2p", "nccl"):
             raise ValueError("exchange must be 'p2p' (NVLink peer memory) or 'nccl'")
         self.exchange = exchange if world_size > 1 else "local"
+        # dense allreduce: peer-memory kernel (deterministic, scale/cast fused) or NCCL
+        self.dense_exchange = (dense_exchange or exchange) if world_size > 1 else "local"
+        if self.dense_exchange not in ("p2p", "nccl", "local"):
+            raise ValueError("dense_exchange must be 'p2p' or 'nccl'")
+        self.dar: dict = {}
         self.xchg: dict = {}
         self.glob_base: dict = {}
         self.plan, self.graph, self.cluster = plan, graph, cluster
@@ -150,6 +156,11 @@ class HybridRunner:
             mech = plan.mech_of[var.name]
             if var.kind == "dense":
                 self.dense.append(var)
+                if self.dense_exchange == "p2p":
+                    from .xchg import DenseExchange
+
+                    self.dar[var.name] = DenseExchange(world_size, rank, var.elements,
+                                                       dense_dtype, self.device)
                 continue
             if mech is Mechanism.PS:
                 P = plan.partitions_of[var.name]
@@ -235,13 +246,16 @@ class HybridRunner:
         return out
 
     def exchange_status(self) -> dict:
-        """Error bits of every table's peer exchange (synchronises)."""
-        return {k: x.status() for k, x in self.xchg.items()}
+        """Error bits of every peer exchange, sparse and dense (synchronises)."""
+        out = {k: x.status() for k, x in self.xchg.items()}
+        out.update({f"dense:{k}": d.status() for k, d in self.dar.items()})
+        return out
 
     def close(self) -> None:
-        for x in self.xchg.values():
+        for x in list(self.xchg.values()) + list(self.dar.values()):
             x.close()
         self.xchg.clear()
+        self.dar.clear()
 
     # ------------------------------------------------------------------ step
     def _buf(self, name: str, key: str, shape, dtype) -> torch.Tensor:
@@ -410,8 +424,11 @@ class HybridRunner:
                 out = g if self.dense_dtype == torch.float32 else torch.empty(
                     g.shape, dtype=self.dense_dtype, device=self.device)
             self._kev(f"k7:{var.name}", True)
-            self.dense_out[var.name] = ops.dense_allreduce_scale_cast(
-                self.comm.ptr if self.comm else None, g, out, self.scale)
+            if var.name in self.dar:
+                self.dense_out[var.name] = self.dar[var.name].allreduce(g, self.scale)
+            else:
+                self.dense_out[var.name] = ops.dense_allreduce_scale_cast(
+                    self.comm.ptr if self.comm else None, g, out, self.scale)
             self._kev(f"k7:{var.name}", False)
 
     def _sparse(self, tab: ShardedTable, ids_vals, ev=None) -> torch.Tensor:

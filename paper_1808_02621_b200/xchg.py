@@ -106,3 +106,49 @@ class PeerExchange:
             torch.cuda.synchronize()
             call("hp_xchg_destroy", self.handle)
             self.handle = None
+
+
+class DenseExchange:
+    """K7 over peer memory for one dense Weight: a symmetric window holding the
+    reduce slots and the output; ``allreduce(grad, scale)`` leaves
+    cast(scale * sum_r grad_r) (summed in rank order) in ``self.out`` on every rank."""
+
+    def __init__(self, n: int, rank: int, numel: int, out_dtype, device, group=None):
+        import torch.distributed as dist
+
+        from ._lib import HP_DTYPE
+
+        if numel % 4:
+            raise ValueError("dense gradient size must be a multiple of 4")
+        self.n, self.rank, self.numel = n, rank, numel
+        self.handle = C.c_void_p()
+        ipc = (C.c_ubyte * 64)()
+        optr = C.c_void_p()
+        code = HP_DTYPE[str(out_dtype).split(".")[1]]
+        call("hp_dar_create", C.byref(self.handle), n, rank, numel, code, C.addressof(ipc),
+             C.byref(optr))
+        handles = [None] * n
+        dist.all_gather_object(handles, bytes(ipc), group=group)
+        for r, h in enumerate(handles):
+            if r != rank:
+                buf = (C.c_ubyte * 64).from_buffer_copy(h)
+                call("hp_dar_open_peer", self.handle, r, C.addressof(buf))
+        typestr = "<f4" if code == 0 else "<u2"
+        t = torch.as_tensor(_DevPtr(optr.value, (numel,), typestr), device=device)
+        self.out = t if code == 0 else t.view(torch.bfloat16)
+
+    def allreduce(self, grad, scale: float) -> torch.Tensor:
+        call("hp_dar_allreduce", self.handle, grad.data_ptr(), scale,
+             torch.cuda.current_stream().cuda_stream)
+        return self.out
+
+    def status(self) -> int:
+        err = C.c_int32(0)
+        call("hp_dar_status", self.handle, C.addressof(err), torch.cuda.current_stream().cuda_stream)
+        return err.value
+
+    def close(self) -> None:
+        if self.handle:
+            torch.cuda.synchronize()
+            call("hp_dar_destroy", self.handle)
+            self.handle = None

@@ -33,16 +33,17 @@ def main():
     comm = hp.Comm.from_torch_distributed()
     opt_kind = os.environ.get("HP_CHECK_OPT", "adagrad")
     xmode = os.environ.get("HP_CHECK_XCHG", "p2p")
+    dmode = os.environ.get("HP_CHECK_DENSE", xmode)
     wl = Workload("check", [TableShape("embedding", 60_000, 128, 2560),
                             TableShape("softmax", 60_000, 256, 2560, sampled=3000)],
-                  {"lstm": 50_001}, {"kind": opt_kind, "lr": 0.1, "init_acc": 0.1}, 2560,
+                  {"lstm": 50_000}, {"kind": opt_kind, "lr": 0.1, "init_acc": 0.1}, 2560,
                   partitions=8)
     graph = hp.load_graph_spec(json.dumps(wl.graph_json()))
     cluster = hp.ClusterSpec.b200_box(world)
     plan = hp.transform_hybrid(graph, cluster, partitions={"embedding": 8, "softmax": 12})
     runner = hp.HybridRunner(plan, graph, cluster, rank=rank, world_size=world, comm=comm,
                              optimizer=hp.OptimizerConfig(kind=opt_kind, lr=0.1), device=dev,
-                             seed=5, exchange=xmode)
+                             seed=5, exchange=xmode, dense_exchange=dmode)
     hpar = {"lr": 0.1, "beta1": 0.9, "beta2": 0.999, "eps": 1e-8}
     states = {t.name: orc.init_state(opt_kind, t.V, t.D, 5 * 1000 + i + 1, 0.1)
               for i, t in enumerate(wl.tables)}
@@ -76,10 +77,17 @@ def main():
                     ok = False
                     why.append(f"step {step} {t.name} partition {p} differs")
         ref = orc.dense_allreduce([b["lstm"] for b in batches], 1.0 / world)
-        got = runner.dense_out["lstm"].cpu().numpy()
+        got = runner.dense_out["lstm"][:ref.size].cpu().numpy()
         if not np.allclose(got, ref, rtol=1e-5, atol=1e-6):
             ok = False
             why.append(f"step {step} dense differs (max {np.abs(got - ref).max():.3g})")
+        if runner.dense_exchange == "p2p":  # rank-order fp32 sum: bit-exact
+            seq = np.zeros_like(batches[0]["lstm"])
+            for b in batches:
+                seq = seq + b["lstm"]
+            if not np.array_equal(got, seq * np.float32(1.0 / world)):
+                ok = False
+                why.append(f"step {step} p2p dense not bit-exact vs rank-order sum")
         eg, ing = stats.per_machine_bytes.per_machine[rank]
         if world > 1 and not (eg > 0 and ing > 0):
             ok = False

@@ -18,12 +18,13 @@ def _ngpu():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("opt,xchg", [("adagrad", "p2p"), ("adam", "p2p"), ("sgd", "nccl")])
-def test_multi_gpu_step_matches_oracle(opt, xchg):
+@pytest.mark.parametrize("opt,xchg,dense", [("adagrad", "p2p", "p2p"), ("adam", "p2p", "nccl"),
+                                            ("sgd", "nccl", "nccl")])
+def test_multi_gpu_step_matches_oracle(opt, xchg, dense):
     n = min(_ngpu(), 8)
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
-    env = dict(os.environ, HP_CHECK_OPT=opt, HP_CHECK_XCHG=xchg)
+    env = dict(os.environ, HP_CHECK_OPT=opt, HP_CHECK_XCHG=xchg, HP_CHECK_DENSE=dense)
     import socket
 
     with socket.socket() as sk:
