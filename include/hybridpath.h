@@ -76,6 +76,9 @@ int64_t hp_launch_count(void);
 /* Instrumentation: device buffer (>= 16 x 16 int64) that the dedup kernels fill
  * with per-phase clock64 stamps; NULL (default) disables it. */
 void hp_debug_set_profile(long long* dev_buf);
+/* Instrumentation: per-kernel-type spans (globaltimer ns, min start / max end)
+ * into dev_buf[2 * 16] (starts pre-filled with ~0, ends with 0); NULL disables. */
+void hp_debug_set_spans(unsigned long long* dev_buf);
 /* Tuning: CTA size (256 | 512 | 1024) of the cluster dedup path. */
 void hp_debug_set_cluster_threads(int nt);
 

@@ -38,6 +38,7 @@ SIGNATURES = {
     "hp_launch_count": (i64, []),
     "hp_debug_set_profile": (None, [vp]),
     "hp_debug_set_cluster_threads": (None, [C.c_int]),
+    "hp_debug_set_spans": (None, [vp]),
     "hp_apply_plan": (C.c_int, [vp, i64, Slab, Optim, vp, sz, vp]),
     "hp_apply_plan_build": (C.c_int, [vp, i64, Slab, vp, sz, vp]),
     "hp_dedup_ws_bytes": (sz, [i64, i32, i32, i32]),

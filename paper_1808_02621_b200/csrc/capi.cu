@@ -7,6 +7,10 @@
 namespace hp {
 
 extern long long* g_prof;
+void set_spans_dedup(unsigned long long*);
+void set_spans_reduce(unsigned long long*);
+void set_spans_rows(unsigned long long*);
+void set_spans_p2p(unsigned long long*);
 void set_cluster_threads(int nt);
 
 static thread_local std::string g_err;
@@ -49,6 +53,16 @@ int64_t hp_launch_count(void) { return hp::g_launches.load(std::memory_order_rel
 
 // Instrumentation only: device buffer for per-phase clock64 stamps of the dedup kernels.
 void hp_debug_set_profile(long long* dev_buf) { hp::g_prof = dev_buf; }
+
+// Instrumentation: kernel spans [first block start, last block end] (globaltimer
+// ns) accumulated with atomicMin/Max into dev_buf[2 * SpanId] (SP_N entries);
+// NULL disables. The caller pre-fills starts with ~0 and ends with 0.
+void hp_debug_set_spans(unsigned long long* dev_buf) {
+  hp::set_spans_dedup(dev_buf);
+  hp::set_spans_reduce(dev_buf);
+  hp::set_spans_rows(dev_buf);
+  hp::set_spans_p2p(dev_buf);
+}
 
 // Tuning only: CTA size (256 | 512 | 1024) of the cluster dedup path.
 void hp_debug_set_cluster_threads(int nt) { hp::set_cluster_threads(nt); }

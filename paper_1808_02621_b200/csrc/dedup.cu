@@ -199,6 +199,7 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
   const int T = (int)pl.T, P = pl.P;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const Router route(pl.V, P);
+  HP_SPAN_BEGIN(SP_DEDUP);
   int nprof = 0;
 #define HP_PROF()                                                     \
   do {                                                                \
@@ -411,6 +412,7 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
   cl.sync();  // no CTA may exit while others still read its shared memory
   HP_PROF();
 #undef HP_PROF
+  HP_SPAN_END(SP_DEDUP);
 }
 
 constexpr size_t tile_smem_bytes() {
@@ -754,6 +756,7 @@ int launch_cluster_nt(const DedupPlan& pl, const int64_t* ids, const int32_t* ow
 int g_cl_threads = HP_CL_THREADS;  // CTA shape of the cluster path (hp_debug_set_cluster_threads)
 
 void set_cluster_threads(int nt) { g_cl_threads = nt; }
+HP_SPAN_SETTER(set_spans_dedup)
 
 template <int CS>
 int launch_cluster(const DedupPlan& pl, const int64_t* ids, const int32_t* owner,

@@ -121,4 +121,28 @@ inline int grid_for(int64_t work, int per_block, int max_blocks) {
 
 int sm_count();
 
+// ---- kernel span profiler (instrumentation only). Each TU that uses it keeps
+// its own device pointer; hp_debug_set_spans() sets all of them. A kernel
+// span = [first block start, last block end] in %globaltimer ns.
+enum SpanId {
+  SP_DEDUP = 0, SP_REDUCE, SP_COMBINE, SP_WAIT_PUSH, SP_SCATTER, SP_APPLY, SP_WAIT_APPLIED,
+  SP_COPY, SP_AR_SCATTER, SP_AR_WAIT0, SP_AR_RG, SP_AR_WAIT1, SP_N = 16
+};
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define HP_SPAN_DECL static __device__ unsigned long long* d_span = nullptr;
+#define HP_SPAN_BEGIN(id) \
+  if (d_span && threadIdx.x == 0) atomicMin(&d_span[2 * (id)], ::hp::globaltimer())
+#define HP_SPAN_END(id)                                   \
+  if (d_span) {                                           \
+    __syncthreads();                                      \
+    if (threadIdx.x == 0) atomicMax(&d_span[2 * (id) + 1], ::hp::globaltimer()); \
+  }
+#define HP_SPAN_SETTER(fn) \
+  void fn(unsigned long long* p) { cudaMemcpyToSymbol(d_span, &p, sizeof(p)); }
+HP_SPAN_DECL
+
 }  // namespace hp

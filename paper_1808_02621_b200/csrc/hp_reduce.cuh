@@ -92,6 +92,7 @@ k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
   constexpr int GPB = 256 / TPI;
   const int q = threadIdx.x % TPI;
   const int lane = threadIdx.x & 31;
+  HP_SPAN_BEGIN(SP_REDUCE);
   const int n_items = pl.counters[C_ITEMS];
   for (int it = blockIdx.x * GPB + threadIdx.x / TPI; it < n_items; it += gridDim.x * GPB) {
     const int4 item = pl.items[it];
@@ -132,6 +133,7 @@ k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
     }
   }
   if constexpr (Epi::kRemote) __threadfence_system();
+  HP_SPAN_END(SP_REDUCE);
 }
 
 // ((0 + r0) + r1) + ... over n <= HP_CHUNK rows of stride D4, 8 loads in flight.
@@ -153,6 +155,7 @@ __device__ __forceinline__ float4 seq_sum_rows(const float4* src, int n, int D4)
 // {partial slot, n0, dst, u}, in place over its partial rows.
 template <class Epi>
 __global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
+  HP_SPAN_BEGIN(SP_COMBINE);
   const int D4 = pl.D >> 2;
   const int n_long = pl.counters[C_LONG];
   float4* partials = reinterpret_cast<float4*>(pl.partials);
@@ -198,6 +201,7 @@ __global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
       epi.grid_done();
     }
   }
+  HP_SPAN_END(SP_COMBINE);
 }
 
 template <int TPI, int VPT, class Epi>

@@ -120,7 +120,8 @@ struct EpiPush {
 };
 
 // ---- wait until flags[s] >= epoch for every s (one block; bounded spin).
-__global__ void k_wait(void* my_win, int which, int n, long long timeout_cycles) {
+__global__ void k_wait(void* my_win, int which, int n, long long timeout_cycles, int span) {
+  HP_SPAN_BEGIN(span);
   SigView sig(my_win);
   const int* flags = which == 0 ? sig.push_flag : sig.applied_flag;
   const int e = *sig.epoch;
@@ -136,6 +137,7 @@ __global__ void k_wait(void* my_win, int which, int n, long long timeout_cycles)
   }
   __syncthreads();
   __threadfence();
+  HP_SPAN_END(span);
 }
 
 // ---- owner: direct-mapped merge. slot[row * n + s] = inbox index of source s
@@ -143,6 +145,7 @@ __global__ void k_wait(void* my_win, int which, int n, long long timeout_cycles)
 __global__ void __launch_bounds__(256)
 k_owner_scatter(void* my_win, WinLayout L, const int64_t* __restrict__ part_base, Router route,
                 int32_t* slot, int32_t* touch, int32_t* list, int32_t* nlist, int64_t rows_cap) {
+  HP_SPAN_BEGIN(SP_SCATTER);
   SigView sig(my_win);
   const int64_t* inbox_ids =
       reinterpret_cast<const int64_t*>(static_cast<char*>(my_win) + L.ids_off);
@@ -164,6 +167,7 @@ k_owner_scatter(void* my_win, WinLayout L, const int64_t* __restrict__ part_base
     slot[row * n + s] = (int32_t)i;
     if (atomicAdd(&touch[row], 1) == 0) list[atomicAdd(nlist, 1)] = (int32_t)row;
   }
+  HP_SPAN_END(SP_SCATTER);
 }
 
 template <int OPT>
@@ -190,6 +194,7 @@ __global__ void __launch_bounds__(256)
 k_owner_apply(PeerTable peers, void* my_win, WinLayout L, float4* s0, float4* s1, hp_optim o,
               int32_t* slot, int32_t* touch, const int32_t* __restrict__ list, int32_t* nlist) {
   __shared__ bool s_last;
+  HP_SPAN_BEGIN(SP_APPLY);
   SigView sig(my_win);
   char* win = static_cast<char*>(my_win);
   float4* w = reinterpret_cast<float4*>(win + L.w_off);
@@ -256,7 +261,10 @@ k_owner_apply(PeerTable peers, void* my_win, WinLayout L, float4* s0, float4* s1
       *nlist = 0;
     }
   }
+  HP_SPAN_END(SP_APPLY);
 }
+
+HP_SPAN_SETTER(set_spans_p2p)
 
 // Spin-wait budget (cycles) before a wait gives up and raises an error bit.
 long long wait_budget() {
@@ -406,7 +414,8 @@ int hp_xchg_push(hp_xchg_t x, const int64_t* ids, const float* vals, int64_t T, 
 // slab, return the updated rows to the contributors, signal "applied".
 int hp_xchg_wait(hp_xchg_t x, int32_t which, void* stream) {
   HP_REQUIRE(x && (which == 0 || which == 1), "bad wait arguments");
-  k_wait<<<1, 64, 0, static_cast<cudaStream_t>(stream)>>>(x->win, which, x->L.n, wait_budget());
+  k_wait<<<1, 64, 0, static_cast<cudaStream_t>(stream)>>>(x->win, which, x->L.n, wait_budget(),
+                                                          which ? SP_WAIT_APPLIED : SP_WAIT_PUSH);
   HP_LAUNCHED(1, "k_wait");
   return HP_OK;
 }
@@ -510,6 +519,7 @@ struct ArLayout {
 __global__ void __launch_bounds__(256)
 k_ar_scatter(PeerTable peers, void* my_win, ArLayout A, const float4* __restrict__ grad) {
   __shared__ bool s_last;
+  HP_SPAN_BEGIN(SP_AR_SCATTER);
   const int64_t n4 = A.S >> 2, c4 = A.chunk >> 2;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -535,6 +545,7 @@ k_ar_scatter(PeerTable peers, void* my_win, ArLayout A, const float4* __restrict
       sig.done[2] = 0;
     }
   }
+  HP_SPAN_END(SP_AR_SCATTER);
 }
 
 template <typename OutT>
@@ -556,6 +567,7 @@ template <typename OutT>
 __global__ void __launch_bounds__(256)
 k_ar_reduce_gather(PeerTable peers, void* my_win, ArLayout A, float scale) {
   __shared__ bool s_last;
+  HP_SPAN_BEGIN(SP_AR_RG);
   const int64_t c4 = A.chunk >> 2;
   const float4* slots =
       reinterpret_cast<const float4*>(static_cast<char*>(my_win) + A.slots_off);
@@ -583,6 +595,7 @@ k_ar_reduce_gather(PeerTable peers, void* my_win, ArLayout A, float scale) {
       st_release_sys(&SigView(peers.base[r]).applied_flag[A.me], e);
     if (threadIdx.x == 0) sig.done[3] = 0;
   }
+  HP_SPAN_END(SP_AR_RG);
 }
 
 }  // namespace
@@ -662,14 +675,14 @@ int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream) {
   const int sms = sm_count();
   k_ar_scatter<<<grid_for(d->A.S / 4, 256, sms * 4), 256, 0, st>>>(
       d->peers, d->win, d->A, reinterpret_cast<const float4*>(grad));
-  k_wait<<<1, 64, 0, st>>>(d->win, 0, d->A.n, wait_budget());
+  k_wait<<<1, 64, 0, st>>>(d->win, 0, d->A.n, wait_budget(), SP_AR_WAIT0);
   if (d->A.out_bytes == 4)
     k_ar_reduce_gather<float><<<grid_for(d->A.chunk / 4, 256, sms * 4), 256, 0, st>>>(
         d->peers, d->win, d->A, scale);
   else
     k_ar_reduce_gather<__nv_bfloat16><<<grid_for(d->A.chunk / 4, 256, sms * 4), 256, 0, st>>>(
         d->peers, d->win, d->A, scale);
-  k_wait<<<1, 64, 0, st>>>(d->win, 1, d->A.n, wait_budget());
+  k_wait<<<1, 64, 0, st>>>(d->win, 1, d->A.n, wait_budget(), SP_AR_WAIT1);
   HP_LAUNCHED(4, "dense p2p allreduce");
   return HP_OK;
 }

@@ -43,6 +43,9 @@ int apply_plan(const DedupPlan& pl, const float* vals, const hp_slab& s, const h
 }
 
 }  // namespace
+
+HP_SPAN_SETTER(set_spans_reduce)
+
 }  // namespace hp
 
 using namespace hp;

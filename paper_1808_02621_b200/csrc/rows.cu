@@ -38,6 +38,7 @@ struct SrcInv {
 template <int VPL, int RPW, class Src>
 __global__ void __launch_bounds__(256)
 k_copy_rows(Src src, int64_t n, const int32_t* n_dev, float4* __restrict__ out, int D4) {
+  HP_SPAN_BEGIN(SP_COPY);
   const int lane = threadIdx.x & 31;
   const int64_t lim = n_dev ? min(n, (int64_t)*n_dev) : n;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -65,6 +66,7 @@ k_copy_rows(Src src, int64_t n, const int32_t* n_dev, float4* __restrict__ out, 
       }
     }
   }
+  HP_SPAN_END(SP_COPY);
 }
 
 template <class Src>
@@ -160,6 +162,8 @@ k_scale_cast(const float* __restrict__ in, OutT* __restrict__ out, int64_t n, fl
 }
 
 }  // namespace
+
+HP_SPAN_SETTER(set_spans_rows)
 
 int scale_cast(const float* in, void* out, int64_t count, int32_t out_dtype, float scale,
                cudaStream_t st) {
