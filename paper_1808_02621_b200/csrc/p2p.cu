@@ -264,8 +264,6 @@ k_owner_apply(PeerTable peers, void* my_win, WinLayout L, float4* s0, float4* s1
   HP_SPAN_END(SP_APPLY);
 }
 
-HP_SPAN_SETTER(set_spans_p2p)
-
 // Spin-wait budget (cycles) before a wait gives up and raises an error bit.
 long long wait_budget() {
   static long long v = [] {
@@ -276,6 +274,9 @@ long long wait_budget() {
 }
 
 }  // namespace
+
+HP_SPAN_SETTER(set_spans_p2p)
+
 }  // namespace hp
 
 using namespace hp;
