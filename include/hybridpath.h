@@ -247,6 +247,9 @@ int hp_dar_open_peer(hp_dar_t d, int32_t rank, const void* ipc_handle);
 int hp_dar_destroy(hp_dar_t d);
 int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream);
 int hp_dar_status(hp_dar_t d, int32_t* out_err, void* stream);
+/* Instrumentation: raw peer throughput over the dense window (mode 0/2 store,
+ * 1/3 load; 2/3 with 4 x 16 B in flight per thread). */
+int hp_debug_nvlink_bench(hp_dar_t d, int32_t peer, int32_t mode, int32_t blocks, void* stream);
 
 #ifdef __cplusplus
 }

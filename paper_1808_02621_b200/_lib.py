@@ -78,6 +78,7 @@ SIGNATURES = {
     "hp_dar_destroy": (C.c_int, [vp]),
     "hp_dar_allreduce": (C.c_int, [vp, vp, f32, vp]),
     "hp_dar_status": (C.c_int, [vp, vp, vp]),
+    "hp_debug_nvlink_bench": (C.c_int, [vp, i32, i32, i32, vp]),
     "hp_xchg_debug_sig": (C.c_int, [vp, vp, vp]),
 }
 

@@ -698,3 +698,49 @@ int hp_dar_status(hp_dar_t d, int32_t* out_err, void* stream) {
 }
 
 }  // extern "C"
+
+// ---- instrumentation: raw peer-memory throughput between this rank and
+// rank `peer` over the dense window's slot region (bytes = S * 4).
+namespace hp {
+namespace {
+template <int U, bool LOAD>
+__global__ void __launch_bounds__(256) k_nvl_bench(float4* local, float4* remote, int64_t n4) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n4; i0 += stride * U) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < n4) v[u] = LOAD ? remote[i] : local[i];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < n4) {
+        if (LOAD) acc = f4_add(acc, v[u]);
+        else remote[i] = v[u];
+      }
+    }
+  }
+  if (LOAD && acc.x == 12345.f) local[0] = acc;  // keep the loads
+}
+}  // namespace
+}  // namespace hp
+
+extern "C" int hp_debug_nvlink_bench(hp_dar_t d, int32_t peer, int32_t mode, int32_t blocks,
+                                     void* stream) {
+  HP_REQUIRE(d && peer >= 0 && peer < d->A.n && d->peers.base[peer], "bad peer");
+  float4* local = reinterpret_cast<float4*>(static_cast<char*>(d->win) + d->A.slots_off);
+  float4* remote = reinterpret_cast<float4*>(static_cast<char*>(d->peers.base[peer]) + d->A.slots_off);
+  const int64_t n4 = d->A.S / 4;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (mode) {
+    case 0: k_nvl_bench<1, false><<<blocks, 256, 0, st>>>(local, remote, n4); break;
+    case 1: k_nvl_bench<1, true><<<blocks, 256, 0, st>>>(local, remote, n4); break;
+    case 2: k_nvl_bench<4, false><<<blocks, 256, 0, st>>>(local, remote, n4); break;
+    default: k_nvl_bench<4, true><<<blocks, 256, 0, st>>>(local, remote, n4); break;
+  }
+  HP_CUDA(cudaGetLastError());
+  return HP_OK;
+}
