@@ -223,7 +223,8 @@ int launch_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaSt
   else if (D4 <= 256) launch_k_reduce<64, 4>(pl, vals, epi, st);
   else launch_k_reduce<128, 4>(pl, vals, epi, st);
   HP_LAUNCHED(1, "k_reduce");
-  const int cblocks = grid_for(pl.T / HP_CHUNK + 1, 1, sm_count() * 2);
+  // long segments are few (<= T/33); a small grid keeps the publication cheap
+  const int cblocks = grid_for(pl.T / (HP_CHUNK + 1) + 1, 1, Epi::kRemote ? 32 : sm_count());
   k_combine<Epi><<<cblocks, 256, 0, st>>>(pl, epi);
   HP_LAUNCHED(1, "k_combine");
   return HP_OK;

@@ -216,32 +216,41 @@ k_owner_apply(PeerTable peers, void* my_win, WinLayout L, float4* s0, float4* s1
       const int c = c0 + lane;
       const bool act = c < D4;
       float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 x[4];
+      // contributions (<= 4 prefetched at once), summed in source order
+      for (int j0 = 0; j0 < cnt; j0 += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int idx = __shfl_sync(0xffffffffu, cidx, (j0 + u) & 31);
+          if (act && j0 + u < cnt) x[u] = inbox[(int64_t)idx * D4 + c];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (act && j0 + u < cnt) g = f4_add(g, x[u]);
+      }
+      const int64_t off = row * D4 + c;
+      float4 wv = make_float4(0.f, 0.f, 0.f, 0.f), a = wv, b = wv;
+      if (act) {
+        wv = w[off];
+        if (OPT != HP_OPT_SGD) a = s0[off];
+        if (OPT == HP_OPT_ADAM) b = s1[off];
+        opt_update<OPT>(wv.x, a.x, b.x, g.x, o);
+        opt_update<OPT>(wv.y, a.y, b.y, g.y, o);
+        opt_update<OPT>(wv.z, a.z, b.z, g.z, o);
+        opt_update<OPT>(wv.w, a.w, b.w, g.w, o);
+        w[off] = wv;
+        if (OPT != HP_OPT_SGD) s0[off] = a;
+        if (OPT == HP_OPT_ADAM) s1[off] = b;
+      }
+      // pull, fused: the updated row goes back to each contributor's send slot
       for (int j = 0; j < cnt; ++j) {
         const int idx = __shfl_sync(0xffffffffu, cidx, j);
-        if (act) g = f4_add(g, inbox[(int64_t)idx * D4 + c]);
+        const int s = (int)(idx / L.cap);
+        const int64_t ret_row = sig.push_off[s] + (idx - (int64_t)s * L.cap);
+        if (act)
+          reinterpret_cast<float4*>(static_cast<char*>(peers.base[s]) + L.ret_off)[ret_row * D4 + c] =
+              wv;
       }
-      if (!act) continue;
-      const int64_t off = row * D4 + c;
-      float4 wv = w[off];
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-      if (OPT != HP_OPT_SGD) a = s0[off];
-      if (OPT == HP_OPT_ADAM) b = s1[off];
-      opt_update<OPT>(wv.x, a.x, b.x, g.x, o);
-      opt_update<OPT>(wv.y, a.y, b.y, g.y, o);
-      opt_update<OPT>(wv.z, a.z, b.z, g.z, o);
-      opt_update<OPT>(wv.w, a.w, b.w, g.w, o);
-      w[off] = wv;
-      if (OPT != HP_OPT_SGD) s0[off] = a;
-      if (OPT == HP_OPT_ADAM) s1[off] = b;
-    }
-    // pull, fused: the updated row goes back to each contributor's send slot
-    for (int j = 0; j < cnt; ++j) {
-      const int idx = __shfl_sync(0xffffffffu, cidx, j);
-      const int s = (int)(idx / L.cap);
-      const int64_t ret_row = sig.push_off[s] + (idx - (int64_t)s * L.cap);
-      float4* dst = reinterpret_cast<float4*>(static_cast<char*>(peers.base[s]) + L.ret_off) +
-                    ret_row * D4;
-      for (int c = lane; c < D4; c += 32) dst[c] = w[row * D4 + c];
     }
     __syncwarp();
     if (lane < n) slot[row * n + lane] = -1;
@@ -517,23 +526,36 @@ struct ArLayout {
   int n, me, out_bytes;
 };
 
+// blockIdx.y = destination chunk; 4 float4 in flight per thread; no division.
 __global__ void __launch_bounds__(256)
 k_ar_scatter(PeerTable peers, void* my_win, ArLayout A, const float4* __restrict__ grad) {
   __shared__ bool s_last;
   HP_SPAN_BEGIN(SP_AR_SCATTER);
-  const int64_t n4 = A.S >> 2, c4 = A.chunk >> 2;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i / c4);
-    const int64_t j = i - (int64_t)c * c4;
-    float4* dst = reinterpret_cast<float4*>(static_cast<char*>(peers.base[c]) + A.slots_off) +
-                  (int64_t)A.me * c4 + j;
-    *dst = i * 4 < A.S_real ? ldg_stream(grad + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const int c = blockIdx.y;
+  const int64_t c4 = A.chunk >> 2, real4 = A.S_real >> 2;
+  const float4* src = grad + (int64_t)c * c4;
+  float4* dst = reinterpret_cast<float4*>(static_cast<char*>(peers.base[c]) + A.slots_off) +
+                (int64_t)A.me * c4;
+  const int64_t lim = min(c4, max((int64_t)0, real4 - (int64_t)c * c4));  // real elements here
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < c4; j0 += 4 * stride) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t j = j0 + u * stride;
+      v[u] = j < lim ? ldg_stream(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t j = j0 + u * stride;
+      if (j < c4) dst[j] = v[u];
+    }
   }
   __threadfence_system();
   __syncthreads();
   SigView sig(my_win);
-  if (threadIdx.x == 0) s_last = atomicAdd(&sig.done[2], 1) == (int)gridDim.x - 1;
+  const int nblocks = gridDim.x * gridDim.y;
+  if (threadIdx.x == 0) s_last = atomicAdd(&sig.done[2], 1) == nblocks - 1;
   __syncthreads();
   if (s_last) {
     __threadfence_system();
@@ -572,17 +594,29 @@ k_ar_reduce_gather(PeerTable peers, void* my_win, ArLayout A, float scale) {
   const int64_t c4 = A.chunk >> 2;
   const float4* slots =
       reinterpret_cast<const float4*>(static_cast<char*>(my_win) + A.slots_off);
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < c4;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s = 0; s < A.n; ++s) acc = f4_add(acc, slots[(int64_t)s * c4 + j]);
-    acc.x = __fmul_rn(acc.x, scale);
-    acc.y = __fmul_rn(acc.y, scale);
-    acc.z = __fmul_rn(acc.z, scale);
-    acc.w = __fmul_rn(acc.w, scale);
-    const int64_t o4 = (int64_t)A.me * c4 + j;
-    for (int r = 0; r < A.n; ++r)
-      put4<OutT>(static_cast<char*>(peers.base[r]) + A.out_off, o4, acc);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < c4; j0 += 2 * stride) {
+    float4 acc[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t j = j0 + u * stride;
+      acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (j < c4)
+        for (int s = 0; s < A.n; ++s) acc[u] = f4_add(acc[u], ldg_stream(slots + (int64_t)s * c4 + j));
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t j = j0 + u * stride;
+      if (j >= c4) continue;
+      float4 v = acc[u];
+      v.x = __fmul_rn(v.x, scale);
+      v.y = __fmul_rn(v.y, scale);
+      v.z = __fmul_rn(v.z, scale);
+      v.w = __fmul_rn(v.w, scale);
+      const int64_t o4 = (int64_t)A.me * c4 + j;
+      for (int r = 0; r < A.n; ++r)
+        put4<OutT>(static_cast<char*>(peers.base[r]) + A.out_off, o4, v);
+    }
   }
   __threadfence_system();
   __syncthreads();
@@ -674,15 +708,17 @@ int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream) {
   HP_REQUIRE(d && grad && ((uintptr_t)grad & 15) == 0, "grad must be a 16-byte aligned buffer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int sms = sm_count();
-  k_ar_scatter<<<grid_for(d->A.S / 4, 256, sms * 4), 256, 0, st>>>(
-      d->peers, d->win, d->A, reinterpret_cast<const float4*>(grad));
+  // ~half the SMs: NVLink saturates well below full occupancy, and the sparse
+  // tables' latency-bound kernels run concurrently on the rest
+  const int bx = std::max(1, std::min(grid_for(d->A.chunk / 16, 256, sms), sms / d->A.n));
+  k_ar_scatter<<<dim3(bx, d->A.n), 256, 0, st>>>(d->peers, d->win, d->A,
+                                                reinterpret_cast<const float4*>(grad));
   k_wait<<<1, 64, 0, st>>>(d->win, 0, d->A.n, wait_budget(), SP_AR_WAIT0);
+  const int brg = grid_for(d->A.chunk / 8, 256, sms / 2);
   if (d->A.out_bytes == 4)
-    k_ar_reduce_gather<float><<<grid_for(d->A.chunk / 4, 256, sms * 4), 256, 0, st>>>(
-        d->peers, d->win, d->A, scale);
+    k_ar_reduce_gather<float><<<brg, 256, 0, st>>>(d->peers, d->win, d->A, scale);
   else
-    k_ar_reduce_gather<__nv_bfloat16><<<grid_for(d->A.chunk / 4, 256, sms * 4), 256, 0, st>>>(
-        d->peers, d->win, d->A, scale);
+    k_ar_reduce_gather<__nv_bfloat16><<<brg, 256, 0, st>>>(d->peers, d->win, d->A, scale);
   k_wait<<<1, 64, 0, st>>>(d->win, 1, d->A.n, wait_budget(), SP_AR_WAIT1);
   HP_LAUNCHED(4, "dense p2p allreduce");
   return HP_OK;
