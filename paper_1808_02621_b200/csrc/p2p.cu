@@ -714,7 +714,7 @@ int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream) {
   k_ar_scatter<<<dim3(bx, d->A.n), 256, 0, st>>>(d->peers, d->win, d->A,
                                                 reinterpret_cast<const float4*>(grad));
   k_wait<<<1, 64, 0, st>>>(d->win, 0, d->A.n, wait_budget(), SP_AR_WAIT0);
-  const int brg = grid_for(d->A.chunk / 8, 256, sms / 2);
+  const int brg = grid_for(d->A.chunk / 8, 256, sms * 2);
   if (d->A.out_bytes == 4)
     k_ar_reduce_gather<float><<<brg, 256, 0, st>>>(d->peers, d->win, d->A, scale);
   else

@@ -79,6 +79,11 @@ WORKLOADS = {
                     2560, partitions=8),
     "dense": Workload("dense", [], {"conv_fc": 25_600_000}, {"kind": "sgd", "lr": 0.1}, 0),
 }
+# diagnosis variants of the LM1B step: only its sparse tables / only its dense part
+WORKLOADS["lm1b_sparse"] = Workload("lm1b_sparse", WORKLOADS["lm1b"].tables, {},
+                                    WORKLOADS["lm1b"].optimizer, 2560, partitions=8)
+WORKLOADS["lm1b_dense"] = Workload("lm1b_dense", [], dict(WORKLOADS["lm1b"].dense),
+                                   WORKLOADS["lm1b"].optimizer, 2560, partitions=8)
 
 
 def micro_workload(draws: int) -> Workload:
