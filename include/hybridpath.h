@@ -203,12 +203,14 @@ int hp_xchg_create(hp_xchg_t* out, int32_t n, int32_t me, int32_t D, int64_t cap
 int hp_xchg_open_peer(hp_xchg_t x, int32_t rank, const void* ipc_handle);
 int hp_xchg_destroy(hp_xchg_t x);
 /* Worker, fused K1+K2+K3: dedup + route ids[T]/vals[T,D] and store every summed
- * row straight into its owner's inbox (NVLink stores); publishes counts,
- * offsets and the step epoch at every owner. Outputs: send_ids[U], inv[T],
+ * row straight into its owner's inbox (NVLink stores) with an epoch-tagged entry
+ * in the owner's slot table (glob_base[p] = slab row of partition p on its
+ * owner); publishes counts, offsets and the step epoch at every owner. Outputs: send_ids[U], inv[T],
  * dest_counts[n], n_uniq[1] (device). ws sized by hp_dedup_ws_bytes. */
 int hp_xchg_push(hp_xchg_t x, const int64_t* ids, const float* vals, int64_t T, int64_t V,
-                 int32_t P, const int32_t* owner, int64_t* send_ids, int32_t* inv,
-                 int32_t* dest_counts, int32_t* n_uniq, void* ws, size_t ws_bytes, void* stream);
+                 int32_t P, const int32_t* owner, const int64_t* glob_base, int64_t* send_ids,
+                 int32_t* inv, int32_t* dest_counts, int32_t* n_uniq, void* ws, size_t ws_bytes,
+                 void* stream);
 /* The two halves of hp_xchg_push (so a plan can be built ahead of its step):
  * hp_xchg_plan dedups/routes ids into a send plan in ws; hp_xchg_push_plan
  * reduces vals with that plan and pushes (same T / V / P / ws). */
@@ -216,8 +218,8 @@ int hp_xchg_plan(hp_xchg_t x, const int64_t* ids, int64_t T, int64_t V, int32_t 
                  const int32_t* owner, int64_t* send_ids, int32_t* inv, int32_t* dest_counts,
                  int32_t* n_uniq, void* ws, size_t ws_bytes, void* stream);
 int hp_xchg_push_plan(hp_xchg_t x, const float* vals, int64_t T, int64_t V, int32_t P,
-                      const int64_t* send_ids, const int32_t* dest_counts, void* ws,
-                      size_t ws_bytes, void* stream);
+                      const int64_t* send_ids, const int32_t* dest_counts,
+                      const int64_t* glob_base, void* ws, size_t ws_bytes, void* stream);
 /* Wait (one spinning block, bounded) until every source pushed (which = 0) or
  * every owner applied (which = 1) for this rank's current epoch. */
 int hp_xchg_wait(hp_xchg_t x, int32_t which, void* stream);

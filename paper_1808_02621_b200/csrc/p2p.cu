@@ -6,13 +6,16 @@
 // capturable. Compute and communication are fused:
 //
 //   worker  dedup plan (k_dedup_*), then k_reduce/k_combine with EpiPush: every
-//           summed row is stored straight into its owner's inbox over NVLink;
-//           the last k_combine block publishes {count, offset, epoch} per owner.
-//   owner   k_wait(push) -> k_owner_scatter (direct-mapped slot table, no sort)
-//           -> k_owner_apply: sum contributions in source order, optimizer
-//           update, and store the updated row straight back into every
-//           contributing worker's return buffer (NVLink); last block publishes
-//           "applied" to every peer.
+//           summed row is stored straight into its owner's inbox over NVLink,
+//           and an epoch-tagged entry {epoch, inbox index} into the owner's
+//           direct-mapped slot table [slab row][source]; the last k_combine
+//           block publishes {count, offset, epoch} per owner.
+//   owner   k_wait(push) -> k_owner_apply: one warp per inbox entry; the entry
+//           of the lowest-ranked source of a row (valid tags) owns the row:
+//           sums the contributions in source order, optimizer update, and
+//           stores the updated row straight back into every contributor's
+//           return buffer (NVLink); last block publishes "applied". No sort,
+//           no atomics, no reset (stale tags never match the epoch).
 //   worker  k_wait(applied) -> stitch from the local return buffer.
 //
 // Windows: each rank cudaMallocs one symmetric window per table and exports
@@ -23,6 +26,7 @@
 //   [ids]   inbox ids  [n][cap] int64   (source-major)
 //   [rows]  inbox rows [n][cap][D] fp32
 //   [ret]   return rows [cap][D] fp32 (indexed by this rank's send slot)
+//   [slot]  uint64 [rows_cap][n] = (epoch << 32) | inbox index (peer-written)
 // Spin-waits run in ONE small block (k_wait) and give up after a bounded time,
 // raising an error bit instead of hanging the GPU.
 #include <algorithm>
@@ -72,7 +76,7 @@ struct PeerTable {
 };
 
 struct WinLayout {
-  int64_t w_off, ids_off, rows_off, ret_off, cap;
+  int64_t w_off, ids_off, rows_off, ret_off, slot_off, cap;
   int n, me, D4;
 };
 
@@ -83,6 +87,8 @@ struct EpiPush {
   WinLayout L;
   const int32_t* dest_counts;  // [n] rows this rank sends to each owner
   const int64_t* send_ids;     // [U] (send order)
+  const int64_t* glob_base;    // [P] slab row of partition p on its owner
+  Router route;
   int* done;                   // last-block counter (own window)
   void* my_win;
   struct Pre {
@@ -93,7 +99,15 @@ struct EpiPush {
     while (o + 1 < L.n && slot >= off + dest_counts[o]) off += dest_counts[o++];
     const int64_t idx = (int64_t)L.me * L.cap + (slot - off);
     char* win = static_cast<char*>(peers.base[o]);
-    if (c4 == 0) reinterpret_cast<int64_t*>(win + L.ids_off)[idx] = send_ids[slot];
+    if (c4 == 0) {
+      const int64_t id = send_ids[slot];
+      reinterpret_cast<int64_t*>(win + L.ids_off)[idx] = id;
+      const int p = route.part(id);
+      const int64_t row = glob_base[p] + (id - route.lo(p));
+      const unsigned long long e = (unsigned long long)(*SigView(my_win).epoch + 1);
+      reinterpret_cast<unsigned long long*>(win + L.slot_off)[row * L.n + L.me] =
+          (e << 32) | (unsigned long long)(uint32_t)idx;
+    }
     return {reinterpret_cast<float4*>(win + L.rows_off) + idx * L.D4};
   }
   __device__ __forceinline__ void store(int, int c4, float4 g, Pre p) const { p.dst[c4] = g; }
@@ -140,36 +154,6 @@ __global__ void k_wait(void* my_win, int which, int n, long long timeout_cycles,
   HP_SPAN_END(span);
 }
 
-// ---- owner: direct-mapped merge. slot[row * n + s] = inbox index of source s
-// for slab row `row` (or -1); every row is listed once in `list`.
-__global__ void __launch_bounds__(256)
-k_owner_scatter(void* my_win, WinLayout L, const int64_t* __restrict__ part_base, Router route,
-                int32_t* slot, int32_t* touch, int32_t* list, int32_t* nlist, int64_t rows_cap) {
-  HP_SPAN_BEGIN(SP_SCATTER);
-  SigView sig(my_win);
-  const int64_t* inbox_ids =
-      reinterpret_cast<const int64_t*>(static_cast<char*>(my_win) + L.ids_off);
-  const int n = L.n;
-  const int64_t total = (int64_t)n * L.cap;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int s = (int)(i / L.cap);
-    const int k = (int)(i - (int64_t)s * L.cap);
-    if (k >= sig.push_count[s]) continue;
-    const int64_t id = inbox_ids[i];
-    const int p = route.part(id);
-    const int64_t b = part_base[p];
-    const int64_t row = b + (id - route.lo(p));
-    if (b < 0 || row >= rows_cap) {
-      atomicOr(sig.err, 16);
-      continue;
-    }
-    slot[row * n + s] = (int32_t)i;
-    if (atomicAdd(&touch[row], 1) == 0) list[atomicAdd(nlist, 1)] = (int32_t)row;
-  }
-  HP_SPAN_END(SP_SCATTER);
-}
-
 template <int OPT>
 __device__ __forceinline__ void opt_update(float& w, float& a, float& b, float g,
                                            const hp_optim& o) {
@@ -186,75 +170,108 @@ __device__ __forceinline__ void opt_update(float& w, float& a, float& b, float g
   }
 }
 
-// ---- owner: per listed row, sum the (<= n) contributions in source order,
-// scale, apply, store the updated row back into every contributor's return
-// buffer (peer stores), reset the slot table; last block raises "applied".
+// ---- owner: one warp per inbox entry (source s, index k). The entry of the
+// lowest-ranked source with a valid tag for its row owns the row: it sums the
+// contributions in source order, scales, applies, stores the updated row back
+// into every contributor's return buffer (peer stores); last block raises
+// "applied". Columns go in pairs per lane with all loads of a pair in flight.
 template <int OPT>
 __global__ void __launch_bounds__(256)
-k_owner_apply(PeerTable peers, void* my_win, WinLayout L, float4* s0, float4* s1, hp_optim o,
-              int32_t* slot, int32_t* touch, const int32_t* __restrict__ list, int32_t* nlist) {
+k_owner_apply(PeerTable peers, void* my_win, WinLayout L, const int64_t* __restrict__ part_base,
+              Router route, float4* s0, float4* s1, hp_optim o, int64_t rows_cap) {
   __shared__ bool s_last;
   HP_SPAN_BEGIN(SP_APPLY);
   SigView sig(my_win);
   char* win = static_cast<char*>(my_win);
   float4* w = reinterpret_cast<float4*>(win + L.w_off);
   const float4* inbox = reinterpret_cast<const float4*>(win + L.rows_off);
+  const int64_t* inbox_ids = reinterpret_cast<const int64_t*>(win + L.ids_off);
+  const unsigned long long* slot = reinterpret_cast<const unsigned long long*>(win + L.slot_off);
   const int n = L.n, D4 = L.D4;
-  const int nl = *nlist;
+  const unsigned epoch = (unsigned)*sig.epoch;
   const int lane = threadIdx.x & 31;
-  const int nw = gridDim.x * (blockDim.x >> 5);
-  for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nl; k += nw) {
-    const int64_t row = list[k];
-    // contributions in source order: lane j (< cnt) holds the j-th contributor's
-    // inbox index, taken from the slot-table lane of that source
-    const int mine = lane < n ? slot[row * n + lane] : -1;
-    const unsigned have = __ballot_sync(0xffffffffu, mine >= 0);
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t total = (int64_t)n * L.cap;
+  for (int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < total; e += nw) {
+    const int s = (int)(e / L.cap);
+    if (e - (int64_t)s * L.cap >= sig.push_count[s]) continue;  // warp-uniform
+    const int64_t id = inbox_ids[e];
+    const int p = route.part(id);
+    const int64_t b = part_base[p];
+    const int64_t row = b + (id - route.lo(p));
+    if (b < 0 || row >= rows_cap) {
+      if (lane == 0) atomicOr(sig.err, 16);
+      continue;
+    }
+    const unsigned long long ent = lane < n ? slot[row * n + lane] : 0ull;
+    const bool valid = lane < n && (unsigned)(ent >> 32) == epoch;
+    const unsigned have = __ballot_sync(0xffffffffu, valid);
+    if (__ffs(have) - 1 != s) continue;  // another source's entry owns this row
     const int cnt = __popc(have);
     const int from = lane < cnt ? (int)__fns(have, 0, lane + 1) : lane;
-    const int cidx = __shfl_sync(0xffffffffu, mine, from);
-    for (int c0 = 0; c0 < D4; c0 += 32) {
-      const int c = c0 + lane;
-      const bool act = c < D4;
-      float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-      float4 x[4];
-      // contributions (<= 4 prefetched at once), summed in source order
-      for (int j0 = 0; j0 < cnt; j0 += 4) {
+    const int cidx = __shfl_sync(0xffffffffu, (int)(uint32_t)ent, from);
+    for (int c0 = 0; c0 < D4; c0 += 64) {
+      const int ca = c0 + lane, cb = c0 + 32 + lane;
+      const bool acta = ca < D4, actb = cb < D4;
+      const int64_t oa = row * D4 + ca, ob = row * D4 + cb;
+      float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 wa = acta ? w[oa] : z, wb = actb ? w[ob] : z;
+      float4 aa = z, ab = z, ba = z, bb = z;
+      if (OPT != HP_OPT_SGD) {
+        if (acta) aa = s0[oa];
+        if (actb) ab = s0[ob];
+      }
+      if (OPT == HP_OPT_ADAM) {
+        if (acta) ba = s1[oa];
+        if (actb) bb = s1[ob];
+      }
+      float4 ga = z, gb = z;
+      for (int j0 = 0; j0 < cnt; j0 += 2) {  // contributions, source order
+        float4 xa[2], xb[2];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 2; ++u) {
           const int idx = __shfl_sync(0xffffffffu, cidx, (j0 + u) & 31);
-          if (act && j0 + u < cnt) x[u] = inbox[(int64_t)idx * D4 + c];
+          if (j0 + u < cnt) {
+            if (acta) xa[u] = inbox[(int64_t)idx * D4 + ca];
+            if (actb) xb[u] = inbox[(int64_t)idx * D4 + cb];
+          }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (act && j0 + u < cnt) g = f4_add(g, x[u]);
+        for (int u = 0; u < 2; ++u)
+          if (j0 + u < cnt) {
+            ga = f4_add(ga, xa[u]);
+            gb = f4_add(gb, xb[u]);
+          }
       }
-      const int64_t off = row * D4 + c;
-      float4 wv = make_float4(0.f, 0.f, 0.f, 0.f), a = wv, b = wv;
-      if (act) {
-        wv = w[off];
-        if (OPT != HP_OPT_SGD) a = s0[off];
-        if (OPT == HP_OPT_ADAM) b = s1[off];
-        opt_update<OPT>(wv.x, a.x, b.x, g.x, o);
-        opt_update<OPT>(wv.y, a.y, b.y, g.y, o);
-        opt_update<OPT>(wv.z, a.z, b.z, g.z, o);
-        opt_update<OPT>(wv.w, a.w, b.w, g.w, o);
-        w[off] = wv;
-        if (OPT != HP_OPT_SGD) s0[off] = a;
-        if (OPT == HP_OPT_ADAM) s1[off] = b;
+      if (acta) {
+        opt_update<OPT>(wa.x, aa.x, ba.x, ga.x, o);
+        opt_update<OPT>(wa.y, aa.y, ba.y, ga.y, o);
+        opt_update<OPT>(wa.z, aa.z, ba.z, ga.z, o);
+        opt_update<OPT>(wa.w, aa.w, ba.w, ga.w, o);
+        w[oa] = wa;
+        if (OPT != HP_OPT_SGD) s0[oa] = aa;
+        if (OPT == HP_OPT_ADAM) s1[oa] = ba;
+      }
+      if (actb) {
+        opt_update<OPT>(wb.x, ab.x, bb.x, gb.x, o);
+        opt_update<OPT>(wb.y, ab.y, bb.y, gb.y, o);
+        opt_update<OPT>(wb.z, ab.z, bb.z, gb.z, o);
+        opt_update<OPT>(wb.w, ab.w, bb.w, gb.w, o);
+        w[ob] = wb;
+        if (OPT != HP_OPT_SGD) s0[ob] = ab;
+        if (OPT == HP_OPT_ADAM) s1[ob] = bb;
       }
       // pull, fused: the updated row goes back to each contributor's send slot
       for (int j = 0; j < cnt; ++j) {
         const int idx = __shfl_sync(0xffffffffu, cidx, j);
-        const int s = (int)(idx / L.cap);
-        const int64_t ret_row = sig.push_off[s] + (idx - (int64_t)s * L.cap);
-        if (act)
-          reinterpret_cast<float4*>(static_cast<char*>(peers.base[s]) + L.ret_off)[ret_row * D4 + c] =
-              wv;
+        const int src = idx / (int)L.cap;
+        const int64_t ret_row = sig.push_off[src] + (idx - (int64_t)src * L.cap);
+        float4* ret = reinterpret_cast<float4*>(static_cast<char*>(peers.base[src]) + L.ret_off) +
+                      ret_row * D4;
+        if (acta) ret[ca] = wa;
+        if (actb) ret[cb] = wb;
       }
     }
-    __syncwarp();
-    if (lane < n) slot[row * n + lane] = -1;
-    if (lane == 0) touch[row] = 0;
   }
   __threadfence_system();
   __syncthreads();
@@ -262,13 +279,9 @@ k_owner_apply(PeerTable peers, void* my_win, WinLayout L, float4* s0, float4* s1
   __syncthreads();
   if (s_last) {
     __threadfence_system();
-    const int e = *sig.epoch;
     for (int r = threadIdx.x; r < n; r += blockDim.x)
-      st_release_sys(&SigView(peers.base[r]).applied_flag[L.me], e);
-    if (threadIdx.x == 0) {
-      sig.done[1] = 0;
-      *nlist = 0;
-    }
+      st_release_sys(&SigView(peers.base[r]).applied_flag[L.me], (int)epoch);
+    if (threadIdx.x == 0) sig.done[1] = 0;
   }
   HP_SPAN_END(SP_APPLY);
 }
@@ -296,10 +309,6 @@ struct hp_xchg_s {
   int64_t rows_cap, bytes;
   void* win;          // own window
   PeerTable peers;    // mapped windows (own = win)
-  int32_t* slot;      // [rows_cap * n]
-  int32_t* touch;     // [rows_cap]
-  int32_t* list;      // [min(n*cap, rows_cap)]
-  int32_t* nlist;     // [1]
 };
 
 extern "C" {
@@ -307,7 +316,7 @@ extern "C" {
 size_t hp_xchg_window_bytes(int32_t n, int32_t D, int64_t cap, int64_t rows_cap) {
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   return al(SIG_INTS * 4) + al((size_t)rows_cap * D * 4) + al((size_t)n * cap * 8) +
-         al((size_t)n * cap * D * 4) + al((size_t)cap * D * 4);
+         al((size_t)n * cap * D * 4) + al((size_t)cap * D * 4) + al((size_t)rows_cap * n * 8);
 }
 
 int hp_xchg_create(hp_xchg_t* out, int32_t n, int32_t me, int32_t D, int64_t cap, int64_t rows_cap,
@@ -327,25 +336,19 @@ int hp_xchg_create(hp_xchg_t* out, int32_t n, int32_t me, int32_t D, int64_t cap
   L.ids_off = L.w_off + al(rows_cap * D * 4);
   L.rows_off = L.ids_off + al((int64_t)n * cap * 8);
   L.ret_off = L.rows_off + al((int64_t)n * cap * D * 4);
-  x->bytes = L.ret_off + al(cap * D * 4);
+  L.slot_off = L.ret_off + al(cap * D * 4);
+  x->bytes = L.slot_off + al(rows_cap * n * 8);
   cudaError_t e = cudaMalloc(&x->win, x->bytes);
   if (e != cudaSuccess) {
     delete x;
     return cuda_fail(e, "cudaMalloc(window)");
   }
   HP_CUDA(cudaMemset(x->win, 0, SIG_INTS * 4));
+  HP_CUDA(cudaMemset(static_cast<char*>(x->win) + L.slot_off, 0, (size_t)rows_cap * n * 8));
   cudaIpcMemHandle_t h;
   HP_CUDA(cudaIpcGetMemHandle(&h, x->win));
   static_assert(sizeof(h) == 64, "IPC handle size");
   memcpy(ipc_handle_out, &h, sizeof(h));
-  const int64_t lb = std::min<int64_t>((int64_t)n * cap, rows_cap);
-  HP_CUDA(cudaMalloc(&x->slot, (size_t)rows_cap * n * 4));
-  HP_CUDA(cudaMemset(x->slot, 0xff, (size_t)rows_cap * n * 4));
-  HP_CUDA(cudaMalloc(&x->touch, (size_t)rows_cap * 4));
-  HP_CUDA(cudaMemset(x->touch, 0, (size_t)rows_cap * 4));
-  HP_CUDA(cudaMalloc(&x->list, (size_t)std::max<int64_t>(lb, 1) * 4));
-  HP_CUDA(cudaMalloc(&x->nlist, 4));
-  HP_CUDA(cudaMemset(x->nlist, 0, 4));
   for (int r = 0; r < 64; ++r) x->peers.base[r] = nullptr;
   x->peers.base[me] = x->win;
   *w_out = static_cast<char*>(x->win) + L.w_off;
@@ -368,10 +371,6 @@ int hp_xchg_destroy(hp_xchg_t x) {
   if (!x) return HP_OK;
   for (int r = 0; r < x->L.n; ++r)
     if (r != x->L.me && x->peers.base[r]) cudaIpcCloseMemHandle(x->peers.base[r]);
-  cudaFree(x->slot);
-  cudaFree(x->touch);
-  cudaFree(x->list);
-  cudaFree(x->nlist);
   cudaFree(x->win);
   delete x;
   return HP_OK;
@@ -396,28 +395,30 @@ int hp_xchg_plan(hp_xchg_t x, const int64_t* ids, int64_t T, int64_t V, int32_t 
 // reduce vals[T, D] and store every summed row straight into its owner's inbox
 // over NVLink; the last block publishes counts / offsets / epoch at every owner.
 int hp_xchg_push_plan(hp_xchg_t x, const float* vals, int64_t T, int64_t V, int32_t P,
-                      const int64_t* send_ids, const int32_t* dest_counts, void* ws,
-                      size_t ws_bytes, void* stream) {
-  HP_REQUIRE(x && send_ids && dest_counts, "NULL argument");
+                      const int64_t* send_ids, const int32_t* dest_counts,
+                      const int64_t* glob_base, void* ws, size_t ws_bytes, void* stream) {
+  HP_REQUIRE(x && send_ids && dest_counts && glob_base, "NULL argument");
   HP_REQUIRE(T == 0 || vals, "NULL vals");
   DedupPlan pl;
   int rc = carve_plan(&pl, ws, ws_bytes, T, x->L.D4 * 4, V, P, x->L.n);
   if (rc) return rc;
   restore_sorted_pos(pl);
   SigView me(x->win);
-  EpiPush epi{x->peers, x->L, dest_counts, send_ids, me.done + 0, x->win};
+  EpiPush epi{x->peers, x->L, dest_counts, send_ids, glob_base, Router(V, P), me.done + 0, x->win};
   pl.T = std::max<int64_t>(T, 1);  // k_combine must run: it carries the publication
   return launch_reduce(pl, vals, epi, static_cast<cudaStream_t>(stream));
 }
 
 // Worker, fused K1+K2+K3 = hp_xchg_plan + hp_xchg_push_plan.
 int hp_xchg_push(hp_xchg_t x, const int64_t* ids, const float* vals, int64_t T, int64_t V,
-                 int32_t P, const int32_t* owner, int64_t* send_ids, int32_t* inv,
-                 int32_t* dest_counts, int32_t* n_uniq, void* ws, size_t ws_bytes, void* stream) {
+                 int32_t P, const int32_t* owner, const int64_t* glob_base, int64_t* send_ids,
+                 int32_t* inv, int32_t* dest_counts, int32_t* n_uniq, void* ws, size_t ws_bytes,
+                 void* stream) {
   int rc = hp_xchg_plan(x, ids, T, V, P, owner, send_ids, inv, dest_counts, n_uniq, ws, ws_bytes,
                         stream);
   if (rc) return rc;
-  return hp_xchg_push_plan(x, vals, T, V, P, send_ids, dest_counts, ws, ws_bytes, stream);
+  return hp_xchg_push_plan(x, vals, T, V, P, send_ids, dest_counts, glob_base, ws, ws_bytes,
+                           stream);
 }
 
 // Owner: wait for every source's push, merge in source order, apply to the
@@ -433,33 +434,33 @@ int hp_xchg_wait(hp_xchg_t x, int32_t which, void* stream) {
 int hp_xchg_merge_apply(hp_xchg_t x, hp_slab slab, hp_optim opt, int32_t wait, void* stream) {
   HP_REQUIRE(x && slab.part_base, "NULL argument");
   HP_REQUIRE(slab.D == x->L.D4 * 4, "slab width differs from the exchange");
+  HP_REQUIRE(opt.kind == HP_OPT_SGD || slab.s0, "optimizer state s0 is NULL");
+  HP_REQUIRE(opt.kind != HP_OPT_ADAM || slab.s1, "Adam state s1 is NULL");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (wait) {
     int rc = hp_xchg_wait(x, 0, stream);
     if (rc) return rc;
   }
   const int64_t total = (int64_t)x->L.n * x->L.cap;
-  k_owner_scatter<<<grid_for(total, 256, sm_count() * 8), 256, 0, st>>>(
-      x->win, x->L, slab.part_base, Router(slab.V, slab.P), x->slot, x->touch, x->list, x->nlist,
-      x->rows_cap);
-  const int lb = (int)std::min<int64_t>(total, x->rows_cap);
-  const int blocks = grid_for(lb, 8, sm_count() * 4);
+  const int blocks = grid_for(total, 8, sm_count() * 8);
   float4* s0 = reinterpret_cast<float4*>(slab.s0);
   float4* s1 = reinterpret_cast<float4*>(slab.s1);
+  const Router route(slab.V, slab.P);
   switch (opt.kind) {
     case HP_OPT_SGD:
-      k_owner_apply<HP_OPT_SGD><<<blocks, 256, 0, st>>>(x->peers, x->win, x->L, s0, s1, opt,
-                                                       x->slot, x->touch, x->list, x->nlist);
+      k_owner_apply<HP_OPT_SGD><<<blocks, 256, 0, st>>>(x->peers, x->win, x->L, slab.part_base,
+                                                       route, s0, s1, opt, x->rows_cap);
       break;
     case HP_OPT_ADAGRAD:
-      k_owner_apply<HP_OPT_ADAGRAD><<<blocks, 256, 0, st>>>(x->peers, x->win, x->L, s0, s1, opt,
-                                                           x->slot, x->touch, x->list, x->nlist);
+      k_owner_apply<HP_OPT_ADAGRAD><<<blocks, 256, 0, st>>>(x->peers, x->win, x->L,
+                                                           slab.part_base, route, s0, s1, opt,
+                                                           x->rows_cap);
       break;
     default:
-      k_owner_apply<HP_OPT_ADAM><<<blocks, 256, 0, st>>>(x->peers, x->win, x->L, s0, s1, opt,
-                                                        x->slot, x->touch, x->list, x->nlist);
+      k_owner_apply<HP_OPT_ADAM><<<blocks, 256, 0, st>>>(x->peers, x->win, x->L, slab.part_base,
+                                                        route, s0, s1, opt, x->rows_cap);
   }
-  HP_LAUNCHED(2, "owner merge/apply");
+  HP_LAUNCHED(1, "owner merge/apply");
   return HP_OK;
 }
 

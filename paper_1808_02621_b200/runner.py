@@ -225,7 +225,7 @@ class HybridRunner:
         if not planned:
             self._plan(tab, ids, slot)
         k(f"push:{name}", True)
-        x.push_plan(vals, tab.V, tab.P, r, tab.wss[slot])
+        x.push_plan(vals, tab.V, tab.P, r, self.glob_base[name], tab.wss[slot])
         k(f"push:{name}", False)
         k(f"wait_push:{name}", True)
         x.wait(0)

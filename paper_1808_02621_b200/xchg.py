@@ -42,14 +42,15 @@ class PeerExchange:
                 call("hp_xchg_open_peer", self.handle, r, C.addressof(buf))
         self.w = torch.as_tensor(_DevPtr(wptr.value, (rows_cap, D)), device=device)
 
-    def push(self, ids, vals, V: int, P: int, owner, out: dict, ws) -> dict:
+    def push(self, ids, vals, V: int, P: int, owner, glob_base, out: dict, ws) -> dict:
         """Fused dedup + route + NVLink push; fills out[send_ids, inv, dest_counts, n_uniq]."""
         from .ops import dedup_ws_bytes
 
         T = ids.numel()
         ws.get(dedup_ws_bytes(T, self.D, P, self.n))
         call("hp_xchg_push", self.handle, ids.data_ptr(), vals.data_ptr(), T, V, P,
-             owner.data_ptr(), out["send_ids"].data_ptr(), out["inv"].data_ptr(),
+             owner.data_ptr(), glob_base.data_ptr(), out["send_ids"].data_ptr(),
+             out["inv"].data_ptr(),
              out["dest_counts"].data_ptr(), out["n_uniq"].data_ptr(), ws.ptr, ws.nbytes,
              torch.cuda.current_stream().cuda_stream)
         return out
@@ -65,11 +66,11 @@ class PeerExchange:
              out["n_uniq"].data_ptr(), ws.ptr, ws.nbytes, torch.cuda.current_stream().cuda_stream)
         return out
 
-    def push_plan(self, vals, V: int, P: int, out: dict, ws) -> None:
+    def push_plan(self, vals, V: int, P: int, out: dict, glob_base, ws) -> None:
         """Value half of push: reduce with the plan in ``ws`` and store into owners' inboxes."""
         call("hp_xchg_push_plan", self.handle, vals.data_ptr(), vals.shape[0], V, P,
-             out["send_ids"].data_ptr(), out["dest_counts"].data_ptr(), ws.ptr, ws.nbytes,
-             torch.cuda.current_stream().cuda_stream)
+             out["send_ids"].data_ptr(), out["dest_counts"].data_ptr(), glob_base.data_ptr(),
+             ws.ptr, ws.nbytes, torch.cuda.current_stream().cuda_stream)
 
     def wait(self, which: int) -> None:
         """0: until every source pushed; 1: until every owner applied."""
