@@ -132,7 +132,10 @@ k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
       }
     }
   }
-  if constexpr (Epi::kRemote) __threadfence_system();
+  if constexpr (Epi::kRemote) {  // one cumulative release per block, after the barrier
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
+  }
   HP_SPAN_END(SP_REDUCE);
 }
 
@@ -192,9 +195,11 @@ __global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
   }
   if constexpr (Epi::kRemote) {
     __shared__ bool s_last;
-    __threadfence_system();
     __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(epi.done, 1) == (int)gridDim.x - 1;
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      s_last = atomicAdd(epi.done, 1) == (int)gridDim.x - 1;
+    }
     __syncthreads();
     if (s_last) {
       __threadfence_system();

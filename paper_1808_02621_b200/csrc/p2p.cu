@@ -273,9 +273,13 @@ k_owner_apply(PeerTable peers, void* my_win, WinLayout L, const int64_t* __restr
       }
     }
   }
-  __threadfence_system();
+  // one cumulative system-scope release per block (after the barrier) orders
+  // every thread's peer stores before the block's arrival
   __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&sig.done[1], 1) == (int)gridDim.x - 1;
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    s_last = atomicAdd(&sig.done[1], 1) == (int)gridDim.x - 1;
+  }
   __syncthreads();
   if (s_last) {
     __threadfence_system();
@@ -552,11 +556,13 @@ k_ar_scatter(PeerTable peers, void* my_win, ArLayout A, const float4* __restrict
       if (j < c4) dst[j] = v[u];
     }
   }
-  __threadfence_system();
   __syncthreads();
   SigView sig(my_win);
   const int nblocks = gridDim.x * gridDim.y;
-  if (threadIdx.x == 0) s_last = atomicAdd(&sig.done[2], 1) == nblocks - 1;
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    s_last = atomicAdd(&sig.done[2], 1) == nblocks - 1;
+  }
   __syncthreads();
   if (s_last) {
     __threadfence_system();
@@ -619,10 +625,12 @@ k_ar_reduce_gather(PeerTable peers, void* my_win, ArLayout A, float scale) {
         put4<OutT>(static_cast<char*>(peers.base[r]) + A.out_off, o4, v);
     }
   }
-  __threadfence_system();
   __syncthreads();
   SigView sig(my_win);
-  if (threadIdx.x == 0) s_last = atomicAdd(&sig.done[3], 1) == (int)gridDim.x - 1;
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    s_last = atomicAdd(&sig.done[3], 1) == (int)gridDim.x - 1;
+  }
   __syncthreads();
   if (s_last) {
     __threadfence_system();
