@@ -170,13 +170,14 @@ __device__ __forceinline__ void opt_update(float& w, float& a, float& b, float g
   }
 }
 
-// ---- owner: one warp per inbox entry (source s, index k). The entry of the
-// lowest-ranked source with a valid tag for its row owns the row: it sums the
-// contributions in source order, scales, applies, stores the updated row back
-// into every contributor's return buffer (peer stores); last block raises
-// "applied". Columns go in pairs per lane with all loads of a pair in flight.
-template <int OPT>
-__global__ void __launch_bounds__(256)
+// ---- owner: one group of TPI threads per inbox entry (source s, index k);
+// each thread owns VPT float4 columns, so a row is one load round trip. The
+// entry of the lowest-ranked source with a valid tag for its row owns the row:
+// it sums the contributions in source order, scales, applies, and stores the
+// updated row back into every contributor's return buffer (peer stores). The
+// last block raises "applied".
+template <int OPT, int TPI, int VPT>
+__global__ void __launch_bounds__(256, VPT >= 4 ? 2 : 3)
 k_owner_apply(PeerTable peers, void* my_win, WinLayout L, const int64_t* __restrict__ part_base,
               Router route, float4* s0, float4* s1, hp_optim o, int64_t rows_cap) {
   __shared__ bool s_last;
@@ -189,18 +190,19 @@ k_owner_apply(PeerTable peers, void* my_win, WinLayout L, const int64_t* __restr
   const unsigned long long* slot = reinterpret_cast<const unsigned long long*>(win + L.slot_off);
   const int n = L.n, D4 = L.D4;
   const unsigned epoch = (unsigned)*sig.epoch;
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31, q = threadIdx.x % TPI;
+  constexpr int GPB = 256 / TPI;
   const int64_t total = (int64_t)n * L.cap;
-  for (int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < total; e += nw) {
+  for (int64_t e = (int64_t)blockIdx.x * GPB + threadIdx.x / TPI; e < total;
+       e += (int64_t)gridDim.x * GPB) {
     const int s = (int)(e / L.cap);
-    if (e - (int64_t)s * L.cap >= sig.push_count[s]) continue;  // warp-uniform
+    if (e - (int64_t)s * L.cap >= sig.push_count[s]) continue;  // group-uniform
     const int64_t id = inbox_ids[e];
     const int p = route.part(id);
     const int64_t b = part_base[p];
     const int64_t row = b + (id - route.lo(p));
     if (b < 0 || row >= rows_cap) {
-      if (lane == 0) atomicOr(sig.err, 16);
+      if (q == 0) atomicOr(sig.err, 16);
       continue;
     }
     const unsigned long long ent = lane < n ? slot[row * n + lane] : 0ull;
@@ -210,67 +212,57 @@ k_owner_apply(PeerTable peers, void* my_win, WinLayout L, const int64_t* __restr
     const int cnt = __popc(have);
     const int from = lane < cnt ? (int)__fns(have, 0, lane + 1) : lane;
     const int cidx = __shfl_sync(0xffffffffu, (int)(uint32_t)ent, from);
-    for (int c0 = 0; c0 < D4; c0 += 64) {
-      const int ca = c0 + lane, cb = c0 + 32 + lane;
-      const bool acta = ca < D4, actb = cb < D4;
-      const int64_t oa = row * D4 + ca, ob = row * D4 + cb;
-      float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-      float4 wa = acta ? w[oa] : z, wb = actb ? w[ob] : z;
-      float4 aa = z, ab = z, ba = z, bb = z;
-      if (OPT != HP_OPT_SGD) {
-        if (acta) aa = s0[oa];
-        if (actb) ab = s0[ob];
-      }
-      if (OPT == HP_OPT_ADAM) {
-        if (acta) ba = s1[oa];
-        if (actb) bb = s1[ob];
-      }
-      float4 ga = z, gb = z;
-      for (int j0 = 0; j0 < cnt; j0 += 2) {  // contributions, source order
-        float4 xa[2], xb[2];
+    float4 wv[VPT], av[VPT], bv[VPT], g[VPT];
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int idx = __shfl_sync(0xffffffffu, cidx, (j0 + u) & 31);
-          if (j0 + u < cnt) {
-            if (acta) xa[u] = inbox[(int64_t)idx * D4 + ca];
-            if (actb) xb[u] = inbox[(int64_t)idx * D4 + cb];
-          }
-        }
+    for (int v = 0; v < VPT; ++v) {
+      const int c = q + v * TPI;
+      const int64_t off = row * D4 + c;
+      wv[v] = av[v] = bv[v] = g[v] = z;
+      if (c < D4) {
+        wv[v] = w[off];
+        if (OPT != HP_OPT_SGD) av[v] = s0[off];
+        if (OPT == HP_OPT_ADAM) bv[v] = s1[off];
+      }
+    }
+    for (int j0 = 0; j0 < cnt; j0 += 2) {  // contributions, in source order
+      float4 x[2][VPT];
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
-          if (j0 + u < cnt) {
-            ga = f4_add(ga, xa[u]);
-            gb = f4_add(gb, xb[u]);
-          }
+      for (int u = 0; u < 2; ++u) {
+        const int idx = __shfl_sync(0xffffffffu, cidx, (j0 + u) & 31);
+#pragma unroll
+        for (int v = 0; v < VPT; ++v)
+          if (j0 + u < cnt && q + v * TPI < D4) x[u][v] = inbox[(int64_t)idx * D4 + q + v * TPI];
       }
-      if (acta) {
-        opt_update<OPT>(wa.x, aa.x, ba.x, ga.x, o);
-        opt_update<OPT>(wa.y, aa.y, ba.y, ga.y, o);
-        opt_update<OPT>(wa.z, aa.z, ba.z, ga.z, o);
-        opt_update<OPT>(wa.w, aa.w, ba.w, ga.w, o);
-        w[oa] = wa;
-        if (OPT != HP_OPT_SGD) s0[oa] = aa;
-        if (OPT == HP_OPT_ADAM) s1[oa] = ba;
-      }
-      if (actb) {
-        opt_update<OPT>(wb.x, ab.x, bb.x, gb.x, o);
-        opt_update<OPT>(wb.y, ab.y, bb.y, gb.y, o);
-        opt_update<OPT>(wb.z, ab.z, bb.z, gb.z, o);
-        opt_update<OPT>(wb.w, ab.w, bb.w, gb.w, o);
-        w[ob] = wb;
-        if (OPT != HP_OPT_SGD) s0[ob] = ab;
-        if (OPT == HP_OPT_ADAM) s1[ob] = bb;
-      }
-      // pull, fused: the updated row goes back to each contributor's send slot
-      for (int j = 0; j < cnt; ++j) {
-        const int idx = __shfl_sync(0xffffffffu, cidx, j);
-        const int src = idx / (int)L.cap;
-        const int64_t ret_row = sig.push_off[src] + (idx - (int64_t)src * L.cap);
-        float4* ret = reinterpret_cast<float4*>(static_cast<char*>(peers.base[src]) + L.ret_off) +
-                      ret_row * D4;
-        if (acta) ret[ca] = wa;
-        if (actb) ret[cb] = wb;
-      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < VPT; ++v)
+          if (j0 + u < cnt) g[v] = f4_add(g[v], x[u][v]);
+    }
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) {
+      const int c = q + v * TPI;
+      if (c >= D4) continue;
+      opt_update<OPT>(wv[v].x, av[v].x, bv[v].x, g[v].x, o);
+      opt_update<OPT>(wv[v].y, av[v].y, bv[v].y, g[v].y, o);
+      opt_update<OPT>(wv[v].z, av[v].z, bv[v].z, g[v].z, o);
+      opt_update<OPT>(wv[v].w, av[v].w, bv[v].w, g[v].w, o);
+      const int64_t off = row * D4 + c;
+      w[off] = wv[v];
+      if (OPT != HP_OPT_SGD) s0[off] = av[v];
+      if (OPT == HP_OPT_ADAM) s1[off] = bv[v];
+    }
+    // pull, fused: the updated row goes back to each contributor's send slot
+    for (int j = 0; j < cnt; ++j) {
+      const int idx = __shfl_sync(0xffffffffu, cidx, j);
+      const int src = idx / (int)L.cap;
+      const int64_t ret_row = sig.push_off[src] + (idx - (int64_t)src * L.cap);
+      float4* ret = reinterpret_cast<float4*>(static_cast<char*>(peers.base[src]) + L.ret_off) +
+                    ret_row * D4;
+#pragma unroll
+      for (int v = 0; v < VPT; ++v)
+        if (q + v * TPI < D4) ret[q + v * TPI] = wv[v];
     }
   }
   // one cumulative system-scope release per block (after the barrier) orders
@@ -435,6 +427,28 @@ int hp_xchg_wait(hp_xchg_t x, int32_t which, void* stream) {
   return HP_OK;
 }
 
+extern "C++" {
+template <int OPT, int TPI, int VPT>
+void launch_owner_apply(const hp_xchg_s* x, const hp_slab& slab, const hp_optim& opt,
+                        cudaStream_t st) {
+  const int64_t total = (int64_t)x->L.n * x->L.cap;
+  const int blocks = grid_for(total, 256 / TPI, sm_count() * (VPT >= 4 ? 2 : 3));  // one wave
+  k_owner_apply<OPT, TPI, VPT><<<blocks, 256, 0, st>>>(
+      x->peers, x->win, x->L, slab.part_base, Router(slab.V, slab.P),
+      reinterpret_cast<float4*>(slab.s0), reinterpret_cast<float4*>(slab.s1), opt, x->rows_cap);
+}
+
+template <int OPT>
+void dispatch_owner_apply(const hp_xchg_s* x, const hp_slab& slab, const hp_optim& opt, int D4,
+                          cudaStream_t st) {
+  if (D4 <= 32) launch_owner_apply<OPT, 32, 1>(x, slab, opt, st);
+  else if (D4 <= 64) launch_owner_apply<OPT, 32, 2>(x, slab, opt, st);
+  else if (D4 <= 128) launch_owner_apply<OPT, 64, 2>(x, slab, opt, st);
+  else if (D4 <= 256) launch_owner_apply<OPT, 64, 4>(x, slab, opt, st);
+  else launch_owner_apply<OPT, 128, 4>(x, slab, opt, st);
+}
+}  // extern "C++"
+
 int hp_xchg_merge_apply(hp_xchg_t x, hp_slab slab, hp_optim opt, int32_t wait, void* stream) {
   HP_REQUIRE(x && slab.part_base, "NULL argument");
   HP_REQUIRE(slab.D == x->L.D4 * 4, "slab width differs from the exchange");
@@ -445,24 +459,11 @@ int hp_xchg_merge_apply(hp_xchg_t x, hp_slab slab, hp_optim opt, int32_t wait, v
     int rc = hp_xchg_wait(x, 0, stream);
     if (rc) return rc;
   }
-  const int64_t total = (int64_t)x->L.n * x->L.cap;
-  const int blocks = grid_for(total, 8, sm_count() * 8);
-  float4* s0 = reinterpret_cast<float4*>(slab.s0);
-  float4* s1 = reinterpret_cast<float4*>(slab.s1);
-  const Router route(slab.V, slab.P);
+  const int D4 = x->L.D4;
   switch (opt.kind) {
-    case HP_OPT_SGD:
-      k_owner_apply<HP_OPT_SGD><<<blocks, 256, 0, st>>>(x->peers, x->win, x->L, slab.part_base,
-                                                       route, s0, s1, opt, x->rows_cap);
-      break;
-    case HP_OPT_ADAGRAD:
-      k_owner_apply<HP_OPT_ADAGRAD><<<blocks, 256, 0, st>>>(x->peers, x->win, x->L,
-                                                           slab.part_base, route, s0, s1, opt,
-                                                           x->rows_cap);
-      break;
-    default:
-      k_owner_apply<HP_OPT_ADAM><<<blocks, 256, 0, st>>>(x->peers, x->win, x->L, slab.part_base,
-                                                        route, s0, s1, opt, x->rows_cap);
+    case HP_OPT_SGD: dispatch_owner_apply<HP_OPT_SGD>(x, slab, opt, D4, st); break;
+    case HP_OPT_ADAGRAD: dispatch_owner_apply<HP_OPT_ADAGRAD>(x, slab, opt, D4, st); break;
+    default: dispatch_owner_apply<HP_OPT_ADAM>(x, slab, opt, D4, st);
   }
   HP_LAUNCHED(1, "owner merge/apply");
   return HP_OK;
