@@ -110,23 +110,6 @@ __device__ __forceinline__ float4 tree_sum_partials(const float4* src, int n0, i
   return acc;
 }
 
-// The last-arriving chunk of long segment li sums all its partials (fixed
-// tree) and runs the epilogue. Out of line: keeps k_reduce's hot loop free of
-// this rarely-taken path's registers.
-template <int TPI, int VPT, class Epi>
-__device__ __forceinline__ void finish_long(const DedupPlan& pl, int li, const Epi& epi, int q) {
-  const int D4 = pl.D >> 2;
-  const int4 d = pl.longs[li];
-  const float4* P = reinterpret_cast<const float4*>(pl.partials) + (int64_t)d.x * D4;
-  if (d.z < 0) return;
-  for (int v = 0; v < VPT; ++v) {
-    const int c4 = q + v * TPI;
-    if (c4 >= D4) continue;
-    typename Epi::Pre pr = epi.load(d.z, c4);
-    epi.store(d.z, c4, tree_sum_partials(P + c4, d.y, D4), pr);
-  }
-}
-
 template <int TPI>
 __device__ __forceinline__ void group_sync() {
   if constexpr (TPI == 32) {
@@ -152,10 +135,6 @@ template <int TPI, int VPT, int B, bool FINISH, class Epi>
 __global__ void __launch_bounds__(256, 3)
 k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
   __shared__ int s_last_grp[256 / TPI];
-  __shared__ int s_nfin;
-  extern __shared__ int s_fin[];  // long segments this block finishes (<= its items)
-  if (FINISH && threadIdx.x == 0) s_nfin = 0;
-  if (FINISH) __syncthreads();
   const float4* __restrict__ vals = reinterpret_cast<const float4*>(vals_f);
   float4* partials = reinterpret_cast<float4*>(pl.partials);
   const int D4 = pl.D >> 2;
@@ -209,13 +188,19 @@ k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
         s_last_grp[grp] = atomicAdd(&pl.long_cnt[li], 1) == n0 - 1;
       }
       group_sync<TPI>();
-      if (q == 0 && s_last_grp[grp]) s_fin[atomicAdd(&s_nfin, 1)] = li;  // finish after the loop
+      if (s_last_grp[grp]) {  // every chunk's partial is in place
+        __threadfence();
+        const int4 d = pl.longs[li];
+        const float4* P = partials + (int64_t)d.x * D4;
+#pragma unroll
+        for (int v = 0; v < VPT; ++v) {
+          const int c4 = q + v * TPI;
+          if (c4 >= D4 || d.z < 0) continue;
+          typename Epi::Pre pr = epi.load(d.z, c4);
+          epi.store(d.z, c4, tree_sum_partials(P + c4, d.y, D4), pr);
+        }
+      }
     }
-  }
-  if constexpr (FINISH) {  // every chunk of these segments is in place: finish them
-    __syncthreads();
-    __threadfence();
-    for (int t = grp; t < s_nfin; t += GPB) finish_long<TPI, VPT>(pl, s_fin[t], epi, q);
   }
   if constexpr (Epi::kRemote) {  // one cumulative release per block, after the barrier
     __syncthreads();
@@ -293,10 +278,9 @@ void launch_k_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, boo
   // <= one group per item; peer-store epilogues stay in one resident wave so
   // each block pays its system-scope fence once
   const int blocks = grid_for(pl.T, 256 / TPI, sm_count() * (Epi::kRemote ? 3 : 16));
-  if (finish) {  // a block records at most one long segment per item it processes
-    const int per_block = (int)((pl.T + blocks - 1) / blocks) + 256 / TPI;
-    k_reduce<TPI, VPT, B, true, Epi><<<blocks, 256, per_block * 4, st>>>(pl, vals, epi);
-  } else
+  if (finish)
+    k_reduce<TPI, VPT, B, true, Epi><<<blocks, 256, 0, st>>>(pl, vals, epi);
+  else
     k_reduce<TPI, VPT, B, false, Epi><<<blocks, 256, 0, st>>>(pl, vals, epi);
 }
 
