@@ -149,14 +149,10 @@ __device__ __forceinline__ void emit_items(const DedupPlan& pl, int u, int j0, i
                                            int bi, int bp, int bl) {
   const int n0 = (L + HP_CHUNK - 1) / HP_CHUNK;
   const bool lg = L > HP_CHUNK;
-  // item.w: 1 = final; -(long index + 1) = chunk of long segment `bl`
   for (int k = 0; k < n0; ++k)
     pl.items[bi + k] = make_int4(j0 + k * HP_CHUNK, min(HP_CHUNK, L - k * HP_CHUNK),
-                                 lg ? bp + k : dst, lg ? -(bl + 1) : 1);
-  if (lg) {
-    pl.longs[bl] = make_int4(bp, n0, dst, u);
-    pl.long_cnt[bl] = 0;
-  }
+                                 lg ? bp + k : dst, lg ? 0 : 1);
+  if (lg) pl.longs[bl] = make_int4(bp, n0, dst, u);
 }
 
 // ------------------------------------------------------------------ cluster path
@@ -681,7 +677,6 @@ size_t dedup_ws_bytes(int64_t T, int32_t D, int32_t P) {
   s += 3 * align256(4 * (Tc + 1));    // uniq_key, seg_start, item_off
   s += 5 * align256(4 * Tc);          // segidx, sigma, part_off, dst, long_tmp
   s += align256(16 * Tc) + align256(16 * (Tc / HP_CHUNK + 2));  // items, longs
-  s += align256(4 * (Tc / HP_CHUNK + 2));                         // long_cnt
   s += align256(4 * ((size_t)P + 1)) + 2 * align256(4 * (size_t)P);
   s += align256(4 * HP_RADIX * ntiles) + align256(4 * HP_RADIX);
   s += align256(4 * nscan);
@@ -728,7 +723,6 @@ int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, i
   pl->long_tmp = (int32_t*)take(4 * Tc);
   pl->items = (int4*)take(16 * Tc);
   pl->longs = (int4*)take(16 * (Tc / HP_CHUNK + 2));
-  pl->long_cnt = (int32_t*)take(4 * (Tc / HP_CHUNK + 2));
   pl->first_u = (int32_t*)take(4 * ((size_t)P + 1));
   pl->part_base = (int32_t*)take(4 * (size_t)P);
   pl->zero_owner = (int32_t*)take(4 * (size_t)P);

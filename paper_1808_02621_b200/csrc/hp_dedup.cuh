@@ -27,7 +27,6 @@ struct DedupPlan {
   int4* items;          // [T] reduce items {j0, n, dst, final}: rows sorted[j0, j0+n)
   int32_t* part_off;    // [T] partial-buffer slot of segment u (large-path scratch)
   int4* longs;          // [T/C+1] long segments {partial slot, n0, dst, u}
-  int32_t* long_cnt;    // [T/C+1] finished-chunk counters (last-arriver finishing)
   int32_t* dst;         // [T] destination row of segment u (send slot or slab row)
   int32_t* long_tmp;    // [T] large-path scratch
   int32_t* first_u;     // [P+1] first unique index of partition p
@@ -53,9 +52,6 @@ int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, i
 int build_plan(DedupPlan& pl, const int64_t* ids, const int32_t* owner,
                const int64_t* dst_part_base, int64_t* send_ids, int32_t* counts, int32_t* inv,
                int32_t* dest_counts, int32_t* n_uniq, cudaStream_t stream);
-
-// True when build_plan takes the single-launch cluster path for this plan.
-inline bool cluster_path(const DedupPlan& pl) { return pl.T <= HP_SMALL_MAX && pl.P <= 2048; }
 
 // Re-point pl.sorted_pos at the buffer a previous build_plan (same T, P, V) left it in.
 void restore_sorted_pos(DedupPlan& pl);

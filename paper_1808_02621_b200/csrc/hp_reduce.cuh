@@ -83,70 +83,21 @@ struct EpiApply {
 // partial row for k_combine. Small groups + <= 64 registers keep many items
 // in flight per SM: the kernel is latency-bound on the item chain
 // (descriptor -> positions/table rows -> gradient rows).
-// ((0 + r0) + r1) + ... over n <= HP_CHUNK rows of stride D4, 8 loads in flight.
-__device__ __forceinline__ float4 seq_sum_rows(const float4* src, int n, int D4) {
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int j0 = 0; j0 < n; j0 += 8) {
-    float4 x[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j0 + j < n) x[j] = src[(int64_t)(j0 + j) * D4];
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j0 + j < n) acc = f4_add(acc, x[j]);
-  }
-  return acc;
-}
-
-// Upper levels for segments longer than HP_CHUNK: one CTA per long segment
-// {partial slot, n0, dst, u}, in place over its partial rows.
-// Sum of n0 <= HP_CHUNK^2 level-0 partials following the tree: sequential
-// groups of HP_CHUNK, then the sequential sum of the group sums.
-__device__ __forceinline__ float4 tree_sum_partials(const float4* src, int n0, int D4) {
-  if (n0 <= HP_CHUNK) return seq_sum_rows(src, n0, D4);
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int g = 0; g < n0; g += HP_CHUNK)
-    acc = f4_add(acc, seq_sum_rows(src + (int64_t)g * D4, min(HP_CHUNK, n0 - g), D4));
-  return acc;
-}
-
-template <int TPI>
-__device__ __forceinline__ void group_sync() {
-  if constexpr (TPI == 32) {
-    __syncwarp();
-  } else {
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)(threadIdx.x / TPI)), "r"(TPI) : "memory");
-  }
-}
-
-// Level 0 of the summation tree. A group of TPI threads owns an item
-// {j0, n <= HP_CHUNK, dst, w}; each thread owns VPT float4 columns
-// (c4 = lane-in-group + k*TPI). Row positions are loaded once per warp and
-// broadcast by shuffle; B rows x VPT columns are in flight per thread before
-// the in-order fp32 adds. Final items (w > 0) run the epilogue (its table-row
-// loads are issued together with the positions); chunks of long segments
-// (w = -(li+1)) write a partial row. With FINISH (every long segment has at
-// most HP_CHUNK^2 rows, i.e. the cluster path), the last chunk to arrive at a
-// long segment computes the rest of the tree and runs the epilogue, so no
-// k_combine launch is needed; for peer-store epilogues the last block then
-// publishes (grid_done). Small groups + few registers keep many items in
-// flight per SM: the kernel is latency-bound on the item chain.
-template <int TPI, int VPT, int B, bool FINISH, class Epi>
+template <int TPI, int VPT, int B, class Epi>
 __global__ void __launch_bounds__(256, 3)
 k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
-  __shared__ int s_last_grp[256 / TPI];
   const float4* __restrict__ vals = reinterpret_cast<const float4*>(vals_f);
   float4* partials = reinterpret_cast<float4*>(pl.partials);
   const int D4 = pl.D >> 2;
   constexpr int GPB = 256 / TPI;
-  const int q = threadIdx.x % TPI, grp = threadIdx.x / TPI;
+  const int q = threadIdx.x % TPI;
   const int lane = threadIdx.x & 31;
   HP_SPAN_BEGIN(SP_REDUCE);
   const int n_items = pl.counters[C_ITEMS];
-  for (int it = blockIdx.x * GPB + grp; it < n_items; it += gridDim.x * GPB) {
+  for (int it = blockIdx.x * GPB + threadIdx.x / TPI; it < n_items; it += gridDim.x * GPB) {
     const int4 item = pl.items[it];
     const int j0 = item.x, n = item.y, dst = item.z;
-    const bool fin = item.w > 0;
+    const bool fin = item.w != 0;
     typename Epi::Pre pre[VPT];
 #pragma unroll
     for (int v = 0; v < VPT; ++v)
@@ -170,54 +121,41 @@ k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
         for (int v = 0; v < VPT; ++v)
           if (jb + e < n) acc[v] = f4_add(acc[v], x[e][v]);
     }
-    if (fin) {
 #pragma unroll
-      for (int v = 0; v < VPT; ++v)
-        if (q + v * TPI < D4 && dst >= 0) epi.store(dst, q + v * TPI, acc[v], pre[v]);
-      continue;
-    }
-#pragma unroll
-    for (int v = 0; v < VPT; ++v)
-      if (q + v * TPI < D4) partials[(int64_t)dst * D4 + q + v * TPI] = acc[v];
-    if constexpr (FINISH) {
-      const int li = -item.w - 1;
-      __threadfence();
-      group_sync<TPI>();
-      if (q == 0) {
-        const int n0 = pl.longs[li].y;
-        s_last_grp[grp] = atomicAdd(&pl.long_cnt[li], 1) == n0 - 1;
-      }
-      group_sync<TPI>();
-      if (s_last_grp[grp]) {  // every chunk's partial is in place
-        __threadfence();
-        const int4 d = pl.longs[li];
-        const float4* P = partials + (int64_t)d.x * D4;
-#pragma unroll
-        for (int v = 0; v < VPT; ++v) {
-          const int c4 = q + v * TPI;
-          if (c4 >= D4 || d.z < 0) continue;
-          typename Epi::Pre pr = epi.load(d.z, c4);
-          epi.store(d.z, c4, tree_sum_partials(P + c4, d.y, D4), pr);
-        }
+    for (int v = 0; v < VPT; ++v) {
+      const int c4 = q + v * TPI;
+      if (c4 >= D4) continue;
+      if (fin) {
+        if (dst >= 0) epi.store(dst, c4, acc[v], pre[v]);
+      } else {
+        partials[(int64_t)dst * D4 + c4] = acc[v];
       }
     }
   }
   if constexpr (Epi::kRemote) {  // one cumulative release per block, after the barrier
     __syncthreads();
     if (threadIdx.x == 0) __threadfence_system();
-    if constexpr (FINISH) {  // every push of this grid is done: the last block publishes
-      __shared__ bool s_last;
-      if (threadIdx.x == 0) s_last = atomicAdd(epi.done, 1) == (int)gridDim.x - 1;
-      __syncthreads();
-      if (s_last) {
-        __threadfence_system();
-        epi.grid_done();
-      }
-    }
   }
   HP_SPAN_END(SP_REDUCE);
 }
 
+// ((0 + r0) + r1) + ... over n <= HP_CHUNK rows of stride D4, 8 loads in flight.
+__device__ __forceinline__ float4 seq_sum_rows(const float4* src, int n, int D4) {
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int j0 = 0; j0 < n; j0 += 8) {
+    float4 x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j0 + j < n) x[j] = src[(int64_t)(j0 + j) * D4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j0 + j < n) acc = f4_add(acc, x[j]);
+  }
+  return acc;
+}
+
+// Upper levels for segments longer than HP_CHUNK: one CTA per long segment
+// {partial slot, n0, dst, u}, in place over its partial rows.
 template <class Epi>
 __global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
   HP_SPAN_BEGIN(SP_COMBINE);
@@ -272,32 +210,24 @@ __global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
 }
 
 template <int TPI, int VPT, class Epi>
-void launch_k_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, bool finish,
-                     cudaStream_t st) {
+void launch_k_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaStream_t st) {
   constexpr int B = VPT >= 8 ? 1 : 8 / VPT;
   // <= one group per item; peer-store epilogues stay in one resident wave so
   // each block pays its system-scope fence once
   const int blocks = grid_for(pl.T, 256 / TPI, sm_count() * (Epi::kRemote ? 3 : 16));
-  if (finish)
-    k_reduce<TPI, VPT, B, true, Epi><<<blocks, 256, 0, st>>>(pl, vals, epi);
-  else
-    k_reduce<TPI, VPT, B, false, Epi><<<blocks, 256, 0, st>>>(pl, vals, epi);
+  k_reduce<TPI, VPT, B, Epi><<<blocks, 256, 0, st>>>(pl, vals, epi);
 }
 
 template <class Epi>
 int launch_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaStream_t st) {
   if (pl.T == 0) return HP_OK;
   const int D4 = pl.D >> 2;
-  // cluster-path plans have T <= 16384, so every long segment has <= 512 chunks
-  // and k_reduce finishes it in place; larger plans need k_combine's levels
-  const bool finish = cluster_path(pl);
-  if (D4 <= 32) launch_k_reduce<32, 1>(pl, vals, epi, finish, st);
-  else if (D4 <= 64) launch_k_reduce<32, 2>(pl, vals, epi, finish, st);
-  else if (D4 <= 128) launch_k_reduce<64, 2>(pl, vals, epi, finish, st);
-  else if (D4 <= 256) launch_k_reduce<64, 4>(pl, vals, epi, finish, st);
-  else launch_k_reduce<128, 4>(pl, vals, epi, finish, st);
+  if (D4 <= 32) launch_k_reduce<32, 1>(pl, vals, epi, st);
+  else if (D4 <= 64) launch_k_reduce<32, 2>(pl, vals, epi, st);
+  else if (D4 <= 128) launch_k_reduce<64, 2>(pl, vals, epi, st);
+  else if (D4 <= 256) launch_k_reduce<64, 4>(pl, vals, epi, st);
+  else launch_k_reduce<128, 4>(pl, vals, epi, st);
   HP_LAUNCHED(1, "k_reduce");
-  if (finish) return HP_OK;
   // long segments are few (<= T/33); a small grid keeps the publication cheap
   const int cblocks = grid_for(pl.T / (HP_CHUNK + 1) + 1, 1, Epi::kRemote ? 32 : sm_count());
   k_combine<Epi><<<cblocks, 256, 0, st>>>(pl, epi);
