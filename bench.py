@@ -40,6 +40,30 @@ METRIC = "hybrid-step words/sec"
 UNIT = "words/s"
 
 
+def metric_for(wl, world: int):
+    """(metric, unit, units per step of the whole job, per-batch helper).
+
+    LM/NMT-shaped workloads: words/s (n * 2560 per step). Sparse
+    microbench: unique sparse rows/s summed over workers. Dense-only: allreduce
+    bus GB/s = 2(n-1)/n * S * 4 / t (NCCL-tests convention; HBM GB/s at n=1).
+    """
+    if wl.words_per_worker:
+        return METRIC, UNIT
+    if wl.tables:
+        return "sparse rows/sec", "rows/s"
+    return "dense allreduce bus GB/s", "GB/s"
+
+
+def units_per_step(wl, world: int, host_batches, rank: int) -> float:
+    if wl.words_per_worker:
+        return float(world * wl.words_per_worker)
+    if wl.tables:
+        u = np.mean([sum(len(np.unique(b[t.name][0])) for t in wl.tables) for b in host_batches])
+        return float(u) * world  # approximation until all-reduced below
+    S = sum(wl.dense.values()) * 4
+    return (2.0 * (world - 1) / world * S if world > 1 else 2.0 * S) / 1e9
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -153,16 +177,20 @@ def run_reference(args, wl):
     n = args.gpus
     for _ in range(max(args.warmup, 0) and 1):
         pass
-    value, dt = time_cpu(wl, n, max(args.steps, 1), seed=0)
+    _, dt = time_cpu(wl, n, max(args.steps, 1), seed=0)
+    from paper_1808_02621_b200.synth import make_batch
+
+    metric, unit = metric_for(wl, n)
+    value = units_per_step(wl, n, [make_batch(wl, 0, 0)], 0) / dt
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n,
+        "impl": "reference", "metric": metric, "value": value, "unit": unit, "n_gpus": n,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": config(args, wl),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": unit, "cores": 1, "kind": "port",
                          "sample": f"{args.steps} full oracle steps of {n} simulated worker(s), "
                                    "numpy single-threaded"},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -227,7 +255,7 @@ def main():
                 for k, v in b.items()}
 
     batches = [to_dev(b) for b in host]
-    use_graph = (world == 1 or args.exchange == "p2p") and not args.no_graph and opt.kind != "adam"
+    use_graph = (world == 1 or args.exchange == "p2p") and not args.no_graph
     stream = torch.cuda.current_stream()
 
     for i in range(args.warmup):
@@ -273,8 +301,13 @@ def main():
         barrier()
         torch.cuda.synchronize()
     t_dev = max_over_ranks(e0.elapsed_time(e1) / 1e3)
-    words = world * wl.words_per_worker * args.steps
-    value = words / t_dev
+    metric, unit = metric_for(wl, world)
+    ups = units_per_step(wl, world, host, rank)
+    if wl.tables and not wl.words_per_worker and world > 1:  # exact sum of unique rows
+        t_u = torch.tensor([ups / world], dtype=torch.float64, device=dev)
+        dist.all_reduce(t_u)
+        ups = float(t_u.item())
+    value = ups * args.steps / t_dev
 
     # ---- per-kernel timing (eager steps, events around K4 / K5 launches)
     kern = {}
@@ -359,25 +392,26 @@ def main():
     b.record(stream)
     torch.cuda.synchronize()
     t_e2e = max_over_ranks(a.elapsed_time(b) / 1e3)
-    e2e_value = world * wl.words_per_worker * ke / t_e2e
+    e2e_value = ups * ke / t_e2e
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, dt = time_cpu(wl, 1, args.cpu_steps)
-        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
+        _, dt = time_cpu(wl, 1, args.cpu_steps)
+        v = ups / dt
+        cpu = {"value": v, "unit": unit, "cores": 1, "kind": "port",
                "sample": f"{args.cpu_steps} full oracle steps (1 worker, numpy), {dt*1e3:.1f} ms/step"}
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_dev / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (Zipf(1.1) ids, normal grads, hash-initialised tables)",
             "config": config(args, wl) | {"rotations": R, "cuda_graph": bool(graphs),
                                           "exchange": runner.exchange,
                                           "dense_exchange": runner.dense_exchange},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": ke},
             "gpu_launches": launches_per_step * args.steps,
             "launches_per_step": launches_per_step,

@@ -53,6 +53,12 @@ typedef struct hp_optim {
   float eps;              /* Adam epsilon */
   float lr_t;             /* Adam bias-corrected step size for this step */
   float agg_scale;        /* 1/n ('mean') or 1 ('sum') applied to the merged gradient */
+  /* Optional (graph replays): when lr_t_table is non-NULL the kernels use
+   * lr_t_table[min(*step_ctr, table_len - 1)] instead of lr_t; the caller
+   * advances *step_ctr on the device with hp_step_counter_inc each step. */
+  const float* lr_t_table;
+  const int32_t* step_ctr;
+  int32_t table_len;
 } hp_optim;
 
 /* Sharded table slab owned by one rank: the rows of every partition it owns,
@@ -109,6 +115,9 @@ int hp_dedup_plan(const int64_t* ids, int64_t T, int32_t D, int64_t V, int32_t P
 /* Error word of the last plan built in ws (bit 0: an id was outside [0, V),
  * bit 1: a row was not homed on this rank). Synchronises the stream. */
 int hp_plan_status(const void* ws, int32_t* out_err, void* stream);
+
+/* Device step counter for hp_optim.step_ctr: ++*ctr on the stream (1 thread). */
+int hp_step_counter_inc(int32_t* ctr, void* stream);
 
 /* ---------------------------------------------------------------- K4
  * Fused merge + scatter-apply on the owner.

@@ -22,7 +22,8 @@ i32, i64, u64, f32, sz = C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_size_t
 class Optim(C.Structure):
     _fields_ = [("kind", i32), ("lr", f32), ("beta1", f32), ("beta2", f32),
                 ("one_minus_beta1", f32), ("one_minus_beta2", f32), ("eps", f32),
-                ("lr_t", f32), ("agg_scale", f32)]
+                ("lr_t", f32), ("agg_scale", f32), ("lr_t_table", vp), ("step_ctr", vp),
+                ("table_len", i32)]
 
 
 class Slab(C.Structure):
@@ -52,6 +53,7 @@ SIGNATURES = {
     "hp_stitch": (C.c_int, [vp, vp, i64, i32, vp, vp]),
     "hp_init_rows": (C.c_int, [vp, i64, i64, i32, u64, f32, vp]),
     "hp_fill": (C.c_int, [vp, i64, f32, vp]),
+    "hp_step_counter_inc": (C.c_int, [vp, vp]),
     "hp_dense_allreduce_scale_cast": (C.c_int, [vp, vp, vp, i64, i32, f32, vp]),
     "hp_nccl_unique_id_bytes": (C.c_int, []),
     "hp_nccl_get_unique_id": (C.c_int, [vp]),

@@ -99,6 +99,14 @@ struct Router {
   }
 };
 
+// Adam's bias-corrected step size: by value, or from the device table at the
+// device step counter (so a captured graph sees the right step on every replay).
+__device__ __forceinline__ float adam_lr_t(const hp_optim& o) {
+  if (!o.lr_t_table) return o.lr_t;
+  const int s = *o.step_ctr;
+  return o.lr_t_table[s < o.table_len ? (s < 0 ? 0 : s) : o.table_len - 1];
+}
+
 __device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
   return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
                      __fadd_rn(a.w, b.w));

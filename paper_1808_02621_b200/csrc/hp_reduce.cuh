@@ -58,7 +58,7 @@ struct EpiApply {
     } else {
       a = __fadd_rn(__fmul_rn(o.beta1, a), __fmul_rn(o.one_minus_beta1, g));
       b = __fadd_rn(__fmul_rn(o.beta2, b), __fmul_rn(o.one_minus_beta2, __fmul_rn(g, g)));
-      wv = __fsub_rn(wv, __fdiv_rn(__fmul_rn(o.lr_t, a), __fadd_rn(__fsqrt_rn(b), o.eps)));
+      wv = __fsub_rn(wv, __fdiv_rn(__fmul_rn(adam_lr_t(o), a), __fadd_rn(__fsqrt_rn(b), o.eps)));
     }
   }
 

@@ -166,7 +166,7 @@ __device__ __forceinline__ void opt_update(float& w, float& a, float& b, float g
   } else {
     a = __fadd_rn(__fmul_rn(o.beta1, a), __fmul_rn(o.one_minus_beta1, g));
     b = __fadd_rn(__fmul_rn(o.beta2, b), __fmul_rn(o.one_minus_beta2, __fmul_rn(g, g)));
-    w = __fsub_rn(w, __fdiv_rn(__fmul_rn(o.lr_t, a), __fadd_rn(__fsqrt_rn(b), o.eps)));
+    w = __fsub_rn(w, __fdiv_rn(__fmul_rn(adam_lr_t(o), a), __fadd_rn(__fsqrt_rn(b), o.eps)));
   }
 }
 

@@ -225,6 +225,19 @@ int hp_init_rows(float* w, int64_t row_lo, int64_t nrows, int32_t D, uint64_t se
   return HP_OK;
 }
 
+namespace hp {
+namespace {
+__global__ void k_inc(int32_t* c) { *c += 1; }
+}  // namespace
+}  // namespace hp
+
+int hp_step_counter_inc(int32_t* ctr, void* stream) {
+  HP_REQUIRE(ctr != nullptr, "NULL counter");
+  k_inc<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(ctr);
+  HP_LAUNCHED(1, "k_inc");
+  return HP_OK;
+}
+
 int hp_fill(float* x, int64_t n, float value, void* stream) {
   if (n <= 0) return HP_OK;
   HP_REQUIRE(x != nullptr && n % 4 == 0 && ((uintptr_t)x & 15) == 0,

@@ -77,12 +77,24 @@ class OptimizerConfig:
         if self.kind not in _lib.HP_OPT:
             raise ValueError(f"unknown optimizer {self.kind!r}")
 
-    def c_struct(self, step: int, agg_scale: float) -> Optim:
-        lr_t = 0.0
-        if self.kind == "adam":
-            lr_t = self.lr * np.sqrt(1.0 - self.beta2 ** step) / (1.0 - self.beta1 ** step)
-        return Optim(_lib.HP_OPT[self.kind], self.lr, self.beta1, self.beta2, 1.0 - self.beta1,
-                     1.0 - self.beta2, self.eps, float(np.float32(lr_t)), agg_scale)
+    def lr_t(self, step) -> np.ndarray:
+        """Adam bias-corrected step size, float64 on the host, rounded to fp32."""
+        step = np.asarray(step, dtype=np.float64)
+        return (self.lr * np.sqrt(1.0 - self.beta2 ** step) / (1.0 - self.beta1 ** step)).astype(
+            np.float32)
+
+    def c_struct(self, step: int, agg_scale: float, lr_t_table=None, step_ctr=None) -> Optim:
+        """Kernel parameters for one step. With ``lr_t_table`` (device float32,
+        index = step) and ``step_ctr`` (device int32) Adam reads its step size
+        on the device, so a captured graph stays correct across replays."""
+        lr_t = float(self.lr_t(step)) if self.kind == "adam" else 0.0
+        o = Optim(_lib.HP_OPT[self.kind], self.lr, self.beta1, self.beta2, 1.0 - self.beta1,
+                  1.0 - self.beta2, self.eps, lr_t, agg_scale)
+        if lr_t_table is not None:
+            o.lr_t_table = lr_t_table.data_ptr()
+            o.step_ctr = step_ctr.data_ptr()
+            o.table_len = lr_t_table.numel()
+        return o
 
     @property
     def n_state(self) -> int:
@@ -179,6 +191,11 @@ def apply_plan(rows: torch.Tensor, n: int, slab: Slab, opt: Optim, ws: Workspace
     """K4 only: reduce + apply with the plan apply_plan_build left in ``ws``."""
     _need(rows, torch.float32, "rows", 2)
     call("hp_apply_plan", _p(rows), n, slab, opt, ws.ptr, ws.nbytes, _stream(stream))
+
+
+def step_counter_inc(ctr: torch.Tensor, stream=None) -> None:
+    """++ctr on the device (the Adam step of graph-captured steps)."""
+    call("hp_step_counter_inc", _p(ctr), _stream(stream))
 
 
 def launch_count() -> int:

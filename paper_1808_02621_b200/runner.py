@@ -178,6 +178,12 @@ class HybridRunner:
                                                  self.device, seed=seed * 1000 + i,
                                                  w_storage=storage)
         self._scratch: dict[str, _Scratch] = {n: _Scratch() for n in self.tables}
+        if self.optimizer.kind == "adam":  # step size read on the device: graph-safe
+            steps = np.arange(1 << 16, dtype=np.float64)
+            steps[0] = 1.0
+            self._lr_t_table = torch.from_numpy(self.optimizer.lr_t(steps)).to(self.device)
+            for tab in self.tables.values():
+                tab.step_dev = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.dense_out: dict[str, torch.Tensor] = {}
         self.outputs: dict[str, torch.Tensor] = {}
         self.step_count = 0
@@ -434,7 +440,12 @@ class HybridRunner:
     def _sparse(self, tab: ShardedTable, ids_vals, ev=None) -> torch.Tensor:
         ids, vals = ids_vals
         tab.step_count += 1
-        opt = self.optimizer.c_struct(tab.step_count, self.scale)
+        if self.optimizer.kind == "adam":
+            ops.step_counter_inc(tab.step_dev)
+            opt = self.optimizer.c_struct(tab.step_count, self.scale, self._lr_t_table,
+                                          tab.step_dev)
+        else:
+            opt = self.optimizer.c_struct(tab.step_count, self.scale)
         planned = tab.ready is not None and tab.ready_ids is ids
         slot = tab.ready if planned else 0
         tab.ready = tab.ready_ids = None
@@ -540,6 +551,46 @@ class HybridRunner:
         return graphs
 
     # ------------------------------------------------------------------ timing / P search
+    def measure_graphs(self, batches: list, iterations: int = 40) -> float:
+        """Mean device step time (us) over the second half of ``iterations``
+        steps, max over ranks. Steps are pipelined graph replays when possible
+        (even ``len(batches)``), eager steps otherwise."""
+        R = len(batches)
+        graphs = None
+        if self.pipelined and R % 2 == 0:
+            graphs = self.capture_pipelined(batches)
+
+        def run(k0, k):
+            for i in range(k0, k0 + k):
+                if graphs:
+                    graphs[i % R].replay()
+                else:
+                    self.step(batches[i % R], timed=False)
+
+        half = max(iterations // 2, 1)
+        run(0, half)  # discarded half (warm-up)
+        stream = torch.cuda.current_stream()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        if self.world_size > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        a.record(stream)
+        run(half, iterations - half)
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = a.elapsed_time(b) * 1e3 / max(iterations - half, 1)
+        del graphs
+        torch.cuda.synchronize()
+        if self.world_size > 1:
+            import torch.distributed as dist
+
+            x = torch.tensor([t], dtype=torch.float64, device=self.device)
+            dist.all_reduce(x, op=dist.ReduceOp.MAX)
+            t = float(x.item())
+        return t
+
     def measure(self, make_batch, iterations: int = 100) -> float:
         """Mean device step time (us) with the first half discarded
         (reference `simulate.py:380-402`, `PAPER.md:485`)."""
@@ -562,11 +613,16 @@ class HybridRunner:
 
 def device_evaluator(graph: GraphSpec, cluster: ClusterSpec, make_batch, *, rank: int = 0,
                      world_size: int = 1, comm=None, optimizer: OptimizerConfig | None = None,
-                     iterations: int = 100, names: list | None = None, **kw):
-    """evaluator(P) -> mean step us, for :func:`tuning.tune_evaluator`.
+                     iterations: int = 40, names: list | None = None, rotations: int = 2,
+                     log: list | None = None, **kw):
+    """evaluator(P) -> mean device step time (us), for :func:`tuning.tune_evaluator`.
 
     Rebuilds the hybrid plan with every partitionable sparse Weight split into P
-    (the reference CLI's shared-P rule, `cli.py:93-102`) and times real steps.
+    (the reference CLI's shared-P rule, `cli.py:93-102`), runs ``iterations``
+    real steps (CUDA-graph replays when the exchange allows it) on
+    ``rotations`` batches from ``make_batch(i)``, discards the first half
+    (`simulate.py:380-402`, `PAPER.md:485`) and returns the mean of the rest,
+    max over ranks — so every rank takes the same search decisions.
     """
     cands = names or [v.name for v in graph.variables if v.kind == "sparse" and v.partitionable]
 
@@ -575,9 +631,15 @@ def device_evaluator(graph: GraphSpec, cluster: ClusterSpec, make_batch, *, rank
         plan = transform_hybrid(graph, cluster, partitions=parts)
         runner = HybridRunner(plan, graph, cluster, rank=rank, world_size=world_size, comm=comm,
                               optimizer=optimizer, **kw)
-        t = runner.measure(make_batch, iterations)
-        del runner
-        torch.cuda.empty_cache()
+        try:
+            batches = [make_batch(i) for i in range(rotations)]
+            t = runner.measure_graphs(batches, iterations)
+        finally:
+            runner.close()
+            del runner
+            torch.cuda.empty_cache()
+        if log is not None:
+            log.append((P, t))
         return t
 
     return evaluator

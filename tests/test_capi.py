@@ -59,5 +59,5 @@ def test_sass_is_sm100a():
 def test_structs_match_header():
     from paper_1808_02621_b200._lib import Optim, Slab
 
-    assert ctypes.sizeof(Optim) == 9 * 4
+    assert ctypes.sizeof(Optim) == 9 * 4 + 4 + 8 + 8 + 4 + 4  # + pad, 2 pointers, len, tail pad
     assert ctypes.sizeof(Slab) == 8 * 4 + 8 + 4 + 4

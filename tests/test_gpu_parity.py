@@ -248,9 +248,10 @@ def test_runner_single_gpu_matches_oracle(cuda):
         assert np.array_equal(runner.tables[t.name].w.cpu().numpy(), states[t.name]["w"])
 
 
-def test_runner_pipelined_and_graphs_match_oracle(cuda):
+@pytest.mark.parametrize("opt", ["adagrad", "adam"])
+def test_runner_pipelined_and_graphs_match_oracle(cuda, opt):
     """Plans built one step ahead (next_batch) and the pipelined graph rotation
-    give bit-identical tables and pulled rows."""
+    give bit-identical tables and pulled rows (Adam: device step counter)."""
     import json
 
     import paper_1808_02621_b200 as hp
@@ -258,25 +259,34 @@ def test_runner_pipelined_and_graphs_match_oracle(cuda):
 
     wl = Workload("pipe", [TableShape("embedding", 40_000, 128, 2560),
                            TableShape("softmax", 40_000, 256, 2560, sampled=3000)],
-                  {"lstm": 10_000}, {"kind": "adagrad", "lr": 0.2, "init_acc": 0.1}, 2560)
+                  {"lstm": 10_000}, {"kind": opt, "lr": 0.2, "init_acc": 0.1}, 2560)
     graph = hp.load_graph_spec(json.dumps(wl.graph_json()))
     cluster = hp.ClusterSpec.b200_box(1)
     plan = hp.transform_hybrid(graph, cluster)
     runner = hp.HybridRunner(plan, graph, cluster, optimizer=hp.OptimizerConfig(**wl.optimizer),
                              device=cuda, seed=7)
-    states = {t.name: orc.init_state("adagrad", t.V, t.D, 7 * 1000 + i + 1, 0.1)
+    states = {t.name: orc.init_state(opt, t.V, t.D, 7 * 1000 + i + 1, 0.1)
               for i, t in enumerate(wl.tables)}
+    hpar = {"lr": 0.2, "beta1": 0.9, "beta2": 0.999, "eps": 1e-8}
+    step = [0]
     host = [make_batch(wl, seed=s, rank=0) for s in (1, 2)]
     dev = [{k: ((_t(v[0], cuda), _t(v[1], cuda)) if isinstance(v, tuple) else _t(v, cuda))
             for k, v in b.items()} for b in host]
     order = []
 
-    def check(r):
+    def advance(r):
+        step[0] += 1
+        out = {}
         for t in wl.tables:
             ids, vals = host[r][t.name]
-            res = orc.sparse_step(states[t.name], "adagrad", {"lr": 0.2}, 1, [(ids, vals)], t.V, 1,
-                                  np.zeros(1, np.int32))
-            assert np.array_equal(runner.outputs[t.name].cpu().numpy(), res[0]["out"]), (r, t.name)
+            out[t.name] = orc.sparse_step(states[t.name], opt, hpar, step[0], [(ids, vals)], t.V,
+                                          1, np.zeros(1, np.int32))[0]["out"]
+        return out
+
+    def check(r):
+        ref = advance(r)
+        for t in wl.tables:
+            assert np.array_equal(runner.outputs[t.name].cpu().numpy(), ref[t.name]), (r, t.name)
 
     runner.prefetch(dev[0])
     for r in (0, 1, 0):
@@ -285,10 +295,7 @@ def test_runner_pipelined_and_graphs_match_oracle(cuda):
     graphs = runner.capture_pipelined(dev)  # eagerly runs batch 0, 1 (rotation warm-up)
     torch.cuda.synchronize()
     for r in (0, 1):
-        for t in wl.tables:
-            ids, vals = host[r][t.name]
-            orc.sparse_step(states[t.name], "adagrad", {"lr": 0.2}, 1, [(ids, vals)], t.V, 1,
-                            np.zeros(1, np.int32))
+        advance(r)
     for rep in range(2):
         for r in (0, 1):
             graphs[r].replay()
