@@ -26,6 +26,12 @@ struct EpiSend {
   }
 };
 
+// Optimizer state a row update needs (only what the optimizer uses, so the
+// prefetched epilogue operands stay in as few registers as possible).
+template <int OPT> struct ApplyPre { float4 w, a, b; };
+template <> struct ApplyPre<HP_OPT_SGD> { float4 w; };
+template <> struct ApplyPre<HP_OPT_ADAGRAD> { float4 w, a; };
+
 template <int OPT>
 struct EpiApply {
   static constexpr bool kRemote = false;
@@ -34,17 +40,14 @@ struct EpiApply {
   float4* s1;
   hp_optim o;
   int D4;
-  struct Pre {
-    float4 w, a, b;
-  };
+  using Pre = ApplyPre<OPT>;
 
   __device__ __forceinline__ Pre load(int dst, int c4) const {
     Pre p;
     const int64_t off = (int64_t)dst * D4 + c4;
     p.w = w[off];
-    p.a = p.b = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (OPT != HP_OPT_SGD) p.a = s0[off];
-    if (OPT == HP_OPT_ADAM) p.b = s1[off];
+    if constexpr (OPT != HP_OPT_SGD) p.a = s0[off];
+    if constexpr (OPT == HP_OPT_ADAM) p.b = s1[off];
     return p;
   }
 
@@ -63,14 +66,17 @@ struct EpiApply {
   }
 
   __device__ __forceinline__ void store(int dst, int c4, float4 g, Pre p) const {
-    upd(p.w.x, p.a.x, p.b.x, g.x);
-    upd(p.w.y, p.a.y, p.b.y, g.y);
-    upd(p.w.z, p.a.z, p.b.z, g.z);
-    upd(p.w.w, p.a.w, p.b.w, g.w);
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+    if constexpr (OPT != HP_OPT_SGD) a = p.a;
+    if constexpr (OPT == HP_OPT_ADAM) b = p.b;
+    upd(p.w.x, a.x, b.x, g.x);
+    upd(p.w.y, a.y, b.y, g.y);
+    upd(p.w.z, a.z, b.z, g.z);
+    upd(p.w.w, a.w, b.w, g.w);
     const int64_t off = (int64_t)dst * D4 + c4;
     w[off] = p.w;
-    if (OPT != HP_OPT_SGD) s0[off] = p.a;
-    if (OPT == HP_OPT_ADAM) s1[off] = p.b;
+    if constexpr (OPT != HP_OPT_SGD) s0[off] = a;
+    if constexpr (OPT == HP_OPT_ADAM) s1[off] = b;
   }
 };
 
@@ -211,7 +217,9 @@ __global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
 
 template <int TPI, int VPT, class Epi>
 void launch_k_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaStream_t st) {
-  constexpr int B = VPT >= 8 ? 1 : 8 / VPT;
+  // rows in flight per batch: most items hold 1-2 rows, so a small batch keeps
+  // registers (and so resident items per SM) up without costing the hot chunks much
+  constexpr int B = VPT >= 4 ? 1 : 4 / VPT;
   // <= one group per item; peer-store epilogues stay in one resident wave so
   // each block pays its system-scope fence once
   const int blocks = grid_for(pl.T, 256 / TPI, sm_count() * (Epi::kRemote ? 3 : 16));
