@@ -108,7 +108,8 @@ k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
 #pragma unroll
     for (int v = 0; v < VPT; ++v)
       if (fin && dst >= 0 && q + v * TPI < D4) pre[v] = epi.load(dst, q + v * TPI);
-    const int myp = lane < n ? pl.sorted_pos[j0 + lane] : 0;
+    // single-row items carry the row's position directly (item.x = -(pos+1))
+    const int myp = j0 < 0 ? -j0 - 1 : (lane < n ? pl.sorted_pos[j0 + lane] : 0);
     float4 acc[VPT];
 #pragma unroll
     for (int v = 0; v < VPT; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
