@@ -8,7 +8,7 @@
 
 #include "../../include/hybridpath.h"
 
-#define HP_CHUNK 32           // rows per sequential group of the summation tree (oracle CHUNK)
+#define HP_CHUNK 16           // rows per sequential group of the summation tree (oracle CHUNK)
 #define HP_CL_CTAS 8          // cluster sort path: CTAs per cluster (portable maximum)
 #define HP_CL_THREADS 1024    // default CTA size (256 / 512 selectable for tuning)
 #define HP_CL_SLICE 2048      // items per CTA

@@ -220,7 +220,7 @@ template <int TPI, int VPT, class Epi>
 void launch_k_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaStream_t st) {
   // rows in flight per batch: most items hold 1-2 rows, so a small batch keeps
   // registers (and so resident items per SM) up without costing the hot chunks much
-  constexpr int B = VPT >= 4 ? 1 : 4 / VPT;
+  constexpr int B = VPT >= 4 ? 2 : 8 / VPT;
   // <= one group per item; peer-store epilogues stay in one resident wave so
   // each block pays its system-scope fence once
   const int blocks = grid_for(pl.T, 256 / TPI, sm_count() * (Epi::kRemote ? 3 : 16));

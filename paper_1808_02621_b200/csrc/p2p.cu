@@ -317,8 +317,10 @@ size_t hp_xchg_window_bytes(int32_t n, int32_t D, int64_t cap, int64_t rows_cap)
 
 int hp_xchg_create(hp_xchg_t* out, int32_t n, int32_t me, int32_t D, int64_t cap, int64_t rows_cap,
                    void* ipc_handle_out /* 64 bytes */, void** w_out) {
-  HP_REQUIRE(out && ipc_handle_out && w_out && n >= 1 && n <= 32 && me >= 0 && me < n,
-             "bad xchg args (1 <= n <= 32)");
+  // n <= HP_CHUNK: the owner's source-order sum is then one sequential group of
+  // the summation tree (oracle.grouped_tree_sum)
+  HP_REQUIRE(out && ipc_handle_out && w_out && n >= 1 && n <= HP_CHUNK && me >= 0 && me < n,
+             "bad xchg args (1 <= n <= 16)");
   HP_REQUIRE(D % 4 == 0 && D >= 4 && D <= 2048 && cap >= 1 && rows_cap >= 1, "bad xchg shape");
   auto* x = new hp_xchg_s{};
   auto al = [](int64_t v) { return (v + 255) & ~(int64_t)255; };
