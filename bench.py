@@ -15,7 +15,8 @@ e2e   : the same metric through HybridRunner with the step's inputs copied
         from pinned host memory inside the timed region and a result read back.
 roofline : the K4 scatter-apply kernel of the largest table, algorithmic bytes
          / its CUDA-event duration, against MEASURED_PEAKS.json.
-cpu_baseline : the oracle port (oracle/oracle.py) timed on this host (rank 0, N=1).
+cpu_baseline : the oracle port (oracle/hp_oracle.c, OpenMP, all host threads) timed on
+               this host (rank 0, N=1).
 --impl reference : the oracle port on this host for the same config/metric.
 """
 
@@ -133,17 +134,25 @@ class Clocks:
 
 # ------------------------------------------------------------------ CPU oracle step
 def cpu_oracle_step(wl, batches, states, step):
-    """The oracle's hybrid step for len(batches) simulated workers (one process)."""
-    from oracle import oracle as orc
+    """The oracle's hybrid step for len(batches) simulated workers (one process),
+    on the OpenMP C restatement (oracle/hp_oracle.c, bit-identical to the numpy
+    oracle; tests/test_oracle.py)."""
+    from oracle import coracle, oracle as orc
 
     n = len(batches)
     for t in wl.tables:
         owner = np.zeros(1, np.int32) if n == 1 else orc.owner_table(t.name, wl.partitions, n)
         P = 1 if n == 1 else wl.partitions
-        orc.sparse_step(states[t.name], wl.optimizer["kind"], wl.optimizer, step,
-                        [b[t.name] for b in batches], t.V, P, owner)
+        coracle.sparse_step(states[t.name], wl.optimizer["kind"], wl.optimizer, step,
+                            [b[t.name] for b in batches], t.V, P, owner)
     for name in wl.dense:
-        orc.dense_allreduce([b[name] for b in batches], 1.0 / n)
+        coracle.dense_mean([b[name] for b in batches], 1.0 / n)
+
+
+def cpu_threads() -> int:
+    from oracle import coracle
+
+    return coracle.threads()
 
 
 def lazy_states(wl):
@@ -187,9 +196,9 @@ def run_reference(args, wl):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": config(args, wl),
-        "cpu_baseline": {"value": value, "unit": unit, "cores": 1, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": unit, "cores": cpu_threads(), "kind": "port",
                          "sample": f"{args.steps} full oracle steps of {n} simulated worker(s), "
-                                   "numpy single-threaded"},
+                                   f"C restatement, OpenMP x{cpu_threads()}"},
         "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -399,8 +408,9 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         _, dt = time_cpu(wl, 1, args.cpu_steps)
         v = ups / dt
-        cpu = {"value": v, "unit": unit, "cores": 1, "kind": "port",
-               "sample": f"{args.cpu_steps} full oracle steps (1 worker, numpy), {dt*1e3:.1f} ms/step"}
+        cpu = {"value": v, "unit": unit, "cores": cpu_threads(), "kind": "port",
+               "sample": f"{args.cpu_steps} full oracle steps (1 worker, C restatement, "
+                         f"OpenMP x{cpu_threads()}), {dt*1e3:.1f} ms/step"}
 
     if rank == 0:
         line = {

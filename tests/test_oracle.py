@@ -108,3 +108,30 @@ def test_owner_table_matches_planner():
         g = hp.GraphSpec("g", (hp.VariableSpec("softmax", 800_000, 2048, 0.01, "sparse", True),), 0)
         plan = hp.transform_ps(g, hp.ClusterSpec.b200_box(n), partitions={"softmax": 16})
         assert np.array_equal(plan.owner_table("softmax"), orc.owner_table("softmax", 16, n))
+
+
+@pytest.mark.parametrize("T,D,V,n,P", [(1, 4, 10, 1, 1), (0, 4, 10, 2, 2), (500, 8, 50, 2, 4),
+                                       (3000, 16, 40, 3, 5), (20000, 64, 100000, 4, 8),
+                                       (40000, 8, 7, 1, 1)])
+def test_c_oracle_bit_exact_vs_numpy(T, D, V, n, P):
+    """oracle/hp_oracle.c (the multithreaded CPU baseline) == oracle.py, bit for bit."""
+    from oracle import coracle as co
+
+    rng = np.random.default_rng(T + D)
+    own = orc.owner_table("emb", P, n)
+    ids = rng.integers(0, V, T)
+    vals = rng.standard_normal((T, D)).astype(F32)
+    a = orc.sort_dedup_route(ids, vals, V, P, own, n)
+    b = co.sort_dedup_route(ids, vals, V, P, own, n)
+    for k in ("send_ids", "send_rows", "counts", "inv", "dest_counts", "n_uniq"):
+        assert np.array_equal(a[k], b[k]), k
+    for opt in ("sgd", "adagrad", "adam"):
+        s1 = orc.init_state(opt, V, D, 3)
+        s2 = {k: v.copy() for k, v in s1.items()}
+        bs = [(rng.integers(0, V, T), rng.standard_normal((T, D)).astype(F32)) for _ in range(n)]
+        r1 = orc.sparse_step(s1, opt, {"lr": 0.1}, 3, bs, V, P, own)
+        r2 = co.sparse_step(s2, opt, {"lr": 0.1}, 3, bs, V, P, own)
+        for k in s1:
+            assert np.array_equal(s1[k], s2[k]), (opt, k)
+        for x, y in zip(r1, r2):
+            assert np.array_equal(x["out"], y["out"])
