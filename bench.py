@@ -78,7 +78,9 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"])
-    ap.add_argument("--dense-exchange", default=None, choices=["p2p", "nccl"])
+    ap.add_argument("--dense-exchange", default=None, choices=["p2p", "p2p-sm", "nccl"])
+    ap.add_argument("--knob", action="append", default=[],
+                    help="instrumentation A/B: NAME=INT calls hp_debug_set_NAME(INT)")
     return ap.parse_args()
 
 
@@ -222,6 +224,12 @@ def main():
         int(args.workload.split("_")[1]))
     if args.impl == "reference":
         return run_reference(args, wl)
+    if args.knob:
+        from paper_1808_02621_b200 import _lib
+
+        for kv in args.knob:
+            k, v = kv.split("=")
+            getattr(_lib.load(), f"hp_debug_set_{k}")(int(v))
 
     import torch
     import torch.distributed as dist

@@ -87,6 +87,15 @@ void hp_debug_set_profile(long long* dev_buf);
 void hp_debug_set_spans(unsigned long long* dev_buf);
 /* Tuning: CTA size (256 | 512 | 1024) of the cluster dedup path. */
 void hp_debug_set_cluster_threads(int nt);
+/* Instrumentation: 1 = level 0 of K4 / K1-reduce runs as the cp.async row
+ * stream (k_rowstream); 0 = the register-batched k_reduce (default). */
+void hp_debug_set_rowstream(int on);
+/* Instrumentation: 1 = launch the chain kernels with programmatic dependent
+ * launch; 0 = full stream serialization (default). */
+void hp_debug_set_pdl(int on);
+/* Instrumentation: cap on row-stream CTAs per SM (shared memory left for
+ * concurrently running kernels); default 4. */
+void hp_debug_set_rs_ctas(int n);
 
 /* ---------------------------------------------------------------- K1 + K2
  * Sort + dedup + route of one worker's IndexedSlices.
@@ -257,6 +266,12 @@ int hp_dar_create(hp_dar_t* out, int32_t n, int32_t me, int64_t S, int32_t out_d
 int hp_dar_open_peer(hp_dar_t d, int32_t rank, const void* ipc_handle);
 int hp_dar_destroy(hp_dar_t d);
 int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream);
+/* Transport of the two NVLink phases: HP_DAR_CE (default) = cudaMemcpyAsync
+ * peer copies on the copy engines (no SMs; overlaps the sparse kernels),
+ * HP_DAR_SM = peer stores from SM kernels. Same result bit for bit. */
+#define HP_DAR_SM 0
+#define HP_DAR_CE 1
+int hp_dar_set_mode(hp_dar_t d, int32_t mode);
 int hp_dar_status(hp_dar_t d, int32_t* out_err, void* stream);
 /* Instrumentation: raw peer throughput over the dense window (mode 0/2 store,
  * 1/3 load; 2/3 with 4 x 16 B in flight per thread). */

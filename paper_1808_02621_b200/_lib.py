@@ -39,6 +39,9 @@ SIGNATURES = {
     "hp_launch_count": (i64, []),
     "hp_debug_set_profile": (None, [vp]),
     "hp_debug_set_cluster_threads": (None, [C.c_int]),
+    "hp_debug_set_rowstream": (None, [C.c_int]),
+    "hp_debug_set_pdl": (None, [C.c_int]),
+    "hp_debug_set_rs_ctas": (None, [C.c_int]),
     "hp_debug_set_spans": (None, [vp]),
     "hp_apply_plan": (C.c_int, [vp, i64, Slab, Optim, vp, sz, vp]),
     "hp_apply_plan_build": (C.c_int, [vp, i64, Slab, vp, sz, vp]),
@@ -78,6 +81,7 @@ SIGNATURES = {
     "hp_dar_create": (C.c_int, [C.POINTER(vp), i32, i32, i64, i32, vp, C.POINTER(vp)]),
     "hp_dar_open_peer": (C.c_int, [vp, i32, vp]),
     "hp_dar_destroy": (C.c_int, [vp]),
+    "hp_dar_set_mode": (C.c_int, [vp, i32]),
     "hp_dar_allreduce": (C.c_int, [vp, vp, f32, vp]),
     "hp_dar_status": (C.c_int, [vp, vp, vp]),
     "hp_debug_nvlink_bench": (C.c_int, [vp, i32, i32, i32, vp]),

@@ -147,17 +147,34 @@ __device__ __forceinline__ int seg_dst(uint32_t id, int p, int slot, const int64
 // slots bp.. and get a long descriptor for k_combine.
 // A single-row segment (the common case) carries its row's original position
 // directly: item.x = -(pos + 1), saving the reduce kernel one dependent load.
+// Item `it` covers sorted rows [r, r+n): record it as the first item of every
+// row-stream warp whose row cut w*R falls at its start, and the next item for
+// cuts inside it.
+__device__ __forceinline__ void emit_bounds(const DedupPlan& pl, int it, int r, int n) {
+  if (pl.nw <= 0) return;
+  const int T = (int)pl.T;
+  const int R = (T + pl.nw - 1) / pl.nw;
+  for (int w = (r + R - 1) / R; (int64_t)w * R < r + n; ++w) {
+    const bool at = w * R == r;
+    pl.wb_item[w] = at ? it : it + 1;
+    pl.wb_row[w] = at ? r : r + n;
+  }
+}
+
 __device__ __forceinline__ void emit_items(const DedupPlan& pl, int u, int j0, int L, int dst,
                                            int bi, int bp, int bl, int pos0) {
   const int n0 = (L + HP_CHUNK - 1) / HP_CHUNK;
   const bool lg = L > HP_CHUNK;
   if (L == 1) {
     pl.items[bi] = make_int4(-(pos0 + 1), 1, dst, 1);
+    emit_bounds(pl, bi, j0, 1);
     return;
   }
-  for (int k = 0; k < n0; ++k)
-    pl.items[bi + k] = make_int4(j0 + k * HP_CHUNK, min(HP_CHUNK, L - k * HP_CHUNK),
-                                 lg ? bp + k : dst, lg ? 0 : 1);
+  for (int k = 0; k < n0; ++k) {
+    const int n = min(HP_CHUNK, L - k * HP_CHUNK);
+    pl.items[bi + k] = make_int4(j0 + k * HP_CHUNK, n, lg ? bp + k : dst, lg ? 0 : 1);
+    emit_bounds(pl, bi + k, j0 + k * HP_CHUNK, n);
+  }
   if (lg) pl.longs[bl] = make_int4(bp, n0, dst, u);
 }
 
@@ -205,7 +222,7 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
   const int T = (int)pl.T, P = pl.P;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const Router route(pl.V, P);
-  HP_SPAN_BEGIN(SP_DEDUP);
+  HP_ENTRY(SP_DEDUP);
   int nprof = 0;
 #define HP_PROF()                                                     \
   do {                                                                \
@@ -687,7 +704,28 @@ size_t dedup_ws_bytes(int64_t T, int32_t D, int32_t P) {
   s += align256(4 * HP_RADIX * ntiles) + align256(4 * HP_RADIX);
   s += align256(4 * nscan);
   s += align256(4 * (size_t)D * prow);
+  s += 2 * align256(4 * (HP_RS_MAX_WARPS + 1));
   return s;
+}
+
+int rs_stages(int32_t D) {
+  switch (D) {
+    case 128: return 16;
+    case 256: return 12;
+    case 512: return 8;
+    case 1024: return 6;
+    default: return 0;
+  }
+}
+
+int rs_warps(int32_t D) {
+  const int S = rs_stages(D);
+  if (S == 0) return 0;
+  const int cta_bytes = 4 * S * D * 4;  // 4 warps x S row slots
+  int ctas = (220 << 10) / cta_bytes;
+  ctas = ctas < 1 ? 1 : (ctas > g_rs_ctas ? g_rs_ctas : ctas);
+  const int nw = sm_count() * 4 * ctas;
+  return nw < HP_RS_MAX_WARPS ? nw : HP_RS_MAX_WARPS - HP_RS_MAX_WARPS % 4;
 }
 
 int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, int64_t V,
@@ -737,6 +775,9 @@ int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, i
   pl->scan_bsum = (int32_t*)take(4 * ((Tc + HP_SCAN_TILE - 1) / HP_SCAN_TILE + 2));
   pl->partial_rows = 2 * Tc / HP_CHUNK + 2;
   pl->partials = (float*)take(4 * (size_t)D * pl->partial_rows);
+  pl->wb_item = (int32_t*)take(4 * (HP_RS_MAX_WARPS + 1));
+  pl->wb_row = (int32_t*)take(4 * (HP_RS_MAX_WARPS + 1));
+  pl->nw = g_rowstream_off ? 0 : rs_warps(D);
   pl->sorted_pos = pl->pos[0];
   pl->prof = g_prof;
   return HP_OK;
@@ -754,7 +795,7 @@ int launch_cluster_nt(const DedupPlan& pl, const int64_t* ids, const int32_t* ow
     HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
-  kern<<<CS, NT, smem, st>>>(pl, ids, owner, dst_pb, send_ids, counts, inv, dest_counts, n_uniq);
+  launch_k(kern, dim3(CS), dim3(NT), smem, st, pl, ids, owner, dst_pb, send_ids, counts, inv, dest_counts, n_uniq);
   HP_LAUNCHED(1, "k_dedup_cluster");
   return HP_OK;
 }
@@ -762,6 +803,8 @@ int launch_cluster_nt(const DedupPlan& pl, const int64_t* ids, const int32_t* ow
 int g_cl_threads = HP_CL_THREADS;  // CTA shape of the cluster path (hp_debug_set_cluster_threads)
 
 void set_cluster_threads(int nt) { g_cl_threads = nt; }
+int g_rowstream_off = 1;  // row stream measured slower on the LM step
+int g_rs_ctas = 4;
 HP_SPAN_SETTER(set_spans_dedup)
 
 template <int CS>

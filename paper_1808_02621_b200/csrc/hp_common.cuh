@@ -129,6 +129,28 @@ inline int grid_for(int64_t work, int per_block, int max_blocks) {
 
 int sm_count();
 
+extern int g_pdl;  // programmatic dependent launch on/off (hp_debug_set_pdl)
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args... args) {
+  if (!g_pdl) {
+    kern<<<grid, block, smem, st>>>(static_cast<KArgs>(args)...);
+    return;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ---- kernel span profiler (instrumentation only). Each TU that uses it keeps
 // its own device pointer; hp_debug_set_spans() sets all of them. A kernel
 // span = [first block start, last block end] in %globaltimer ns.
@@ -149,6 +171,20 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     __syncthreads();                                      \
     if (threadIdx.x == 0) atomicMax(&d_span[2 * (id) + 1], ::hp::globaltimer()); \
   }
+// Programmatic dependent launch: chain kernels are launched with launch_k
+// (stream serialization relaxed) and start with HP_ENTRY, which waits for the
+// previous kernel's memory (griddepcontrol.wait; a no-op for a normal launch),
+// then lets the next kernel's CTAs be scheduled while this one runs. Every
+// kernel launched through launch_k must execute HP_ENTRY before touching
+// global memory, so completion stays transitive along the stream.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+#define HP_ENTRY(id) \
+  ::hp::pdl_wait();  \
+  ::hp::pdl_trigger(); \
+  HP_SPAN_BEGIN(id)
 #define HP_SPAN_SETTER(fn) \
   void fn(unsigned long long* p) { cudaMemcpyToSymbol(d_span, &p, sizeof(p)); }
 HP_SPAN_DECL

@@ -39,7 +39,22 @@ struct DedupPlan {
   float* partials;      // [(2T/C + 2) * D]
   int64_t partial_rows;
   long long* prof;      // optional per-phase clock64 stamps (HP_PROFILE_PTR), else nullptr
+  // Row-stream partition (k_rowstream): warp w owns the items that start in
+  // sorted rows [w*R, (w+1)*R), R = ceil(T / nw); wb_item[w] / wb_row[w] are
+  // its first item and that item's first sorted row. nw == 0: not used.
+  int32_t nw;
+  int32_t* wb_item;     // [HP_RS_MAX_WARPS + 1]
+  int32_t* wb_row;      // [HP_RS_MAX_WARPS + 1]
 };
+
+constexpr int HP_RS_MAX_WARPS = 4096;
+
+// Row-stream geometry for a row width of D floats: stages per warp (0 = the
+// row stream does not handle this width) and warps per plan.
+int rs_stages(int32_t D);
+int rs_warps(int32_t D);
+extern int g_rowstream_off;
+extern int g_rs_ctas;  // row-stream CTAs per SM cap (hp_debug_set_rs_ctas)  // hp_debug_set_rowstream(0): use k_reduce (A/B instrumentation)
 
 size_t dedup_ws_bytes(int64_t T, int32_t D, int32_t P);
 int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, int64_t V,

@@ -17,6 +17,8 @@ namespace hp {
 // only depends on the item), store(dst, c4, g, pre) consumes the summed float4.
 struct EpiSend {
   static constexpr bool kRemote = false;
+  static constexpr int kPre = 0;  // table rows the epilogue reads (row stream stages them)
+  __device__ __forceinline__ const float4* pre_row(int, int) const { return nullptr; }
   float4* rows;
   int D4;
   struct Pre {};
@@ -32,15 +34,29 @@ template <int OPT> struct ApplyPre { float4 w, a, b; };
 template <> struct ApplyPre<HP_OPT_SGD> { float4 w; };
 template <> struct ApplyPre<HP_OPT_ADAGRAD> { float4 w, a; };
 
+// field k of a Pre (0 = w, 1 = s0, 2 = s1)
+template <class Pre>
+__device__ __forceinline__ void set_pre(Pre& p, int k, float4 v) {
+  if constexpr (sizeof(Pre) >= 16) { if (k == 0) p.w = v; }
+  if constexpr (sizeof(Pre) >= 32) { if (k == 1) p.a = v; }
+  if constexpr (sizeof(Pre) >= 48) { if (k == 2) p.b = v; }
+}
+
 template <int OPT>
 struct EpiApply {
   static constexpr bool kRemote = false;
+  static constexpr int kPre = OPT == HP_OPT_SGD ? 1 : (OPT == HP_OPT_ADAGRAD ? 2 : 3);
   float4* w;
   float4* s0;
   float4* s1;
   hp_optim o;
   int D4;
   using Pre = ApplyPre<OPT>;
+
+  __device__ __forceinline__ const float4* pre_row(int k, int dst) const {
+    const float4* b = k == 0 ? w : (k == 1 ? s0 : s1);
+    return b + (int64_t)dst * D4;
+  }
 
   __device__ __forceinline__ Pre load(int dst, int c4) const {
     Pre p;
@@ -98,7 +114,7 @@ k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
   constexpr int GPB = 256 / TPI;
   const int q = threadIdx.x % TPI;
   const int lane = threadIdx.x & 31;
-  HP_SPAN_BEGIN(SP_REDUCE);
+  HP_ENTRY(SP_REDUCE);
   const int n_items = pl.counters[C_ITEMS];
   for (int it = blockIdx.x * GPB + threadIdx.x / TPI; it < n_items; it += gridDim.x * GPB) {
     const int4 item = pl.items[it];
@@ -165,7 +181,7 @@ __device__ __forceinline__ float4 seq_sum_rows(const float4* src, int n, int D4)
 // {partial slot, n0, dst, u}, in place over its partial rows.
 template <class Epi>
 __global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
-  HP_SPAN_BEGIN(SP_COMBINE);
+  HP_ENTRY(SP_COMBINE);
   const int D4 = pl.D >> 2;
   const int n_long = pl.counters[C_LONG];
   float4* partials = reinterpret_cast<float4*>(pl.partials);
@@ -216,6 +232,186 @@ __global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
   HP_SPAN_END(SP_COMBINE);
 }
 
+// ------------------------------------------------------------------ row stream
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+enum { RS_FIRST = 1, RS_PRE = 2, RS_END = 4, RS_FIN = 8 };
+
+// Level 0 of the summation tree as a per-warp row stream. Warp w walks the
+// items that start in its slice of sorted rows (plan bounds wb_*); each item
+// becomes n gradient-row elements followed by the epilogue's kPre table rows.
+// Every element is one row copied global -> shared with cp.async (each lane
+// copies and later reads only its own VPT float4 columns, so no cross-lane
+// smem sync is needed), F = S - kPre elements in flight, so a warp keeps F
+// rows (F*D*4 bytes) of loads outstanding regardless of how the rows group
+// into items, and no registers are held by in-flight loads. Positions and
+// item descriptors are read 32 at a time (coalesced) one batch ahead. The sum
+// is the same ((0 + r0) + r1) + ... in sorted order as k_reduce.
+template <int VPT, int S, class Epi>
+__global__ void __launch_bounds__(128) k_rowstream(DedupPlan pl, const float* __restrict__ vals_f,
+                                                   Epi epi) {
+  constexpr int D4 = VPT * 32;
+  constexpr int F = S - Epi::kPre;
+  static_assert(F >= 2, "row stream needs >= 2 rows in flight");
+  extern __shared__ __align__(16) float4 s_rows[];  // [4 warps][S][D4]
+  __shared__ int2 s_meta[4][S];
+  const float4* __restrict__ vals = reinterpret_cast<const float4*>(vals_f);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gw = blockIdx.x * 4 + wid;
+  const int T = (int)pl.T;
+  const int R = (T + pl.nw - 1) / pl.nw;
+  HP_ENTRY(SP_REDUCE);
+  float4* ring = s_rows + (size_t)wid * S * D4;
+  int ib = 0, ie = 0, rb = 0, re = 0;
+  if ((int64_t)gw * R < T) {
+    ib = pl.wb_item[gw];
+    rb = pl.wb_row[gw];
+    if ((int64_t)(gw + 1) * R >= T) {
+      ie = pl.counters[C_ITEMS];
+      re = T;
+    } else {
+      ie = pl.wb_item[gw + 1];
+      re = pl.wb_row[gw + 1];
+    }
+  }
+  // descriptor / position batches (lane l holds entry base + l), next batch prefetched
+  int dbase = ib, pbase = rb;
+  int4 dcur = make_int4(0, 0, 0, 0), dnxt = dcur;
+  int pcur = 0, pnxt = 0;
+  if (ib + lane < ie) dcur = pl.items[ib + lane];
+  if (ib + 32 + lane < ie) dnxt = pl.items[ib + 32 + lane];
+  if (rb + lane < re) pcur = pl.sorted_pos[rb + lane];
+  if (rb + 32 + lane < re) pnxt = pl.sorted_pos[rb + 32 + lane];
+  // producer cursor: item pi, element pj of pn + pnpre
+  int pi = ib, pj = 0, pn = 0, pdst = 0, pfin = 0, pnpre = 0, gp = rb;
+  auto fetch_item = [&]() {
+    if (pi - dbase == 32) {
+      dcur = dnxt;
+      dbase += 32;
+      if (dbase + 32 + lane < ie) dnxt = pl.items[dbase + 32 + lane];
+    }
+    const int k = pi - dbase;
+    pn = __shfl_sync(0xffffffffu, dcur.y, k);
+    pdst = __shfl_sync(0xffffffffu, dcur.z, k);
+    pfin = __shfl_sync(0xffffffffu, dcur.w, k);
+    pnpre = (pfin && pdst >= 0) ? Epi::kPre : 0;
+  };
+  if (pi < ie) fetch_item();
+  auto issue = [&](int e) {
+    const int slot = e % S;
+    const float4* src;
+    int flags;
+    if (pj < pn) {
+      if (gp - pbase == 32) {
+        pcur = pnxt;
+        pbase += 32;
+        if (pbase + 32 + lane < re) pnxt = pl.sorted_pos[pbase + 32 + lane];
+      }
+      const int pos = __shfl_sync(0xffffffffu, pcur, gp - pbase);
+      ++gp;
+      src = vals + (int64_t)pos * D4;
+      flags = pj == 0 ? RS_FIRST : 0;
+    } else {
+      src = epi.pre_row(pj - pn, pdst);
+      flags = RS_PRE;
+    }
+    float4* dstp = ring + slot * D4;
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) cp_async16(dstp + lane + v * 32, src + lane + v * 32);
+    const bool end = pj + 1 == pn + pnpre;
+    if (lane == 0)
+      s_meta[wid][slot] = make_int2(pdst, flags | (end ? RS_END : 0) | (pfin ? RS_FIN : 0) |
+                                              (pnpre << 8));
+    if (end) {
+      ++pi;
+      pj = 0;
+      if (pi < ie) fetch_item();
+    } else {
+      ++pj;
+    }
+  };
+  int issued = 0;
+#pragma unroll 1
+  for (int s = 0; s < F; ++s) {
+    if (pi < ie) issue(issued++);
+    cp_async_commit();
+  }
+  float4* partials = reinterpret_cast<float4*>(pl.partials);
+  float4 acc[VPT];
+#pragma unroll
+  for (int v = 0; v < VPT; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+  for (int m = 0; m < issued; ++m) {
+    cp_async_wait<F - 1>();
+    __syncwarp();
+    const int slot = m % S;
+    const int2 mt = s_meta[wid][slot];
+    const float4* row = ring + slot * D4;
+    if (!(mt.y & RS_PRE)) {
+      const bool first = mt.y & RS_FIRST;
+#pragma unroll
+      for (int v = 0; v < VPT; ++v) {
+        const float4 x = row[lane + v * 32];
+        acc[v] = f4_add(first ? make_float4(0.f, 0.f, 0.f, 0.f) : acc[v], x);
+      }
+    }
+    if (mt.y & RS_END) {
+      const int dst = mt.x;
+      if (!(mt.y & RS_FIN)) {
+#pragma unroll
+        for (int v = 0; v < VPT; ++v) partials[(int64_t)dst * D4 + lane + v * 32] = acc[v];
+      } else if (dst >= 0) {
+        const int npre = mt.y >> 8;
+#pragma unroll
+        for (int v = 0; v < VPT; ++v) {
+          const int c4 = lane + v * 32;
+          typename Epi::Pre pre;
+          if constexpr (Epi::kPre > 0) {
+#pragma unroll
+            for (int k = 0; k < Epi::kPre; ++k)
+              set_pre(pre, k, ring[((m - npre + 1 + k + S) % S) * D4 + c4]);
+          } else {
+            pre = epi.load(dst, c4);
+          }
+          epi.store(dst, c4, acc[v], pre);
+        }
+      }
+    }
+    __syncwarp();
+    if (pi < ie) issue(issued++);
+    cp_async_commit();
+  }
+  cp_async_wait<0>();
+  if constexpr (Epi::kRemote) {  // one cumulative release per block, after the barrier
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
+  }
+  HP_SPAN_END(SP_REDUCE);
+}
+
+template <int VPT, class Epi>
+void launch_rowstream(const DedupPlan& pl, const float* vals, const Epi& epi, cudaStream_t st) {
+  constexpr int S = VPT == 1 ? 16 : (VPT == 2 ? 12 : (VPT == 4 ? 8 : 6));
+  constexpr size_t smem = (size_t)4 * S * VPT * 32 * sizeof(float4);
+  auto kern = k_rowstream<VPT, S, Epi>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  launch_k(kern, dim3(pl.nw / 4), dim3(128), smem, st, pl, vals, epi);
+}
+
 template <int TPI, int VPT, class Epi>
 void launch_k_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaStream_t st) {
   // rows in flight per batch: most items hold 1-2 rows, so a small batch keeps
@@ -224,22 +420,32 @@ void launch_k_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cud
   // <= one group per item; peer-store epilogues stay in one resident wave so
   // each block pays its system-scope fence once
   const int blocks = grid_for(pl.T, 256 / TPI, sm_count() * (Epi::kRemote ? 3 : 16));
-  k_reduce<TPI, VPT, B, Epi><<<blocks, 256, 0, st>>>(pl, vals, epi);
+  launch_k(k_reduce<TPI, VPT, B, Epi>, dim3(blocks), dim3(256), 0, st, pl, vals, epi);
 }
 
 template <class Epi>
 int launch_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaStream_t st) {
   if (pl.T == 0) return HP_OK;
   const int D4 = pl.D >> 2;
-  if (D4 <= 32) launch_k_reduce<32, 1>(pl, vals, epi, st);
-  else if (D4 <= 64) launch_k_reduce<32, 2>(pl, vals, epi, st);
-  else if (D4 <= 128) launch_k_reduce<64, 2>(pl, vals, epi, st);
-  else if (D4 <= 256) launch_k_reduce<64, 4>(pl, vals, epi, st);
-  else launch_k_reduce<128, 4>(pl, vals, epi, st);
-  HP_LAUNCHED(1, "k_reduce");
+  if (pl.nw > 0 && rs_stages(pl.D) > 0 && !g_rowstream_off) {
+    switch (D4) {
+      case 32: launch_rowstream<1>(pl, vals, epi, st); break;
+      case 64: launch_rowstream<2>(pl, vals, epi, st); break;
+      case 128: launch_rowstream<4>(pl, vals, epi, st); break;
+      default: launch_rowstream<8>(pl, vals, epi, st); break;
+    }
+    HP_LAUNCHED(1, "k_rowstream");
+  } else {
+    if (D4 <= 32) launch_k_reduce<32, 1>(pl, vals, epi, st);
+    else if (D4 <= 64) launch_k_reduce<32, 2>(pl, vals, epi, st);
+    else if (D4 <= 128) launch_k_reduce<64, 2>(pl, vals, epi, st);
+    else if (D4 <= 256) launch_k_reduce<64, 4>(pl, vals, epi, st);
+    else launch_k_reduce<128, 4>(pl, vals, epi, st);
+    HP_LAUNCHED(1, "k_reduce");
+  }
   // long segments are few (<= T/33); a small grid keeps the publication cheap
   const int cblocks = grid_for(pl.T / (HP_CHUNK + 1) + 1, 1, Epi::kRemote ? 32 : sm_count());
-  k_combine<Epi><<<cblocks, 256, 0, st>>>(pl, epi);
+  launch_k(k_combine<Epi>, dim3(cblocks), dim3(256), 0, st, pl, epi);
   HP_LAUNCHED(1, "k_combine");
   return HP_OK;
 }

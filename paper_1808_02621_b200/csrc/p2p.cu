@@ -83,6 +83,8 @@ struct WinLayout {
 // ---- push epilogue: the summed row of send slot `dst` goes to its owner's inbox.
 struct EpiPush {
   static constexpr bool kRemote = true;
+  static constexpr int kPre = 0;
+  __device__ __forceinline__ const float4* pre_row(int, int) const { return nullptr; }
   PeerTable peers;
   WinLayout L;
   const int32_t* dest_counts;  // [n] rows this rank sends to each owner
@@ -135,7 +137,7 @@ struct EpiPush {
 
 // ---- wait until flags[s] >= epoch for every s (one block; bounded spin).
 __global__ void k_wait(void* my_win, int which, int n, long long timeout_cycles, int span) {
-  HP_SPAN_BEGIN(span);
+  HP_ENTRY(span);
   SigView sig(my_win);
   const int* flags = which == 0 ? sig.push_flag : sig.applied_flag;
   const int e = *sig.epoch;
@@ -181,7 +183,7 @@ __global__ void __launch_bounds__(256, VPT >= 4 ? 2 : 3)
 k_owner_apply(PeerTable peers, void* my_win, WinLayout L, const int64_t* __restrict__ part_base,
               Router route, float4* s0, float4* s1, hp_optim o, int64_t rows_cap) {
   __shared__ bool s_last;
-  HP_SPAN_BEGIN(SP_APPLY);
+  HP_ENTRY(SP_APPLY);
   SigView sig(my_win);
   char* win = static_cast<char*>(my_win);
   float4* w = reinterpret_cast<float4*>(win + L.w_off);
@@ -423,7 +425,7 @@ int hp_xchg_push(hp_xchg_t x, const int64_t* ids, const float* vals, int64_t T, 
 // slab, return the updated rows to the contributors, signal "applied".
 int hp_xchg_wait(hp_xchg_t x, int32_t which, void* stream) {
   HP_REQUIRE(x && (which == 0 || which == 1), "bad wait arguments");
-  k_wait<<<1, 64, 0, static_cast<cudaStream_t>(stream)>>>(x->win, which, x->L.n, wait_budget(),
+  launch_k(k_wait, dim3(1), dim3(64), 0, static_cast<cudaStream_t>(stream), x->win, which, x->L.n, wait_budget(),
                                                           which ? SP_WAIT_APPLIED : SP_WAIT_PUSH);
   HP_LAUNCHED(1, "k_wait");
   return HP_OK;
@@ -435,7 +437,7 @@ void launch_owner_apply(const hp_xchg_s* x, const hp_slab& slab, const hp_optim&
                         cudaStream_t st) {
   const int64_t total = (int64_t)x->L.n * x->L.cap;
   const int blocks = grid_for(total, 256 / TPI, sm_count() * (VPT >= 4 ? 2 : 3));  // one wave
-  k_owner_apply<OPT, TPI, VPT><<<blocks, 256, 0, st>>>(
+  launch_k(k_owner_apply<OPT, TPI, VPT>, dim3(blocks), dim3(256), 0, st, 
       x->peers, x->win, x->L, slab.part_base, Router(slab.V, slab.P),
       reinterpret_cast<float4*>(slab.s0), reinterpret_cast<float4*>(slab.s1), opt, x->rows_cap);
 }
@@ -538,7 +540,7 @@ struct ArLayout {
 __global__ void __launch_bounds__(256)
 k_ar_scatter(PeerTable peers, void* my_win, ArLayout A, const float4* __restrict__ grad) {
   __shared__ bool s_last;
-  HP_SPAN_BEGIN(SP_AR_SCATTER);
+  HP_ENTRY(SP_AR_SCATTER);
   const int c = blockIdx.y;
   const int64_t c4 = A.chunk >> 2, real4 = A.S_real >> 2;
   const float4* src = grad + (int64_t)c * c4;
@@ -600,7 +602,7 @@ template <typename OutT>
 __global__ void __launch_bounds__(256)
 k_ar_reduce_gather(PeerTable peers, void* my_win, ArLayout A, float scale) {
   __shared__ bool s_last;
-  HP_SPAN_BEGIN(SP_AR_RG);
+  HP_ENTRY(SP_AR_RG);
   const int64_t c4 = A.chunk >> 2;
   const float4* slots =
       reinterpret_cast<const float4*>(static_cast<char*>(my_win) + A.slots_off);
@@ -645,6 +647,65 @@ k_ar_reduce_gather(PeerTable peers, void* my_win, ArLayout A, float scale) {
   HP_SPAN_END(SP_AR_RG);
 }
 
+
+// ---- copy-engine variant: the NVLink phases are cudaMemcpyAsync peer copies
+// (no SMs), flags are raised by one-warp kernels after the copies complete in
+// stream order; only the local source-order sum runs on the SMs.
+__global__ void k_signal(void* my_win, PeerTable peers, int n, int me, int which) {
+  HP_ENTRY(which ? SP_AR_WAIT1 : SP_AR_WAIT0);
+  SigView sig(my_win);
+  const int e = *sig.epoch + (which == 0 ? 1 : 0);
+  __threadfence_system();
+  for (int r = threadIdx.x; r < n; r += blockDim.x) {
+    SigView peer(peers.base[r]);
+    st_release_sys(which == 0 ? &peer.push_flag[me] : &peer.applied_flag[me], e);
+  }
+  __syncwarp();
+  if (which == 0 && threadIdx.x == 0) *sig.epoch = e;
+  HP_SPAN_END(which ? SP_AR_WAIT1 : SP_AR_WAIT0);
+}
+
+// out[my chunk] = cast(scale * sum_s slot_s) in source-rank order; my own
+// contribution is read straight from grad (zero past S_real).
+template <typename OutT>
+__global__ void __launch_bounds__(256)
+k_ar_reduce_local(void* my_win, ArLayout A, const float4* __restrict__ grad, float scale) {
+  HP_ENTRY(SP_AR_RG);
+  const int64_t c4 = A.chunk >> 2;
+  const int64_t own_lim = min(c4, max((int64_t)0, (A.S_real >> 2) - (int64_t)A.me * c4));
+  const float4* slots = reinterpret_cast<const float4*>(static_cast<char*>(my_win) + A.slots_off);
+  const float4* mine = grad + (int64_t)A.me * c4;
+  char* out = static_cast<char*>(my_win) + A.out_off;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < c4; j0 += 2 * stride) {
+    float4 acc[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t j = j0 + u * stride;
+      acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (j < c4)
+        for (int sidx = 0; sidx < A.n; ++sidx) {
+          const float4 x = sidx == A.me ? (j < own_lim ? ldg_stream(mine + j)
+                                                        : make_float4(0.f, 0.f, 0.f, 0.f))
+                                        : ldg_stream(slots + (int64_t)sidx * c4 + j);
+          acc[u] = f4_add(acc[u], x);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t j = j0 + u * stride;
+      if (j >= c4) continue;
+      float4 v = acc[u];
+      v.x = __fmul_rn(v.x, scale);
+      v.y = __fmul_rn(v.y, scale);
+      v.z = __fmul_rn(v.z, scale);
+      v.w = __fmul_rn(v.w, scale);
+      put4<OutT>(out, (int64_t)A.me * c4 + j, v);
+    }
+  }
+  HP_SPAN_END(SP_AR_RG);
+}
+
 }  // namespace
 }  // namespace hp
 
@@ -652,6 +713,9 @@ struct hp_dar_s {
   ArLayout A;
   void* win;
   PeerTable peers;
+  int mode;                  // HP_DAR_SM | HP_DAR_CE
+  cudaStream_t side[4];      // CE mode: copies to different peers run concurrently
+  cudaEvent_t fork, join[4];
 };
 
 extern "C" {
@@ -683,7 +747,13 @@ int hp_dar_create(hp_dar_t* out, int32_t n, int32_t me, int64_t S_real, int32_t 
     delete d;
     return cuda_fail(e, "cudaMalloc(dense window)");
   }
-  HP_CUDA(cudaMemset(d->win, 0, SIG_INTS * 4));
+  HP_CUDA(cudaMemset(d->win, 0, bytes));  // slot padding must read as zeros
+  d->mode = HP_DAR_CE;
+  for (int k = 0; k < 4; ++k) {
+    HP_CUDA(cudaStreamCreateWithFlags(&d->side[k], cudaStreamNonBlocking));
+    HP_CUDA(cudaEventCreateWithFlags(&d->join[k], cudaEventDisableTiming));
+  }
+  HP_CUDA(cudaEventCreateWithFlags(&d->fork, cudaEventDisableTiming));
   cudaIpcMemHandle_t h;
   HP_CUDA(cudaIpcGetMemHandle(&h, d->win));
   memcpy(ipc_handle_out, &h, sizeof(h));
@@ -709,6 +779,11 @@ int hp_dar_destroy(hp_dar_t d) {
   if (!d) return HP_OK;
   for (int r = 0; r < d->A.n; ++r)
     if (r != d->A.me && d->peers.base[r]) cudaIpcCloseMemHandle(d->peers.base[r]);
+  for (int k = 0; k < 4; ++k) {
+    cudaStreamDestroy(d->side[k]);
+    cudaEventDestroy(d->join[k]);
+  }
+  cudaEventDestroy(d->fork);
   cudaFree(d->win);
   delete d;
   return HP_OK;
@@ -716,22 +791,77 @@ int hp_dar_destroy(hp_dar_t d) {
 
 // out (the window's output, every rank) = cast(scale * sum_r grad_r), summed in
 // rank order. grad is this rank's fp32 gradient [S] (any device buffer).
+int hp_dar_set_mode(hp_dar_t d, int32_t mode) {
+  HP_REQUIRE(d && (mode == HP_DAR_SM || mode == HP_DAR_CE), "mode must be HP_DAR_SM or HP_DAR_CE");
+  d->mode = mode;
+  return HP_OK;
+}
+
+// CE mode: chunk copies to every peer, fanned out over the side streams.
+static int dar_copies(hp_dar_t d, cudaStream_t st, bool gather, const float* grad) {
+  const ArLayout& A = d->A;
+  const int npeer = A.n - 1;
+  const int ns = npeer < 4 ? npeer : 4;
+  HP_CUDA(cudaEventRecord(d->fork, st));
+  for (int k = 0; k < ns; ++k) HP_CUDA(cudaStreamWaitEvent(d->side[k], d->fork, 0));
+  int q = 0;
+  for (int r = 0; r < A.n; ++r) {
+    if (r == A.me) continue;
+    cudaStream_t cs = d->side[q++ % ns];
+    if (!gather) {  // my chunk r -> rank r's slot [me]
+      const int64_t real = std::min(A.chunk, std::max((int64_t)0, A.S_real - (int64_t)r * A.chunk));
+      if (real > 0)
+        HP_CUDA(cudaMemcpyAsync(static_cast<char*>(d->peers.base[r]) + A.slots_off +
+                                    (int64_t)A.me * A.chunk * 4,
+                                grad + (int64_t)r * A.chunk, real * 4, cudaMemcpyDeviceToDevice, cs));
+    } else {  // my reduced chunk -> rank r's output
+      const int64_t off = A.out_off + (int64_t)A.me * A.chunk * A.out_bytes;
+      HP_CUDA(cudaMemcpyAsync(static_cast<char*>(d->peers.base[r]) + off,
+                              static_cast<char*>(d->win) + off, A.chunk * A.out_bytes,
+                              cudaMemcpyDeviceToDevice, cs));
+    }
+  }
+  for (int k = 0; k < ns; ++k) {
+    HP_CUDA(cudaEventRecord(d->join[k], d->side[k]));
+    HP_CUDA(cudaStreamWaitEvent(st, d->join[k], 0));
+  }
+  return HP_OK;
+}
+
 int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream) {
   HP_REQUIRE(d && grad && ((uintptr_t)grad & 15) == 0, "grad must be a 16-byte aligned buffer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int sms = sm_count();
+  if (d->mode == HP_DAR_CE) {
+    int rc;
+    if (d->A.n > 1 && (rc = dar_copies(d, st, false, grad))) return rc;
+    launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 0);
+    launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 0, d->A.n, wait_budget(), SP_AR_WAIT0);
+    const int brg = grid_for(d->A.chunk / 8, 256, sms * 2);
+    if (d->A.out_bytes == 4)
+      launch_k(k_ar_reduce_local<float>, dim3(brg), dim3(256), 0, st, d->win, d->A,
+               reinterpret_cast<const float4*>(grad), scale);
+    else
+      launch_k(k_ar_reduce_local<__nv_bfloat16>, dim3(brg), dim3(256), 0, st, d->win, d->A,
+               reinterpret_cast<const float4*>(grad), scale);
+    if (d->A.n > 1 && (rc = dar_copies(d, st, true, grad))) return rc;
+    launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 1);
+    launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 1, d->A.n, wait_budget(), SP_AR_WAIT1);
+    HP_LAUNCHED(5, "dense p2p allreduce (copy engines)");
+    return HP_OK;
+  }
   // ~half the SMs: NVLink saturates well below full occupancy, and the sparse
   // tables' latency-bound kernels run concurrently on the rest
   const int bx = std::max(1, std::min(grid_for(d->A.chunk / 16, 256, sms), sms / d->A.n));
-  k_ar_scatter<<<dim3(bx, d->A.n), 256, 0, st>>>(d->peers, d->win, d->A,
+  launch_k(k_ar_scatter, dim3(bx, d->A.n), dim3(256), 0, st, d->peers, d->win, d->A,
                                                 reinterpret_cast<const float4*>(grad));
-  k_wait<<<1, 64, 0, st>>>(d->win, 0, d->A.n, wait_budget(), SP_AR_WAIT0);
+  launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 0, d->A.n, wait_budget(), SP_AR_WAIT0);
   const int brg = grid_for(d->A.chunk / 8, 256, sms * 2);
   if (d->A.out_bytes == 4)
-    k_ar_reduce_gather<float><<<brg, 256, 0, st>>>(d->peers, d->win, d->A, scale);
+    launch_k(k_ar_reduce_gather<float>, dim3(brg), dim3(256), 0, st, d->peers, d->win, d->A, scale);
   else
-    k_ar_reduce_gather<__nv_bfloat16><<<brg, 256, 0, st>>>(d->peers, d->win, d->A, scale);
-  k_wait<<<1, 64, 0, st>>>(d->win, 1, d->A.n, wait_budget(), SP_AR_WAIT1);
+    launch_k(k_ar_reduce_gather<__nv_bfloat16>, dim3(brg), dim3(256), 0, st, d->peers, d->win, d->A, scale);
+  launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 1, d->A.n, wait_budget(), SP_AR_WAIT1);
   HP_LAUNCHED(4, "dense p2p allreduce");
   return HP_OK;
 }

@@ -38,7 +38,7 @@ struct SrcInv {
 template <int VPL, int RPW, class Src>
 __global__ void __launch_bounds__(256)
 k_copy_rows(Src src, int64_t n, const int32_t* n_dev, float4* __restrict__ out, int D4) {
-  HP_SPAN_BEGIN(SP_COPY);
+  HP_ENTRY(SP_COPY);
   const int lane = threadIdx.x & 31;
   const int64_t lim = n_dev ? min(n, (int64_t)*n_dev) : n;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -77,15 +77,15 @@ int launch_copy(const Src& src, int64_t n, const int32_t* n_dev, float* out, int
   const int sms = sm_count();
   float4* o = reinterpret_cast<float4*>(out);
   if (D4 <= 32) {
-    k_copy_rows<1, 8, Src><<<grid_for(n, 64, sms * 8), 256, 0, st>>>(src, n, n_dev, o, D4);
+    launch_k(k_copy_rows<1, 8, Src>, dim3(grid_for(n, 64, sms * 8)), dim3(256), 0, st, src, n, n_dev, o, D4);
   } else if (D4 <= 64) {
-    k_copy_rows<2, 4, Src><<<grid_for(n, 32, sms * 8), 256, 0, st>>>(src, n, n_dev, o, D4);
+    launch_k(k_copy_rows<2, 4, Src>, dim3(grid_for(n, 32, sms * 8)), dim3(256), 0, st, src, n, n_dev, o, D4);
   } else if (D4 <= 128) {
-    k_copy_rows<4, 2, Src><<<grid_for(n, 16, sms * 8), 256, 0, st>>>(src, n, n_dev, o, D4);
+    launch_k(k_copy_rows<4, 2, Src>, dim3(grid_for(n, 16, sms * 8)), dim3(256), 0, st, src, n, n_dev, o, D4);
   } else if (D4 <= 256) {
-    k_copy_rows<8, 1, Src><<<grid_for(n, 8, sms * 8), 256, 0, st>>>(src, n, n_dev, o, D4);
+    launch_k(k_copy_rows<8, 1, Src>, dim3(grid_for(n, 8, sms * 8)), dim3(256), 0, st, src, n, n_dev, o, D4);
   } else {
-    k_copy_rows<16, 1, Src><<<grid_for(n, 8, sms * 8), 256, 0, st>>>(src, n, n_dev, o, D4);
+    launch_k(k_copy_rows<16, 1, Src>, dim3(grid_for(n, 8, sms * 8)), dim3(256), 0, st, src, n, n_dev, o, D4);
   }
   HP_LAUNCHED(1, "k_copy_rows");
   return HP_OK;

@@ -137,8 +137,8 @@ class HybridRunner:
         self.exchange = exchange if world_size > 1 else "local"
         # dense allreduce: peer-memory kernel (deterministic, scale/cast fused) or NCCL
         self.dense_exchange = (dense_exchange or exchange) if world_size > 1 else "local"
-        if self.dense_exchange not in ("p2p", "nccl", "local"):
-            raise ValueError("dense_exchange must be 'p2p' or 'nccl'")
+        if self.dense_exchange not in ("p2p", "p2p-sm", "nccl", "local"):
+            raise ValueError("dense_exchange must be 'p2p' (copy engines), 'p2p-sm' or 'nccl'")
         self.dar: dict = {}
         self.xchg: dict = {}
         self.glob_base: dict = {}
@@ -156,11 +156,12 @@ class HybridRunner:
             mech = plan.mech_of[var.name]
             if var.kind == "dense":
                 self.dense.append(var)
-                if self.dense_exchange == "p2p":
+                if self.dense_exchange in ("p2p", "p2p-sm"):
                     from .xchg import DenseExchange
 
-                    self.dar[var.name] = DenseExchange(world_size, rank, var.elements,
-                                                       dense_dtype, self.device)
+                    self.dar[var.name] = DenseExchange(
+                        world_size, rank, var.elements, dense_dtype, self.device,
+                        mode="sm" if self.dense_exchange == "p2p-sm" else "ce")
                 continue
             if mech is Mechanism.PS:
                 P = plan.partitions_of[var.name]

@@ -114,7 +114,10 @@ class DenseExchange:
     reduce slots and the output; ``allreduce(grad, scale)`` leaves
     cast(scale * sum_r grad_r) (summed in rank order) in ``self.out`` on every rank."""
 
-    def __init__(self, n: int, rank: int, numel: int, out_dtype, device, group=None):
+    MODES = {"sm": 0, "ce": 1}  # HP_DAR_SM / HP_DAR_CE (include/hybridpath.h)
+
+    def __init__(self, n: int, rank: int, numel: int, out_dtype, device, group=None,
+                 mode: str = "ce"):
         import torch.distributed as dist
 
         from ._lib import HP_DTYPE
@@ -134,6 +137,7 @@ class DenseExchange:
             if r != rank:
                 buf = (C.c_ubyte * 64).from_buffer_copy(h)
                 call("hp_dar_open_peer", self.handle, r, C.addressof(buf))
+        call("hp_dar_set_mode", self.handle, self.MODES[mode])
         typestr = "<f4" if code == 0 else "<u2"
         t = torch.as_tensor(_DevPtr(optr.value, (numel,), typestr), device=device)
         self.out = t if code == 0 else t.view(torch.bfloat16)

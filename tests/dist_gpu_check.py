@@ -81,7 +81,7 @@ def main():
         if not np.allclose(got, ref, rtol=1e-5, atol=1e-6):
             ok = False
             why.append(f"step {step} dense differs (max {np.abs(got - ref).max():.3g})")
-        if runner.dense_exchange == "p2p":  # rank-order fp32 sum: bit-exact
+        if runner.dense_exchange in ("p2p", "p2p-sm"):  # rank-order fp32 sum: bit-exact
             seq = np.zeros_like(batches[0]["lstm"])
             for b in batches:
                 seq = seq + b["lstm"]

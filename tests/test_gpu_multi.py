@@ -19,6 +19,7 @@ def _ngpu():
 
 
 @pytest.mark.parametrize("opt,xchg,dense", [("adagrad", "p2p", "p2p"), ("adam", "p2p", "nccl"),
+                                            ("adagrad", "p2p", "p2p-sm"),
                                             ("sgd", "nccl", "nccl")])
 def test_multi_gpu_step_matches_oracle(opt, xchg, dense):
     n = min(_ngpu(), 8)

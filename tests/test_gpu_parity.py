@@ -53,8 +53,19 @@ K1_CASES = [
 ]
 
 
+@pytest.fixture(params=[0, 1], ids=["k_reduce", "k_rowstream"])
+def level0(request, cuda):
+    """Run the test with each level-0 reduce kernel (hp_debug_set_rowstream)."""
+    from paper_1808_02621_b200 import _lib
+
+    lib = _lib.load()
+    lib.hp_debug_set_rowstream(request.param)
+    yield request.param
+    lib.hp_debug_set_rowstream(0)
+
+
 @pytest.mark.parametrize("T,V,D,P,n,kind", K1_CASES)
-def test_sort_dedup_route_bit_exact(cuda, T, V, D, P, n, kind):
+def test_sort_dedup_route_bit_exact(cuda, level0, T, V, D, P, n, kind):
     from paper_1808_02621_b200 import ops
 
     rng = np.random.default_rng(T + V + D)
@@ -122,7 +133,7 @@ def _gather_full(tab):
 @pytest.mark.parametrize("opt", ["sgd", "adagrad", "adam"])
 @pytest.mark.parametrize("V,D,P,n,T", [(5000, 128, 6, 3, 3000), (800_000, 512, 8, 8, 2560),
                                        (37_000, 1024, 4, 2, 20000)])
-def test_merge_apply_bit_exact(cuda, opt, V, D, P, n, T):
+def test_merge_apply_bit_exact(cuda, level0, opt, V, D, P, n, T):
     """Owner K4: rows received from n sources (in source order) merged + applied."""
     from paper_1808_02621_b200 import ops
 
@@ -162,7 +173,7 @@ def test_merge_apply_bit_exact(cuda, opt, V, D, P, n, T):
 
 
 @pytest.mark.parametrize("opt", ["sgd", "adagrad", "adam"])
-def test_local_apply_and_gather(cuda, opt):
+def test_local_apply_and_gather(cuda, level0, opt):
     """n == 1 fused step (K1+K4 then K5) == oracle.sparse_step with one worker."""
     from paper_1808_02621_b200 import ops
     from paper_1808_02621_b200.synth import zipf_ids
