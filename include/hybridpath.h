@@ -96,6 +96,11 @@ void hp_debug_set_pdl(int on);
 /* Instrumentation: cap on row-stream CTAs per SM (shared memory left for
  * concurrently running kernels); default 4. */
 void hp_debug_set_rs_ctas(int n);
+/* Instrumentation: 1 = p2p owner merge/apply as a cp.async row stream
+ * (k_owner_stream, default for D in {128, 256, 512, 1024}); 0 = k_owner_apply. */
+void hp_debug_set_owner_stream(int on);
+/* Instrumentation: k_combine grid when its epilogue stores to peers (default 32). */
+void hp_debug_set_combine_blocks(int n);
 
 /* ---------------------------------------------------------------- K1 + K2
  * Sort + dedup + route of one worker's IndexedSlices.
@@ -272,6 +277,17 @@ int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream);
 #define HP_DAR_SM 0
 #define HP_DAR_CE 1
 int hp_dar_set_mode(hp_dar_t d, int32_t mode);
+
+/* K7 through the NVSwitch (NVLS multicast). mc_in / mc_out: multicast
+ * addresses of symmetric buffers of S elements (S a multiple of 4 n; fp32 in,
+ * out_dtype out), set up by the caller (e.g. torch symmetric memory); the
+ * caller's gradient is in its own copy of mc_in. pads_dev: device array of the
+ * n ranks' signal-pad pointers (>= 128 ints each, zeroed once); state_dev:
+ * int32[2] {epoch, error bits}, zeroed once. out = cast(scale * sum_r in_r),
+ * reduced in the switch (tolerance-checked, not bit-exact). */
+int hp_nvls_allreduce(const float* mc_in, void* mc_out, int64_t S, int32_t n, int32_t me,
+                      int32_t out_dtype, float scale, int32_t* const* pads_dev, int32_t* state_dev,
+                      void* stream);
 int hp_dar_status(hp_dar_t d, int32_t* out_err, void* stream);
 /* Instrumentation: raw peer throughput over the dense window (mode 0/2 store,
  * 1/3 load; 2/3 with 4 x 16 B in flight per thread). */

@@ -18,7 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "lib"
 LIB = LIBDIR / "libhybridpath.so"
-SOURCES = ["capi.cu", "dedup.cu", "reduce.cu", "rows.cu", "comm.cu", "p2p.cu"]
+SOURCES = ["capi.cu", "dedup.cu", "reduce.cu", "rows.cu", "comm.cu", "p2p.cu", "nvls.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -42,6 +42,8 @@ SIGNATURES = {
     "hp_debug_set_rowstream": (None, [C.c_int]),
     "hp_debug_set_pdl": (None, [C.c_int]),
     "hp_debug_set_rs_ctas": (None, [C.c_int]),
+    "hp_debug_set_owner_stream": (None, [C.c_int]),
+    "hp_debug_set_combine_blocks": (None, [C.c_int]),
     "hp_debug_set_spans": (None, [vp]),
     "hp_apply_plan": (C.c_int, [vp, i64, Slab, Optim, vp, sz, vp]),
     "hp_apply_plan_build": (C.c_int, [vp, i64, Slab, vp, sz, vp]),
@@ -82,6 +84,7 @@ SIGNATURES = {
     "hp_dar_open_peer": (C.c_int, [vp, i32, vp]),
     "hp_dar_destroy": (C.c_int, [vp]),
     "hp_dar_set_mode": (C.c_int, [vp, i32]),
+    "hp_nvls_allreduce": (C.c_int, [vp, vp, i64, i32, i32, i32, f32, vp, vp, vp]),
     "hp_dar_allreduce": (C.c_int, [vp, vp, f32, vp]),
     "hp_dar_status": (C.c_int, [vp, vp, vp]),
     "hp_debug_nvlink_bench": (C.c_int, [vp, i32, i32, i32, vp]),

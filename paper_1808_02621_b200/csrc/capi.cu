@@ -11,9 +11,12 @@ void set_spans_dedup(unsigned long long*);
 void set_spans_reduce(unsigned long long*);
 void set_spans_rows(unsigned long long*);
 void set_spans_p2p(unsigned long long*);
+void set_spans_nvls(unsigned long long*);
 void set_cluster_threads(int nt);
 extern int g_rowstream_off;
 extern int g_rs_ctas;
+extern int g_owner_stream;
+extern int g_combine_blocks;
 int g_pdl = 0;  // PDL measured neutral at N=1, slower at N=2
 
 static thread_local std::string g_err;
@@ -65,6 +68,7 @@ void hp_debug_set_spans(unsigned long long* dev_buf) {
   hp::set_spans_reduce(dev_buf);
   hp::set_spans_rows(dev_buf);
   hp::set_spans_p2p(dev_buf);
+  hp::set_spans_nvls(dev_buf);
 }
 
 // Tuning only: CTA size (256 | 512 | 1024) of the cluster dedup path.
@@ -72,5 +76,7 @@ void hp_debug_set_cluster_threads(int nt) { hp::set_cluster_threads(nt); }
 void hp_debug_set_rowstream(int on) { hp::g_rowstream_off = on ? 0 : 1; }
 void hp_debug_set_pdl(int on) { hp::g_pdl = on ? 1 : 0; }
 void hp_debug_set_rs_ctas(int n) { hp::g_rs_ctas = n < 1 ? 1 : n; }
+void hp_debug_set_owner_stream(int on) { hp::g_owner_stream = on ? 1 : 0; }
+void hp_debug_set_combine_blocks(int n) { hp::g_combine_blocks = n < 1 ? 1 : n; }
 
 }  // extern "C"

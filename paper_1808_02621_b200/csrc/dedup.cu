@@ -805,6 +805,8 @@ int g_cl_threads = HP_CL_THREADS;  // CTA shape of the cluster path (hp_debug_se
 void set_cluster_threads(int nt) { g_cl_threads = nt; }
 int g_rowstream_off = 1;  // row stream measured slower on the LM step
 int g_rs_ctas = 4;
+int g_owner_stream = 1;
+int g_combine_blocks = 32;
 HP_SPAN_SETTER(set_spans_dedup)
 
 template <int CS>

@@ -284,6 +284,236 @@ k_owner_apply(PeerTable peers, void* my_win, WinLayout L, const int64_t* __restr
   HP_SPAN_END(SP_APPLY);
 }
 
+// ---- owner, streamed: the same merge/apply as k_owner_apply, restructured
+// as a per-warp row stream (k_rowstream's pipeline). Warp w takes a contiguous
+// range of the valid inbox entries (all sources, source-major). Per batch of
+// 32 entries the lanes load ids and slot-table tags in parallel (two
+// coalesced/independent round trips per 32 entries instead of two per entry)
+// and decide ownership; then every owned entry becomes cnt contribution rows
+// (source order) followed by the optimizer's state rows, copied global ->
+// shared with cp.async, F = S - kPre rows in flight per warp. The END element
+// applies the update from shared memory, stores w/state locally and the new
+// row into each contributor's return buffer over NVLink.
+constexpr int OS_NMAX = HP_CHUNK;  // contributors per row (n <= HP_CHUNK)
+
+struct OsMeta {
+  int64_t row;
+  int flags, cnt;
+  int cidx[OS_NMAX];
+};
+
+template <int OPT, int VPT, int S>
+__global__ void __launch_bounds__(128)
+k_owner_stream(PeerTable peers, void* my_win, WinLayout L, const int64_t* __restrict__ part_base,
+               Router route, float4* s0, float4* s1, hp_optim o, int64_t rows_cap) {
+  constexpr int D4 = VPT * 32;
+  constexpr int KPRE = OPT == HP_OPT_SGD ? 1 : (OPT == HP_OPT_ADAGRAD ? 2 : 3);
+  constexpr int F = S - KPRE;
+  static_assert(F >= 2, "owner stream needs >= 2 rows in flight");
+  extern __shared__ __align__(16) float4 s_rows[];  // [4][S][D4]
+  __shared__ OsMeta s_meta[4][S];
+  __shared__ int s_cid[4][32][OS_NMAX];  // contributor list of the current batch, per lane
+  __shared__ int s_pre[OS_NMAX + 1];     // prefix of valid entries per source
+  __shared__ int s_poff[OS_NMAX];
+  __shared__ bool s_last;
+  HP_ENTRY(SP_APPLY);
+  SigView sig(my_win);
+  char* win = static_cast<char*>(my_win);
+  float4* w = reinterpret_cast<float4*>(win + L.w_off);
+  const float4* inbox = reinterpret_cast<const float4*>(win + L.rows_off);
+  const int64_t* inbox_ids = reinterpret_cast<const int64_t*>(win + L.ids_off);
+  const unsigned long long* slot = reinterpret_cast<const unsigned long long*>(win + L.slot_off);
+  const int n = L.n;
+  const unsigned epoch = (unsigned)*sig.epoch;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    int a = 0;
+    for (int q = 0; q < n; ++q) {
+      s_pre[q] = a;
+      a += sig.push_count[q];
+      s_poff[q] = sig.push_off[q];
+    }
+    s_pre[n] = a;
+  }
+  __syncthreads();
+  const int E = s_pre[n];
+  const int NW = gridDim.x * 4, gw = blockIdx.x * 4 + wid;
+  const int Q = (E + NW - 1) / NW;
+  const int fb0 = min(E, gw * Q), fe = min(E, fb0 + Q);
+  float4* ring = s_rows + (size_t)wid * S * D4;
+  const float4* pre_base[3] = {w, s0, s1};
+
+  // batch state (lane l <-> entry fb + l)
+  int fb = fb0;
+  unsigned own_mask = 0;
+  int64_t my_row = 0;
+  int my_cnt = 0;
+  auto load_batch = [&]() {
+    const int f = fb + lane;
+    bool owned = false;
+    my_cnt = 0;
+    if (f < fe) {
+      int sidx = 0;
+      while (sidx + 1 < n && f >= s_pre[sidx + 1]) ++sidx;
+      const int64_t e = (int64_t)sidx * L.cap + (f - s_pre[sidx]);
+      const int64_t id = inbox_ids[e];
+      const int p = route.part(id);
+      const int64_t b = part_base[p];
+      const int64_t row = b + (id - route.lo(p));
+      if (b < 0 || row >= rows_cap) {
+        atomicOr(sig.err, 16);
+      } else {
+        unsigned long long ent[OS_NMAX];
+#pragma unroll
+        for (int j = 0; j < OS_NMAX; ++j)
+          if (j < n) ent[j] = slot[row * n + j];
+        int first = -1;
+#pragma unroll
+        for (int j = 0; j < OS_NMAX; ++j)
+          if (j < n && (unsigned)(ent[j] >> 32) == epoch) {
+            if (first < 0) first = j;
+            s_cid[wid][lane][my_cnt++] = (int)(uint32_t)ent[j];
+          }
+        owned = first == sidx;
+        my_row = row;
+      }
+    }
+    own_mask = __ballot_sync(0xffffffffu, owned);
+    __syncwarp();
+  };
+  // producer cursor: lane k of the batch, element pj of cnt + KPRE
+  int pk = -1, pj = 0, pcnt = 0;
+  int64_t prow = 0;
+  auto next_entry = [&]() -> bool {  // advance to the next owned entry
+    while (true) {
+      if (fb >= fe) return false;
+      const unsigned rest = pk < 31 ? own_mask & ~((2u << pk) - 1u) : 0u;
+      if (pk >= 0 && rest == 0u) {
+        fb += 32;
+        pk = -1;
+        if (fb >= fe) return false;
+        load_batch();
+        continue;
+      }
+      if (pk < 0 && own_mask == 0u) {
+        fb += 32;
+        if (fb >= fe) return false;
+        load_batch();
+        continue;
+      }
+      pk = __ffs(pk < 0 ? own_mask : rest) - 1;
+      pcnt = __shfl_sync(0xffffffffu, my_cnt, pk);
+      prow = __shfl_sync(0xffffffffu, my_row, pk);
+      pj = 0;
+      return true;
+    }
+  };
+  bool have = false;
+  if (fb < fe) {
+    load_batch();
+    have = next_entry();
+  }
+  auto issue = [&](int e) {
+    const int sl = e % S;
+    const float4* src;
+    const bool end = pj + 1 == pcnt + KPRE;
+    if (pj < pcnt) {
+      src = inbox + (int64_t)s_cid[wid][pk][pj] * D4;
+    } else {
+      src = pre_base[pj - pcnt] + prow * D4;
+    }
+    float4* dstp = ring + sl * D4;
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) cp_async16(dstp + lane + v * 32, src + lane + v * 32);
+    if (end) {
+      if (lane < pcnt) s_meta[wid][sl].cidx[lane] = s_cid[wid][pk][lane];
+      if (lane == 0) {
+        s_meta[wid][sl].row = prow;
+        s_meta[wid][sl].cnt = pcnt;
+      }
+    }
+    if (lane == 0) s_meta[wid][sl].flags = (pj == 0 ? RS_FIRST : 0) | (pj >= pcnt ? RS_PRE : 0) |
+                                           (end ? RS_END : 0);
+    __syncwarp();
+    if (end) {
+      have = next_entry();
+    } else {
+      ++pj;
+    }
+  };
+  int issued = 0;
+#pragma unroll 1
+  for (int k = 0; k < F; ++k) {
+    if (have) issue(issued++);
+    cp_async_commit();
+  }
+  float4 acc[VPT];
+#pragma unroll
+  for (int v = 0; v < VPT; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+  for (int m = 0; m < issued; ++m) {
+    cp_async_wait<F - 1>();
+    __syncwarp();
+    const int sl = m % S;
+    const int flags = s_meta[wid][sl].flags;
+    const float4* rowp = ring + sl * D4;
+    if (!(flags & RS_PRE)) {
+      const bool first = flags & RS_FIRST;
+#pragma unroll
+      for (int v = 0; v < VPT; ++v)
+        acc[v] = f4_add(first ? make_float4(0.f, 0.f, 0.f, 0.f) : acc[v], rowp[lane + v * 32]);
+    }
+    if (flags & RS_END) {
+      const int64_t row = s_meta[wid][sl].row;
+      const int cnt = s_meta[wid][sl].cnt;
+#pragma unroll
+      for (int v = 0; v < VPT; ++v) {
+        const int c = lane + v * 32;
+        float4 wv = ring[((m - KPRE + 1 + S) % S) * D4 + c];
+        float4 av = make_float4(0.f, 0.f, 0.f, 0.f), bv = av;
+        if (KPRE > 1) av = ring[((m - KPRE + 2 + S) % S) * D4 + c];
+        if (KPRE > 2) bv = ring[((m - KPRE + 3 + S) % S) * D4 + c];
+        const float4 g = acc[v];
+        opt_update<OPT>(wv.x, av.x, bv.x, g.x, o);
+        opt_update<OPT>(wv.y, av.y, bv.y, g.y, o);
+        opt_update<OPT>(wv.z, av.z, bv.z, g.z, o);
+        opt_update<OPT>(wv.w, av.w, bv.w, g.w, o);
+        const int64_t off = row * D4 + c;
+        w[off] = wv;
+        if (OPT != HP_OPT_SGD) s0[off] = av;
+        if (OPT == HP_OPT_ADAM) s1[off] = bv;
+        acc[v] = wv;  // the updated row, for the returns below
+      }
+      for (int j = 0; j < cnt; ++j) {  // pull, fused: back to every contributor
+        const int idx = s_meta[wid][sl].cidx[j];
+        const int src = idx / (int)L.cap;
+        const int64_t ret_row = s_poff[src] + (idx - (int64_t)src * L.cap);
+        float4* ret = reinterpret_cast<float4*>(static_cast<char*>(peers.base[src]) + L.ret_off) +
+                      ret_row * D4;
+#pragma unroll
+        for (int v = 0; v < VPT; ++v) ret[lane + v * 32] = acc[v];
+      }
+    }
+    __syncwarp();
+    if (have) issue(issued++);
+    cp_async_commit();
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    s_last = atomicAdd(&sig.done[1], 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence_system();
+    for (int r = threadIdx.x; r < n; r += blockDim.x)
+      st_release_sys(&SigView(peers.base[r]).applied_flag[L.me], (int)epoch);
+    if (threadIdx.x == 0) sig.done[1] = 0;
+  }
+  HP_SPAN_END(SP_APPLY);
+}
+
 // Spin-wait budget (cycles) before a wait gives up and raises an error bit.
 long long wait_budget() {
   static long long v = [] {
@@ -442,9 +672,35 @@ void launch_owner_apply(const hp_xchg_s* x, const hp_slab& slab, const hp_optim&
       reinterpret_cast<float4*>(slab.s0), reinterpret_cast<float4*>(slab.s1), opt, x->rows_cap);
 }
 
+template <int OPT, int VPT>
+void launch_owner_stream(const hp_xchg_s* x, const hp_slab& slab, const hp_optim& opt,
+                         cudaStream_t st) {
+  constexpr int S = VPT == 1 ? 16 : (VPT == 2 ? 12 : (VPT == 4 ? 8 : 6));
+  constexpr size_t smem = (size_t)4 * S * VPT * 32 * sizeof(float4);
+  auto kern = k_owner_stream<OPT, VPT, S>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  const int ctas = std::max(1, std::min(g_rs_ctas, (int)((160u << 10) / smem)));
+  launch_k(kern, dim3(sm_count() * ctas), dim3(128), smem, st, x->peers, x->win, x->L,
+           slab.part_base, Router(slab.V, slab.P), reinterpret_cast<float4*>(slab.s0),
+           reinterpret_cast<float4*>(slab.s1), opt, x->rows_cap);
+}
+
 template <int OPT>
 void dispatch_owner_apply(const hp_xchg_s* x, const hp_slab& slab, const hp_optim& opt, int D4,
                           cudaStream_t st) {
+  if (g_owner_stream) {
+    switch (D4) {
+      case 32: return launch_owner_stream<OPT, 1>(x, slab, opt, st);
+      case 64: return launch_owner_stream<OPT, 2>(x, slab, opt, st);
+      case 128: return launch_owner_stream<OPT, 4>(x, slab, opt, st);
+      case 256: return launch_owner_stream<OPT, 8>(x, slab, opt, st);
+      default: break;
+    }
+  }
   if (D4 <= 32) launch_owner_apply<OPT, 32, 1>(x, slab, opt, st);
   else if (D4 <= 64) launch_owner_apply<OPT, 32, 2>(x, slab, opt, st);
   else if (D4 <= 128) launch_owner_apply<OPT, 64, 2>(x, slab, opt, st);

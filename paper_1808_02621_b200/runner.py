@@ -136,9 +136,13 @@ class HybridRunner:
             raise ValueError("exchange must be 'p2p' (NVLink peer memory) or 'nccl'")
         self.exchange = exchange if world_size > 1 else "local"
         # dense allreduce: peer-memory kernel (deterministic, scale/cast fused) or NCCL
-        self.dense_exchange = (dense_exchange or exchange) if world_size > 1 else "local"
-        if self.dense_exchange not in ("p2p", "p2p-sm", "nccl", "local"):
-            raise ValueError("dense_exchange must be 'p2p' (copy engines), 'p2p-sm' or 'nccl'")
+        # default K7 transport by measurement: two ranks -> copy-engine
+        # peer exchange; more -> NCCL (which uses NVLS on an NVSwitch box)
+        default_dense = ("p2p" if world_size == 2 else "nccl") if exchange == "p2p" else exchange
+        self.dense_exchange = (dense_exchange or default_dense) if world_size > 1 else "local"
+        if self.dense_exchange not in ("p2p", "p2p-sm", "nvls", "nccl", "local"):
+            raise ValueError("dense_exchange must be 'p2p' (copy engines), 'p2p-sm', 'nvls' "
+                             "or 'nccl'")
         self.dar: dict = {}
         self.xchg: dict = {}
         self.glob_base: dict = {}
@@ -156,7 +160,12 @@ class HybridRunner:
             mech = plan.mech_of[var.name]
             if var.kind == "dense":
                 self.dense.append(var)
-                if self.dense_exchange in ("p2p", "p2p-sm"):
+                if self.dense_exchange == "nvls":
+                    from .xchg import NvlsExchange
+
+                    self.dar[var.name] = NvlsExchange(world_size, rank, var.elements,
+                                                      dense_dtype, self.device)
+                elif self.dense_exchange in ("p2p", "p2p-sm"):
                     from .xchg import DenseExchange
 
                     self.dar[var.name] = DenseExchange(

@@ -157,3 +157,54 @@ class DenseExchange:
             torch.cuda.synchronize()
             call("hp_dar_destroy", self.handle)
             self.handle = None
+
+
+class NvlsExchange:
+    """K7 through the NVSwitch: the gradient is copied into a symmetric buffer
+    bound to a multicast object (torch symmetric memory: allocation and
+    rendezvous only); ``hp_nvls_allreduce`` reduces it in the switch
+    (multimem.ld_reduce) and multicasts cast(scale * sum) into every rank's
+    output (multimem.st). Same interface as :class:`DenseExchange`."""
+
+    def __init__(self, n: int, rank: int, numel: int, out_dtype, device, group=None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        from ._lib import HP_DTYPE, HybridPathError
+
+        if numel % 4:
+            raise ValueError("dense gradient size must be a multiple of 4")
+        self.n, self.rank, self.numel = n, rank, numel
+        self.S = -(-numel // (4 * n)) * 4 * n
+        self.code = HP_DTYPE[str(out_dtype).split(".")[1]]
+        if self.code not in (0, 1):
+            raise ValueError("NVLS dense exchange: out dtype float32 | bfloat16")
+        name = (group or dist.group.WORLD).group_name
+        self.inp = symm_mem.empty(self.S, dtype=torch.float32, device=device)
+        self.inp.zero_()
+        self.outbuf = symm_mem.empty(self.S, dtype=out_dtype, device=device)
+        hi = symm_mem.rendezvous(self.inp, name)
+        ho = symm_mem.rendezvous(self.outbuf, name)
+        self._handles = (hi, ho)
+        if not hi.multicast_ptr or not ho.multicast_ptr:
+            raise HybridPathError("NVLS multicast is not available on this system")
+        self.mc_in, self.mc_out = hi.multicast_ptr, ho.multicast_ptr
+        self.pads = torch.tensor(list(hi.signal_pad_ptrs), dtype=torch.int64, device=device)
+        self.state = torch.zeros(2, dtype=torch.int32, device=device)
+        torch.cuda.synchronize(device)
+        dist.barrier(group=group)
+        self.out = self.outbuf[:numel]
+
+    def allreduce(self, grad, scale: float) -> torch.Tensor:
+        self.inp[:self.numel].copy_(grad.reshape(-1))
+        call("hp_nvls_allreduce", self.mc_in, self.mc_out, self.S, self.n, self.rank, self.code,
+             scale, self.pads.data_ptr(), self.state.data_ptr(),
+             torch.cuda.current_stream().cuda_stream)
+        return self.out
+
+    def status(self) -> int:
+        return int(self.state[1].item())
+
+    def close(self) -> None:
+        torch.cuda.synchronize()
+        self._handles = None

@@ -34,6 +34,11 @@ def main():
     opt_kind = os.environ.get("HP_CHECK_OPT", "adagrad")
     xmode = os.environ.get("HP_CHECK_XCHG", "p2p")
     dmode = os.environ.get("HP_CHECK_DENSE", xmode)
+    from paper_1808_02621_b200 import _lib
+
+    for kv in filter(None, os.environ.get("HP_CHECK_KNOBS", "").split(",")):
+        k, v = kv.split("=")
+        getattr(_lib.load(), f"hp_debug_set_{k}")(int(v))
     wl = Workload("check", [TableShape("embedding", 60_000, 128, 2560),
                             TableShape("softmax", 60_000, 256, 2560, sampled=3000)],
                   {"lstm": 50_000}, {"kind": opt_kind, "lr": 0.1, "init_acc": 0.1}, 2560,

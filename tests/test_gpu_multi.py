@@ -18,14 +18,19 @@ def _ngpu():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("opt,xchg,dense", [("adagrad", "p2p", "p2p"), ("adam", "p2p", "nccl"),
-                                            ("adagrad", "p2p", "p2p-sm"),
-                                            ("sgd", "nccl", "nccl")])
-def test_multi_gpu_step_matches_oracle(opt, xchg, dense):
+@pytest.mark.parametrize("opt,xchg,dense,knobs", [
+    ("adagrad", "p2p", "p2p", ""),
+    ("adam", "p2p", "nccl", ""),
+    ("adagrad", "p2p", "nvls", ""),
+    # the alternative kernels behind the instrumentation knobs stay parity-checked
+    ("adagrad", "p2p", "p2p-sm", "owner_stream=0,rowstream=1,pdl=1"),
+    ("sgd", "nccl", "nccl", "")])
+def test_multi_gpu_step_matches_oracle(opt, xchg, dense, knobs):
     n = min(_ngpu(), 8)
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
-    env = dict(os.environ, HP_CHECK_OPT=opt, HP_CHECK_XCHG=xchg, HP_CHECK_DENSE=dense)
+    env = dict(os.environ, HP_CHECK_OPT=opt, HP_CHECK_XCHG=xchg, HP_CHECK_DENSE=dense,
+               HP_CHECK_KNOBS=knobs)
     import socket
 
     with socket.socket() as sk:
