@@ -79,6 +79,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"])
     ap.add_argument("--dense-exchange", default=None, choices=["p2p", "p2p-sm", "nvls", "nccl"])
+    ap.add_argument("--arch", default="hybrid", choices=["hybrid", "ar", "ps"],
+                    help="mechanism plan: transform_hybrid (default) / transform_ar / transform_ps")
     ap.add_argument("--knob", action="append", default=[],
                     help="instrumentation A/B: NAME=INT calls hp_debug_set_NAME(INT)")
     return ap.parse_args()
@@ -211,7 +213,7 @@ def config(args, wl):
                                             for t in wl.tables],
             "dense_elems": sum(wl.dense.values()), "optimizer": wl.optimizer["kind"],
             "partitions": args.partitions or wl.partitions, "words_per_worker": wl.words_per_worker,
-            "parallelism": f"hybrid dp{args.gpus}",
+            "parallelism": f"{args.arch} dp{args.gpus}",
             "l2_policy": "inputs rotated over distinct resident batches totalling > 2x L2"}
 
 
@@ -252,7 +254,13 @@ def main():
     P = args.partitions or wl.partitions
     graph = hp.load_graph_spec(json.dumps(wl.graph_json()))
     cluster = hp.ClusterSpec.b200_box(world)
-    plan = hp.transform_hybrid(graph, cluster, partitions={t.name: P for t in wl.tables})
+    parts = {t.name: P for t in wl.tables}
+    if args.arch == "ar":  # SURVEY §8f baselines: the same Weights under AR / PS
+        plan = hp.transform_ar(graph, cluster)
+    elif args.arch == "ps":
+        plan = hp.transform_ps(graph, cluster, local_agg=True, partitions=parts)
+    else:
+        plan = hp.transform_hybrid(graph, cluster, partitions=parts)
     opt = hp.OptimizerConfig(**wl.optimizer)
     runner = hp.HybridRunner(plan, graph, cluster, rank=rank, world_size=world, comm=comm,
                              optimizer=opt, device=dev, seed=0, exchange=args.exchange,

@@ -187,6 +187,19 @@ typedef struct hp_comm_s* hp_comm_t;
 int hp_dense_allreduce_scale_cast(hp_comm_t comm, float* in, void* out, int64_t count,
                                   int32_t out_dtype, float scale, void* stream);
 
+/* ---------------------------------------------------------------- other mechanisms
+ * (SURVEY §8f baselines: the same Weights under transform_ar / transform_ps.)
+ * hp_allgather: AR for a sparse Weight — AllGatherv of every worker's
+ *   IndexedSlices (`simulate.py:138-180`); rank r's `bytes` land at recv + r*bytes.
+ *   The concatenation is then applied locally on a full replica
+ *   (hp_apply_plan_build / hp_apply_plan with agg_scale).
+ * hp_dense_reduce_bcast: PS for a dense Weight — summed at its owner `root`
+ *   (greedy placement, `placement.py:195-198`), scale + cast there, broadcast
+ *   to every rank's out. in is clobbered on the owner. */
+int hp_allgather(hp_comm_t comm, const void* send, void* recv, int64_t bytes, void* stream);
+int hp_dense_reduce_bcast(hp_comm_t comm, float* in, void* out, int64_t count, int32_t out_dtype,
+                          float scale, int32_t root, void* stream);
+
 /* ---------------------------------------------------------------- comm / K3
  * One communicator per process/GPU over NCCL (NVLink 5 / NVSwitch).
  * Replaces: the modelled PS pull/push messages (`simulate.py:183-240`). */

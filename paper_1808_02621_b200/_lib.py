@@ -59,6 +59,8 @@ SIGNATURES = {
     "hp_init_rows": (C.c_int, [vp, i64, i64, i32, u64, f32, vp]),
     "hp_fill": (C.c_int, [vp, i64, f32, vp]),
     "hp_step_counter_inc": (C.c_int, [vp, vp]),
+    "hp_allgather": (C.c_int, [vp, vp, vp, i64, vp]),
+    "hp_dense_reduce_bcast": (C.c_int, [vp, vp, vp, i64, i32, f32, i32, vp]),
     "hp_dense_allreduce_scale_cast": (C.c_int, [vp, vp, vp, i64, i32, f32, vp]),
     "hp_nccl_unique_id_bytes": (C.c_int, []),
     "hp_nccl_get_unique_id": (C.c_int, [vp]),

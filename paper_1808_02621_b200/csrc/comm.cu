@@ -140,4 +140,36 @@ int hp_dense_allreduce_scale_cast(hp_comm_t comm, float* in, void* out, int64_t 
   return scale_cast(in, out, count, out_dtype, scale, st);
 }
 
+// AR for a sparse Weight (reference AllGatherv, `simulate.py:138-180`): every
+// rank's block of `bytes` lands at recv + r * bytes, in rank order.
+int hp_allgather(hp_comm_t comm, const void* send, void* recv, int64_t bytes, void* stream) {
+  HP_REQUIRE(comm && send && recv && bytes >= 0, "bad allgather arguments");
+  if (bytes == 0) return HP_OK;
+  HP_NCCL(ncclAllGather(send, recv, (size_t)bytes, ncclUint8, comm->comm,
+                        static_cast<cudaStream_t>(stream)));
+  return HP_OK;
+}
+
+// PS for a dense Weight (its one owner `root`, reference `placement.py:195-198`):
+// the gradients are summed at the owner (ncclReduce, in place in `in` there),
+// scaled + cast into `out` at the owner, and broadcast to every rank's `out`.
+// `in` is clobbered on the owner.
+int hp_dense_reduce_bcast(hp_comm_t comm, float* in, void* out, int64_t count, int32_t out_dtype,
+                          float scale, int32_t root, void* stream) {
+  HP_REQUIRE(count >= 0 && (count == 0 || (in && out)), "bad dense arguments");
+  HP_REQUIRE(comm && root >= 0 && root < comm->nranks, "bad root");
+  HP_REQUIRE(out_dtype == HP_DTYPE_F32 || out_dtype == HP_DTYPE_BF16 || out_dtype == HP_DTYPE_F16,
+             "unknown out dtype");
+  if (count == 0) return HP_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  HP_NCCL(ncclReduce(in, in, count, ncclFloat32, ncclSum, root, comm->comm, st));
+  if (comm->rank == root) {
+    int rc = scale_cast(in, out, count, out_dtype, scale, st);
+    if (rc) return rc;
+  }
+  const size_t ob = out_dtype == HP_DTYPE_F32 ? 4 : 2;
+  HP_NCCL(ncclBroadcast(out, out, (size_t)count * ob, ncclUint8, root, comm->comm, st));
+  return HP_OK;
+}
+
 }  // extern "C"

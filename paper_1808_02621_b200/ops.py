@@ -245,3 +245,26 @@ def dense_allreduce_scale_cast(comm, grad: torch.Tensor, out: torch.Tensor, scal
     call("hp_dense_allreduce_scale_cast", comm, _p(grad), _p(out), grad.numel(), code, scale,
          _stream(stream))
     return out
+
+
+def allgather(comm, src: torch.Tensor, dst: torch.Tensor, stream=None) -> torch.Tensor:
+    """AR for a sparse Weight: dst = concat over ranks of src (rank order)."""
+    if not (src.is_contiguous() and dst.is_contiguous()) or src.dtype != dst.dtype:
+        raise TypeError("src and dst must be contiguous tensors of one dtype")
+    nb = src.numel() * src.element_size()
+    if dst.numel() * dst.element_size() < nb * _lib.load().hp_comm_size(comm):
+        raise ValueError("dst too small for the allgather")
+    call("hp_allgather", comm, _p(src), _p(dst), nb, _stream(stream))
+    return dst
+
+
+def dense_reduce_bcast(comm, grad: torch.Tensor, out: torch.Tensor, scale: float, root: int,
+                       stream=None) -> torch.Tensor:
+    """PS for a dense Weight: out = cast(scale * sum over ranks of grad), reduced at ``root``."""
+    _need(grad, torch.float32, "grad")
+    if out.numel() != grad.numel() or not out.is_contiguous():
+        raise ValueError("out must be contiguous with grad's size")
+    code = _lib.HP_DTYPE[str(out.dtype).split(".")[1]]
+    call("hp_dense_reduce_bcast", comm, _p(grad), _p(out), grad.numel(), code, scale, root,
+         _stream(stream))
+    return out

@@ -145,6 +145,8 @@ class HybridRunner:
                              "or 'nccl'")
         self.dar: dict = {}
         self.xchg: dict = {}
+        self.ar_tables: set = set()   # sparse Weights under AR at n > 1 (AllGatherv baseline)
+        self.dense_ps: dict = {}      # dense Weights under PS at n > 1: name -> owner rank
         self.glob_base: dict = {}
         self.plan, self.graph, self.cluster = plan, graph, cluster
         self.rank, self.world_size, self.comm = rank, world_size, comm
@@ -160,7 +162,9 @@ class HybridRunner:
             mech = plan.mech_of[var.name]
             if var.kind == "dense":
                 self.dense.append(var)
-                if self.dense_exchange == "nvls":
+                if mech is Mechanism.PS and world_size > 1:  # reduce at the owner + broadcast
+                    self.dense_ps[var.name] = plan.owner_of(var.name, 0)
+                elif self.dense_exchange == "nvls":
                     from .xchg import NvlsExchange
 
                     self.dar[var.name] = NvlsExchange(world_size, rank, var.elements,
@@ -177,12 +181,11 @@ class HybridRunner:
                 owner = plan.owner_table(var.name)
             elif world_size == 1:
                 P, owner = 1, np.zeros(1, dtype=np.int32)  # AR over one replica: local apply
-            else:
-                raise NotImplementedError(
-                    f"sparse Weight {var.name!r} resolved to AR at n={world_size}: the "
-                    "AllGatherv baseline is SURVEY §8(f) 'next', not built yet")
+            else:  # AR at n > 1: a full replica per rank, fed by an AllGatherv of the slices
+                P, owner = 1, np.array([rank], dtype=np.int32)
+                self.ar_tables.add(var.name)
             storage = None
-            if self.exchange == "p2p":
+            if self.exchange == "p2p" and var.name not in self.ar_tables:
                 storage = self._make_window(var, P, owner, (max_ids or {}).get(var.name))
             self.tables[var.name] = ShardedTable(var, P, owner, rank, self.optimizer,
                                                  self.device, seed=seed * 1000 + i,
@@ -325,6 +328,26 @@ class HybridRunner:
         self._kev(f"k5:{tab.name}", False)
         return out
 
+    def _sparse_ar(self, tab: ShardedTable, ids, vals, opt) -> torch.Tensor:
+        """A sparse Weight under AR (SURVEY §8f baseline; reference AllGatherv,
+        `simulate.py:138-180`): every rank gathers every rank's raw slices and
+        applies the concatenation to its own full replica (same result on all
+        ranks), then pulls its rows locally. T must be equal on all ranks."""
+        n, T, D = self.world_size, ids.numel(), tab.D
+        comm = self.comm.ptr
+        ids_all = self._buf(tab.name, "ar_ids", (n * T,), torch.int64)
+        vals_all = self._buf(tab.name, "ar_vals", (n * T, D), torch.float32)
+        ops.allgather(comm, ids.contiguous(), ids_all)
+        ops.allgather(comm, vals.contiguous(), vals_all)
+        slab = tab.slab()
+        ops.apply_plan_build(ids_all, slab, tab.wss[0])
+        self._kev(f"k4:{tab.name}", True)
+        ops.apply_plan(vals_all, n * T, slab, opt, tab.wss[0])
+        self._kev(f"k4:{tab.name}", False)
+        out = self._buf(tab.name, "out", (T, D), torch.float32)
+        ops.gather_rows(slab, ids, out)
+        return out
+
     def _sparse_exchange(self, tab: ShardedTable, ids, vals, opt, ev) -> torch.Tensor:
         n, D, T = self.world_size, tab.D, ids.numel()
         name = tab.name
@@ -380,7 +403,11 @@ class HybridRunner:
 
         ev("start")
         t0 = time.perf_counter()
-        concurrent = self.concurrent_tables and (self.world_size == 1 or self.exchange == "p2p")
+        # NCCL calls of one communicator must not run on concurrent streams: the
+        # AR-sparse / PS-dense baselines (NCCL on the table streams) run serially
+        concurrent = self.concurrent_tables and (
+            self.world_size == 1 or (self.exchange == "p2p" and not self.ar_tables
+                                     and not self.dense_ps))
         if concurrent:
             # The dense allreduce and every table are independent: each runs on
             # its own stream (parallel branches when captured as a CUDA graph).
@@ -440,7 +467,10 @@ class HybridRunner:
                 out = g if self.dense_dtype == torch.float32 else torch.empty(
                     g.shape, dtype=self.dense_dtype, device=self.device)
             self._kev(f"k7:{var.name}", True)
-            if var.name in self.dar:
+            if var.name in self.dense_ps:
+                self.dense_out[var.name] = ops.dense_reduce_bcast(
+                    self.comm.ptr, g, out, self.scale, self.dense_ps[var.name])
+            elif var.name in self.dar:
                 self.dense_out[var.name] = self.dar[var.name].allreduce(g, self.scale)
             else:
                 self.dense_out[var.name] = ops.dense_allreduce_scale_cast(
@@ -463,6 +493,10 @@ class HybridRunner:
             out = self._sparse_local(tab, ids, vals, opt, slot, planned)
             if ev:
                 ev("update")
+        elif tab.name in self.ar_tables:
+            out = self._sparse_ar(tab, ids, vals, opt)
+            if ev:
+                ev("network")
         elif self.exchange == "p2p":
             out = self._sparse_p2p(tab, ids, vals, opt, slot, planned)
             if ev:
@@ -474,7 +508,8 @@ class HybridRunner:
 
     @property
     def pipelined(self) -> bool:
-        return self.world_size == 1 or self.exchange == "p2p"
+        return ((self.world_size == 1 or self.exchange == "p2p") and not self.ar_tables
+                and not self.dense_ps)
 
     def prefetch(self, batch: dict) -> None:
         """Build the plans of ``batch`` now (stream-ordered) so its step skips dedup."""
@@ -546,8 +581,10 @@ class HybridRunner:
         R = len(batches)
         if R < 2 or R % 2:
             raise ValueError("capture_pipelined needs an even number (>= 2) of batches")
-        if not self.pipelined:
+        if self.world_size > 1 and self.exchange != "p2p":
             raise NotImplementedError("the NCCL a2a-v path reads counts on the host")
+        # (the AR-sparse / PS-dense baselines are not pipelined: each graph then
+        # plans its own batch; prefetch() and next_batch are no-ops for them)
         self.prefetch(batches[0])
         for r in range(R):  # eager warm-up rotation (sizes every buffer)
             self.step(batches[r], timed=False, next_batch=batches[(r + 1) % R])

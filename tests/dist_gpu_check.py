@@ -45,7 +45,14 @@ def main():
                   partitions=8)
     graph = hp.load_graph_spec(json.dumps(wl.graph_json()))
     cluster = hp.ClusterSpec.b200_box(world)
-    plan = hp.transform_hybrid(graph, cluster, partitions={"embedding": 8, "softmax": 12})
+    arch = os.environ.get("HP_CHECK_ARCH", "hybrid")
+    parts = {"embedding": 8, "softmax": 12}
+    if arch == "ar":  # SURVEY §8f baselines: every Weight AR / every Weight PS
+        plan = hp.transform_ar(graph, cluster)
+    elif arch == "ps":
+        plan = hp.transform_ps(graph, cluster, local_agg=True, partitions=parts)
+    else:
+        plan = hp.transform_hybrid(graph, cluster, partitions=parts)
     runner = hp.HybridRunner(plan, graph, cluster, rank=rank, world_size=world, comm=comm,
                              optimizer=hp.OptimizerConfig(kind=opt_kind, lr=0.1), device=dev,
                              seed=5, exchange=xmode, dense_exchange=dmode)
@@ -53,6 +60,14 @@ def main():
     states = {t.name: orc.init_state(opt_kind, t.V, t.D, 5 * 1000 + i + 1, 0.1)
               for i, t in enumerate(wl.tables)}
     ok, why = True, []
+
+    def oracle_step(name, step, tb):
+        if name in runner.ar_tables:
+            orc.ar_sparse_step(states[name], opt_kind, hpar, step, tb)
+        else:
+            V = next(t.V for t in wl.tables if t.name == name)
+            orc.sparse_step(states[name], opt_kind, hpar, step, tb, V, plan.partitions_of[name],
+                            plan.owner_table(name))
     def to_dev(b):
         return {k: ((torch.from_numpy(v[0]).to(dev), torch.from_numpy(v[1]).to(dev))
                     if isinstance(v, tuple) else torch.from_numpy(v).to(dev)) for k, v in b.items()}
@@ -66,9 +81,7 @@ def main():
         batch = staged[step]
         stats = runner.step(batch, next_batch=staged.get(step + 1) if xmode == "p2p" else None)
         for t in wl.tables:
-            owner = plan.owner_table(t.name)
-            orc.sparse_step(states[t.name], opt_kind, hpar, step, [b[t.name] for b in batches],
-                            t.V, plan.partitions_of[t.name], owner)
+            oracle_step(t.name, step, [b[t.name] for b in batches])
             got = runner.outputs[t.name].cpu().numpy()
             if not np.array_equal(got, states[t.name]["w"][mine[t.name][0]]):
                 ok = False
@@ -86,7 +99,7 @@ def main():
         if not np.allclose(got, ref, rtol=1e-5, atol=1e-6):
             ok = False
             why.append(f"step {step} dense differs (max {np.abs(got - ref).max():.3g})")
-        if runner.dense_exchange in ("p2p", "p2p-sm"):  # rank-order fp32 sum: bit-exact
+        if runner.dense_exchange in ("p2p", "p2p-sm") and not runner.dense_ps:  # rank order
             seq = np.zeros_like(batches[0]["lstm"])
             for b in batches:
                 seq = seq + b["lstm"]
@@ -116,8 +129,7 @@ def main():
             del g  # release the captured NCCL/peer work before tearing the comms down
             for st_ in (4, 5):
                 for t in wl.tables:
-                    orc.sparse_step(states[t.name], opt_kind, hpar, st_, [b[t.name] for b in batches],
-                                    t.V, plan.partitions_of[t.name], plan.owner_table(t.name))
+                    oracle_step(t.name, st_, [b[t.name] for b in batches])
             torch.cuda.synchronize()
             if True:  # Adam's step size comes from the device step counter
                 for t in wl.tables:

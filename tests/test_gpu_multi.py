@@ -18,19 +18,22 @@ def _ngpu():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("opt,xchg,dense,knobs", [
-    ("adagrad", "p2p", "p2p", ""),
-    ("adam", "p2p", "nccl", ""),
-    ("adagrad", "p2p", "nvls", ""),
+@pytest.mark.parametrize("opt,xchg,dense,knobs,arch", [
+    ("adagrad", "p2p", "p2p", "", "hybrid"),
+    ("adam", "p2p", "nccl", "", "hybrid"),
+    ("adagrad", "p2p", "nvls", "", "hybrid"),
     # the alternative kernels behind the instrumentation knobs stay parity-checked
-    ("adagrad", "p2p", "p2p-sm", "owner_stream=0,rowstream=1,pdl=1"),
-    ("sgd", "nccl", "nccl", "")])
-def test_multi_gpu_step_matches_oracle(opt, xchg, dense, knobs):
+    ("adagrad", "p2p", "p2p-sm", "owner_stream=0,rowstream=1,pdl=1", "hybrid"),
+    ("sgd", "nccl", "nccl", "", "hybrid"),
+    # SURVEY §8f baselines: sparse under AR (AllGatherv), dense under PS (reduce + bcast)
+    ("adagrad", "p2p", "p2p", "", "ar"),
+    ("adam", "p2p", "p2p", "", "ps")])
+def test_multi_gpu_step_matches_oracle(opt, xchg, dense, knobs, arch):
     n = min(_ngpu(), 8)
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     env = dict(os.environ, HP_CHECK_OPT=opt, HP_CHECK_XCHG=xchg, HP_CHECK_DENSE=dense,
-               HP_CHECK_KNOBS=knobs)
+               HP_CHECK_KNOBS=knobs, HP_CHECK_ARCH=arch)
     import socket
 
     with socket.socket() as sk:

@@ -135,3 +135,21 @@ def test_c_oracle_bit_exact_vs_numpy(T, D, V, n, P):
             assert np.array_equal(s1[k], s2[k]), (opt, k)
         for x, y in zip(r1, r2):
             assert np.array_equal(x["out"], y["out"])
+
+
+def test_ar_sparse_step_is_one_worker_step_over_the_concatenation():
+    """AR for a sparse Weight = the concatenated slices applied once, scaled by 1/n."""
+    rng = np.random.default_rng(3)
+    V, D, n, T = 500, 8, 3, 200
+    batches = [(rng.integers(0, V, T), rng.standard_normal((T, D)).astype(F32)) for _ in range(n)]
+    a = orc.init_state("adagrad", V, D, 1)
+    b = {k: v.copy() for k, v in a.items()}
+    res = orc.ar_sparse_step(a, "adagrad", {"lr": 0.1}, 1, batches)
+    ids = np.concatenate([x[0] for x in batches])
+    vals = np.concatenate([x[1] for x in batches])
+    uniq, sums, _, _ = orc.grouped_tree_sum(ids, vals)
+    orc.apply_rows("adagrad", b, uniq, sums * F32(1.0 / n), {"lr": 0.1}, 1)
+    for k in a:
+        assert np.array_equal(a[k], b[k])
+    for r, (i, _) in enumerate(batches):
+        assert np.array_equal(res[r]["out"], b["w"][i])
