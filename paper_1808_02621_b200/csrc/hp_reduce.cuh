@@ -96,6 +96,18 @@ struct EpiApply {
   }
 };
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 // Level 0 of the summation tree. A group of TPI threads owns an item
 // {j0, n <= HP_CHUNK, dst, final}; each thread owns VPT float4 columns
 // (c4 = lane-in-group + k*TPI). Row positions are loaded once per warp and
@@ -105,8 +117,13 @@ struct EpiApply {
 // partial row for k_combine. Small groups + <= 64 registers keep many items
 // in flight per SM: the kernel is latency-bound on the item chain
 // (descriptor -> positions/table rows -> gradient rows).
+template <int TPI, int VPT, class Epi>
+__host__ __device__ constexpr bool reduce_smem_pre() {
+  return Epi::kPre > 0 && VPT <= 2 && (256 / TPI) * Epi::kPre * TPI * VPT * 16 <= 32768;
+}
+
 template <int TPI, int VPT, int B, class Epi>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, reduce_smem_pre<TPI, VPT, Epi>() ? 4 : 3)
 k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
   const float4* __restrict__ vals = reinterpret_cast<const float4*>(vals_f);
   float4* partials = reinterpret_cast<float4*>(pl.partials);
@@ -115,15 +132,34 @@ k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
   const int q = threadIdx.x % TPI;
   const int lane = threadIdx.x & 31;
   HP_ENTRY(SP_REDUCE);
+  // The epilogue's table rows (w, optimizer state) are staged through shared
+  // memory with cp.async (each thread copies and later reads only its own
+  // columns) instead of registers: ~16 fewer registers per thread at LM shapes.
+  constexpr int KP = Epi::kPre;
+  constexpr bool SP = reduce_smem_pre<TPI, VPT, Epi>();
+  __shared__ float4 s_pre[SP ? GPB * KP * VPT * TPI : 1];
+  float4* my_pre = s_pre + (threadIdx.x / TPI) * KP * VPT * TPI + q;  // [g][k][v][TPI]
   const int n_items = pl.counters[C_ITEMS];
   for (int it = blockIdx.x * GPB + threadIdx.x / TPI; it < n_items; it += gridDim.x * GPB) {
     const int4 item = pl.items[it];
     const int j0 = item.x, n = item.y, dst = item.z;
     const bool fin = item.w != 0;
-    typename Epi::Pre pre[VPT];
+    typename Epi::Pre pre[SP ? 1 : VPT];
+    if (fin && dst >= 0) {
+      if constexpr (SP) {
 #pragma unroll
-    for (int v = 0; v < VPT; ++v)
-      if (fin && dst >= 0 && q + v * TPI < D4) pre[v] = epi.load(dst, q + v * TPI);
+        for (int k = 0; k < KP; ++k)
+#pragma unroll
+          for (int v = 0; v < VPT; ++v)
+            if (q + v * TPI < D4)
+              cp_async16(my_pre + (k * VPT + v) * TPI, epi.pre_row(k, dst) + q + v * TPI);
+        cp_async_commit();
+      } else {
+#pragma unroll
+        for (int v = 0; v < VPT; ++v)
+          if (q + v * TPI < D4) pre[v] = epi.load(dst, q + v * TPI);
+      }
+    }
     // single-row items carry the row's position directly (item.x = -(pos+1))
     const int myp = j0 < 0 ? -j0 - 1 : (lane < n ? pl.sorted_pos[j0 + lane] : 0);
     float4 acc[VPT];
@@ -144,12 +180,24 @@ k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
         for (int v = 0; v < VPT; ++v)
           if (jb + e < n) acc[v] = f4_add(acc[v], x[e][v]);
     }
+    if constexpr (SP) {
+      if (fin && dst >= 0) cp_async_wait<0>();
+    }
 #pragma unroll
     for (int v = 0; v < VPT; ++v) {
       const int c4 = q + v * TPI;
       if (c4 >= D4) continue;
       if (fin) {
-        if (dst >= 0) epi.store(dst, c4, acc[v], pre[v]);
+        if (dst >= 0) {
+          if constexpr (SP) {
+            typename Epi::Pre p;
+#pragma unroll
+            for (int k = 0; k < KP; ++k) set_pre(p, k, my_pre[(k * VPT + v) * TPI]);
+            epi.store(dst, c4, acc[v], p);
+          } else {
+            epi.store(dst, c4, acc[v], pre[v]);
+          }
+        }
       } else {
         partials[(int64_t)dst * D4 + c4] = acc[v];
       }
@@ -233,17 +281,6 @@ __global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
 }
 
 // ------------------------------------------------------------------ row stream
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
 
 enum { RS_FIRST = 1, RS_PRE = 2, RS_END = 4, RS_FIN = 8 };
 
