@@ -101,6 +101,8 @@ void hp_debug_set_rs_ctas(int n);
 void hp_debug_set_owner_stream(int on);
 /* Instrumentation: k_combine grid when its epilogue stores to peers (default 32). */
 void hp_debug_set_combine_blocks(int n);
+/* Instrumentation: k_reduce rows in flight per thread at 2 float4 columns (2 = default, 4, 8). */
+void hp_debug_set_reduce_b(int b);
 
 /* ---------------------------------------------------------------- K1 + K2
  * Sort + dedup + route of one worker's IndexedSlices.

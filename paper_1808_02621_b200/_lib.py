@@ -8,9 +8,12 @@ can check the ABI without a GPU.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libhybridpath.so"
+# HP_LIB overrides the library path (A/B of two builds of the same sources)
+LIB_PATH = Path(os.environ.get("HP_LIB") or Path(__file__).resolve().parent / "lib" /
+                "libhybridpath.so")
 
 HP_OPT = {"sgd": 0, "adagrad": 1, "adam": 2}
 HP_DTYPE = {"float32": 0, "bfloat16": 1, "float16": 2}
@@ -44,6 +47,7 @@ SIGNATURES = {
     "hp_debug_set_rs_ctas": (None, [C.c_int]),
     "hp_debug_set_owner_stream": (None, [C.c_int]),
     "hp_debug_set_combine_blocks": (None, [C.c_int]),
+    "hp_debug_set_reduce_b": (None, [C.c_int]),
     "hp_debug_set_spans": (None, [vp]),
     "hp_apply_plan": (C.c_int, [vp, i64, Slab, Optim, vp, sz, vp]),
     "hp_apply_plan_build": (C.c_int, [vp, i64, Slab, vp, sz, vp]),

@@ -453,11 +453,16 @@ template <int TPI, int VPT, class Epi>
 void launch_k_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaStream_t st) {
   // rows in flight per batch: most items hold 1-2 rows, so a small batch keeps
   // registers (and so resident items per SM) up without costing the hot chunks much
-  constexpr int B = VPT >= 4 ? 2 : 8 / VPT;
+  constexpr int B = VPT >= 2 ? 2 : 8;  // measured: B=2 beats 4 and 8 at VPT=2
   // <= one group per item; peer-store epilogues stay in one resident wave so
   // each block pays its system-scope fence once
   const int blocks = grid_for(pl.T, 256 / TPI, sm_count() * (Epi::kRemote ? 3 : 16));
-  launch_k(k_reduce<TPI, VPT, B, Epi>, dim3(blocks), dim3(256), 0, st, pl, vals, epi);
+  if (VPT == 2 && g_reduce_b == 4)
+    launch_k(k_reduce<TPI, VPT, 4, Epi>, dim3(blocks), dim3(256), 0, st, pl, vals, epi);
+  else if (VPT == 2 && g_reduce_b == 8)
+    launch_k(k_reduce<TPI, VPT, 8, Epi>, dim3(blocks), dim3(256), 0, st, pl, vals, epi);
+  else
+    launch_k(k_reduce<TPI, VPT, B, Epi>, dim3(blocks), dim3(256), 0, st, pl, vals, epi);
 }
 
 template <class Epi>
