@@ -19,6 +19,7 @@ measured phase times (CUDA events) and measured exchange bytes.
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -202,9 +203,15 @@ class HybridRunner:
         self.step_count = 0
         self.last_counts: dict = {}
         self.kernel_events: dict | None = None
-        self._streams = {n: torch.cuda.Stream(device=self.device) for n in self.tables}
-        self._dense_stream = torch.cuda.Stream(device=self.device)
-        self._plan_streams = {n: torch.cuda.Stream(device=self.device) for n in self.tables}
+        # Stream priorities (lower = scheduled first; measured): the
+        # next step's plans (latency-bound cluster sort) first, then the tables'
+        # apply chains, the dense allreduce last. HP_STREAM_PRIO="table,dense,plan".
+        pt, pd, pp = (int(x) for x in os.environ.get("HP_STREAM_PRIO", "-1,0,-2").split(","))
+        self._streams = {n: torch.cuda.Stream(device=self.device, priority=pt)
+                         for n in self.tables}
+        self._dense_stream = torch.cuda.Stream(device=self.device, priority=pd)
+        self._plan_streams = {n: torch.cuda.Stream(device=self.device, priority=pp)
+                              for n in self.tables}
         self._pending_counts: dict = {}
         self.concurrent_tables = True
 
