@@ -78,7 +78,7 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"])
-    ap.add_argument("--dense-exchange", default=None, choices=["p2p", "p2p-sm", "nvls", "nccl"])
+    ap.add_argument("--dense-exchange", default=None, choices=["p2p", "p2p-sm", "p2p-pipe", "nvls", "nccl"])
     ap.add_argument("--arch", default="hybrid", choices=["hybrid", "ar", "ps"],
                     help="mechanism plan: transform_hybrid (default) / transform_ar / transform_ps")
     ap.add_argument("--knob", action="append", default=[],

@@ -101,6 +101,8 @@ void hp_debug_set_rs_ctas(int n);
 void hp_debug_set_owner_stream(int on);
 /* Instrumentation: k_combine grid when its epilogue stores to peers (default 32). */
 void hp_debug_set_combine_blocks(int n);
+/* Grid of the pipelined dense allreduce (HP_DAR_PIPE); 0 = one block per SM. */
+void hp_debug_set_dar_blocks(int n);
 /* Instrumentation: k_reduce rows in flight per thread at 2 float4 columns (2 = default, 4, 8). */
 void hp_debug_set_reduce_b(int b);
 
@@ -291,6 +293,7 @@ int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream);
  * HP_DAR_SM = peer stores from SM kernels. Same result bit for bit. */
 #define HP_DAR_SM 0
 #define HP_DAR_CE 1
+#define HP_DAR_PIPE 2 /* one persistent kernel; scatter and reduce-gather pipelined by 64 KB pieces */
 int hp_dar_set_mode(hp_dar_t d, int32_t mode);
 
 /* K7 through the NVSwitch (NVLS multicast). mc_in / mc_out: multicast

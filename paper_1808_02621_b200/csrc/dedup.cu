@@ -807,6 +807,7 @@ int g_rowstream_off = 1;  // row stream measured slower on the LM step (DESIGN.m
 int g_rs_ctas = 4;
 int g_owner_stream = 1;
 int g_combine_blocks = 32;
+int g_dar_blocks = 0;  // HP_DAR_PIPE grid (0 = one block per SM)
 int g_reduce_b = 2;
 HP_SPAN_SETTER(set_spans_dedup)
 

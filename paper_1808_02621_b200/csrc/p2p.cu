@@ -962,6 +962,136 @@ k_ar_reduce_local(void* my_win, ArLayout A, const float4* __restrict__ grad, flo
   HP_SPAN_END(SP_AR_RG);
 }
 
+// ---- pipelined variant (HP_DAR_PIPE): ONE persistent kernel per rank. Every
+// chunk is cut into pieces of AR_PIECE4 float4; the work items are, in queue
+// order, (a) "scatter piece k of chunk c to rank c" for every peer c, then
+// (b) "reduce piece k of my chunk". A block that finished storing a scatter
+// piece raises the piece's arrival counter at its owner (system-scope atomic
+// after a system fence); a reduce item waits for the n-1 arrivals of its piece,
+// sums the n contributions in source-rank order (own contribution read from
+// grad), scales, casts and stores the result into every rank's output. Items
+// are taken from a device queue in order, so no block spins on a reduce item
+// before every scatter item of its rank has been taken by a running block:
+// no deadlock whatever the residency. The scatter of piece k+1 and the reduce
+// of piece k overlap, so both NVLink directions carry both phases at once.
+// Arrival counters are monotonic (epoch e expects e * (n-1)); the last block
+// raises applied_flag[me] = e at every rank, resets the queue and bumps epoch.
+constexpr int64_t AR_PIECE4 = 4096;  // 64 KB of fp32 per work item
+
+template <typename OutT>
+__global__ void __launch_bounds__(256)
+k_ar_pipe(PeerTable peers, void* my_win, ArLayout A, const float4* __restrict__ grad, float scale,
+          int* __restrict__ arrive, int* __restrict__ queue, long long timeout_cycles) {
+  __shared__ int s_item;
+  __shared__ bool s_last;
+  HP_ENTRY(SP_AR_SCATTER);
+  SigView sig(my_win);
+  const int n = A.n, me = A.me;
+  const int e = *sig.epoch + 1;
+  const int64_t c4 = A.chunk >> 2, real4 = A.S_real >> 2;
+  const int K = (int)((c4 + AR_PIECE4 - 1) / AR_PIECE4);
+  const int n_sc = (n - 1) * K, n_items = n_sc + K;
+  const float4* slots = reinterpret_cast<const float4*>(static_cast<char*>(my_win) + A.slots_off);
+  while (true) {
+    if (threadIdx.x == 0) s_item = atomicAdd(queue, 1);
+    __syncthreads();
+    const int it = s_item;
+    __syncthreads();
+    if (it >= n_items) break;
+    if (it < n_sc) {  // scatter piece k of chunk c (the j-th peer after me) into rank c's slot [me]
+      const int k = it / (n - 1), c = (me + 1 + it % (n - 1)) % n;
+      const int64_t lo = (int64_t)k * AR_PIECE4, hi = min(c4, lo + AR_PIECE4);
+      const int64_t lim = min(hi, max((int64_t)0, real4 - (int64_t)c * c4));
+      const float4* src = grad + (int64_t)c * c4;
+      float4* dst = reinterpret_cast<float4*>(static_cast<char*>(peers.base[c]) + A.slots_off) +
+                    (int64_t)me * c4;
+      for (int64_t j0 = lo + threadIdx.x; j0 < hi; j0 += 4 * 256) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t j = j0 + u * 256;
+          v[u] = j < lim ? ldg_stream(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t j = j0 + u * 256;
+          if (j < hi) dst[j] = v[u];
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence_system();
+        int* ctr = reinterpret_cast<int*>(static_cast<char*>(peers.base[c]) +
+                                          (reinterpret_cast<char*>(arrive) - static_cast<char*>(my_win))) + k;
+        asm volatile("red.release.sys.global.add.s32 [%0], 1;" ::"l"(ctr) : "memory");
+      }
+    } else {  // reduce piece k of my chunk
+      const int k = it - n_sc;
+      if (threadIdx.x == 0 && n > 1) {
+        const long long t0 = clock64();
+        while (ld_acquire_sys(&arrive[k]) < e * (n - 1)) {
+          if (clock64() - t0 > timeout_cycles) {
+            atomicOr(sig.err, 4);
+            break;
+          }
+          __nanosleep(32);
+        }
+      }
+      __syncthreads();
+      const int64_t lo = (int64_t)k * AR_PIECE4, hi = min(c4, lo + AR_PIECE4);
+      const int64_t own_lim = min(c4, max((int64_t)0, real4 - (int64_t)me * c4));
+      const float4* mine = grad + (int64_t)me * c4;
+      for (int64_t j0 = lo + threadIdx.x; j0 < hi; j0 += 2 * 256) {
+        float4 acc[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int64_t j = j0 + u * 256;
+          acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (j < hi)
+            for (int s = 0; s < n; ++s) {
+              const float4 x = s == me ? (j < own_lim ? ldg_stream(mine + j)
+                                                      : make_float4(0.f, 0.f, 0.f, 0.f))
+                                       : ldg_stream(slots + (int64_t)s * c4 + j);
+              acc[u] = f4_add(acc[u], x);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int64_t j = j0 + u * 256;
+          if (j >= hi) continue;
+          float4 v = acc[u];
+          v.x = __fmul_rn(v.x, scale);
+          v.y = __fmul_rn(v.y, scale);
+          v.z = __fmul_rn(v.z, scale);
+          v.w = __fmul_rn(v.w, scale);
+          const int64_t o4 = (int64_t)me * c4 + j;
+          for (int r = 0; r < n; ++r) {
+            const int d = (me + 1 + r) % n;  // peers first, own output last
+            put4<OutT>(static_cast<char*>(peers.base[d]) + A.out_off, o4, v);
+          }
+        }
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    s_last = atomicAdd(&sig.done[3], 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence_system();
+    for (int r = threadIdx.x; r < n; r += blockDim.x)
+      st_release_sys(&SigView(peers.base[r]).applied_flag[me], e);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      *sig.epoch = e;
+      *queue = 0;
+      sig.done[3] = 0;
+    }
+  }
+  HP_SPAN_END(SP_AR_SCATTER);
+}
+
 }  // namespace
 }  // namespace hp
 
@@ -969,7 +1099,8 @@ struct hp_dar_s {
   ArLayout A;
   void* win;
   PeerTable peers;
-  int mode;                  // HP_DAR_SM | HP_DAR_CE
+  int64_t arrive_off, queue_off;  // HP_DAR_PIPE: piece arrival counters, work queue
+  int mode;                  // HP_DAR_SM | HP_DAR_CE | HP_DAR_PIPE
   cudaStream_t side[4];      // CE mode: copies to different peers run concurrently
   cudaEvent_t fork, join[4];
 };
@@ -997,7 +1128,9 @@ int hp_dar_create(hp_dar_t* out, int32_t n, int32_t me, int64_t S_real, int32_t 
   d->A.out_bytes = out_dtype == HP_DTYPE_F32 ? 4 : 2;
   d->A.slots_off = al(SIG_INTS * 4);
   d->A.out_off = d->A.slots_off + al(S * 4);
-  const int64_t bytes = d->A.out_off + al(S * d->A.out_bytes);
+  d->arrive_off = d->A.out_off + al(S * d->A.out_bytes);
+  d->queue_off = d->arrive_off + al(((S / n / 4 + AR_PIECE4 - 1) / AR_PIECE4) * 4);
+  const int64_t bytes = d->queue_off + 256;
   cudaError_t e = cudaMalloc(&d->win, bytes);
   if (e != cudaSuccess) {
     delete d;
@@ -1048,7 +1181,8 @@ int hp_dar_destroy(hp_dar_t d) {
 // out (the window's output, every rank) = cast(scale * sum_r grad_r), summed in
 // rank order. grad is this rank's fp32 gradient [S] (any device buffer).
 int hp_dar_set_mode(hp_dar_t d, int32_t mode) {
-  HP_REQUIRE(d && (mode == HP_DAR_SM || mode == HP_DAR_CE), "mode must be HP_DAR_SM or HP_DAR_CE");
+  HP_REQUIRE(d && (mode == HP_DAR_SM || mode == HP_DAR_CE || mode == HP_DAR_PIPE),
+             "mode must be HP_DAR_SM, HP_DAR_CE or HP_DAR_PIPE");
   d->mode = mode;
   return HP_OK;
 }
@@ -1104,6 +1238,22 @@ int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream) {
     launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 1);
     launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 1, d->A.n, wait_budget(), SP_AR_WAIT1);
     HP_LAUNCHED(5, "dense p2p allreduce (copy engines)");
+    return HP_OK;
+  }
+  if (d->mode == HP_DAR_PIPE) {
+    const int64_t c4 = d->A.chunk / 4;
+    const int K = (int)((c4 + AR_PIECE4 - 1) / AR_PIECE4);
+    const int blocks = std::max(1, std::min(d->A.n * K, g_dar_blocks > 0 ? g_dar_blocks : sms));
+    int* arrive = reinterpret_cast<int*>(static_cast<char*>(d->win) + d->arrive_off);
+    int* queue = reinterpret_cast<int*>(static_cast<char*>(d->win) + d->queue_off);
+    if (d->A.out_bytes == 4)
+      launch_k(k_ar_pipe<float>, dim3(blocks), dim3(256), 0, st, d->peers, d->win, d->A,
+               reinterpret_cast<const float4*>(grad), scale, arrive, queue, wait_budget());
+    else
+      launch_k(k_ar_pipe<__nv_bfloat16>, dim3(blocks), dim3(256), 0, st, d->peers, d->win, d->A,
+               reinterpret_cast<const float4*>(grad), scale, arrive, queue, wait_budget());
+    launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 1, d->A.n, wait_budget(), SP_AR_WAIT1);
+    HP_LAUNCHED(2, "dense p2p allreduce (pipelined)");
     return HP_OK;
   }
   // ~half the SMs: NVLink saturates well below full occupancy, and the sparse

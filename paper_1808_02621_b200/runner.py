@@ -141,9 +141,9 @@ class HybridRunner:
         # peer exchange; more -> NCCL (which uses NVLS on an NVSwitch box)
         default_dense = ("p2p" if world_size == 2 else "nccl") if exchange == "p2p" else exchange
         self.dense_exchange = (dense_exchange or default_dense) if world_size > 1 else "local"
-        if self.dense_exchange not in ("p2p", "p2p-sm", "nvls", "nccl", "local"):
-            raise ValueError("dense_exchange must be 'p2p' (copy engines), 'p2p-sm', 'nvls' "
-                             "or 'nccl'")
+        if self.dense_exchange not in ("p2p", "p2p-sm", "p2p-pipe", "nvls", "nccl", "local"):
+            raise ValueError("dense_exchange must be 'p2p' (copy engines), 'p2p-sm', "
+                             "'p2p-pipe', 'nvls' or 'nccl'")
         self.dar: dict = {}
         self.xchg: dict = {}
         self.ar_tables: set = set()   # sparse Weights under AR at n > 1 (AllGatherv baseline)
@@ -170,12 +170,12 @@ class HybridRunner:
 
                     self.dar[var.name] = NvlsExchange(world_size, rank, var.elements,
                                                       dense_dtype, self.device)
-                elif self.dense_exchange in ("p2p", "p2p-sm"):
+                elif self.dense_exchange in ("p2p", "p2p-sm", "p2p-pipe"):
                     from .xchg import DenseExchange
 
                     self.dar[var.name] = DenseExchange(
                         world_size, rank, var.elements, dense_dtype, self.device,
-                        mode="sm" if self.dense_exchange == "p2p-sm" else "ce")
+                        mode={"p2p": "ce", "p2p-sm": "sm", "p2p-pipe": "pipe"}[self.dense_exchange])
                 continue
             if mech is Mechanism.PS:
                 P = plan.partitions_of[var.name]

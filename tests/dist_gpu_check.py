@@ -41,7 +41,7 @@ def main():
         getattr(_lib.load(), f"hp_debug_set_{k}")(int(v))
     wl = Workload("check", [TableShape("embedding", 60_000, 128, 2560),
                             TableShape("softmax", 60_000, 256, 2560, sampled=3000)],
-                  {"lstm": 50_000}, {"kind": opt_kind, "lr": 0.1, "init_acc": 0.1}, 2560,
+                  {"lstm": int(os.environ.get("HP_CHECK_DENSE_ELEMS", "50000"))}, {"kind": opt_kind, "lr": 0.1, "init_acc": 0.1}, 2560,
                   partitions=8)
     graph = hp.load_graph_spec(json.dumps(wl.graph_json()))
     cluster = hp.ClusterSpec.b200_box(world)
@@ -99,7 +99,7 @@ def main():
         if not np.allclose(got, ref, rtol=1e-5, atol=1e-6):
             ok = False
             why.append(f"step {step} dense differs (max {np.abs(got - ref).max():.3g})")
-        if runner.dense_exchange in ("p2p", "p2p-sm") and not runner.dense_ps:  # rank order
+        if runner.dense_exchange in ("p2p", "p2p-sm", "p2p-pipe") and not runner.dense_ps:  # rank order
             seq = np.zeros_like(batches[0]["lstm"])
             for b in batches:
                 seq = seq + b["lstm"]

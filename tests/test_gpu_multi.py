@@ -22,6 +22,7 @@ def _ngpu():
     ("adagrad", "p2p", "p2p", "", "hybrid"),
     ("adam", "p2p", "nccl", "", "hybrid"),
     ("adagrad", "p2p", "nvls", "", "hybrid"),
+    ("adagrad", "p2p", "p2p-pipe", "", "hybrid"),
     # the alternative kernels behind the instrumentation knobs stay parity-checked
     ("adagrad", "p2p", "p2p-sm", "owner_stream=0,rowstream=1,pdl=1", "hybrid"),
     ("sgd", "nccl", "nccl", "", "hybrid"),
@@ -33,7 +34,9 @@ def test_multi_gpu_step_matches_oracle(opt, xchg, dense, knobs, arch):
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     env = dict(os.environ, HP_CHECK_OPT=opt, HP_CHECK_XCHG=xchg, HP_CHECK_DENSE=dense,
-               HP_CHECK_KNOBS=knobs, HP_CHECK_ARCH=arch)
+               HP_CHECK_KNOBS=knobs, HP_CHECK_ARCH=arch,
+               # the pipelined dense exchange cuts each chunk into 64 KB pieces: many of them
+               HP_CHECK_DENSE_ELEMS="1000004" if dense == "p2p-pipe" else "50000")
     import socket
 
     with socket.socket() as sk:

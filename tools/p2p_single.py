@@ -41,5 +41,20 @@ for s in range(steps):
     x.merge_apply(tab.slab(), tab.optimizer.c_struct(s + 1, 1.0))
     x.stitch(out_b["inv"][:cap], out)
 torch.cuda.synchronize()
+if len(sys.argv) > 2 and sys.argv[2] == "time":  # per-phase CUDA-event times, GPU backlogged
+    names = ["plan", "push", "apply", "stitch"]
+    acc = {k: [] for k in names}
+    for s in range(20):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        torch.cuda._sleep(20_000_000)
+        ev[0].record()
+        x.plan(ids, t.V, P, tab.owner_dev, out_b, tab.ws); ev[1].record()
+        x.push_plan(vals, t.V, P, out_b, gb, tab.ws); ev[2].record()
+        x.merge_apply(tab.slab(), tab.optimizer.c_struct(s + 10, 1.0)); ev[3].record()
+        x.stitch(out_b["inv"][:cap], out); ev[4].record()
+        torch.cuda.synchronize()
+        for i, k in enumerate(names):
+            acc[k].append(ev[i].elapsed_time(ev[i + 1]) * 1e3)
+    print({k: round(float(np.median(v)), 1) for k, v in acc.items()})
 print("status", x.status(), "U", out_b["n_uniq"].item())
 x.close()
