@@ -96,10 +96,12 @@ void hp_debug_set_pdl(int on);
 /* Instrumentation: cap on row-stream CTAs per SM (shared memory left for
  * concurrently running kernels); default 4. */
 void hp_debug_set_rs_ctas(int n);
-/* Instrumentation: 1 = p2p owner merge/apply as a cp.async row stream
- * (k_owner_stream, default for D in {128, 256, 512, 1024}); 0 = k_owner_apply. */
+/* Instrumentation: p2p owner merge/apply kernel. 2 (default) = k_owner_scan
+ * (ownership + contributor lists, one thread per entry) + k_owner_rows (one
+ * group per merged row); 1 = k_owner_stream (cp.async row stream, D in {128,
+ * 256, 512, 1024}); 0 = k_owner_apply (one group per entry). */
 void hp_debug_set_owner_stream(int on);
-/* Instrumentation: k_combine grid when its epilogue stores to peers (default 32). */
+/* Instrumentation: k_combine grid cap when its epilogue stores to peers (0 = SM count, default). */
 void hp_debug_set_combine_blocks(int n);
 /* Grid of the pipelined dense allreduce (HP_DAR_PIPE); 0 = one block per SM. */
 void hp_debug_set_dar_blocks(int n);
@@ -255,8 +257,8 @@ int hp_xchg_push(hp_xchg_t x, const int64_t* ids, const float* vals, int64_t T, 
  * hp_xchg_plan dedups/routes ids into a send plan in ws; hp_xchg_push_plan
  * reduces vals with that plan and pushes (same T / V / P / ws). */
 int hp_xchg_plan(hp_xchg_t x, const int64_t* ids, int64_t T, int64_t V, int32_t P,
-                 const int32_t* owner, int64_t* send_ids, int32_t* inv, int32_t* dest_counts,
-                 int32_t* n_uniq, void* ws, size_t ws_bytes, void* stream);
+                 const int32_t* owner, const int64_t* glob_base, int64_t* send_ids, int32_t* inv,
+                 int32_t* dest_counts, int32_t* n_uniq, void* ws, size_t ws_bytes, void* stream);
 int hp_xchg_push_plan(hp_xchg_t x, const float* vals, int64_t T, int64_t V, int32_t P,
                       const int64_t* send_ids, const int32_t* dest_counts,
                       const int64_t* glob_base, void* ws, size_t ws_bytes, void* stream);

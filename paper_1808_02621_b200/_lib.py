@@ -48,6 +48,7 @@ SIGNATURES = {
     "hp_debug_set_owner_stream": (None, [C.c_int]),
     "hp_debug_set_combine_blocks": (None, [C.c_int]),
     "hp_debug_set_reduce_b": (None, [C.c_int]),
+    "hp_debug_set_dar_blocks": (None, [C.c_int]),
     "hp_debug_set_spans": (None, [vp]),
     "hp_apply_plan": (C.c_int, [vp, i64, Slab, Optim, vp, sz, vp]),
     "hp_apply_plan_build": (C.c_int, [vp, i64, Slab, vp, sz, vp]),
@@ -81,7 +82,7 @@ SIGNATURES = {
     "hp_xchg_push": (C.c_int, [vp, vp, vp, i64, i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
     "hp_xchg_merge_apply": (C.c_int, [vp, Slab, Optim, i32, vp]),
     "hp_xchg_wait": (C.c_int, [vp, i32, vp]),
-    "hp_xchg_plan": (C.c_int, [vp, vp, i64, i64, i32, vp, vp, vp, vp, vp, vp, sz, vp]),
+    "hp_xchg_plan": (C.c_int, [vp, vp, i64, i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
     "hp_xchg_push_plan": (C.c_int, [vp, vp, i64, i64, i32, vp, vp, vp, vp, sz, vp]),
     "hp_xchg_stitch": (C.c_int, [vp, vp, i64, vp, i32, vp]),
     "hp_xchg_status": (C.c_int, [vp, vp, vp]),

@@ -78,8 +78,8 @@ void hp_debug_set_cluster_threads(int nt) { hp::set_cluster_threads(nt); }
 void hp_debug_set_rowstream(int on) { hp::g_rowstream_off = on ? 0 : 1; }
 void hp_debug_set_pdl(int on) { hp::g_pdl = on ? 1 : 0; }
 void hp_debug_set_rs_ctas(int n) { hp::g_rs_ctas = n < 1 ? 1 : n; }
-void hp_debug_set_owner_stream(int on) { hp::g_owner_stream = on ? 1 : 0; }
-void hp_debug_set_combine_blocks(int n) { hp::g_combine_blocks = n < 1 ? 1 : n; }
+void hp_debug_set_owner_stream(int on) { hp::g_owner_stream = on < 0 ? 0 : (on > 2 ? 2 : on); }
+void hp_debug_set_combine_blocks(int n) { hp::g_combine_blocks = n < 0 ? 0 : n; }
 void hp_debug_set_dar_blocks(int n) { hp::g_dar_blocks = n < 0 ? 0 : n; }
 void hp_debug_set_reduce_b(int b) { hp::g_reduce_b = b; }
 

@@ -705,6 +705,7 @@ size_t dedup_ws_bytes(int64_t T, int32_t D, int32_t P) {
   s += align256(4 * nscan);
   s += align256(4 * (size_t)D * prow);
   s += 2 * align256(4 * (HP_RS_MAX_WARPS + 1));
+  s += align256(16 * Tc);             // send_info
   return s;
 }
 
@@ -777,6 +778,7 @@ int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, i
   pl->partials = (float*)take(4 * (size_t)D * pl->partial_rows);
   pl->wb_item = (int32_t*)take(4 * (HP_RS_MAX_WARPS + 1));
   pl->wb_row = (int32_t*)take(4 * (HP_RS_MAX_WARPS + 1));
+  pl->send_info = (int4*)take(16 * Tc);
   pl->nw = g_rowstream_off ? 0 : rs_warps(D);
   pl->sorted_pos = pl->pos[0];
   pl->prof = g_prof;
@@ -805,8 +807,8 @@ int g_cl_threads = HP_CL_THREADS;  // CTA shape of the cluster path (hp_debug_se
 void set_cluster_threads(int nt) { g_cl_threads = nt; }
 int g_rowstream_off = 1;  // row stream measured slower on the LM step
 int g_rs_ctas = 4;
-int g_owner_stream = 1;
-int g_combine_blocks = 32;
+int g_owner_stream = 2;  // 0: k_owner_apply, 1: k_owner_stream, 2: k_owner_scan + k_owner_rows
+int g_combine_blocks = 0;  // 0: one CTA per long segment up to the SM count
 int g_dar_blocks = 0;  // HP_DAR_PIPE grid (0 = one block per SM)
 int g_reduce_b = 2;
 HP_SPAN_SETTER(set_spans_dedup)

@@ -45,6 +45,10 @@ struct DedupPlan {
   int32_t nw;
   int32_t* wb_item;     // [HP_RS_MAX_WARPS + 1]
   int32_t* wb_row;      // [HP_RS_MAX_WARPS + 1]
+  // p2p send plans: per send slot u {inbox index at its owner, owner rank,
+  // slab row at the owner, 0}, filled on the plan stream (k_send_info) so the
+  // push epilogue's destination is one independent 16-byte load
+  int4* send_info;      // [T]
 };
 
 constexpr int HP_RS_MAX_WARPS = 4096;

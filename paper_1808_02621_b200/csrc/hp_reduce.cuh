@@ -485,8 +485,9 @@ int launch_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaSt
     else launch_k_reduce<128, 4>(pl, vals, epi, st);
     HP_LAUNCHED(1, "k_reduce");
   }
-  // long segments are few (<= T/33); a small grid keeps the publication cheap
-  const int cblocks = grid_for(pl.T / (HP_CHUNK + 1) + 1, 1, Epi::kRemote ? g_combine_blocks : sm_count());
+  // one CTA per long segment (<= T/17); hp_debug_set_combine_blocks caps it for peer epilogues
+  const int cblocks = grid_for(pl.T / (HP_CHUNK + 1) + 1, 1,
+                               Epi::kRemote && g_combine_blocks > 0 ? g_combine_blocks : sm_count());
   launch_k(k_combine<Epi>, dim3(cblocks), dim3(256), 0, st, pl, epi);
   HP_LAUNCHED(1, "k_combine");
   return HP_OK;

@@ -50,6 +50,7 @@ struct SigView {
   int* err;           // [1]
   int* done;          // [4] last-block counters
   int* push_off;      // [n] source s's send offset of its block for this owner
+  int* own_items;     // [1] owner merge items written by k_owner_scan this step
   __host__ __device__ explicit SigView(void* base) {
     int* b = static_cast<int*>(base);
     push_flag = b;
@@ -59,6 +60,7 @@ struct SigView {
     err = b + 193;
     done = b + 196;
     push_off = b + 256;
+    own_items = b + 194;
   }
 };
 
@@ -76,11 +78,14 @@ struct PeerTable {
 };
 
 struct WinLayout {
-  int64_t w_off, ids_off, rows_off, ret_off, slot_off, cap;
+  int64_t w_off, ids_off, rows_off, ret_off, slot_off, items_off, cidx_off, cap;
   int n, me, D4;
 };
 
 // ---- push epilogue: the summed row of send slot `dst` goes to its owner's inbox.
+// The destination of every send slot {inbox index, owner, slab row} was
+// resolved on the plan stream (k_send_info), so load() issues independent
+// loads only and the item's row loads are not held behind an index chain.
 struct EpiPush {
   static constexpr bool kRemote = true;
   static constexpr int kPre = 0;
@@ -89,30 +94,32 @@ struct EpiPush {
   WinLayout L;
   const int32_t* dest_counts;  // [n] rows this rank sends to each owner
   const int64_t* send_ids;     // [U] (send order)
-  const int64_t* glob_base;    // [P] slab row of partition p on its owner
-  Router route;
+  const int4* info;            // [U] {inbox index, owner, slab row, 0}
   int* done;                   // last-block counter (own window)
   void* my_win;
   struct Pre {
-    float4* dst;
+    int4 inf;
+    int64_t id;
+    int epoch;
   };
   __device__ __forceinline__ Pre load(int slot, int c4) const {
-    int o = 0, off = 0;
-    while (o + 1 < L.n && slot >= off + dest_counts[o]) off += dest_counts[o++];
-    const int64_t idx = (int64_t)L.me * L.cap + (slot - off);
-    char* win = static_cast<char*>(peers.base[o]);
+    Pre p;
+    p.inf = info[slot];
     if (c4 == 0) {
-      const int64_t id = send_ids[slot];
-      reinterpret_cast<int64_t*>(win + L.ids_off)[idx] = id;
-      const int p = route.part(id);
-      const int64_t row = glob_base[p] + (id - route.lo(p));
-      const unsigned long long e = (unsigned long long)(*SigView(my_win).epoch + 1);
-      reinterpret_cast<unsigned long long*>(win + L.slot_off)[row * L.n + L.me] =
-          (e << 32) | (unsigned long long)(uint32_t)idx;
+      p.id = send_ids[slot];
+      p.epoch = *SigView(my_win).epoch + 1;
     }
-    return {reinterpret_cast<float4*>(win + L.rows_off) + idx * L.D4};
+    return p;
   }
-  __device__ __forceinline__ void store(int, int c4, float4 g, Pre p) const { p.dst[c4] = g; }
+  __device__ __forceinline__ void store(int, int c4, float4 g, const Pre& p) const {
+    char* win = static_cast<char*>(peers.base[p.inf.y]);
+    reinterpret_cast<float4*>(win + L.rows_off)[(int64_t)p.inf.x * L.D4 + c4] = g;
+    if (c4 == 0) {
+      reinterpret_cast<int64_t*>(win + L.ids_off)[p.inf.x] = p.id;
+      reinterpret_cast<unsigned long long*>(win + L.slot_off)[(int64_t)p.inf.z * L.n + L.me] =
+          ((unsigned long long)(unsigned)p.epoch << 32) | (unsigned long long)(uint32_t)p.inf.x;
+    }
+  }
   // Runs once, in the last k_combine block, after every block fenced its
   // peer stores: publish {count, offset} then the epoch flag at every owner.
   __device__ void grid_done() const {
@@ -134,6 +141,24 @@ struct EpiPush {
     }
   }
 };
+
+// ---- plan stream: destination of every send slot u < U (owners in ascending
+// rank order, each owner's block of slots contiguous): inbox index
+// me * cap + (u - first slot of the owner), owner rank, slab row at the owner.
+__global__ void k_send_info(const int64_t* __restrict__ send_ids, const int32_t* __restrict__ dest_counts,
+                            const int32_t* __restrict__ n_uniq, const int64_t* __restrict__ glob_base,
+                            Router route, WinLayout L, int4* __restrict__ info, int64_t T) {
+  const int U = *n_uniq;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < U && u < T;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    int o = 0, off = 0;
+    while (o + 1 < L.n && u >= off + dest_counts[o]) off += dest_counts[o++];
+    const int64_t id = send_ids[u];
+    const int p = route.part(id);
+    const int64_t row = glob_base[p] + (id - route.lo(p));
+    info[u] = make_int4((int)((int64_t)L.me * L.cap + (u - off)), o, (int)row, 0);
+  }
+}
 
 // ---- wait until flags[s] >= epoch for every s (one block; bounded spin).
 __global__ void k_wait(void* my_win, int which, int n, long long timeout_cycles, int span) {
@@ -514,6 +539,179 @@ k_owner_stream(PeerTable peers, void* my_win, WinLayout L, const int64_t* __rest
   HP_SPAN_END(SP_APPLY);
 }
 
+// ---- owner, two passes (default). k_owner_scan: one thread per received
+// entry (all sources, source-major) resolves id -> slab row and reads the
+// row's n slot-table tags; the entry of the lowest-ranked source with a valid
+// tag owns the row and writes a merge item {row, cnt} + its contributor list
+// (inbox indices in source order) with a warp-aggregated atomic. The whole
+// index chain is thus paid once, in parallel, instead of once per entry
+// inside the apply loop.
+__global__ void __launch_bounds__(256)
+k_owner_scan(void* my_win, WinLayout L, const int64_t* __restrict__ part_base, Router route,
+             int64_t rows_cap) {
+  __shared__ int s_pre[OS_NMAX + 1];
+  HP_ENTRY(SP_SCATTER);
+  SigView sig(my_win);
+  char* win = static_cast<char*>(my_win);
+  const int64_t* inbox_ids = reinterpret_cast<const int64_t*>(win + L.ids_off);
+  const unsigned long long* slot = reinterpret_cast<const unsigned long long*>(win + L.slot_off);
+  int2* items = reinterpret_cast<int2*>(win + L.items_off);
+  int* cidx = reinterpret_cast<int*>(win + L.cidx_off);
+  const int n = L.n;
+  if (threadIdx.x == 0) {
+    int a = 0;
+    for (int q = 0; q < n; ++q) {
+      s_pre[q] = a;
+      a += sig.push_count[q];
+    }
+    s_pre[n] = a;
+  }
+  __syncthreads();
+  const int E = s_pre[n];
+  const unsigned epoch = (unsigned)*sig.epoch;
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t f0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); f0 < E; f0 += wstride) {
+    const int f = (int)f0 + lane;
+    bool owned = false;
+    int row = 0, cnt = 0, sidx = 0;
+    unsigned have = 0;
+    unsigned long long ent[OS_NMAX];
+    if (f < E) {
+      while (sidx + 1 < n && f >= s_pre[sidx + 1]) ++sidx;
+      const int64_t id = inbox_ids[(int64_t)sidx * L.cap + (f - s_pre[sidx])];
+      const int p = route.part(id);
+      const int64_t b = part_base[p];
+      const int64_t r = b + (id - route.lo(p));
+      if (b < 0 || r >= rows_cap) {
+        atomicOr(sig.err, 16);
+      } else {
+        row = (int)r;
+#pragma unroll
+        for (int j = 0; j < OS_NMAX; ++j)
+          if (j < n) ent[j] = slot[r * n + j];
+#pragma unroll
+        for (int j = 0; j < OS_NMAX; ++j)
+          if (j < n && (unsigned)(ent[j] >> 32) == epoch) have |= 1u << j;
+        cnt = __popc(have);
+        owned = have != 0 && __ffs(have) - 1 == sidx;
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, owned);
+    int base = 0;
+    if (lane == 0 && m) base = atomicAdd(sig.own_items, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (owned) {
+      const int pos = base + __popc(m & lanemask_lt());
+      items[pos] = make_int2(row, cnt);
+      int k = 0;
+#pragma unroll
+      for (int j = 0; j < OS_NMAX; ++j)
+        if (j < n && ((have >> j) & 1u)) cidx[(int64_t)pos * n + k++] = (int)(uint32_t)ent[j];
+    }
+  }
+  HP_SPAN_END(SP_SCATTER);
+}
+
+// k_owner_rows: one group of TPI threads (VPT float4 columns each) per merge
+// item: the item and its contributor list are one round trip, then the row's
+// state and all contributions are loaded together; sums in source order,
+// scales, applies, stores the state and returns the updated row into each
+// contributor's return buffer (NVLink). The last block raises "applied".
+template <int OPT, int TPI, int VPT>
+__global__ void __launch_bounds__(256, 3)
+k_owner_rows(PeerTable peers, void* my_win, WinLayout L, float4* s0, float4* s1, hp_optim o) {
+  __shared__ int s_poff[OS_NMAX];
+  __shared__ bool s_last;
+  HP_ENTRY(SP_APPLY);
+  SigView sig(my_win);
+  char* win = static_cast<char*>(my_win);
+  float4* w = reinterpret_cast<float4*>(win + L.w_off);
+  const float4* inbox = reinterpret_cast<const float4*>(win + L.rows_off);
+  const int2* items = reinterpret_cast<const int2*>(win + L.items_off);
+  const int* cidx_all = reinterpret_cast<const int*>(win + L.cidx_off);
+  const int n = L.n, D4 = L.D4;
+  if (threadIdx.x < n) s_poff[threadIdx.x] = sig.push_off[threadIdx.x];
+  __syncthreads();
+  const int NI = *sig.own_items;
+  const unsigned epoch = (unsigned)*sig.epoch;
+  const int lane = threadIdx.x & 31, q = threadIdx.x % TPI;
+  constexpr int GPB = 256 / TPI;
+  for (int it = blockIdx.x * GPB + threadIdx.x / TPI; it < NI; it += gridDim.x * GPB) {
+    const int2 item = items[it];
+    const int myc = lane < n ? cidx_all[(int64_t)it * n + lane] : 0;
+    const int64_t row = item.x;
+    const int cnt = item.y;
+    float4 wv[VPT], av[VPT], bv[VPT], g[VPT];
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) {
+      const int c = q + v * TPI;
+      const int64_t off = row * D4 + c;
+      wv[v] = av[v] = bv[v] = g[v] = z;
+      if (c < D4) {
+        wv[v] = w[off];
+        if (OPT != HP_OPT_SGD) av[v] = s0[off];
+        if (OPT == HP_OPT_ADAM) bv[v] = s1[off];
+      }
+    }
+    for (int j0 = 0; j0 < cnt; j0 += 2) {  // contributions, in source order
+      float4 x[2][VPT];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int idx = __shfl_sync(0xffffffffu, myc, (j0 + u) & 31);
+#pragma unroll
+        for (int v = 0; v < VPT; ++v)
+          if (j0 + u < cnt && q + v * TPI < D4) x[u][v] = inbox[(int64_t)idx * D4 + q + v * TPI];
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < VPT; ++v)
+          if (j0 + u < cnt) g[v] = f4_add(g[v], x[u][v]);
+    }
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) {
+      const int c = q + v * TPI;
+      if (c >= D4) continue;
+      opt_update<OPT>(wv[v].x, av[v].x, bv[v].x, g[v].x, o);
+      opt_update<OPT>(wv[v].y, av[v].y, bv[v].y, g[v].y, o);
+      opt_update<OPT>(wv[v].z, av[v].z, bv[v].z, g[v].z, o);
+      opt_update<OPT>(wv[v].w, av[v].w, bv[v].w, g[v].w, o);
+      const int64_t off = row * D4 + c;
+      w[off] = wv[v];
+      if (OPT != HP_OPT_SGD) s0[off] = av[v];
+      if (OPT == HP_OPT_ADAM) s1[off] = bv[v];
+    }
+    for (int j = 0; j < cnt; ++j) {  // pull, fused: back to every contributor's send slot
+      const int idx = __shfl_sync(0xffffffffu, myc, j);
+      const int src = idx / (int)L.cap;
+      const int64_t ret_row = s_poff[src] + (idx - (int64_t)src * L.cap);
+      float4* ret = reinterpret_cast<float4*>(static_cast<char*>(peers.base[src]) + L.ret_off) +
+                    ret_row * D4;
+#pragma unroll
+      for (int v = 0; v < VPT; ++v)
+        if (q + v * TPI < D4) ret[q + v * TPI] = wv[v];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    s_last = atomicAdd(&sig.done[1], 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence_system();
+    for (int r = threadIdx.x; r < n; r += blockDim.x)
+      st_release_sys(&SigView(peers.base[r]).applied_flag[L.me], (int)epoch);
+    if (threadIdx.x == 0) {
+      sig.done[1] = 0;
+      *sig.own_items = 0;
+    }
+  }
+  HP_SPAN_END(SP_APPLY);
+}
+
 // Spin-wait budget (cycles) before a wait gives up and raises an error bit.
 long long wait_budget() {
   static long long v = [] {
@@ -544,7 +742,8 @@ extern "C" {
 size_t hp_xchg_window_bytes(int32_t n, int32_t D, int64_t cap, int64_t rows_cap) {
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   return al(SIG_INTS * 4) + al((size_t)rows_cap * D * 4) + al((size_t)n * cap * 8) +
-         al((size_t)n * cap * D * 4) + al((size_t)cap * D * 4) + al((size_t)rows_cap * n * 8);
+         al((size_t)n * cap * D * 4) + al((size_t)cap * D * 4) + al((size_t)rows_cap * n * 8) +
+         al((size_t)n * cap * 8) + al((size_t)n * cap * n * 4);
 }
 
 int hp_xchg_create(hp_xchg_t* out, int32_t n, int32_t me, int32_t D, int64_t cap, int64_t rows_cap,
@@ -567,7 +766,9 @@ int hp_xchg_create(hp_xchg_t* out, int32_t n, int32_t me, int32_t D, int64_t cap
   L.rows_off = L.ids_off + al((int64_t)n * cap * 8);
   L.ret_off = L.rows_off + al((int64_t)n * cap * D * 4);
   L.slot_off = L.ret_off + al(cap * D * 4);
-  x->bytes = L.slot_off + al(rows_cap * n * 8);
+  L.items_off = L.slot_off + al(rows_cap * n * 8);
+  L.cidx_off = L.items_off + al((int64_t)n * cap * 8);
+  x->bytes = L.cidx_off + al((int64_t)n * cap * n * 4);
   cudaError_t e = cudaMalloc(&x->win, x->bytes);
   if (e != cudaSuccess) {
     delete x;
@@ -609,16 +810,21 @@ int hp_xchg_destroy(hp_xchg_t x) {
 // Worker K1+K2 (index half of hp_xchg_push): dedup + route ids[T] into a send
 // plan left in ws; outputs send_ids[U], inv[T], dest_counts[n], n_uniq.
 int hp_xchg_plan(hp_xchg_t x, const int64_t* ids, int64_t T, int64_t V, int32_t P,
-                 const int32_t* owner, int64_t* send_ids, int32_t* inv, int32_t* dest_counts,
-                 int32_t* n_uniq, void* ws, size_t ws_bytes, void* stream) {
-  HP_REQUIRE(x && owner && send_ids && inv && dest_counts && n_uniq, "NULL argument");
+                 const int32_t* owner, const int64_t* glob_base, int64_t* send_ids, int32_t* inv,
+                 int32_t* dest_counts, int32_t* n_uniq, void* ws, size_t ws_bytes, void* stream) {
+  HP_REQUIRE(x && owner && glob_base && send_ids && inv && dest_counts && n_uniq, "NULL argument");
   HP_REQUIRE(T <= x->L.cap, "more ids than the inbox capacity");
   HP_REQUIRE(T == 0 || ids, "NULL ids");
   DedupPlan pl;
   int rc = carve_plan(&pl, ws, ws_bytes, T, x->L.D4 * 4, V, P, x->L.n);
   if (rc) return rc;
-  return build_plan(pl, ids, owner, nullptr, send_ids, nullptr, inv, dest_counts, n_uniq,
-                    static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  rc = build_plan(pl, ids, owner, nullptr, send_ids, nullptr, inv, dest_counts, n_uniq, st);
+  if (rc || T == 0) return rc;
+  k_send_info<<<grid_for(T, 256, sm_count() * 4), 256, 0, st>>>(
+      send_ids, dest_counts, n_uniq, glob_base, Router(V, P), x->L, pl.send_info, T);
+  HP_LAUNCHED(1, "k_send_info");
+  return HP_OK;
 }
 
 // Worker K1 values + K3, fused: with the plan in ws (hp_xchg_plan, same T / V / P),
@@ -634,7 +840,7 @@ int hp_xchg_push_plan(hp_xchg_t x, const float* vals, int64_t T, int64_t V, int3
   if (rc) return rc;
   restore_sorted_pos(pl);
   SigView me(x->win);
-  EpiPush epi{x->peers, x->L, dest_counts, send_ids, glob_base, Router(V, P), me.done + 0, x->win};
+  EpiPush epi{x->peers, x->L, dest_counts, send_ids, pl.send_info, me.done + 0, x->win};
   pl.T = std::max<int64_t>(T, 1);  // k_combine must run: it carries the publication
   return launch_reduce(pl, vals, epi, static_cast<cudaStream_t>(stream));
 }
@@ -644,8 +850,8 @@ int hp_xchg_push(hp_xchg_t x, const int64_t* ids, const float* vals, int64_t T, 
                  int32_t P, const int32_t* owner, const int64_t* glob_base, int64_t* send_ids,
                  int32_t* inv, int32_t* dest_counts, int32_t* n_uniq, void* ws, size_t ws_bytes,
                  void* stream) {
-  int rc = hp_xchg_plan(x, ids, T, V, P, owner, send_ids, inv, dest_counts, n_uniq, ws, ws_bytes,
-                        stream);
+  int rc = hp_xchg_plan(x, ids, T, V, P, owner, glob_base, send_ids, inv, dest_counts, n_uniq, ws,
+                        ws_bytes, stream);
   if (rc) return rc;
   return hp_xchg_push_plan(x, vals, T, V, P, send_ids, dest_counts, glob_base, ws, ws_bytes,
                            stream);
@@ -689,10 +895,29 @@ void launch_owner_stream(const hp_xchg_s* x, const hp_slab& slab, const hp_optim
            reinterpret_cast<float4*>(slab.s1), opt, x->rows_cap);
 }
 
+template <int OPT, int TPI, int VPT>
+void launch_owner_rows(const hp_xchg_s* x, const hp_slab& slab, const hp_optim& opt,
+                       cudaStream_t st) {
+  const int64_t total = (int64_t)x->L.n * x->L.cap;
+  launch_k(k_owner_scan, dim3(grid_for(total, 256, sm_count() * 8)), dim3(256), 0, st, x->win, x->L,
+           slab.part_base, Router(slab.V, slab.P), x->rows_cap);
+  const int blocks = grid_for(total, 256 / TPI, sm_count() * 3);  // one resident wave
+  launch_k(k_owner_rows<OPT, TPI, VPT>, dim3(blocks), dim3(256), 0, st, x->peers, x->win, x->L,
+           reinterpret_cast<float4*>(slab.s0), reinterpret_cast<float4*>(slab.s1), opt);
+}
+
 template <int OPT>
 void dispatch_owner_apply(const hp_xchg_s* x, const hp_slab& slab, const hp_optim& opt, int D4,
                           cudaStream_t st) {
-  if (g_owner_stream) {
+  if (g_owner_stream == 2) {
+    if (D4 <= 32) launch_owner_rows<OPT, 32, 1>(x, slab, opt, st);
+    else if (D4 <= 64) launch_owner_rows<OPT, 32, 2>(x, slab, opt, st);
+    else if (D4 <= 128) launch_owner_rows<OPT, 64, 2>(x, slab, opt, st);
+    else if (D4 <= 256) launch_owner_rows<OPT, 64, 4>(x, slab, opt, st);
+    else launch_owner_rows<OPT, 128, 4>(x, slab, opt, st);
+    return;
+  }
+  if (g_owner_stream == 1) {
     switch (D4) {
       case 32: return launch_owner_stream<OPT, 1>(x, slab, opt, st);
       case 64: return launch_owner_stream<OPT, 2>(x, slab, opt, st);
@@ -725,7 +950,7 @@ int hp_xchg_merge_apply(hp_xchg_t x, hp_slab slab, hp_optim opt, int32_t wait, v
     case HP_OPT_ADAGRAD: dispatch_owner_apply<HP_OPT_ADAGRAD>(x, slab, opt, D4, st); break;
     default: dispatch_owner_apply<HP_OPT_ADAM>(x, slab, opt, D4, st);
   }
-  HP_LAUNCHED(1, "owner merge/apply");
+  HP_LAUNCHED(g_owner_stream == 2 ? 2 : 1, "owner merge/apply");
   return HP_OK;
 }
 

@@ -306,7 +306,7 @@ class HybridRunner:
         if self.world_size == 1:
             ops.apply_plan_build(ids, tab.slab(), tab.wss[slot])
         else:
-            self.xchg[tab.name].plan(ids, tab.V, tab.P, tab.owner_dev,
+            self.xchg[tab.name].plan(ids, tab.V, tab.P, tab.owner_dev, self.glob_base[tab.name],
                                      self._p2p_bufs(tab, slot), tab.wss[slot])
 
     def _p2p_bufs(self, tab: ShardedTable, slot: int) -> dict:

@@ -55,14 +55,15 @@ class PeerExchange:
              torch.cuda.current_stream().cuda_stream)
         return out
 
-    def plan(self, ids, V: int, P: int, owner, out: dict, ws) -> dict:
-        """Index half of push: dedup + route into a send plan in ``ws``."""
+    def plan(self, ids, V: int, P: int, owner, glob_base, out: dict, ws) -> dict:
+        """Index half of push: dedup + route into a send plan in ``ws`` (plus each
+        send slot's destination: owner inbox index and slab row, from ``glob_base``)."""
         from .ops import dedup_ws_bytes
 
         T = ids.numel()
         ws.get(dedup_ws_bytes(T, self.D, P, self.n))
         call("hp_xchg_plan", self.handle, ids.data_ptr(), T, V, P, owner.data_ptr(),
-             out["send_ids"].data_ptr(), out["inv"].data_ptr(), out["dest_counts"].data_ptr(),
+             glob_base.data_ptr(), out["send_ids"].data_ptr(), out["inv"].data_ptr(), out["dest_counts"].data_ptr(),
              out["n_uniq"].data_ptr(), ws.ptr, ws.nbytes, torch.cuda.current_stream().cuda_stream)
         return out
 

@@ -15,6 +15,10 @@ from paper_1808_02621_b200.xchg import PeerExchange
 os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
 os.environ.setdefault("MASTER_PORT", "29650")
 dist.init_process_group("gloo", rank=0, world_size=1)
+from paper_1808_02621_b200 import _lib
+for kv in filter(None, os.environ.get("HP_KNOBS", "").split(",")):  # A/B: NAME=INT
+    k, v = kv.split("=")
+    getattr(_lib.load(), f"hp_debug_set_{k}")(int(v))
 dev = torch.device("cuda:0")
 t = TableShape("softmax", 800_000, 512, 2560, sampled=8192)
 P = 8
@@ -36,7 +40,7 @@ out_b = {"send_ids": torch.empty(cap, dtype=torch.int64, device=dev),
 out = torch.empty(cap, t.D, device=dev)
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 for s in range(steps):
-    x.plan(ids, t.V, P, tab.owner_dev, out_b, tab.ws)
+    x.plan(ids, t.V, P, tab.owner_dev, gb, out_b, tab.ws)
     x.push_plan(vals, t.V, P, out_b, gb, tab.ws)
     x.merge_apply(tab.slab(), tab.optimizer.c_struct(s + 1, 1.0))
     x.stitch(out_b["inv"][:cap], out)
@@ -48,7 +52,7 @@ if len(sys.argv) > 2 and sys.argv[2] == "time":  # per-phase CUDA-event times, G
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         torch.cuda._sleep(20_000_000)
         ev[0].record()
-        x.plan(ids, t.V, P, tab.owner_dev, out_b, tab.ws); ev[1].record()
+        x.plan(ids, t.V, P, tab.owner_dev, gb, out_b, tab.ws); ev[1].record()
         x.push_plan(vals, t.V, P, out_b, gb, tab.ws); ev[2].record()
         x.merge_apply(tab.slab(), tab.optimizer.c_struct(s + 10, 1.0)); ev[3].record()
         x.stitch(out_b["inv"][:cap], out); ev[4].record()

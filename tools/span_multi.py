@@ -17,7 +17,8 @@ from paper_1808_02621_b200.synth import WORKLOADS, TableShape, Workload, make_ba
 NAMES = ["dedup", "reduce", "combine", "wait_push", "scatter", "apply", "wait_applied", "copy",
          "ar_scatter", "ar_wait0", "ar_rg", "ar_wait1"]
 which = sys.argv[1] if len(sys.argv) > 1 else "table"
-pipelined = len(sys.argv) > 2 and sys.argv[2] == "pipelined"
+pipelined = len(sys.argv) > 2 and sys.argv[2] in ("pipelined", "graph")
+use_graph = len(sys.argv) > 2 and sys.argv[2] == "graph"  # replay the bench's pipelined graphs
 if which == "table":
     wl = Workload("t", [TableShape("softmax", 800_000, 512, 2560, sampled=8192)], {},
                   {"kind": "adagrad", "lr": 0.2, "init_acc": 0.1}, 2560)
@@ -42,9 +43,14 @@ for s in (1, 2):
                    if isinstance(v, tuple) else torch.from_numpy(v).to(dev)) for k, v in b.items()})
 lib = _lib.load()
 span = torch.zeros(32, dtype=torch.int64, device=dev)
-if pipelined:
+graphs = None
+if use_graph:
+    graphs = runner.capture_pipelined(bs)
+    for i in range(4):
+        graphs[i % 2].replay()
+elif pipelined:
     runner.prefetch(bs[0])
-for i in range(4):
+for i in range(0 if use_graph else 4):
     runner.step(bs[i % 2], timed=False, next_batch=bs[(i + 1) % 2] if pipelined else None)
 torch.cuda.synchronize()
 rows = []
@@ -55,7 +61,10 @@ for it in range(8):
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda._sleep(20_000_000)
-    runner.step(bs[it % 2], timed=False, next_batch=bs[(it + 1) % 2] if pipelined else None)
+    if graphs:
+        graphs[it % 2].replay()
+    else:
+        runner.step(bs[it % 2], timed=False, next_batch=bs[(it + 1) % 2] if pipelined else None)
     torch.cuda.synchronize()
     lib.hp_debug_set_spans(None)
     v = span.view(16, 2).cpu().numpy().astype(np.uint64)
@@ -74,6 +83,8 @@ dist.all_gather_object(out, {"rank": rank, "spans_us": dict(sorted(summ.items(),
 if rank == 0:
     for o in out:
         print(json.dumps(o))
+del graphs
+torch.cuda.synchronize()
 runner.close()
 comm.close()
 dist.destroy_process_group()
