@@ -105,6 +105,9 @@ void hp_debug_set_owner_stream(int on);
 void hp_debug_set_combine_blocks(int n);
 /* Grid of the pipelined dense allreduce (HP_DAR_PIPE); 0 = one block per SM. */
 void hp_debug_set_dar_blocks(int n);
+/* Instrumentation: grids of the peer-store kernels (push reduce, owner rows):
+ * 1 (default) = one group per item, many waves; 0 = one resident wave. */
+void hp_debug_set_owner_waves(int on);
 /* Instrumentation: k_reduce rows in flight per thread at 2 float4 columns (2 = default, 4, 8). */
 void hp_debug_set_reduce_b(int b);
 
@@ -312,6 +315,9 @@ int hp_dar_status(hp_dar_t d, int32_t* out_err, void* stream);
 /* Instrumentation: raw peer throughput over the dense window (mode 0/2 store,
  * 1/3 load; 2/3 with 4 x 16 B in flight per thread). */
 int hp_debug_nvlink_bench(hp_dar_t d, int32_t peer, int32_t mode, int32_t blocks, void* stream);
+/* Instrumentation: per-block publication cost (peer stores + fence variant). */
+int hp_debug_fence_bench(hp_dar_t d, int32_t peer, int32_t mode, int32_t blocks, int32_t per_block,
+                         void* stream);
 
 #ifdef __cplusplus
 }

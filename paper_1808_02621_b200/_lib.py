@@ -49,6 +49,7 @@ SIGNATURES = {
     "hp_debug_set_combine_blocks": (None, [C.c_int]),
     "hp_debug_set_reduce_b": (None, [C.c_int]),
     "hp_debug_set_dar_blocks": (None, [C.c_int]),
+    "hp_debug_set_owner_waves": (None, [C.c_int]),
     "hp_debug_set_spans": (None, [vp]),
     "hp_apply_plan": (C.c_int, [vp, i64, Slab, Optim, vp, sz, vp]),
     "hp_apply_plan_build": (C.c_int, [vp, i64, Slab, vp, sz, vp]),
@@ -95,6 +96,7 @@ SIGNATURES = {
     "hp_dar_allreduce": (C.c_int, [vp, vp, f32, vp]),
     "hp_dar_status": (C.c_int, [vp, vp, vp]),
     "hp_debug_nvlink_bench": (C.c_int, [vp, i32, i32, i32, vp]),
+    "hp_debug_fence_bench": (C.c_int, [vp, i32, i32, i32, i32, vp]),
     "hp_xchg_debug_sig": (C.c_int, [vp, vp, vp]),
 }
 

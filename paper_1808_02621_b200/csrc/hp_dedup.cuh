@@ -61,7 +61,8 @@ extern int g_rowstream_off;
 extern int g_rs_ctas;
 extern int g_owner_stream;
 extern int g_combine_blocks;
-extern int g_dar_blocks;  // HP_DAR_PIPE grid (hp_debug_set_dar_blocks)
+extern int g_dar_blocks;
+extern int g_owner_waves;  // peer-store kernels: many waves (1) or one resident wave (0)  // HP_DAR_PIPE grid (hp_debug_set_dar_blocks)
 extern int g_reduce_b;  // k_reduce rows in flight at VPT=2 (A/B: 2, 4, 8)  // k_combine grid for peer-store epilogues (hp_debug_set_combine_blocks)  // p2p owner apply as a row stream (hp_debug_set_owner_stream)  // row-stream CTAs per SM cap (hp_debug_set_rs_ctas)  // hp_debug_set_rowstream(0): use k_reduce (A/B instrumentation)
 
 size_t dedup_ws_bytes(int64_t T, int32_t D, int32_t P);

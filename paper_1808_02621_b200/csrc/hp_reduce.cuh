@@ -9,9 +9,11 @@ namespace hp {
 // Epilogue contract:
 //   Pre load(dst, c4)            issued before the row loads (depends on the item only)
 //   void store(dst, c4, g, pre)  consumes the summed float4
-//   kRemote                      stores go to peer memory: every block fences at
-//                                system scope before exit and the last k_combine
-//                                block calls grid_done() (publication hook)
+//   kRemote                      stores go to peer memory: the caller launches
+//                                k_publish (one block: system fence, then
+//                                grid_done()) after k_combine; stream order makes
+//                                every block's stores happen-before that fence, so
+//                                the reduce / combine blocks do not fence or drain
 
 // Epilogue interface: Pre load(dst, c4) is issued BEFORE the row loads (it
 // only depends on the item), store(dst, c4, g, pre) consumes the summed float4.
@@ -203,25 +205,20 @@ k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
       }
     }
   }
-  if constexpr (Epi::kRemote) {  // one cumulative release per block, after the barrier
-    __syncthreads();
-    if (threadIdx.x == 0) __threadfence_system();
-  }
   HP_SPAN_END(SP_REDUCE);
 }
 
-// ((0 + r0) + r1) + ... over n <= HP_CHUNK rows of stride D4, 8 loads in flight.
+// ((0 + r0) + r1) + ... over n <= HP_CHUNK rows of stride D4: all HP_CHUNK
+// loads in flight (one round trip per tree level).
 __device__ __forceinline__ float4 seq_sum_rows(const float4* src, int n, int D4) {
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int j0 = 0; j0 < n; j0 += 8) {
-    float4 x[8];
+  float4 x[HP_CHUNK];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j0 + j < n) x[j] = src[(int64_t)(j0 + j) * D4];
+  for (int j = 0; j < HP_CHUNK; ++j)
+    if (j < n) x[j] = src[(int64_t)j * D4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j0 + j < n) acc = f4_add(acc, x[j]);
-  }
+  for (int j = 0; j < HP_CHUNK; ++j)
+    if (j < n) acc = f4_add(acc, x[j]);
   return acc;
 }
 
@@ -264,19 +261,17 @@ __global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
     }
     __syncthreads();
   }
-  if constexpr (Epi::kRemote) {
-    __shared__ bool s_last;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence_system();
-      s_last = atomicAdd(epi.done, 1) == (int)gridDim.x - 1;
-    }
-    __syncthreads();
-    if (s_last) {
-      __threadfence_system();
-      epi.grid_done();
-    }
-  }
+  HP_SPAN_END(SP_COMBINE);
+}
+
+// Publication after a peer-store reduce (one block, launched after k_combine):
+// the system-scope fence is cumulative over every store the previous kernels
+// of this stream made, then the epilogue publishes (flags / counts).
+template <class Epi>
+__global__ void k_publish(Epi epi) {
+  HP_ENTRY(SP_COMBINE);
+  __threadfence_system();
+  epi.grid_done();
   HP_SPAN_END(SP_COMBINE);
 }
 
@@ -429,10 +424,6 @@ __global__ void __launch_bounds__(128) k_rowstream(DedupPlan pl, const float* __
     cp_async_commit();
   }
   cp_async_wait<0>();
-  if constexpr (Epi::kRemote) {  // one cumulative release per block, after the barrier
-    __syncthreads();
-    if (threadIdx.x == 0) __threadfence_system();
-  }
   HP_SPAN_END(SP_REDUCE);
 }
 
@@ -454,9 +445,9 @@ void launch_k_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cud
   // rows in flight per batch: most items hold 1-2 rows, so a small batch keeps
   // registers (and so resident items per SM) up without costing the hot chunks much
   constexpr int B = VPT >= 2 ? 2 : 8;  // measured: B=2 beats 4 and 8 at VPT=2
-  // <= one group per item; peer-store epilogues stay in one resident wave so
-  // each block pays its system-scope fence once
-  const int blocks = grid_for(pl.T, 256 / TPI, sm_count() * (Epi::kRemote ? 3 : 16));
+  // <= one group per item, many waves (each block fences once if its epilogue
+  // stores to peers; hp_debug_set_owner_waves(0) keeps those in one resident wave)
+  const int blocks = grid_for(pl.T, 256 / TPI, sm_count() * (Epi::kRemote && !g_owner_waves ? 3 : 16));
   if (VPT == 2 && g_reduce_b == 4)
     launch_k(k_reduce<TPI, VPT, 4, Epi>, dim3(blocks), dim3(256), 0, st, pl, vals, epi);
   else if (VPT == 2 && g_reduce_b == 8)
@@ -490,6 +481,10 @@ int launch_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaSt
                                Epi::kRemote && g_combine_blocks > 0 ? g_combine_blocks : sm_count());
   launch_k(k_combine<Epi>, dim3(cblocks), dim3(256), 0, st, pl, epi);
   HP_LAUNCHED(1, "k_combine");
+  if constexpr (Epi::kRemote) {
+    launch_k(k_publish<Epi>, dim3(1), dim3(64), 0, st, epi);
+    HP_LAUNCHED(1, "k_publish");
+  }
   return HP_OK;
 }
 

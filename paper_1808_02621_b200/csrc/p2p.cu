@@ -120,8 +120,9 @@ struct EpiPush {
           ((unsigned long long)(unsigned)p.epoch << 32) | (unsigned long long)(uint32_t)p.inf.x;
     }
   }
-  // Runs once, in the last k_combine block, after every block fenced its
-  // peer stores: publish {count, offset} then the epoch flag at every owner.
+  // Runs once, in k_publish after k_combine (after a system fence that covers
+  // every peer store of the reduce): publish {count, offset}, then the epoch
+  // flag at every owner.
   __device__ void grid_done() const {
     SigView me(my_win);
     const int e = *me.epoch + 1;
@@ -135,10 +136,7 @@ struct EpiPush {
       st_release_sys(&peer.push_flag[L.me], e);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      *me.epoch = e;
-      *done = 0;
-    }
+    if (threadIdx.x == 0) *me.epoch = e;
   }
 };
 
@@ -617,12 +615,12 @@ k_owner_scan(void* my_win, WinLayout L, const int64_t* __restrict__ part_base, R
 // item: the item and its contributor list are one round trip, then the row's
 // state and all contributions are loaded together; sums in source order,
 // scales, applies, stores the state and returns the updated row into each
-// contributor's return buffer (NVLink). The last block raises "applied".
+// contributor's return buffer (NVLink). No block fences: k_applied (one block,
+// next in the stream) fences once at system scope and raises "applied".
 template <int OPT, int TPI, int VPT>
 __global__ void __launch_bounds__(256, 3)
 k_owner_rows(PeerTable peers, void* my_win, WinLayout L, float4* s0, float4* s1, hp_optim o) {
   __shared__ int s_poff[OS_NMAX];
-  __shared__ bool s_last;
   HP_ENTRY(SP_APPLY);
   SigView sig(my_win);
   char* win = static_cast<char*>(my_win);
@@ -634,12 +632,23 @@ k_owner_rows(PeerTable peers, void* my_win, WinLayout L, float4* s0, float4* s1,
   if (threadIdx.x < n) s_poff[threadIdx.x] = sig.push_off[threadIdx.x];
   __syncthreads();
   const int NI = *sig.own_items;
-  const unsigned epoch = (unsigned)*sig.epoch;
   const int lane = threadIdx.x & 31, q = threadIdx.x % TPI;
   constexpr int GPB = 256 / TPI;
-  for (int it = blockIdx.x * GPB + threadIdx.x / TPI; it < NI; it += gridDim.x * GPB) {
-    const int2 item = items[it];
-    const int myc = lane < n ? cidx_all[(int64_t)it * n + lane] : 0;
+  // one item per group, many waves (blocks past the item count exit at once and
+  // take no part in the last-block election); with a capped grid the group
+  // loops, the next descriptor loaded while this item streams
+  if ((int)blockIdx.x * GPB >= NI) return;
+  const int istride = gridDim.x * GPB;
+  int it = blockIdx.x * GPB + threadIdx.x / TPI;
+  int2 item_n = make_int2(0, 0);
+  int myc_n = 0;
+  if (it < NI) {
+    item_n = items[it];
+    myc_n = lane < n ? cidx_all[(int64_t)it * n + lane] : 0;
+  }
+  for (; it < NI; it += istride) {
+    const int2 item = item_n;
+    const int myc = myc_n;
     const int64_t row = item.x;
     const int cnt = item.y;
     float4 wv[VPT], av[VPT], bv[VPT], g[VPT];
@@ -663,6 +672,10 @@ k_owner_rows(PeerTable peers, void* my_win, WinLayout L, float4* s0, float4* s1,
 #pragma unroll
         for (int v = 0; v < VPT; ++v)
           if (j0 + u < cnt && q + v * TPI < D4) x[u][v] = inbox[(int64_t)idx * D4 + q + v * TPI];
+      }
+      if (j0 == 0 && it + istride < NI) {  // prefetch the next descriptor
+        item_n = items[it + istride];
+        myc_n = lane < n ? cidx_all[(int64_t)(it + istride) * n + lane] : 0;
       }
 #pragma unroll
       for (int u = 0; u < 2; ++u)
@@ -694,21 +707,19 @@ k_owner_rows(PeerTable peers, void* my_win, WinLayout L, float4* s0, float4* s1,
         if (q + v * TPI < D4) ret[q + v * TPI] = wv[v];
     }
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    s_last = atomicAdd(&sig.done[1], 1) == (int)gridDim.x - 1;
-  }
-  __syncthreads();
-  if (s_last) {
-    __threadfence_system();
-    for (int r = threadIdx.x; r < n; r += blockDim.x)
-      st_release_sys(&SigView(peers.base[r]).applied_flag[L.me], (int)epoch);
-    if (threadIdx.x == 0) {
-      sig.done[1] = 0;
-      *sig.own_items = 0;
-    }
-  }
+  HP_SPAN_END(SP_APPLY);
+}
+
+// After k_owner_rows (stream order): one system fence covering every store of
+// the apply, then "applied" at every rank; resets the item counter.
+__global__ void k_applied(PeerTable peers, void* my_win, WinLayout L) {
+  HP_ENTRY(SP_APPLY);
+  SigView sig(my_win);
+  __threadfence_system();
+  const int epoch = *sig.epoch;
+  for (int r = threadIdx.x; r < L.n; r += blockDim.x)
+    st_release_sys(&SigView(peers.base[r]).applied_flag[L.me], epoch);
+  if (threadIdx.x == 0) *sig.own_items = 0;
   HP_SPAN_END(SP_APPLY);
 }
 
@@ -901,9 +912,10 @@ void launch_owner_rows(const hp_xchg_s* x, const hp_slab& slab, const hp_optim& 
   const int64_t total = (int64_t)x->L.n * x->L.cap;
   launch_k(k_owner_scan, dim3(grid_for(total, 256, sm_count() * 8)), dim3(256), 0, st, x->win, x->L,
            slab.part_base, Router(slab.V, slab.P), x->rows_cap);
-  const int blocks = grid_for(total, 256 / TPI, sm_count() * 3);  // one resident wave
+  const int blocks = grid_for(total, 256 / TPI, g_owner_waves ? 1 << 30 : sm_count() * 3);
   launch_k(k_owner_rows<OPT, TPI, VPT>, dim3(blocks), dim3(256), 0, st, x->peers, x->win, x->L,
            reinterpret_cast<float4*>(slab.s0), reinterpret_cast<float4*>(slab.s1), opt);
+  launch_k(k_applied, dim3(1), dim3(64), 0, st, x->peers, x->win, x->L);
 }
 
 template <int OPT>
@@ -950,7 +962,7 @@ int hp_xchg_merge_apply(hp_xchg_t x, hp_slab slab, hp_optim opt, int32_t wait, v
     case HP_OPT_ADAGRAD: dispatch_owner_apply<HP_OPT_ADAGRAD>(x, slab, opt, D4, st); break;
     default: dispatch_owner_apply<HP_OPT_ADAM>(x, slab, opt, D4, st);
   }
-  HP_LAUNCHED(g_owner_stream == 2 ? 2 : 1, "owner merge/apply");
+  HP_LAUNCHED(g_owner_stream == 2 ? 3 : 1, "owner merge/apply");
   return HP_OK;
 }
 
@@ -1536,6 +1548,37 @@ __global__ void __launch_bounds__(256) k_nvl_bench(float4* local, float4* remote
 }
 }  // namespace
 }  // namespace hp
+
+// ---- instrumentation: cost of the per-block publication pattern. Every block
+// stores `per_block` float4 to the peer (0 = none), then: mode 0 nothing,
+// 1 __syncthreads + thread 0 fence.sc.sys, 2 fence.sc.gpu, 3 fence.acq_rel.sys.
+namespace hp {
+namespace {
+__global__ void k_fence_bench(float4* remote, int per_block, int mode, int* ctr) {
+  float4 v = make_float4(1.f, 2.f, 3.f, 4.f);
+  float4* dst = remote + (int64_t)blockIdx.x * per_block;
+  for (int i = threadIdx.x; i < per_block; i += blockDim.x) dst[i] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (mode == 1) __threadfence_system();
+    else if (mode == 2) __threadfence();
+    else if (mode == 3) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    atomicAdd(ctr, 1);
+  }
+}
+}  // namespace
+}  // namespace hp
+
+extern "C" int hp_debug_fence_bench(hp_dar_t d, int32_t peer, int32_t mode, int32_t blocks,
+                                    int32_t per_block, void* stream) {
+  HP_REQUIRE(d && peer >= 0 && peer < d->A.n && d->peers.base[peer], "bad peer");
+  HP_REQUIRE((int64_t)blocks * per_block <= d->A.S / 4, "fence bench exceeds the slot region");
+  float4* remote = reinterpret_cast<float4*>(static_cast<char*>(d->peers.base[peer]) + d->A.slots_off);
+  int* ctr = reinterpret_cast<int*>(static_cast<char*>(d->win) + d->queue_off) + 8;
+  k_fence_bench<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(remote, per_block, mode, ctr);
+  HP_CUDA(cudaGetLastError());
+  return HP_OK;
+}
 
 extern "C" int hp_debug_nvlink_bench(hp_dar_t d, int32_t peer, int32_t mode, int32_t blocks,
                                      void* stream) {
