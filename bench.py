@@ -79,6 +79,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"])
     ap.add_argument("--dense-exchange", default=None, choices=["p2p", "p2p-sm", "p2p-pipe", "nvls", "nccl"])
+    ap.add_argument("--dense-split", default="auto", choices=["auto", "uniform"],
+                    help="peer-memory dense exchange: reduction share per rank")
     ap.add_argument("--arch", default="hybrid", choices=["hybrid", "ar", "ps"],
                     help="mechanism plan: transform_hybrid (default) / transform_ar / transform_ps")
     ap.add_argument("--knob", action="append", default=[],
@@ -92,6 +94,18 @@ def peaks() -> dict:
         d = json.loads(p.read_text())
         return {"hbm_gbs": d["hbm_gbs"], "src": "measured (MEASURED_PEAKS.json)"}
     return {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)"}
+
+
+def k4_traffic(workload: str, table: str):
+    """DRAM bytes (read + write) per K4 launch pair from the committed ncu capture
+    (profiles/r1b_k4_traffic.json), for the workload/table it was taken on."""
+    p = ROOT / "profiles" / "r1b_k4_traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    if d.get("workload") != workload or d.get("table") != table:
+        return None
+    return d["traffic_bytes_per_launch"]
 
 
 # ------------------------------------------------------------------ clocks
@@ -264,7 +278,7 @@ def main():
     opt = hp.OptimizerConfig(**wl.optimizer)
     runner = hp.HybridRunner(plan, graph, cluster, rank=rank, world_size=world, comm=comm,
                              optimizer=opt, device=dev, seed=0, exchange=args.exchange,
-                             dense_exchange=args.dense_exchange)
+                             dense_exchange=args.dense_exchange, dense_split=args.dense_split)
 
     # resident batches, rotated so their total exceeds 2x L2 (126 MB)
     host = [make_batch(wl, seed=1 + i, rank=rank) for i in range(1)]
@@ -365,7 +379,7 @@ def main():
         achieved = algo / (us * 1e-6) / 1e9
         roof = {"kernel": f"K4 merge+apply ({big.name}, k_reduce+k_combine)", "bound": "hbm",
                 "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                "frac": achieved / pk["hbm_gbs"], "traffic": k4_traffic(wl.name, big.name),
                 "algorithmic_bytes": algo, "launch_us": us, "peak_src": pk["src"],
                 "unique_rows": U, "T": T,
                 "step_share": us / (t_dev / args.steps * 1e6)}
@@ -436,7 +450,8 @@ def main():
             "data": "synthetic (Zipf(1.1) ids, normal grads, hash-initialised tables)",
             "config": config(args, wl) | {"rotations": R, "cuda_graph": bool(graphs),
                                           "exchange": runner.exchange,
-                                          "dense_exchange": runner.dense_exchange},
+                                          "dense_exchange": runner.dense_exchange,
+                                          "dense_split": runner.dense_weights or "uniform"},
             "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": ke},
             "gpu_launches": launches_per_step * args.steps,

@@ -300,6 +300,12 @@ int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream);
 #define HP_DAR_CE 1
 #define HP_DAR_PIPE 2 /* one persistent kernel; scatter and reduce-gather pipelined by 64 KB pieces */
 int hp_dar_set_mode(hp_dar_t d, int32_t mode);
+/* Split of the reduction between ranks: rank r reduces a share of S
+ * proportional to weights[n] (double, >= 0, identical on every rank; default
+ * uniform). Weight 0 takes a rank out of the reduce/gather work, so its NVLink
+ * egress is S instead of 2(n-1)/n S (a rank that homes a hot sparse partition).
+ * HP_DAR_SM and HP_DAR_CE; HP_DAR_PIPE needs the uniform split. */
+int hp_dar_set_split(hp_dar_t d, const double* weights);
 
 /* K7 through the NVSwitch (NVLS multicast). mc_in / mc_out: multicast
  * addresses of symmetric buffers of S elements (S a multiple of 4 n; fp32 in,

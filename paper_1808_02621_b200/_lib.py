@@ -92,6 +92,7 @@ SIGNATURES = {
     "hp_dar_open_peer": (C.c_int, [vp, i32, vp]),
     "hp_dar_destroy": (C.c_int, [vp]),
     "hp_dar_set_mode": (C.c_int, [vp, i32]),
+    "hp_dar_set_split": (C.c_int, [vp, vp]),
     "hp_nvls_allreduce": (C.c_int, [vp, vp, i64, i32, i32, i32, f32, vp, vp, vp]),
     "hp_dar_allreduce": (C.c_int, [vp, vp, f32, vp]),
     "hp_dar_status": (C.c_int, [vp, vp, vp]),

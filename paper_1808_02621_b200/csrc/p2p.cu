@@ -1024,9 +1024,14 @@ int hp_xchg_status(hp_xchg_t x, int32_t* out_err, void* stream) {
 namespace hp {
 namespace {
 
+constexpr int AR_MAXN = 32;
 struct ArLayout {
   int64_t S, S_real, chunk, slots_off, out_off;  // S = S_real padded to a multiple of 4n
   int n, me, out_bytes;
+  // chunk of rank r = float4 range [off4[r], off4[r+1]) (uniform S/n unless
+  // hp_dar_set_split weighted it); source s's slot at every rank starts at s * sstride4
+  int64_t sstride4;
+  int64_t off4[AR_MAXN + 1];
 };
 
 // blockIdx.y = destination chunk; 4 float4 in flight per thread; no division.
@@ -1035,11 +1040,11 @@ k_ar_scatter(PeerTable peers, void* my_win, ArLayout A, const float4* __restrict
   __shared__ bool s_last;
   HP_ENTRY(SP_AR_SCATTER);
   const int c = blockIdx.y;
-  const int64_t c4 = A.chunk >> 2, real4 = A.S_real >> 2;
-  const float4* src = grad + (int64_t)c * c4;
+  const int64_t b4 = A.off4[c], c4 = A.off4[c + 1] - b4, real4 = A.S_real >> 2;
+  const float4* src = grad + b4;
   float4* dst = reinterpret_cast<float4*>(static_cast<char*>(peers.base[c]) + A.slots_off) +
-                (int64_t)A.me * c4;
-  const int64_t lim = min(c4, max((int64_t)0, real4 - (int64_t)c * c4));  // real elements here
+                (int64_t)A.me * A.sstride4;
+  const int64_t lim = min(c4, max((int64_t)0, real4 - b4));  // real elements here
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < c4; j0 += 4 * stride) {
     float4 v[4];
@@ -1096,7 +1101,7 @@ __global__ void __launch_bounds__(256)
 k_ar_reduce_gather(PeerTable peers, void* my_win, ArLayout A, float scale) {
   __shared__ bool s_last;
   HP_ENTRY(SP_AR_RG);
-  const int64_t c4 = A.chunk >> 2;
+  const int64_t b4 = A.off4[A.me], c4 = A.off4[A.me + 1] - b4;
   const float4* slots =
       reinterpret_cast<const float4*>(static_cast<char*>(my_win) + A.slots_off);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -1107,7 +1112,7 @@ k_ar_reduce_gather(PeerTable peers, void* my_win, ArLayout A, float scale) {
       const int64_t j = j0 + u * stride;
       acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (j < c4)
-        for (int s = 0; s < A.n; ++s) acc[u] = f4_add(acc[u], ldg_stream(slots + (int64_t)s * c4 + j));
+        for (int s = 0; s < A.n; ++s) acc[u] = f4_add(acc[u], ldg_stream(slots + (int64_t)s * A.sstride4 + j));
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -1118,7 +1123,7 @@ k_ar_reduce_gather(PeerTable peers, void* my_win, ArLayout A, float scale) {
       v.y = __fmul_rn(v.y, scale);
       v.z = __fmul_rn(v.z, scale);
       v.w = __fmul_rn(v.w, scale);
-      const int64_t o4 = (int64_t)A.me * c4 + j;
+      const int64_t o4 = b4 + j;
       for (int r = 0; r < A.n; ++r)
         put4<OutT>(static_cast<char*>(peers.base[r]) + A.out_off, o4, v);
     }
@@ -1164,10 +1169,10 @@ template <typename OutT>
 __global__ void __launch_bounds__(256)
 k_ar_reduce_local(void* my_win, ArLayout A, const float4* __restrict__ grad, float scale) {
   HP_ENTRY(SP_AR_RG);
-  const int64_t c4 = A.chunk >> 2;
-  const int64_t own_lim = min(c4, max((int64_t)0, (A.S_real >> 2) - (int64_t)A.me * c4));
+  const int64_t b4 = A.off4[A.me], c4 = A.off4[A.me + 1] - b4;
+  const int64_t own_lim = min(c4, max((int64_t)0, (A.S_real >> 2) - b4));
   const float4* slots = reinterpret_cast<const float4*>(static_cast<char*>(my_win) + A.slots_off);
-  const float4* mine = grad + (int64_t)A.me * c4;
+  const float4* mine = grad + b4;
   char* out = static_cast<char*>(my_win) + A.out_off;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < c4; j0 += 2 * stride) {
@@ -1180,7 +1185,7 @@ k_ar_reduce_local(void* my_win, ArLayout A, const float4* __restrict__ grad, flo
         for (int sidx = 0; sidx < A.n; ++sidx) {
           const float4 x = sidx == A.me ? (j < own_lim ? ldg_stream(mine + j)
                                                         : make_float4(0.f, 0.f, 0.f, 0.f))
-                                        : ldg_stream(slots + (int64_t)sidx * c4 + j);
+                                        : ldg_stream(slots + (int64_t)sidx * A.sstride4 + j);
           acc[u] = f4_add(acc[u], x);
         }
     }
@@ -1193,7 +1198,7 @@ k_ar_reduce_local(void* my_win, ArLayout A, const float4* __restrict__ grad, flo
       v.y = __fmul_rn(v.y, scale);
       v.z = __fmul_rn(v.z, scale);
       v.w = __fmul_rn(v.w, scale);
-      put4<OutT>(out, (int64_t)A.me * c4 + j, v);
+      put4<OutT>(out, b4 + j, v);
     }
   }
   HP_SPAN_END(SP_AR_RG);
@@ -1241,7 +1246,7 @@ k_ar_pipe(PeerTable peers, void* my_win, ArLayout A, const float4* __restrict__ 
       const int64_t lim = min(hi, max((int64_t)0, real4 - (int64_t)c * c4));
       const float4* src = grad + (int64_t)c * c4;
       float4* dst = reinterpret_cast<float4*>(static_cast<char*>(peers.base[c]) + A.slots_off) +
-                    (int64_t)me * c4;
+                    (int64_t)me * A.sstride4;
       for (int64_t j0 = lo + threadIdx.x; j0 < hi; j0 += 4 * 256) {
         float4 v[4];
 #pragma unroll
@@ -1288,7 +1293,7 @@ k_ar_pipe(PeerTable peers, void* my_win, ArLayout A, const float4* __restrict__ 
             for (int s = 0; s < n; ++s) {
               const float4 x = s == me ? (j < own_lim ? ldg_stream(mine + j)
                                                       : make_float4(0.f, 0.f, 0.f, 0.f))
-                                       : ldg_stream(slots + (int64_t)s * c4 + j);
+                                       : ldg_stream(slots + (int64_t)s * A.sstride4 + j);
               acc[u] = f4_add(acc[u], x);
             }
         }
@@ -1337,6 +1342,7 @@ struct hp_dar_s {
   void* win;
   PeerTable peers;
   int64_t arrive_off, queue_off;  // HP_DAR_PIPE: piece arrival counters, work queue
+  bool weighted;                  // hp_dar_set_split gave a non-uniform split
   int mode;                  // HP_DAR_SM | HP_DAR_CE | HP_DAR_PIPE
   cudaStream_t side[4];      // CE mode: copies to different peers run concurrently
   cudaEvent_t fork, join[4];
@@ -1350,7 +1356,7 @@ extern "C" {
 // or HP_DTYPE_BF16; the first S elements are the result).
 int hp_dar_create(hp_dar_t* out, int32_t n, int32_t me, int64_t S_real, int32_t out_dtype,
                   void* ipc_handle_out, void** out_ptr) {
-  HP_REQUIRE(out && ipc_handle_out && out_ptr && n >= 1 && n <= 32 && me >= 0 && me < n,
+  HP_REQUIRE(out && ipc_handle_out && out_ptr && n >= 1 && n <= AR_MAXN && me >= 0 && me < n,
              "bad dense allreduce args");
   HP_REQUIRE(S_real > 0 && S_real % 4 == 0, "S must be a positive multiple of 4");
   const int64_t S = (S_real + 4 * n - 1) / (4 * n) * (4 * n);
@@ -1363,8 +1369,11 @@ int hp_dar_create(hp_dar_t* out, int32_t n, int32_t me, int64_t S_real, int32_t 
   d->A.me = me;
   d->A.chunk = S / n;
   d->A.out_bytes = out_dtype == HP_DTYPE_F32 ? 4 : 2;
+  // slots sized for any split (a chunk may be all of S): n sources x S
+  d->A.sstride4 = S / 4;
+  for (int r = 0; r <= n; ++r) d->A.off4[r] = (int64_t)r * (S / n) / 4;
   d->A.slots_off = al(SIG_INTS * 4);
-  d->A.out_off = d->A.slots_off + al(S * 4);
+  d->A.out_off = d->A.slots_off + al((int64_t)n * S * 4);
   d->arrive_off = d->A.out_off + al(S * d->A.out_bytes);
   d->queue_off = d->arrive_off + al(((S / n / 4 + AR_PIECE4 - 1) / AR_PIECE4) * 4);
   const int64_t bytes = d->queue_off + 256;
@@ -1417,6 +1426,35 @@ int hp_dar_destroy(hp_dar_t d) {
 
 // out (the window's output, every rank) = cast(scale * sum_r grad_r), summed in
 // rank order. grad is this rank's fp32 gradient [S] (any device buffer).
+// Chunk split of the reduction: rank r reduces (and gathers) a share of S
+// proportional to weights[r] >= 0 (rounded to float4; identical weights on
+// every rank). A rank with weight 0 only scatters its gradient and receives the
+// result: its NVLink egress drops from 2(n-1)/n S to S - its chunk = S, which
+// relieves a rank whose links also carry a hot sparse partition.
+int hp_dar_set_split(hp_dar_t d, const double* weights) {
+  HP_REQUIRE(d && weights, "NULL argument");
+  const int n = d->A.n;
+  double tot = 0;
+  for (int r = 0; r < n; ++r) {
+    HP_REQUIRE(weights[r] >= 0, "weights must be >= 0");
+    tot += weights[r];
+  }
+  HP_REQUIRE(tot > 0, "at least one weight must be > 0");
+  const int64_t S4 = d->A.S / 4;
+  double acc = 0;
+  bool uniform = true;
+  for (int r = 0; r < n; ++r) {
+    d->A.off4[r] = (int64_t)(acc / tot * (double)S4 + 0.5);
+    acc += weights[r];
+    uniform = uniform && weights[r] == weights[0];
+  }
+  d->A.off4[n] = S4;
+  if (uniform)
+    for (int r = 0; r <= n; ++r) d->A.off4[r] = (int64_t)r * (d->A.S / n) / 4;
+  d->weighted = !uniform;
+  return HP_OK;
+}
+
 int hp_dar_set_mode(hp_dar_t d, int32_t mode) {
   HP_REQUIRE(d && (mode == HP_DAR_SM || mode == HP_DAR_CE || mode == HP_DAR_PIPE),
              "mode must be HP_DAR_SM, HP_DAR_CE or HP_DAR_PIPE");
@@ -1436,16 +1474,19 @@ static int dar_copies(hp_dar_t d, cudaStream_t st, bool gather, const float* gra
     if (r == A.me) continue;
     cudaStream_t cs = d->side[q++ % ns];
     if (!gather) {  // my chunk r -> rank r's slot [me]
-      const int64_t real = std::min(A.chunk, std::max((int64_t)0, A.S_real - (int64_t)r * A.chunk));
+      const int64_t b = A.off4[r] * 4, len = A.off4[r + 1] * 4 - b;
+      const int64_t real = std::min(len, std::max((int64_t)0, A.S_real - b));
       if (real > 0)
         HP_CUDA(cudaMemcpyAsync(static_cast<char*>(d->peers.base[r]) + A.slots_off +
-                                    (int64_t)A.me * A.chunk * 4,
-                                grad + (int64_t)r * A.chunk, real * 4, cudaMemcpyDeviceToDevice, cs));
+                                    (int64_t)A.me * A.sstride4 * 16,
+                                grad + b, real * 4, cudaMemcpyDeviceToDevice, cs));
     } else {  // my reduced chunk -> rank r's output
-      const int64_t off = A.out_off + (int64_t)A.me * A.chunk * A.out_bytes;
-      HP_CUDA(cudaMemcpyAsync(static_cast<char*>(d->peers.base[r]) + off,
-                              static_cast<char*>(d->win) + off, A.chunk * A.out_bytes,
-                              cudaMemcpyDeviceToDevice, cs));
+      const int64_t b = A.off4[A.me] * 4, len = A.off4[A.me + 1] * 4 - b;
+      const int64_t off = A.out_off + b * A.out_bytes;
+      if (len > 0)
+        HP_CUDA(cudaMemcpyAsync(static_cast<char*>(d->peers.base[r]) + off,
+                                static_cast<char*>(d->win) + off, len * A.out_bytes,
+                                cudaMemcpyDeviceToDevice, cs));
     }
   }
   for (int k = 0; k < ns; ++k) {
@@ -1459,12 +1500,14 @@ int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream) {
   HP_REQUIRE(d && grad && ((uintptr_t)grad & 15) == 0, "grad must be a 16-byte aligned buffer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int sms = sm_count();
+  int64_t maxc = 0, myc = (d->A.off4[d->A.me + 1] - d->A.off4[d->A.me]) * 4;
+  for (int r = 0; r < d->A.n; ++r) maxc = std::max(maxc, (d->A.off4[r + 1] - d->A.off4[r]) * 4);
   if (d->mode == HP_DAR_CE) {
     int rc;
     if (d->A.n > 1 && (rc = dar_copies(d, st, false, grad))) return rc;
     launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 0);
     launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 0, d->A.n, wait_budget(), SP_AR_WAIT0);
-    const int brg = grid_for(d->A.chunk / 8, 256, sms * 2);
+    const int brg = grid_for(myc / 8, 256, sms * 2);
     if (d->A.out_bytes == 4)
       launch_k(k_ar_reduce_local<float>, dim3(brg), dim3(256), 0, st, d->win, d->A,
                reinterpret_cast<const float4*>(grad), scale);
@@ -1478,6 +1521,7 @@ int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream) {
     return HP_OK;
   }
   if (d->mode == HP_DAR_PIPE) {
+    HP_REQUIRE(!d->weighted, "the pipelined dense exchange needs the uniform split");
     const int64_t c4 = d->A.chunk / 4;
     const int K = (int)((c4 + AR_PIECE4 - 1) / AR_PIECE4);
     const int blocks = std::max(1, std::min(d->A.n * K, g_dar_blocks > 0 ? g_dar_blocks : sms));
@@ -1495,11 +1539,11 @@ int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream) {
   }
   // ~half the SMs: NVLink saturates well below full occupancy, and the sparse
   // tables' latency-bound kernels run concurrently on the rest
-  const int bx = std::max(1, std::min(grid_for(d->A.chunk / 16, 256, sms), sms / d->A.n));
+  const int bx = std::max(1, std::min(grid_for(maxc / 16, 256, sms), sms / d->A.n));
   launch_k(k_ar_scatter, dim3(bx, d->A.n), dim3(256), 0, st, d->peers, d->win, d->A,
                                                 reinterpret_cast<const float4*>(grad));
   launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 0, d->A.n, wait_budget(), SP_AR_WAIT0);
-  const int brg = grid_for(d->A.chunk / 8, 256, sms * 2);
+  const int brg = grid_for(std::max<int64_t>(myc, 8) / 8, 256, sms * 2);
   if (d->A.out_bytes == 4)
     launch_k(k_ar_reduce_gather<float>, dim3(brg), dim3(256), 0, st, d->peers, d->win, d->A, scale);
   else

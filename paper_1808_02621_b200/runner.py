@@ -124,7 +124,7 @@ class HybridRunner:
                  optimizer: OptimizerConfig | None = None, aggregation: str = "mean",
                  dense_dtype: torch.dtype = torch.float32, device=None, seed: int = 0,
                  exchange: str = "p2p", max_ids: dict | None = None,
-                 dense_exchange: str | None = None):
+                 dense_exchange: str | None = None, dense_split="auto"):
         if aggregation not in ("mean", "sum"):
             raise ValueError("aggregation must be 'mean' or 'sum'")
         if cluster.total_gpus != world_size:
@@ -137,14 +137,15 @@ class HybridRunner:
             raise ValueError("exchange must be 'p2p' (NVLink peer memory) or 'nccl'")
         self.exchange = exchange if world_size > 1 else "local"
         # dense allreduce: peer-memory kernel (deterministic, scale/cast fused) or NCCL
-        # default K7 transport by measurement: two ranks -> copy-engine
-        # peer exchange; more -> NCCL (which uses NVLS on an NVSwitch box)
-        default_dense = ("p2p" if world_size == 2 else "nccl") if exchange == "p2p" else exchange
+        # default K7 transport by measurement: two ranks -> SM-store
+        # peer exchange (bit-exact, rank-order sum); more -> NCCL (NVLS on NVSwitch)
+        default_dense = ("p2p-sm" if world_size == 2 else "nccl") if exchange == "p2p" else exchange
         self.dense_exchange = (dense_exchange or default_dense) if world_size > 1 else "local"
         if self.dense_exchange not in ("p2p", "p2p-sm", "p2p-pipe", "nvls", "nccl", "local"):
             raise ValueError("dense_exchange must be 'p2p' (copy engines), 'p2p-sm', "
                              "'p2p-pipe', 'nvls' or 'nccl'")
         self.dar: dict = {}
+        self.dense_weights = None  # reduction share per rank of the peer dense exchange
         self.xchg: dict = {}
         self.ar_tables: set = set()   # sparse Weights under AR at n > 1 (AllGatherv baseline)
         self.dense_ps: dict = {}      # dense Weights under PS at n > 1: name -> owner rank
@@ -176,6 +177,10 @@ class HybridRunner:
                     self.dar[var.name] = DenseExchange(
                         world_size, rank, var.elements, dense_dtype, self.device,
                         mode={"p2p": "ce", "p2p-sm": "sm", "p2p-pipe": "pipe"}[self.dense_exchange])
+                    w = self._dense_split_weights(dense_split)
+                    if w is not None:
+                        self.dar[var.name].set_split(w)
+                    self.dense_weights = w
                 continue
             if mech is Mechanism.PS:
                 P = plan.partitions_of[var.name]
@@ -214,6 +219,31 @@ class HybridRunner:
                               for n in self.tables}
         self._pending_counts: dict = {}
         self.concurrent_tables = True
+
+    def _dense_split_weights(self, dense_split):
+        """Reduction share per rank for the peer-memory dense exchange.
+
+        'auto': with frequency-ranked row ids (LM vocabularies, the Zipf inputs of
+        BASELINE's configs) partition 0 of a sparse Weight is its hot range, so
+        the rank homing it carries most of that Weight's push/return NVLink
+        traffic. 'auto' gives those ranks no dense reduction
+        chunk (weight 0) when n >= 4 and at least one rank stays. 'uniform', or
+        an explicit list of n weights, overrides it. The pipelined transport
+        keeps the uniform split."""
+        n = self.world_size
+        if isinstance(dense_split, (list, tuple)):
+            if len(dense_split) != n:
+                raise ValueError(f"dense_split needs {n} weights")
+            return list(dense_split)
+        if dense_split in (None, "uniform") or self.dense_exchange == "p2p-pipe" or n < 4:
+            return None
+        if dense_split != "auto":
+            raise ValueError("dense_split: 'auto', 'uniform' or a list of weights")
+        hot = {self.plan.owner_of(v.name, 0) for v in self.graph.variables
+               if v.kind == "sparse" and self.plan.mech_of[v.name] is Mechanism.PS}
+        if not hot or len(hot) >= n:
+            return None
+        return [0.0 if r in hot else 1.0 for r in range(n)]
 
     def _make_window(self, var: VariableSpec, P: int, owner: np.ndarray, max_ids):
         """Create the table's peer window; returns the slab allocator for ShardedTable.

@@ -143,6 +143,11 @@ class DenseExchange:
         t = torch.as_tensor(_DevPtr(optr.value, (numel,), typestr), device=device)
         self.out = t if code == 0 else t.view(torch.bfloat16)
 
+    def set_split(self, weights) -> None:
+        """Share of the reduction per rank (hp_dar_set_split); identical on every rank."""
+        w = (C.c_double * self.n)(*[float(x) for x in weights])
+        call("hp_dar_set_split", self.handle, C.addressof(w))
+
     def allreduce(self, grad, scale: float) -> torch.Tensor:
         call("hp_dar_allreduce", self.handle, grad.data_ptr(), scale,
              torch.cuda.current_stream().cuda_stream)

@@ -24,6 +24,11 @@ from oracle import oracle as orc  # noqa: E402
 from paper_1808_02621_b200.synth import TableShape, Workload, make_batch  # noqa: E402
 
 
+def _split(spec: str, world: int):
+    """'auto' | 'uniform' | 'first0' (rank 0 takes no dense reduction chunk)."""
+    return [0.0] + [1.0] * (world - 1) if spec == "first0" else spec
+
+
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -55,7 +60,8 @@ def main():
         plan = hp.transform_hybrid(graph, cluster, partitions=parts)
     runner = hp.HybridRunner(plan, graph, cluster, rank=rank, world_size=world, comm=comm,
                              optimizer=hp.OptimizerConfig(kind=opt_kind, lr=0.1), device=dev,
-                             seed=5, exchange=xmode, dense_exchange=dmode)
+                             seed=5, exchange=xmode, dense_exchange=dmode,
+                             dense_split=_split(os.environ.get("HP_CHECK_SPLIT", "auto"), world))
     hpar = {"lr": 0.1, "beta1": 0.9, "beta2": 0.999, "eps": 1e-8}
     states = {t.name: orc.init_state(opt_kind, t.V, t.D, 5 * 1000 + i + 1, 0.1)
               for i, t in enumerate(wl.tables)}

@@ -20,6 +20,9 @@ def _ngpu():
 
 @pytest.mark.parametrize("opt,xchg,dense,knobs,arch", [
     ("adagrad", "p2p", "p2p", "", "hybrid"),
+    # weighted reduction split (rank 0 takes no chunk), SM stores and copy engines
+    ("adagrad", "p2p", "p2p-sm", "split=first0", "hybrid"),
+    ("sgd", "p2p", "p2p", "split=first0", "hybrid"),
     ("adam", "p2p", "nccl", "", "hybrid"),
     ("adagrad", "p2p", "nvls", "", "hybrid"),
     ("adagrad", "p2p", "p2p-pipe", "", "hybrid"),
@@ -33,8 +36,11 @@ def test_multi_gpu_step_matches_oracle(opt, xchg, dense, knobs, arch):
     n = min(_ngpu(), 8)
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
+    split = "auto"
+    if knobs.startswith("split="):
+        split, knobs = knobs.split("=", 1)[1], ""
     env = dict(os.environ, HP_CHECK_OPT=opt, HP_CHECK_XCHG=xchg, HP_CHECK_DENSE=dense,
-               HP_CHECK_KNOBS=knobs, HP_CHECK_ARCH=arch,
+               HP_CHECK_KNOBS=knobs, HP_CHECK_ARCH=arch, HP_CHECK_SPLIT=split,
                # the pipelined dense exchange cuts each chunk into 64 KB pieces: many of them
                HP_CHECK_DENSE_ELEMS="1000004" if dense == "p2p-pipe" else "50000")
     import socket
