@@ -210,7 +210,7 @@ k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
 
 // ((0 + r0) + r1) + ... over n <= HP_CHUNK rows of stride D4: all HP_CHUNK
 // loads in flight (one round trip per tree level).
-__device__ __forceinline__ float4 seq_sum_rows(const float4* src, int n, int D4) {
+static __device__ __noinline__ float4 seq_sum_rows(const float4* src, int n, int D4) {
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   float4 x[HP_CHUNK];
 #pragma unroll
@@ -223,20 +223,68 @@ __device__ __forceinline__ float4 seq_sum_rows(const float4* src, int n, int D4)
 }
 
 // Upper levels for segments longer than HP_CHUNK: one CTA per long segment
-// {partial slot, n0, dst, u}, in place over its partial rows.
+// {partial slot, n0, dst, u}. Latency-bound (a chain per hot id), so:
+//  * the CTA's first descriptor is loaded with the segment count (capacity
+//    T/C + 2 entries, so the speculative read is in bounds);
+//  * the epilogue's table rows (thread c4's column) are loaded before the tree;
+//  * for n0 <= HP_CHUNK^2 partials (L <= 4096 rows) one level of group sums
+//    goes to shared memory and the final level reads it from there.
+// Same tree as before: groups of HP_CHUNK partials summed sequentially from
+// +0, then the group sums sequentially (oracle.grouped_tree_sum).
+constexpr int CMB_D4 = 256;  // widest row (float4) of the shared-memory path
 template <class Epi>
 __global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
+  extern __shared__ __align__(16) float4 s_grp[];  // [HP_CHUNK][D4] group sums
   HP_ENTRY(SP_COMBINE);
   const int D4 = pl.D >> 2;
   const int n_long = pl.counters[C_LONG];
+  const int4 d_first = pl.longs[blockIdx.x];
   float4* partials = reinterpret_cast<float4*>(pl.partials);
+#pragma unroll 1
   for (int li = blockIdx.x; li < n_long; li += gridDim.x) {
-    const int4 d = pl.longs[li];
+    const int4 d = li == (int)blockIdx.x ? d_first : pl.longs[li];
     int n = d.y;
     float4* Pp = partials + (int64_t)d.x * D4;
+    constexpr int PV = CMB_D4 / 256;  // epilogue columns per thread on the fast path
+    typename Epi::Pre pre[PV];
+    const bool fast = n <= HP_CHUNK * HP_CHUNK && D4 <= CMB_D4;
+    if (fast) {
+#pragma unroll
+      for (int v = 0; v < PV; ++v) {
+        const int c4 = threadIdx.x + v * 256;
+        if (c4 < D4 && d.z >= 0) pre[v] = epi.load(d.z, c4);
+      }
+      const int ng = (n + HP_CHUNK - 1) / HP_CHUNK;
+      if (ng > 1) {
+#pragma unroll 1
+        for (int unit = threadIdx.x; unit < ng * D4; unit += blockDim.x) {
+          const int g = unit / D4, c4 = unit - g * D4;
+          const int e = min(HP_CHUNK, n - g * HP_CHUNK);
+          s_grp[g * D4 + c4] = seq_sum_rows(Pp + (int64_t)g * HP_CHUNK * D4 + c4, e, D4);
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int v = 0; v < PV; ++v) {
+        const int c4 = threadIdx.x + v * 256;
+        if (c4 >= D4) continue;
+        float4 acc;
+        if (ng > 1) {
+          acc = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int g = 0; g < ng; ++g) acc = f4_add(acc, s_grp[g * D4 + c4]);
+        } else {
+          acc = seq_sum_rows(Pp + c4, n, D4);
+        }
+        if (d.z >= 0) epi.store(d.z, c4, acc, pre[v]);
+      }
+      __syncthreads();
+      continue;
+    }
+#pragma unroll 1
     while (n > HP_CHUNK) {
       const int ng = (n + HP_CHUNK - 1) / HP_CHUNK;
       const int units = ng * D4;
+#pragma unroll 1
       for (int ub = 0; ub < units; ub += blockDim.x) {
         const int unit = ub + threadIdx.x;
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -253,11 +301,12 @@ __global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
       }
       n = ng;
     }
+#pragma unroll 1
     for (int c4 = threadIdx.x; c4 < D4; c4 += blockDim.x) {
-      typename Epi::Pre pre{};
-      if (d.z >= 0) pre = epi.load(d.z, c4);
+      typename Epi::Pre p{};
+      if (d.z >= 0) p = epi.load(d.z, c4);
       const float4 acc = seq_sum_rows(Pp + c4, n, D4);
-      if (d.z >= 0) epi.store(d.z, c4, acc, pre);
+      if (d.z >= 0) epi.store(d.z, c4, acc, p);
     }
     __syncthreads();
   }
@@ -479,7 +528,14 @@ int launch_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaSt
   // one CTA per long segment (<= T/17); hp_debug_set_combine_blocks caps it for peer epilogues
   const int cblocks = grid_for(pl.T / (HP_CHUNK + 1) + 1, 1,
                                Epi::kRemote && g_combine_blocks > 0 ? g_combine_blocks : sm_count());
-  launch_k(k_combine<Epi>, dim3(cblocks), dim3(256), 0, st, pl, epi);
+  const size_t csmem = (size_t)HP_CHUNK * std::min(D4, CMB_D4) * sizeof(float4);
+  static bool cconf = false;
+  if (!cconf) {
+    HP_CUDA(cudaFuncSetAttribute(k_combine<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)((size_t)HP_CHUNK * CMB_D4 * sizeof(float4))));
+    cconf = true;
+  }
+  launch_k(k_combine<Epi>, dim3(cblocks), dim3(256), csmem, st, pl, epi);
   HP_LAUNCHED(1, "k_combine");
   if constexpr (Epi::kRemote) {
     launch_k(k_publish<Epi>, dim3(1), dim3(64), 0, st, epi);
