@@ -1,0 +1,295 @@
+"""Planner CLI with a device backend.
+
+The reference's command-line pipeline (`sparseplan/cli.py:1-276`) plans,
+costs, simulates and tunes from JSON specs. This module keeps its
+subcommands, flags, report schema (JSON with sorted keys, or CSV) and exit
+codes (0 ok, 1 validation error, 2 usage error), and answers ``simulate``,
+``tune`` and ``compare`` by MEASURING the step on the B200 instead of
+simulating it: synthetic batches shaped from the graph spec run through
+:class:`HybridRunner` (one process per GPU; launch with
+``python -m torch.distributed.run --nproc-per-node N -m paper_1808_02621_b200.cli …``,
+rank 0 prints). ``transform`` is host-only, as in the reference.
+
+Graph specs are read in row form (a sparse Weight: ``elements`` = rows V,
+``elem_bytes`` = 4·D, ``alpha`` = ids per worker per step / V). A spec in the
+reference's element form (``elem_bytes`` 4, ``elements`` = V·D) converts with
+``--row-width D``. Ids are Zipf(1.1) over the rows (frequency-ranked), values
+standard normal; the report says so in ``data``.
+"""
+
+from __future__ import annotations
+
+import argparse
+import csv
+import io
+import json
+import os
+import sys
+
+import numpy as np
+
+from .model import ClusterSpec, GraphSpec, SpecError, VariableSpec, load_cluster_spec, load_graph_spec
+from .placement import plan_to_dict, transform_ar, transform_hybrid, transform_ps, validate_plan
+from .tuning import TuningError, tune_evaluator
+
+_ARCH = ("ar", "hybrid", "ps-naive", "ps-opt")
+
+
+class UsageError(Exception):
+    pass
+
+
+def _parser() -> argparse.ArgumentParser:
+    p = argparse.ArgumentParser(prog="paper_1808_02621_b200.cli",
+                                description="Plan, measure and tune hybrid communication on B200.")
+    sub = p.add_subparsers(dest="command", required=True)
+    for name in ("transform", "simulate", "tune", "compare"):
+        c = sub.add_parser(name)
+        c.add_argument("--graph", required=True)
+        c.add_argument("--cluster", required=True)
+        c.add_argument("--architecture", choices=_ARCH, default="hybrid")
+        c.add_argument("--local-agg", dest="local_agg", action=argparse.BooleanOptionalAction,
+                       default=None)
+        c.add_argument("--partitions", type=int, default=None)
+        c.add_argument("--threshold", type=float, default=0.10)
+        c.add_argument("--seed", type=int, default=0)
+        c.add_argument("--iterations", type=int, default=40)
+        c.add_argument("--output", choices=("json", "csv"), default="json")
+        c.add_argument("--trace", default=None, metavar="PATH")
+        c.add_argument("--row-width", type=int, default=None,
+                       help="convert element-form sparse specs to rows of this width")
+        c.add_argument("--optimizer", choices=("sgd", "adagrad", "adam"), default="adagrad")
+        c.add_argument("--lr", type=float, default=0.1)
+    return p
+
+
+def _load(args) -> tuple[GraphSpec, ClusterSpec]:
+    for path in (args.graph, args.cluster):
+        if not os.path.isfile(path):
+            raise UsageError(f"cannot read {path}")
+    with open(args.graph) as fh:
+        g = json.load(fh)
+    if args.row_width:
+        D = args.row_width
+        for v in g.get("variables", []):
+            if v.get("kind") == "sparse" and v.get("elem_bytes", 4) == 4:
+                v["elements"] = max(1, int(v["elements"]) // D)
+                v["elem_bytes"] = 4 * D
+    graph = load_graph_spec(json.dumps(g))
+    with open(args.cluster) as fh:
+        cluster = load_cluster_spec(fh.read())
+    return graph, cluster
+
+
+def _partitions(graph: GraphSpec, count):
+    if count is None:
+        return None
+    if count < 1:
+        raise SpecError(f"--partitions must be >= 1, got {count}")
+    return {v.name: min(count, v.elements) for v in graph.variables
+            if v.kind == "sparse" and v.partitionable}
+
+
+def _plan(arch: str, graph, cluster, parts, local_agg=None):
+    if arch == "ar":
+        plan = transform_ar(graph, cluster)
+    elif arch in ("ps-naive", "ps-opt"):
+        la = (arch == "ps-opt") if local_agg is None else local_agg
+        plan = transform_ps(graph, cluster, local_agg=la, partitions=parts)
+    else:
+        plan = transform_hybrid(graph, cluster, partitions=parts)
+    problems = validate_plan(plan, graph, cluster)
+    if problems:
+        raise SpecError("invalid plan: " + "; ".join(problems))
+    return plan
+
+
+# ------------------------------------------------------------------ device side
+class _Device:
+    """One process per GPU (torchrun env) or a single GPU."""
+
+    def __init__(self, cluster: ClusterSpec):
+        import torch
+        import torch.distributed as dist
+
+        from .comm import Comm
+
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        if cluster.total_gpus != self.world:
+            raise SpecError(f"cluster has {cluster.total_gpus} GPUs but {self.world} processes run "
+                            "(one box: machines = GPUs, gpus_per_machine = 1)")
+        torch.cuda.set_device(local)
+        self.dev = torch.device("cuda", local)
+        self.comm = None
+        if self.world > 1:
+            dist.init_process_group("nccl", device_id=self.dev)
+            self.comm = Comm.from_torch_distributed()
+
+    def batches(self, graph: GraphSpec, seed: int, count: int = 2) -> list:
+        import torch
+
+        from .synth import zipf_ids
+
+        out = []
+        for i in range(count):
+            rng = np.random.default_rng((seed + i) * 1000 + self.rank)
+            b = {}
+            for v in graph.variables:
+                if v.kind == "sparse":
+                    D = v.elem_bytes // 4
+                    T = max(1, int(round(v.alpha * v.elements)))
+                    ids = zipf_ids(rng, v.elements, T)
+                    vals = rng.standard_normal((T, D), dtype=np.float32)
+                    b[v.name] = (torch.from_numpy(ids).to(self.dev),
+                                 torch.from_numpy(vals).to(self.dev))
+                else:
+                    n = v.elements - v.elements % 4
+                    b[v.name] = torch.from_numpy(
+                        rng.standard_normal(max(n, 4), dtype=np.float32)).to(self.dev)
+            out.append(b)
+        return out
+
+    def close(self):
+        if self.comm is not None:
+            import torch.distributed as dist
+
+            self.comm.close()
+            dist.destroy_process_group()
+
+
+def _runner(dv: _Device, plan, graph, cluster, args):
+    from .ops import OptimizerConfig
+    from .runner import HybridRunner
+
+    return HybridRunner(plan, graph, cluster, rank=dv.rank, world_size=dv.world, comm=dv.comm,
+                        optimizer=OptimizerConfig(args.optimizer, lr=args.lr), device=dv.dev,
+                        seed=args.seed)
+
+
+def _throughput(graph: GraphSpec, cluster: ClusterSpec, t_us: float) -> float:
+    return graph.batch_per_gpu * cluster.total_gpus / (t_us * 1e-6)
+
+
+def _measure(dv, plan, graph, cluster, args) -> tuple:
+    r = _runner(dv, plan, graph, cluster, args)
+    try:
+        bs = dv.batches(graph, args.seed)
+        for b in bs:  # warm-up; the last one is the reported single iteration
+            r.step(b, timed=False)
+        stats = r.step(bs[0], timed=True)
+        mean = r.measure_graphs(bs, args.iterations)
+    finally:
+        r.close()
+    return stats, mean
+
+
+def _cmd_transform(args, graph, cluster, dv) -> dict:
+    return plan_to_dict(_plan(args.architecture, graph, cluster,
+                              _partitions(graph, args.partitions), args.local_agg))
+
+
+def _cmd_simulate(args, graph, cluster, dv) -> dict:
+    plan = _plan(args.architecture, graph, cluster, _partitions(graph, args.partitions),
+                 args.local_agg)
+    stats, mean = _measure(dv, plan, graph, cluster, args)
+    if args.trace and dv.rank == 0:
+        with open(args.trace, "w") as fh:
+            for m in stats.trace:
+                fh.write(json.dumps(m.to_dict(), sort_keys=True) + "\n")
+    return {"architecture": plan.architecture, "iter_time_us": stats.iter_time_us,
+            "mean_iter_time_us": mean, "phase_times_us": stats.phase_times,
+            "per_machine": stats.per_machine_bytes.to_rows(),
+            "throughput_items_per_sec": _throughput(graph, cluster, mean),
+            "backend": "device", "n_gpus": dv.world,
+            "data": "synthetic: Zipf(1.1) ids (alpha*V per worker), normal values"}
+
+
+def _cmd_tune(args, graph, cluster, dv) -> dict:
+    from .ops import OptimizerConfig
+    from .runner import device_evaluator
+
+    cands = [v for v in graph.variables if v.kind == "sparse" and v.partitionable]
+    if not cands:
+        raise SpecError("no partitionable sparse variable to tune")
+    log: list = []
+    ev = device_evaluator(graph, cluster, lambda i: dv.batches(graph, args.seed + 7 * i, 1)[0],
+                          rank=dv.rank, world_size=dv.world, comm=dv.comm,
+                          optimizer=OptimizerConfig(args.optimizer, lr=args.lr),
+                          iterations=args.iterations, log=log, device=dv.dev, seed=args.seed)
+    max_p = min(v.elements for v in cands)
+    res = tune_evaluator(ev, start_p=min(cluster.machines, max_p), threshold=args.threshold,
+                         max_p=max_p)
+    final = ev(res.best_p)
+    doc = res.to_dict()
+    doc.update({"final_mean_iter_time_us": final,
+                "final_throughput_items_per_sec": _throughput(graph, cluster, final),
+                "backend": "device", "n_gpus": dv.world})
+    return doc
+
+
+def _cmd_compare(args, graph, cluster, dv) -> dict:
+    parts = _partitions(graph, args.partitions or cluster.machines)
+    rows = []
+    for arch in ("ar", "ps-naive", "ps-opt", "hybrid"):
+        plan = _plan(arch, graph, cluster, parts)
+        stats, mean = _measure(dv, plan, graph, cluster, args)
+        rows.append({"architecture": plan.architecture, "simulated_time_us": mean,
+                     "measured": True, "bottleneck_bytes": stats.per_machine_bytes.bottleneck_bytes,
+                     "total_bytes": stats.per_machine_bytes.total_bytes,
+                     "throughput_items_per_sec": _throughput(graph, cluster, mean)})
+    return {"graph": graph.name, "rows": rows, "backend": "device", "n_gpus": dv.world}
+
+
+_COMMANDS = {"transform": _cmd_transform, "simulate": _cmd_simulate, "tune": _cmd_tune,
+             "compare": _cmd_compare}
+
+
+def emit_report(report: dict, output: str = "json") -> str:
+    """JSON with sorted keys, or CSV of the report's rows (reference `cli.py:233-254`)."""
+    if output == "csv":
+        rows = report.get("rows") or report.get("per_machine") or [
+            {k: v for k, v in report.items() if not isinstance(v, (list, dict))}]
+        buf = io.StringIO()
+        fields = sorted({k for row in rows for k in row})
+        w = csv.DictWriter(buf, fieldnames=fields)
+        w.writeheader()
+        for row in rows:
+            w.writerow({k: row.get(k) for k in fields})
+        return buf.getvalue()
+    return json.dumps(report, sort_keys=True, indent=2)
+
+
+def run(argv=None) -> int:
+    parser = _parser()
+    try:
+        args = parser.parse_args(argv)
+    except SystemExit as exc:
+        return 2 if exc.code else 0
+    dv = None
+    try:
+        graph, cluster = _load(args)
+        if args.command != "transform":
+            dv = _Device(cluster)
+        report = _COMMANDS[args.command](args, graph, cluster, dv)
+    except UsageError as exc:
+        print(f"error: {exc}", file=sys.stderr)
+        return 2
+    except (SpecError, TuningError) as exc:
+        print(f"error: {exc}", file=sys.stderr)
+        return 1
+    finally:
+        if dv is not None:
+            dv.close()
+    if dv is None or dv.rank == 0:
+        sys.stdout.write(emit_report(report, args.output) + "\n")
+    return 0
+
+
+def main() -> None:
+    raise SystemExit(run())
+
+
+if __name__ == "__main__":
+    main()
