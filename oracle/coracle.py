@@ -46,6 +46,9 @@ def lib():
         L.hpo_dense_mean.restype = None
         L.hpo_dense_mean.argtypes = [vp, C.c_int, i64, f, vp]
         L.hpo_chunk.restype = C.c_int
+        L.hpo_set_threads.restype = C.c_int
+        L.hpo_set_threads.argtypes = [C.c_int]
+        L.hpo_set_threads(os.cpu_count() or 1)  # every host thread (torchrun sets OMP=1)
         assert L.hpo_chunk() == orc.CHUNK, "C and numpy oracles disagree on CHUNK"
         _lib = L
     return _lib
@@ -56,7 +59,7 @@ def _p(a):
 
 
 def threads() -> int:
-    return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return int(lib().hpo_set_threads(0))
 
 
 def sort_dedup_route(ids, vals, total_rows, parts, owner, nranks):

@@ -14,6 +14,9 @@
  * (placement.py:95-97, 185-193) — the owner table is an input here.
  */
 #include <math.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -206,3 +209,15 @@ void hpo_dense_mean(const float* const* grads, int n, int64_t S, float scale, fl
 }
 
 int hpo_chunk(void) { return CHUNK; }
+
+/* Thread count of the OpenMP loops (the bench's CPU arms use every host thread,
+ * also under torchrun, which exports OMP_NUM_THREADS=1). Returns the count set. */
+int hpo_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+  return omp_get_max_threads();
+#else
+  (void)n;
+  return 1;
+#endif
+}

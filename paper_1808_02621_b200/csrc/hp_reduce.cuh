@@ -318,10 +318,10 @@ __global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
 // of this stream made, then the epilogue publishes (flags / counts).
 template <class Epi>
 __global__ void k_publish(Epi epi) {
-  HP_ENTRY(SP_COMBINE);
+  HP_ENTRY(SP_PUBLISH);
   __threadfence_system();
   epi.grid_done();
-  HP_SPAN_END(SP_COMBINE);
+  HP_SPAN_END(SP_PUBLISH);
 }
 
 // ------------------------------------------------------------------ row stream

@@ -132,8 +132,7 @@ struct EpiPush {
       SigView peer(peers.base[o]);
       peer.push_count[L.me] = dest_counts[o];
       peer.push_off[L.me] = off;
-      __threadfence_system();
-      st_release_sys(&peer.push_flag[L.me], e);
+      st_release_sys(&peer.push_flag[L.me], e);  // release: orders this thread's stores above
     }
     __syncthreads();
     if (threadIdx.x == 0) *me.epoch = e;
@@ -713,14 +712,14 @@ k_owner_rows(PeerTable peers, void* my_win, WinLayout L, float4* s0, float4* s1,
 // After k_owner_rows (stream order): one system fence covering every store of
 // the apply, then "applied" at every rank; resets the item counter.
 __global__ void k_applied(PeerTable peers, void* my_win, WinLayout L) {
-  HP_ENTRY(SP_APPLY);
+  HP_ENTRY(SP_APPLIED);
   SigView sig(my_win);
   __threadfence_system();
   const int epoch = *sig.epoch;
   for (int r = threadIdx.x; r < L.n; r += blockDim.x)
     st_release_sys(&SigView(peers.base[r]).applied_flag[L.me], epoch);
   if (threadIdx.x == 0) *sig.own_items = 0;
-  HP_SPAN_END(SP_APPLY);
+  HP_SPAN_END(SP_APPLIED);
 }
 
 // Spin-wait budget (cycles) before a wait gives up and raises an error bit.

@@ -15,7 +15,7 @@ from paper_1808_02621_b200 import _lib
 from paper_1808_02621_b200.synth import WORKLOADS, TableShape, Workload, make_batch
 
 NAMES = ["dedup", "reduce", "combine", "wait_push", "scatter", "apply", "wait_applied", "copy",
-         "ar_scatter", "ar_wait0", "ar_rg", "ar_wait1"]
+         "ar_scatter", "ar_wait0", "ar_rg", "ar_wait1", "publish", "applied"]
 which = sys.argv[1] if len(sys.argv) > 1 else "table"
 pipelined = len(sys.argv) > 2 and sys.argv[2] in ("pipelined", "graph")
 use_graph = len(sys.argv) > 2 and sys.argv[2] == "graph"  # replay the bench's pipelined graphs
@@ -72,7 +72,7 @@ for it in range(8):
 t0s = []
 res = {}
 for v in rows:
-    valid = [(i, v[i, 0], v[i, 1]) for i in range(12) if v[i, 1] > 0]
+    valid = [(i, v[i, 0], v[i, 1]) for i in range(len(NAMES)) if v[i, 1] > 0]
     t0 = min(s for _, s, _ in valid)
     for i, s, e in valid:
         res.setdefault(NAMES[i], []).append(((s - t0) / 1e3, (e - t0) / 1e3))
