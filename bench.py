@@ -75,12 +75,15 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rotations", type=int, default=0, help="distinct resident batches")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--steps-per-graph", type=int, default=2,
+                    help="consecutive steps captured in one CUDA graph (divides the rotation)")
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"])
     ap.add_argument("--dense-exchange", default=None, choices=["p2p", "p2p-sm", "p2p-pipe", "nvls", "nccl"])
-    ap.add_argument("--dense-split", default="auto", choices=["auto", "uniform"],
-                    help="peer-memory dense exchange: reduction share per rank")
+    ap.add_argument("--dense-split", default="auto",
+                    help="peer-memory dense exchange: reduction share per rank "
+                         "('auto', 'uniform' or comma-separated weights)")
     ap.add_argument("--arch", default="hybrid", choices=["hybrid", "ar", "ps"],
                     help="mechanism plan: transform_hybrid (default) / transform_ar / transform_ps")
     ap.add_argument("--knob", action="append", default=[],
@@ -278,7 +281,9 @@ def main():
     opt = hp.OptimizerConfig(**wl.optimizer)
     runner = hp.HybridRunner(plan, graph, cluster, rank=rank, world_size=world, comm=comm,
                              optimizer=opt, device=dev, seed=0, exchange=args.exchange,
-                             dense_exchange=args.dense_exchange, dense_split=args.dense_split)
+                             dense_exchange=args.dense_exchange,
+                             dense_split=(args.dense_split if args.dense_split in ("auto", "uniform")
+                                          else [float(x) for x in args.dense_split.split(",")]))
 
     # resident batches, rotated so their total exceeds 2x L2 (126 MB)
     host = [make_batch(wl, seed=1 + i, rank=rank) for i in range(1)]
@@ -307,14 +312,28 @@ def main():
     # Graph r applies batch r with the plan graph r-1 built, and builds batch r+1's
     # plan on a side stream meanwhile (plans depend only on the ids).
     graphs = runner.capture_pipelined(batches) if use_graph else None
+    G = args.steps_per_graph if graphs and R % max(args.steps_per_graph, 1) == 0 else 1
+    # G > 1: graphs of G consecutive steps (same rotation and plan-slot order as
+    # the single-step graphs), so K steps replay as K // G launches (+ singles)
+    multi = runner.capture_pipelined(batches, steps_per_graph=G) if G > 1 else None
     torch.cuda.synchronize()
+    pos = [0]  # next step's index in the rotation
 
     def run_steps(k):
-        for i in range(k):
-            if graphs:
+        done = 0
+        while done < k:
+            i = pos[0]
+            if multi and i % G == 0 and k - done >= G:
+                multi[(i % R) // G].replay()
+                n = G
+            elif graphs:
                 graphs[i % R].replay()
+                n = 1
             else:
                 runner.step(batches[i % R], timed=False)
+                n = 1
+            pos[0] = (i + n) % R
+            done += n
 
     def barrier():
         if world > 1:
@@ -449,6 +468,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (Zipf(1.1) ids, normal grads, hash-initialised tables)",
             "config": config(args, wl) | {"rotations": R, "cuda_graph": bool(graphs),
+                                          "steps_per_graph": G,
                                           "exchange": runner.exchange,
                                           "dense_exchange": runner.dense_exchange,
                                           "dense_split": runner.dense_weights or "uniform"},

@@ -609,16 +609,23 @@ class HybridRunner:
             self.step(batch, timed=False)
         return g
 
-    def capture_pipelined(self, batches: list) -> list:
-        """One CUDA graph per batch of a rotation: graph r applies batches[r]
-        with the plan built by graph r-1 and builds the plan of batches[r+1].
+    def capture_pipelined(self, batches: list, steps_per_graph: int = 1) -> list:
+        """CUDA graphs over a rotation of batches: graph r applies batches[r]
+        with the plan built by the step before and builds the plan of
+        batches[r+1]. With ``steps_per_graph`` = G > 1 one graph holds G
+        consecutive steps (batches[G·r … G·r+G-1]), so the step boundary inside
+        it is a dependency edge instead of a graph launch.
 
         Replay them in order, repeatedly. ``len(batches)`` must be even (the
-        plan slots alternate). The first plan is built eagerly here.
+        plan slots alternate) and a multiple of G. The first plan is built
+        eagerly here.
         """
         R = len(batches)
+        G = steps_per_graph
         if R < 2 or R % 2:
             raise ValueError("capture_pipelined needs an even number (>= 2) of batches")
+        if G < 1 or R % G:
+            raise ValueError("steps_per_graph must divide the number of batches")
         if self.world_size > 1 and self.exchange != "p2p":
             raise NotImplementedError("the NCCL a2a-v path reads counts on the host")
         # (the AR-sparse / PS-dense baselines are not pipelined: each graph then
@@ -628,10 +635,11 @@ class HybridRunner:
             self.step(batches[r], timed=False, next_batch=batches[(r + 1) % R])
         torch.cuda.synchronize()
         graphs = []
-        for r in range(R):
+        for r in range(0, R, G):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                self.step(batches[r], timed=False, next_batch=batches[(r + 1) % R])
+                for j in range(r, r + G):
+                    self.step(batches[j], timed=False, next_batch=batches[(j + 1) % R])
             graphs.append(g)
         return graphs
 
