@@ -232,8 +232,9 @@ static __device__ __noinline__ float4 seq_sum_rows(const float4* src, int n, int
 // Same tree as before: groups of HP_CHUNK partials summed sequentially from
 // +0, then the group sums sequentially (oracle.grouped_tree_sum).
 constexpr int CMB_D4 = 256;  // widest row (float4) of the shared-memory path
+constexpr int CMB_NT = 512;  // threads per long segment: one pass over <= 4 groups at D = 512
 template <class Epi>
-__global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
+__global__ void __launch_bounds__(CMB_NT) k_combine(DedupPlan pl, Epi epi) {
   extern __shared__ __align__(16) float4 s_grp[];  // [HP_CHUNK][D4] group sums
   HP_ENTRY(SP_COMBINE);
   const int D4 = pl.D >> 2;
@@ -245,13 +246,13 @@ __global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
     const int4 d = li == (int)blockIdx.x ? d_first : pl.longs[li];
     int n = d.y;
     float4* Pp = partials + (int64_t)d.x * D4;
-    constexpr int PV = CMB_D4 / 256;  // epilogue columns per thread on the fast path
+    constexpr int PV = (CMB_D4 + CMB_NT - 1) / CMB_NT;  // epilogue columns per thread (fast path)
     typename Epi::Pre pre[PV];
     const bool fast = n <= HP_CHUNK * HP_CHUNK && D4 <= CMB_D4;
     if (fast) {
 #pragma unroll
       for (int v = 0; v < PV; ++v) {
-        const int c4 = threadIdx.x + v * 256;
+        const int c4 = threadIdx.x + v * CMB_NT;
         if (c4 < D4 && d.z >= 0) pre[v] = epi.load(d.z, c4);
       }
       const int ng = (n + HP_CHUNK - 1) / HP_CHUNK;
@@ -266,7 +267,7 @@ __global__ void __launch_bounds__(256) k_combine(DedupPlan pl, Epi epi) {
       }
 #pragma unroll
       for (int v = 0; v < PV; ++v) {
-        const int c4 = threadIdx.x + v * 256;
+        const int c4 = threadIdx.x + v * CMB_NT;
         if (c4 >= D4) continue;
         float4 acc;
         if (ng > 1) {
@@ -535,7 +536,7 @@ int launch_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaSt
                                  (int)((size_t)HP_CHUNK * CMB_D4 * sizeof(float4))));
     cconf = true;
   }
-  launch_k(k_combine<Epi>, dim3(cblocks), dim3(256), csmem, st, pl, epi);
+  launch_k(k_combine<Epi>, dim3(cblocks), dim3(CMB_NT), csmem, st, pl, epi);
   HP_LAUNCHED(1, "k_combine");
   if constexpr (Epi::kRemote) {
     launch_k(k_publish<Epi>, dim3(1), dim3(64), 0, st, epi);
