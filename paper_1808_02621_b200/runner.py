@@ -209,10 +209,13 @@ class HybridRunner:
         self.step_count = 0
         self.last_counts: dict = {}
         self.kernel_events: dict | None = None
-        # Stream priorities (lower = scheduled first; measured): the
-        # next step's plans (latency-bound cluster sort) first, then the tables'
-        # apply chains, the dense allreduce last. HP_STREAM_PRIO="table,dense,plan".
-        pt, pd, pp = (int(x) for x in os.environ.get("HP_STREAM_PRIO", "-1,0,-2").split(","))
+        # Stream priorities (lower = scheduled first; measured). One
+        # GPU: the next step's plans (latency-bound cluster sort) first, then the
+        # tables' apply chains, the dense scale/cast last. Several GPUs: the dense
+        # exchange (NVLink-bound, on the step's critical path) with the plans,
+        # ahead of the tables. HP_STREAM_PRIO="table,dense,plan" overrides.
+        default_prio = "-1,0,-2" if world_size == 1 else "-1,-2,-2"
+        pt, pd, pp = (int(x) for x in os.environ.get("HP_STREAM_PRIO", default_prio).split(","))
         self._streams = {n: torch.cuda.Stream(device=self.device, priority=pt)
                          for n in self.tables}
         self._dense_stream = torch.cuda.Stream(device=self.device, priority=pd)
