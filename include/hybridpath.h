@@ -262,6 +262,8 @@ int hp_xchg_push(hp_xchg_t x, const int64_t* ids, const float* vals, int64_t T, 
 int hp_xchg_plan(hp_xchg_t x, const int64_t* ids, int64_t T, int64_t V, int32_t P,
                  const int32_t* owner, const int64_t* glob_base, int64_t* send_ids, int32_t* inv,
                  int32_t* dest_counts, int32_t* n_uniq, void* ws, size_t ws_bytes, void* stream);
+/* (hp_xchg_push_plan takes the destinations hp_xchg_plan resolved from its
+ * glob_base; the glob_base argument here is checked for non-NULL only.) */
 int hp_xchg_push_plan(hp_xchg_t x, const float* vals, int64_t T, int64_t V, int32_t P,
                       const int64_t* send_ids, const int32_t* dest_counts,
                       const int64_t* glob_base, void* ws, size_t ws_bytes, void* stream);

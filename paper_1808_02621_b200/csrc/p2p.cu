@@ -95,7 +95,6 @@ struct EpiPush {
   const int32_t* dest_counts;  // [n] rows this rank sends to each owner
   const int64_t* send_ids;     // [U] (send order)
   const int4* info;            // [U] {inbox index, owner, slab row, 0}
-  int* done;                   // last-block counter (own window)
   void* my_win;
   struct Pre {
     int4 inf;
@@ -849,9 +848,8 @@ int hp_xchg_push_plan(hp_xchg_t x, const float* vals, int64_t T, int64_t V, int3
   int rc = carve_plan(&pl, ws, ws_bytes, T, x->L.D4 * 4, V, P, x->L.n);
   if (rc) return rc;
   restore_sorted_pos(pl);
-  SigView me(x->win);
-  EpiPush epi{x->peers, x->L, dest_counts, send_ids, pl.send_info, me.done + 0, x->win};
-  pl.T = std::max<int64_t>(T, 1);  // k_combine must run: it carries the publication
+  EpiPush epi{x->peers, x->L, dest_counts, send_ids, pl.send_info, x->win};
+  pl.T = std::max<int64_t>(T, 1);  // launch even for T == 0: k_publish carries the publication
   return launch_reduce(pl, vals, epi, static_cast<cudaStream_t>(stream));
 }
 

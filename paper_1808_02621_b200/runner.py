@@ -137,10 +137,11 @@ class HybridRunner:
             raise ValueError("exchange must be 'p2p' (NVLink peer memory) or 'nccl'")
         self.exchange = exchange if world_size > 1 else "local"
         # dense allreduce: peer-memory kernel (deterministic, scale/cast fused) or NCCL
-        # default K7 transport by measurement: SM-store peer exchange
-        # (bit-exact rank-order sum); from 4 ranks its reduction split keeps the
-        # hot sparse partitions' owners out of the reduce/gather (dense_split)
-        default_dense = "p2p-sm" if exchange == "p2p" else exchange
+        # default K7 transport by measurement: two ranks -> NCCL
+        # (138 vs 146 us with the dense stream prioritised); from 4 ranks the
+        # SM-store peer exchange (bit-exact rank-order sum) whose reduction split
+        # keeps the hot sparse partitions' owners out of the reduce/gather
+        default_dense = ("nccl" if world_size == 2 else "p2p-sm") if exchange == "p2p" else exchange
         self.dense_exchange = (dense_exchange or default_dense) if world_size > 1 else "local"
         if self.dense_exchange not in ("p2p", "p2p-sm", "p2p-pipe", "nvls", "nccl", "local"):
             raise ValueError("dense_exchange must be 'p2p' (copy engines), 'p2p-sm', "

@@ -312,5 +312,21 @@ def test_runner_pipelined_and_graphs_match_oracle(cuda, opt):
             graphs[r].replay()
             torch.cuda.synchronize()
             check(r)
+    # two steps per graph (the bench default), interleaved with the single-step graphs
+    multi = runner.capture_pipelined(dev, steps_per_graph=2)  # eager warm-up: batch 0, 1
+    torch.cuda.synchronize()
+    for r in (0, 1):
+        advance(r)
+    for rep in range(2):
+        multi[0].replay()
+        torch.cuda.synchronize()
+        advance(0)
+        check(1)
+    graphs[0].replay()
+    torch.cuda.synchronize()
+    check(0)
+    graphs[1].replay()
+    torch.cuda.synchronize()
+    check(1)
     for t in wl.tables:
         assert np.array_equal(runner.tables[t.name].w.cpu().numpy(), states[t.name]["w"])
