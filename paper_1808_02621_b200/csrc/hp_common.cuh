@@ -92,6 +92,10 @@ struct Router {
   int64_t q, e, split;  // split = e * (q + 1)
   __host__ __device__ Router(int64_t V, int32_t P) : q(V / P), e(V % P), split((V % P) * (V / P + 1)) {}
   __device__ __forceinline__ int part(int64_t r) const {
+    if (r >= 0 && r <= 0x7fffffff) {  // every in-range row (V < 2^31): 32-bit divisions
+      const uint32_t u = (uint32_t)r, sp = (uint32_t)split;
+      return u < sp ? (int)(u / (uint32_t)(q + 1)) : (int)(e + (u - sp) / (uint32_t)q);
+    }
     return r < split ? (int)(r / (q + 1)) : (int)(e + (r - split) / q);
   }
   __device__ __forceinline__ int64_t lo(int p) const {
