@@ -408,6 +408,40 @@ def main():
             roof["gather"] = {"launch_us": kern[gk], "algorithmic_bytes": g_algo,
                               "achieved": g_algo / (kern[gk] * 1e-6) / 1e9}
 
+    # ---- N > 1: NVLink roofline of K7 (the dense exchange, the step's critical
+    # path), timed alone with events: every rank starts together (barrier + a
+    # queued sleep), max over ranks, median of 10. Bytes = the most any rank
+    # must send over NVLink for the transport and split in use.
+    if world > 1 and wl.dense and not runner.dense_ps:
+        S = sum(v.elements for v in runner.dense) * 4
+        w = runner.dense_weights or [1.0] * world
+        if runner.dense_exchange in ("p2p", "p2p-sm", "p2p-pipe"):
+            c = [x / sum(w) * S for x in w]
+            egress = max((S - c[r]) + (world - 1) * c[r] for r in range(world))
+            how = "max over ranks of (S - chunk_r) + (n-1) chunk_r"
+        else:
+            egress = 2.0 * (world - 1) / world * S
+            how = "ring-equivalent bus bytes 2(n-1)/n S"
+        ts = []
+        for i in range(10):
+            barrier()
+            torch.cuda._sleep(2_000_000)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            runner._dense(batches[i % R])
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(max_over_ranks(a.elapsed_time(b) * 1e3))
+        us = float(np.median(ts))
+        nvl_peak = 770.0
+        achieved = egress / (us * 1e-6) / 1e9
+        roof = {"kernel": f"K7 dense exchange ({runner.dense_exchange}, split {w})",
+                "bound": "nvlink", "achieved": achieved, "peak": nvl_peak, "unit": "GB/s",
+                "frac": achieved / nvl_peak, "traffic": None, "algorithmic_bytes": egress,
+                "bytes_rule": how, "launch_us": us,
+                "peak_src": "fallback: measured peer copy 770 GB/s per direction (B200_PROFILING.md)",
+                "step_share": us / (t_dev / args.steps * 1e6)}
+
     # ---- e2e through the public API: pinned host inputs -> step -> result to host
     pinned = []
     for b in host:
