@@ -78,11 +78,22 @@ def main():
         return {k: ((torch.from_numpy(v[0]).to(dev), torch.from_numpy(v[1]).to(dev))
                     if isinstance(v, tuple) else torch.from_numpy(v).to(dev)) for k, v in b.items()}
 
-    staged = {s: to_dev(make_batch(wl, seed=s, rank=rank)) for s in (1, 2, 3)}
+    empty = os.environ.get("HP_CHECK_EMPTY") == "1"
+
+    def batch_of(step, r):
+        """Seeded batch of rank r; with HP_CHECK_EMPTY=1 the last rank sends no
+        embedding ids at step 2 (an empty IndexedSlices through the exchange)."""
+        b = make_batch(wl, seed=step, rank=r)
+        if empty and step == 2 and r == world - 1:
+            ids, vals = b["embedding"]
+            b["embedding"] = (ids[:0].copy(), vals[:0].copy())
+        return b
+
+    staged = {s: to_dev(batch_of(s, rank)) for s in (1, 2, 3)}
     if xmode == "p2p":
         runner.prefetch(staged[1])  # steps 1-3 run pipelined (plan of step s+1 built during s)
     for step in (1, 2, 3):
-        batches = [make_batch(wl, seed=step, rank=r) for r in range(world)]
+        batches = [batch_of(step, r) for r in range(world)]
         mine = batches[rank]
         batch = staged[step]
         stats = runner.step(batch, next_batch=staged.get(step + 1) if xmode == "p2p" else None)
@@ -124,7 +135,7 @@ def main():
         # the same step replayed from a CUDA graph must give the same bytes
         if ok:
             step = 4
-            batches = [make_batch(wl, seed=step, rank=r) for r in range(world)]
+            batches = [batch_of(step, r) for r in range(world)]
             mine = batches[rank]
             static = {k: ((torch.from_numpy(v[0]).to(dev), torch.from_numpy(v[1]).to(dev))
                           if isinstance(v, tuple) else torch.from_numpy(v).to(dev))

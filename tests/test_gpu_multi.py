@@ -22,6 +22,8 @@ def _ngpu():
     ("adagrad", "p2p", "p2p", "", "hybrid"),
     # weighted reduction split (rank 0 takes no chunk), SM stores and copy engines
     ("adagrad", "p2p", "p2p-sm", "split=first0", "hybrid"),
+    # the last rank pushes an empty IndexedSlices for one table at step 2
+    ("sgd", "p2p", "nccl", "empty=1", "hybrid"),
     ("sgd", "p2p", "p2p", "split=first0", "hybrid"),
     ("adam", "p2p", "nccl", "", "hybrid"),
     ("adagrad", "p2p", "nvls", "", "hybrid"),
@@ -36,11 +38,14 @@ def test_multi_gpu_step_matches_oracle(opt, xchg, dense, knobs, arch):
     n = min(_ngpu(), 8)
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
-    split = "auto"
+    split, empty = "auto", "0"
     if knobs.startswith("split="):
         split, knobs = knobs.split("=", 1)[1], ""
+    if knobs.startswith("empty="):
+        empty, knobs = knobs.split("=", 1)[1], ""
     env = dict(os.environ, HP_CHECK_OPT=opt, HP_CHECK_XCHG=xchg, HP_CHECK_DENSE=dense,
                HP_CHECK_KNOBS=knobs, HP_CHECK_ARCH=arch, HP_CHECK_SPLIT=split,
+               HP_CHECK_EMPTY=empty,
                # the pipelined dense exchange cuts each chunk into 64 KB pieces: many of them
                HP_CHECK_DENSE_ELEMS="1000004" if dense == "p2p-pipe" else "50000")
     import socket
