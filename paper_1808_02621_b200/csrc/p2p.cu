@@ -966,11 +966,12 @@ int hp_xchg_merge_apply(hp_xchg_t x, hp_slab slab, hp_optim opt, int32_t wait, v
 // Worker: wait for every owner's apply, then out[t] = returned row of send slot inv[t].
 int hp_xchg_stitch(hp_xchg_t x, const int32_t* inv, int64_t T, float* out, int32_t wait,
                    void* stream) {
-  HP_REQUIRE(x && inv && out, "NULL argument");
-  if (wait) {
+  HP_REQUIRE(x && (T == 0 || (inv && out)), "NULL argument");
+  if (wait) {  // also with no ids: the next push must follow every owner's apply
     int rc = hp_xchg_wait(x, 1, stream);
     if (rc) return rc;
   }
+  if (T == 0) return HP_OK;
   const float* ret = reinterpret_cast<const float*>(static_cast<char*>(x->win) + x->L.ret_off);
   return hp_stitch(ret, inv, T, x->L.D4 * 4, out, stream);
 }
