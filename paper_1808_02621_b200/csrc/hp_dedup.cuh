@@ -57,13 +57,14 @@ constexpr int HP_RS_MAX_WARPS = 4096;
 // row stream does not handle this width) and warps per plan.
 int rs_stages(int32_t D);
 int rs_warps(int32_t D);
-extern int g_rowstream_off;
-extern int g_rs_ctas;
-extern int g_owner_stream;
-extern int g_combine_blocks;
-extern int g_dar_blocks;
-extern int g_owner_waves;  // peer-store kernels: many waves (1) or one resident wave (0)  // HP_DAR_PIPE grid (hp_debug_set_dar_blocks)
-extern int g_reduce_b;  // k_reduce rows in flight at VPT=2 (A/B: 2, 4, 8)  // k_combine grid for peer-store epilogues (hp_debug_set_combine_blocks)  // p2p owner apply as a row stream (hp_debug_set_owner_stream)  // row-stream CTAs per SM cap (hp_debug_set_rs_ctas)  // hp_debug_set_rowstream(0): use k_reduce (A/B instrumentation)
+// Instrumentation / A-B switches (hp_debug_set_*; defaults in dedup.cu):
+extern int g_rowstream_off;   // 1: level 0 runs k_reduce, 0: k_rowstream
+extern int g_rs_ctas;         // row-stream CTAs per SM cap
+extern int g_owner_stream;    // p2p owner merge: 0 k_owner_apply, 1 k_owner_stream, 2 scan + rows
+extern int g_combine_blocks;  // k_combine grid cap for peer-store epilogues (0: SM count)
+extern int g_dar_blocks;      // HP_DAR_PIPE grid (0: one block per SM)
+extern int g_owner_waves;     // peer-store kernels: many waves (1) or one resident wave (0)
+extern int g_reduce_b;        // k_reduce rows in flight at VPT=2 (2, 4, 8)
 
 size_t dedup_ws_bytes(int64_t T, int32_t D, int32_t P);
 int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, int64_t V,
