@@ -407,6 +407,20 @@ def main():
             g_algo = T * 8 + U * 4 * big.D + T * 4 * big.D
             roof["gather"] = {"launch_us": kern[gk], "algorithmic_bytes": g_algo,
                               "achieved": g_algo / (kern[gk] * 1e-6) / 1e9}
+        # the whole step against HBM: every kernel's algorithmic bytes once
+        # (K4 + K5 per table, dense scale/cast in + out; dedup is < 1%)
+        step_bytes = 2.0 * sum(wl.dense.values()) * 4
+        for t in wl.tables:
+            tb = runner.tables[t.name]
+            Tt = t.T + t.sampled
+            ops.apply_plan_build(batches[0][t.name][0], tb.slab(), tb.ws)
+            Ut = int(tb.ws.buf[:4].view(torch.int32).item())
+            step_bytes += Tt * (4 + 4 * t.D) + Ut * (4 + 4 * t.D * 2 * k)
+            step_bytes += Tt * 8 + Ut * 4 * t.D + Tt * 4 * t.D
+        step_us = t_dev / args.steps * 1e6
+        roof["step"] = {"algorithmic_bytes": step_bytes, "us": step_us,
+                        "achieved": step_bytes / (step_us * 1e-6) / 1e9,
+                        "frac": step_bytes / (step_us * 1e-6) / 1e9 / pk["hbm_gbs"]}
 
     # ---- N > 1: NVLink roofline of K7 (the dense exchange, the step's critical
     # path), timed alone with events: every rank starts together (barrier + a
