@@ -216,8 +216,14 @@ class HybridRunner:
         # exchange (NVLink-bound, on the step's critical path) with the plans,
         # ahead of the tables. HP_STREAM_PRIO="table,dense,plan" overrides.
         default_prio = "-1,0,-2" if world_size == 1 else "-1,-2,-2"
-        pt, pd, pp = (int(x) for x in os.environ.get("HP_STREAM_PRIO", default_prio).split(","))
-        self._streams = {n: torch.cuda.Stream(device=self.device, priority=pt)
+        prio = [int(x) for x in os.environ.get("HP_STREAM_PRIO", default_prio).split(",")]
+        pt, pd, pp = prio[:3]
+        pbig = prio[3] if len(prio) > 3 else pt  # optional: the largest table's chain
+        big = max(self.tables.values(), default=None,  # most rows touched per step
+                  key=lambda t: graph.variable(t.name).touched_elements * t.D)
+        self._streams = {n: torch.cuda.Stream(device=self.device,
+                                              priority=pbig if big is not None and n == big.name
+                                              else pt)
                          for n in self.tables}
         self._dense_stream = torch.cuda.Stream(device=self.device, priority=pd)
         self._plan_streams = {n: torch.cuda.Stream(device=self.device, priority=pp)
