@@ -86,6 +86,9 @@ def parse():
                          "('auto', 'uniform' or comma-separated weights)")
     ap.add_argument("--arch", default="hybrid", choices=["hybrid", "ar", "ps"],
                     help="mechanism plan: transform_hybrid (default) / transform_ar / transform_ps")
+    ap.add_argument("--check", action="store_true",
+                    help="N=1: before timing, run the bench's own pipelined-graph path on its "
+                         "workload against the C oracle (oracle/check.py), bit-exact")
     ap.add_argument("--knob", action="append", default=[],
                     help="instrumentation A/B: NAME=INT calls hp_debug_set_NAME(INT)")
     return ap.parse_args()
@@ -205,8 +208,6 @@ def run_reference(args, wl):
     if rank != 0:
         return
     n = args.gpus
-    for _ in range(max(args.warmup, 0) and 1):
-        pass
     _, dt = time_cpu(wl, n, max(args.steps, 1), seed=0)
     from paper_1808_02621_b200.synth import make_batch
 
@@ -301,6 +302,13 @@ def main():
     batches = [to_dev(b) for b in host]
     use_graph = (world == 1 or args.exchange == "p2p") and not args.no_graph
     stream = torch.cuda.current_stream()
+    check = None
+    if args.check and world == 1:  # parity of this exact config, before (not in) the timing
+        from oracle.check import check_runner_n1
+
+        G0 = args.steps_per_graph if R % max(args.steps_per_graph, 1) == 0 else 1
+        check = check_runner_n1(runner, wl, host, batches, steps_per_graph=G0, replays=1)
+        check = {"ok": True, "vs": "C oracle (oracle/check.py), bit-exact"} | check
 
     for i in range(args.warmup):
         runner.step(batches[i % R], timed=False)
@@ -408,8 +416,9 @@ def main():
             roof["gather"] = {"launch_us": kern[gk], "algorithmic_bytes": g_algo,
                               "achieved": g_algo / (kern[gk] * 1e-6) / 1e9}
         # the whole step against HBM: every kernel's algorithmic bytes once
-        # (K4 + K5 per table, dense scale/cast in + out; dedup is < 1%)
-        step_bytes = 2.0 * sum(wl.dense.values()) * 4
+        # (K4 + K5 per table, + the dense scale/cast in + out only when it runs:
+        # at n = 1 with fp32 'mean' K7 is a no-op and launches nothing; dedup < 1%)
+        step_bytes = 0.0 if runner.dense_is_noop() else 2.0 * sum(wl.dense.values()) * 4
         for t in wl.tables:
             tb = runner.tables[t.name]
             Tt = t.T + t.sampled
@@ -527,10 +536,13 @@ def main():
             "roofline": roof, "kernels_us": kern, "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }
+        if check is not None:
+            line["parity_check"] = check
         print(json.dumps(line), flush=True)
     # release captured graphs (they reference NCCL and peer windows) before teardown
     graphs = e2e_graph = None
     torch.cuda.synchronize()
+    runner.check_errors(sync=True)  # any device error bit of the run raises here
     if world > 1:
         errs = runner.exchange_status()
         if any(errs.values()):

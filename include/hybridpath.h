@@ -110,6 +110,26 @@ void hp_debug_set_dar_blocks(int n);
 void hp_debug_set_owner_waves(int on);
 /* Instrumentation: k_reduce rows in flight per thread at 2 float4 columns (2 = default, 4, 8). */
 void hp_debug_set_reduce_b(int b);
+/* Spin-wait budget (clock cycles) of every exchange wait before it gives up and
+ * raises an error bit; <= 0 restores the default (HP_WAIT_TIMEOUT_CYCLES or ~2 s). */
+void hp_debug_set_wait_timeout(long long cycles);
+
+/* ---------------------------------------------------------------- asynchronous errors
+ * Device-side failures (an id outside [0, V), a row not homed here, an exchange
+ * wait that timed out) raise bits in device error words; nothing on the hot path
+ * synchronises to read them. hp_err_collect ORs up to 8 such words (each shifted
+ * left by shifts[i]) into a pinned, device-mapped host word with one 1-thread
+ * kernel on the caller's stream (graph-capturable); the caller reads the host word
+ * whenever it likes (HybridRunner: at the next step) and raises.
+ * Replaces: nothing in the reference (it has no data path); TF1's SparseApply*
+ * rejects out-of-range indices, which is the behaviour restored here. */
+int hp_err_host_alloc(int32_t n, int32_t** host_out, int32_t** dev_out);
+int hp_err_host_free(int32_t* host);
+int hp_err_collect(const int32_t* const* words, const int32_t* shifts, int32_t n,
+                   int32_t* dev_word, void* stream);
+/* Device address of a dedup plan's error word (bit 0: id outside [0, V), dropped;
+ * bit 1: row not homed on this rank). */
+int hp_plan_err_ptr(const void* ws, const int32_t** out);
 
 /* ---------------------------------------------------------------- K1 + K2
  * Sort + dedup + route of one worker's IndexedSlices.
@@ -120,6 +140,8 @@ void hp_debug_set_reduce_b(int b);
  * (ascending (owner[p(id)], id)), counts int32[U] multiplicity,
  * inv int32[T] send slot per position, dest_counts int32[nranks],
  * n_uniq int32[1]. Capacity: U <= T.
+ * Ids outside [0, V) are dropped (never clamped onto a row): no slot, inv = -1,
+ * error bit 0 of the plan (hp_plan_status / hp_plan_err_ptr).
  */
 size_t hp_dedup_ws_bytes(int64_t T, int32_t D, int32_t P, int32_t nranks);
 int hp_sort_dedup_route(const int64_t* ids, const float* vals, int64_t T, int32_t D,
@@ -170,13 +192,15 @@ int hp_apply_plan(const float* rows, int64_t R, hp_slab slab, hp_optim opt, void
                   size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------- K5 / K6
- * Gather: out[i] = slab row of global id ids[i], i < n (coalesced row copy).
+ * Gather: out[i] = slab row of global id ids[i], i < n (coalesced row copy); a
+ * zero row for an id outside [0, V) or not homed on this rank.
  * Replaces: PS pull (`simulate.py:195-199`).
  * n_dev (nullable) = device count bounding i (rows i >= *n_dev are skipped). */
 int hp_gather_rows(hp_slab slab, const int64_t* ids, int64_t n, const int32_t* n_dev,
                    float* out, void* stream);
 
-/* Stitch: out[t] = rows[inv[t]] (t < T). Replaces the partition stitch
+/* Stitch: out[t] = rows[inv[t]] (t < T); inv[t] = -1 (a dropped id) gives a zero row.
+ * Replaces the partition stitch
  * (`PAPER.md:473`, `simulate.py:317-323` "stitch" term). */
 int hp_stitch(const float* rows, const int32_t* inv, int64_t T, int32_t D, float* out,
               void* stream);
@@ -242,7 +266,9 @@ int hp_exchange_pull(hp_comm_t comm, const float* owner_rows, const int32_t* own
 typedef struct hp_xchg_s* hp_xchg_t;
 size_t hp_xchg_window_bytes(int32_t n, int32_t D, int64_t cap, int64_t rows_cap);
 /* Allocates this rank's window (slab of rows_cap x D fp32 + inboxes for n
- * sources x cap rows); returns the 64-byte cudaIpc handle and the slab pointer. */
+ * sources x cap rows); returns the 64-byte cudaIpc handle and the slab pointer.
+ * (n, D, cap, rows_cap) must be IDENTICAL on every rank: a rank addresses its
+ * peers' inboxes with its own layout, so size rows_cap for the largest slab. */
 int hp_xchg_create(hp_xchg_t* out, int32_t n, int32_t me, int32_t D, int64_t cap,
                    int64_t rows_cap, void* ipc_handle_out, void** w_out);
 int hp_xchg_open_peer(hp_xchg_t x, int32_t rank, const void* ipc_handle);
@@ -280,8 +306,17 @@ int hp_xchg_stitch(hp_xchg_t x, const int32_t* inv, int64_t T, float* out, int32
 int hp_xchg_debug_sig(hp_xchg_t x, int32_t* host_out, void* stream);
 /* Rows received from each source in the last push -> device int32[n] (async). */
 int hp_xchg_recv_counts(hp_xchg_t x, int32_t* out_dev, void* stream);
-/* Error bits (4/8: a wait timed out, 16: a received id is not homed here). */
+/* Error bits (4/8: a wait timed out, 16: a received id is not homed here). After a
+ * push wait timed out (4) the owner merges nothing: partially written inboxes are
+ * never applied. */
 int hp_xchg_status(hp_xchg_t x, int32_t* out_err, void* stream);
+/* Device address of the exchange's error word (for hp_err_collect). */
+int hp_xchg_err_ptr(hp_xchg_t x, const int32_t** out);
+/* Single-process emulation of n ranks (parity tests on ONE GPU): instead of
+ * cudaIpc handles, peers are set from the raw window addresses of the other
+ * emulated ranks' exchanges in this process. Same kernels and protocol. */
+int hp_xchg_window_ptr(hp_xchg_t x, void** out);
+int hp_xchg_set_peer_ptr(hp_xchg_t x, int32_t rank, void* window);
 
 /* ---------------------------------------------------------------- K7 over NVLink
  * Dense allreduce fused with scale + cast, over peer memory: every rank stores
@@ -320,6 +355,10 @@ int hp_nvls_allreduce(const float* mc_in, void* mc_out, int64_t S, int32_t n, in
                       int32_t out_dtype, float scale, int32_t* const* pads_dev, int32_t* state_dev,
                       void* stream);
 int hp_dar_status(hp_dar_t d, int32_t* out_err, void* stream);
+int hp_dar_err_ptr(hp_dar_t d, const int32_t** out);
+/* Single-process emulation (see hp_xchg_set_peer_ptr). */
+int hp_dar_window_ptr(hp_dar_t d, void** out);
+int hp_dar_set_peer_ptr(hp_dar_t d, int32_t rank, void* window);
 /* Instrumentation: raw peer throughput over the dense window (mode 0/2 store,
  * 1/3 load; 2/3 with 4 x 16 B in flight per thread). */
 int hp_debug_nvlink_bench(hp_dar_t d, int32_t peer, int32_t mode, int32_t blocks, void* stream);

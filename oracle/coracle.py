@@ -42,7 +42,7 @@ def lib():
         L.hpo_merge_apply.argtypes = [vp, vp, i64, C.c_int, C.c_int, vp, vp, vp,
                                       f, f, f, f, f, f, f, f]
         L.hpo_gather.restype = None
-        L.hpo_gather.argtypes = [vp, vp, i64, C.c_int, vp]
+        L.hpo_gather.argtypes = [vp, i64, vp, i64, C.c_int, vp]
         L.hpo_dense_mean.restype = None
         L.hpo_dense_mean.argtypes = [vp, C.c_int, i64, f, vp]
         L.hpo_chunk.restype = C.c_int
@@ -100,7 +100,7 @@ def merge_apply(opt, state, ids, rows, hp, step, scale):
 def gather(w, ids):
     ids = np.ascontiguousarray(ids, dtype=np.int64)
     out = np.empty((len(ids), w.shape[1]), F32)
-    lib().hpo_gather(_p(w), _p(ids), len(ids), w.shape[1], _p(out))
+    lib().hpo_gather(_p(w), w.shape[0], _p(ids), len(ids), w.shape[1], _p(out))
     return out
 
 

@@ -84,13 +84,17 @@ static int64_t part_of(int64_t r, int64_t V, int32_t P) {
 
 /* Group ids stably; return U and fill uniq[U], start[U+1], order[T] (positions
  * sorted by (id, pos)). Arrays are caller-allocated with capacity T (+1). */
-static int64_t group_ids(const int64_t* ids, int64_t T, int64_t* uniq, int64_t* start,
+static int64_t group_ids(const int64_t* ids, int64_t T, int64_t V, int64_t* uniq, int64_t* start,
                          int64_t* order) {
   kv_t* kv = (kv_t*)malloc(sizeof(kv_t) * (T > 0 ? T : 1));
+  int64_t nv = 0; /* out-of-range ids are dropped (oracle.valid_ids) */
   for (int64_t i = 0; i < T; ++i) {
-    kv[i].id = ids[i];
-    kv[i].pos = i;
+    if (ids[i] < 0 || ids[i] >= V) continue;
+    kv[nv].id = ids[i];
+    kv[nv].pos = i;
+    ++nv;
   }
+  T = nv;
   qsort(kv, (size_t)T, sizeof(kv_t), cmp_kv);
   int64_t U = 0;
   for (int64_t i = 0; i < T; ++i) {
@@ -114,7 +118,8 @@ int64_t hpo_sort_dedup_route(const int64_t* ids, const float* vals, int64_t T, i
   int64_t* uniq = (int64_t*)malloc(sizeof(int64_t) * (T + 1));
   int64_t* start = (int64_t*)malloc(sizeof(int64_t) * (T + 2));
   int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (T + 1));
-  const int64_t U = group_ids(ids, T, uniq, start, order);
+  const int64_t U = group_ids(ids, T, V, uniq, start, order);
+  for (int64_t t = 0; t < T; ++t) inv[t] = -1;
   /* send slots: stable by owner, ids ascending within an owner */
   int64_t* slot = (int64_t*)malloc(sizeof(int64_t) * (U + 1));
   for (int r = 0; r < n; ++r) dest_counts[r] = 0;
@@ -170,7 +175,7 @@ int64_t hpo_merge_apply(const int64_t* ids, const float* rows, int64_t R, int D,
   int64_t* uniq = (int64_t*)malloc(sizeof(int64_t) * (R + 1));
   int64_t* start = (int64_t*)malloc(sizeof(int64_t) * (R + 2));
   int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (R + 1));
-  const int64_t U = group_ids(ids, R, uniq, start, order);
+  const int64_t U = group_ids(ids, R, INT64_MAX, uniq, start, order); /* owner ids are valid */
 #pragma omp parallel
   {
     float* g = (float*)malloc(sizeof(float) * D);
@@ -192,10 +197,16 @@ int64_t hpo_merge_apply(const int64_t* ids, const float* rows, int64_t R, int D,
   return U;
 }
 
-/* out[t] = w[ids[t]] (pull + stitch on a full table). */
-void hpo_gather(const float* w, const int64_t* ids, int64_t T, int D, float* out) {
+/* out[t] = w[ids[t]] (pull + stitch on a full table of V rows); a zero row for
+ * a dropped (out-of-range) id (oracle.pull_rows). */
+void hpo_gather(const float* w, int64_t V, const int64_t* ids, int64_t T, int D, float* out) {
 #pragma omp parallel for schedule(static)
-  for (int64_t t = 0; t < T; ++t) memcpy(out + t * (int64_t)D, w + ids[t] * (int64_t)D, sizeof(float) * D);
+  for (int64_t t = 0; t < T; ++t) {
+    if (ids[t] < 0 || ids[t] >= V)
+      memset(out + t * (int64_t)D, 0, sizeof(float) * D);
+    else
+      memcpy(out + t * (int64_t)D, w + ids[t] * (int64_t)D, sizeof(float) * D);
+  }
 }
 
 /* out = sum over k of grads[k] (sequential in rank order, fp32) * scale. */

@@ -37,7 +37,8 @@ from .placement import (
     transform_ps,
     validate_plan,
 )
-from .stats import IterationStats, Message, TransferReport
+from .stats import ComputeProfile, IterationStats, Message, TransferReport
+from .transfer import payload_transfer, transfer_model
 from .tuning import (
     CostModelParams,
     TuneResult,
@@ -56,6 +57,7 @@ _LAZY = {
     "HybridRunner": ("runner", "HybridRunner"),
     "ShardedTable": ("runner", "ShardedTable"),
     "device_evaluator": ("runner", "device_evaluator"),
+    "simulate_training": ("runner", "simulate_training"),
     "OptimizerConfig": ("ops", "OptimizerConfig"),
     "Comm": ("comm", "Comm"),
 }

@@ -99,6 +99,17 @@ SIGNATURES = {
     "hp_debug_nvlink_bench": (C.c_int, [vp, i32, i32, i32, vp]),
     "hp_debug_fence_bench": (C.c_int, [vp, i32, i32, i32, i32, vp]),
     "hp_xchg_debug_sig": (C.c_int, [vp, vp, vp]),
+    "hp_debug_set_wait_timeout": (None, [C.c_longlong]),
+    "hp_err_host_alloc": (C.c_int, [i32, C.POINTER(vp), C.POINTER(vp)]),
+    "hp_err_host_free": (C.c_int, [vp]),
+    "hp_err_collect": (C.c_int, [vp, vp, i32, vp, vp]),
+    "hp_plan_err_ptr": (C.c_int, [vp, C.POINTER(vp)]),
+    "hp_xchg_err_ptr": (C.c_int, [vp, C.POINTER(vp)]),
+    "hp_xchg_window_ptr": (C.c_int, [vp, C.POINTER(vp)]),
+    "hp_xchg_set_peer_ptr": (C.c_int, [vp, i32, vp]),
+    "hp_dar_err_ptr": (C.c_int, [vp, C.POINTER(vp)]),
+    "hp_dar_window_ptr": (C.c_int, [vp, C.POINTER(vp)]),
+    "hp_dar_set_peer_ptr": (C.c_int, [vp, i32, vp]),
 }
 
 _lib = None

@@ -128,28 +128,9 @@ class _Device:
             self.comm = Comm.from_torch_distributed()
 
     def batches(self, graph: GraphSpec, seed: int, count: int = 2) -> list:
-        import torch
+        from .synth import graph_batches
 
-        from .synth import zipf_ids
-
-        out = []
-        for i in range(count):
-            rng = np.random.default_rng((seed + i) * 1000 + self.rank)
-            b = {}
-            for v in graph.variables:
-                if v.kind == "sparse":
-                    D = v.elem_bytes // 4
-                    T = max(1, int(round(v.alpha * v.elements)))
-                    ids = zipf_ids(rng, v.elements, T)
-                    vals = rng.standard_normal((T, D), dtype=np.float32)
-                    b[v.name] = (torch.from_numpy(ids).to(self.dev),
-                                 torch.from_numpy(vals).to(self.dev))
-                else:
-                    n = v.elements - v.elements % 4
-                    b[v.name] = torch.from_numpy(
-                        rng.standard_normal(max(n, 4), dtype=np.float32)).to(self.dev)
-            out.append(b)
-        return out
+        return graph_batches(graph, seed, self.rank, count, self.dev)
 
     def close(self):
         if self.comm is not None:

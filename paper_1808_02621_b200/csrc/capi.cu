@@ -2,7 +2,9 @@
 #include <atomic>
 #include <string>
 
-#include "hp_common.cuh"
+#include <cstring>
+
+#include "hp_dedup.cuh"
 
 namespace hp {
 
@@ -20,6 +22,7 @@ extern int g_combine_blocks;
 extern int g_dar_blocks;
 extern int g_owner_waves;
 extern int g_reduce_b;
+extern long long g_wait_cycles;
 int g_pdl = 0;  // PDL measured neutral at N=1, slower at N=2
 
 static thread_local std::string g_err;
@@ -48,9 +51,68 @@ int sm_count() {
   return cached;
 }
 
+// ---- asynchronous error words (HybridRunner raises one step later, no host sync)
+constexpr int ERR_MAX = 8;
+struct ErrSrc {
+  const int32_t* w[ERR_MAX];
+  int32_t shift[ERR_MAX];
+  int32_t n;
+};
+// OR the sources' device error words (shifted) into ONE host-mapped word. The
+// runner gives every stream that collects its own word, so the read-modify-
+// write below has a single writer.
+__global__ void k_err_collect(ErrSrc s, int32_t* host_word) {
+  int v = 0;
+  for (int i = 0; i < s.n; ++i)
+    if (s.w[i]) v |= *reinterpret_cast<const volatile int32_t*>(s.w[i]) << s.shift[i];
+  if (v) {
+    volatile int32_t* h = host_word;
+    *h = *h | v;
+  }
+}
+
 }  // namespace hp
 
 extern "C" {
+
+// Pinned, device-mapped host words (zeroed) for hp_err_collect.
+int hp_err_host_alloc(int32_t n, int32_t** host_out, int32_t** dev_out) {
+  HP_REQUIRE(n > 0 && host_out && dev_out, "bad error-word arguments");
+  void* h = nullptr;
+  HP_CUDA(cudaHostAlloc(&h, sizeof(int32_t) * (size_t)n, cudaHostAllocMapped));
+  memset(h, 0, sizeof(int32_t) * (size_t)n);
+  void* d = nullptr;
+  HP_CUDA(cudaHostGetDevicePointer(&d, h, 0));
+  *host_out = static_cast<int32_t*>(h);
+  *dev_out = static_cast<int32_t*>(d);
+  return HP_OK;
+}
+
+int hp_err_host_free(int32_t* host) {
+  if (host) HP_CUDA(cudaFreeHost(host));
+  return HP_OK;
+}
+
+int hp_err_collect(const int32_t* const* words, const int32_t* shifts, int32_t n,
+                   int32_t* dev_word, void* stream) {
+  HP_REQUIRE(n >= 0 && n <= hp::ERR_MAX && dev_word && (n == 0 || (words && shifts)),
+             "bad error-collect arguments (at most 8 words)");
+  hp::ErrSrc s{};
+  for (int i = 0; i < n; ++i) {
+    s.w[i] = words[i];
+    s.shift[i] = shifts[i];
+  }
+  s.n = n;
+  hp::k_err_collect<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(s, dev_word);
+  HP_LAUNCHED(1, "k_err_collect");
+  return HP_OK;
+}
+
+int hp_plan_err_ptr(const void* ws, const int32_t** out) {
+  HP_REQUIRE(ws && out, "NULL argument");
+  *out = static_cast<const int32_t*>(ws) + hp::C_ERR;  // counters are carved first
+  return HP_OK;
+}
 
 int hp_version(void) { return 100; /* 0.1.0 */ }
 
@@ -84,5 +146,6 @@ void hp_debug_set_combine_blocks(int n) { hp::g_combine_blocks = n < 0 ? 0 : n; 
 void hp_debug_set_dar_blocks(int n) { hp::g_dar_blocks = n < 0 ? 0 : n; }
 void hp_debug_set_owner_waves(int on) { hp::g_owner_waves = on ? 1 : 0; }
 void hp_debug_set_reduce_b(int b) { hp::g_reduce_b = b; }
+void hp_debug_set_wait_timeout(long long cycles) { hp::g_wait_cycles = cycles; }
 
 }  // extern "C"

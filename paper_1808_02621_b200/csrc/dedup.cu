@@ -23,11 +23,16 @@ namespace {
 
 constexpr int HS = HP_RADIX + 1;  // padded histogram row (bank spread)
 
+// Sort key of position i. An id outside [0, V) is DROPPED, never clamped onto a
+// real row: its key becomes the sentinel V (key_bits holds V, so it sorts after
+// every row), its segment gets no send slot and destination -1 (the reduce
+// skips it), inv = -1 (stitch writes a zero row), and error bit 1 is raised
+// for the runner. TF1's SparseApply* rejects such indices the same way.
 __device__ __forceinline__ uint32_t load_key(const int64_t* ids, int64_t i, int64_t V, int* err) {
   int64_t id = ids[i];
   if (id < 0 || id >= V) {
     if (err) atomicOr(err, 1);
-    id = id < 0 ? 0 : V - 1;
+    id = V;
   }
   return (uint32_t)id;
 }
@@ -391,12 +396,15 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
     const int u = seg_base + sidx;
     const int li = s_hpos[sidx];
     const uint32_t id = s_buf[li].x;
-    const int p = route.part(id);
-    const int slot = s_pbase[p] + (u - s_first[p]);
+    int slot = -1, dst = -1;  // the dropped-id sentinel segment (id == V): no slot, no store
+    if ((int64_t)id < pl.V) {
+      const int p = route.part(id);
+      slot = s_pbase[p] + (u - s_first[p]);
+      if (send_ids) send_ids[slot] = id;
+      if (counts) counts[slot] = L;
+      dst = seg_dst(id, p, slot, dst_pb, route, &pl.counters[C_ERR]);
+    }
     s_sig[sidx] = slot;
-    if (send_ids) send_ids[slot] = id;
-    if (counts) counts[slot] = L;
-    const int dst = seg_dst(id, p, slot, dst_pb, route, &pl.counters[C_ERR]);
     emit_items(pl, u, c * S + li, L, dst, bi_, bp_, bl_, (int)s_buf[li].y);
     const int n0 = (L + HP_CHUNK - 1) / HP_CHUNK;
     bi_ += n0;
@@ -411,7 +419,7 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
     pl.counters[C_ITEMS] = tot_i;
     pl.counters[C_PARTIALS] = tot_p;
     pl.counters[C_LONG] = tot_l;
-    if (n_uniq) *n_uniq = U;
+    if (n_uniq) *n_uniq = s_first[P];  // valid unique rows (the sentinel segment excluded)
   }
   __syncthreads();
   HP_PROF();
@@ -420,8 +428,12 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
     int spill_slot = 0;
     if (c > 0 && (cta_heads == 0 || s_hpos[0] > 0) && nvalid > 0) {
       const uint32_t id = s_buf[0].x;
-      const int p = route.part(id);
-      spill_slot = s_pbase[p] + (seg_base - 1 - s_first[p]);
+      if ((int64_t)id < pl.V) {
+        const int p = route.part(id);
+        spill_slot = s_pbase[p] + (seg_base - 1 - s_first[p]);
+      } else {
+        spill_slot = -1;
+      }
     }
     int hcount = hb;
 #pragma unroll
@@ -616,7 +628,7 @@ __global__ void k_heads(DedupPlan pl, const uint32_t* __restrict__ skey) {
     pl.segidx[i] = (i == 0 || skey[i] != skey[i - 1]) ? 1 : 0;
 }
 
-__global__ void k_heads_write(DedupPlan pl, const uint32_t* __restrict__ skey, int32_t* n_uniq) {
+__global__ void k_heads_write(DedupPlan pl, const uint32_t* __restrict__ skey) {
   const int U = pl.counters[C_UNIQ];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pl.T;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -627,18 +639,19 @@ __global__ void k_heads_write(DedupPlan pl, const uint32_t* __restrict__ skey, i
       pl.uniq_key[ex] = skey[i];
     }
     pl.segidx[i] = ex + (h ? 1 : 0) - 1;
-    if (i == 0) {
-      pl.seg_start[U] = (int)pl.T;
-      if (n_uniq) *n_uniq = U;
-    }
+    if (i == 0) pl.seg_start[U] = (int)pl.T;
   }
 }
 
-__global__ void k_first_u(DedupPlan pl) {
+// first_u[P] = valid unique rows: the dropped-id sentinel segment (key V) is last
+__global__ void k_first_u(DedupPlan pl, int32_t* n_uniq) {
   const Router route(pl.V, pl.P);
   const int U = pl.counters[C_UNIQ];
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p <= pl.P; p += gridDim.x * blockDim.x)
-    pl.first_u[p] = p == pl.P ? U : lower_bound_u32(pl.uniq_key, U, (uint32_t)route.lo(p));
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p <= pl.P; p += gridDim.x * blockDim.x) {
+    const int f = lower_bound_u32(pl.uniq_key, U, (uint32_t)(p == pl.P ? pl.V : route.lo(p)));
+    pl.first_u[p] = f;
+    if (p == pl.P && n_uniq) *n_uniq = f;
+  }
 }
 
 __global__ void __launch_bounds__(1024)
@@ -657,12 +670,17 @@ __global__ void k_seg_counts(DedupPlan pl, const int64_t* __restrict__ dst_pb, i
     const int L = pl.seg_start[u + 1] - pl.seg_start[u];
     const int n0 = (L + HP_CHUNK - 1) / HP_CHUNK;
     const uint32_t id = pl.uniq_key[u];
-    const int p = route.part(id);
-    const int slot = pl.part_base[p] + (u - pl.first_u[p]);
-    pl.sigma[u] = slot;
-    if (send_ids) send_ids[slot] = id;
-    if (counts) counts[slot] = L;
-    pl.dst[u] = seg_dst(id, p, slot, dst_pb, route, &pl.counters[C_ERR]);
+    if ((int64_t)id < pl.V) {
+      const int p = route.part(id);
+      const int slot = pl.part_base[p] + (u - pl.first_u[p]);
+      pl.sigma[u] = slot;
+      if (send_ids) send_ids[slot] = id;
+      if (counts) counts[slot] = L;
+      pl.dst[u] = seg_dst(id, p, slot, dst_pb, route, &pl.counters[C_ERR]);
+    } else {  // dropped ids (sentinel V): no slot, no destination
+      pl.sigma[u] = -1;
+      pl.dst[u] = -1;
+    }
     pl.item_off[u] = n0;
     pl.part_off[u] = L > HP_CHUNK ? n0 : 0;
     pl.long_tmp[u] = L > HP_CHUNK ? 1 : 0;
@@ -751,7 +769,7 @@ int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, i
   pl->nranks = nranks;
   pl->V = V;
   int bits = 0;
-  while (bits < 31 && (int64_t(1) << bits) < V) ++bits;
+  while (bits < 31 && (int64_t(1) << bits) <= V) ++bits;  // holds V: the dropped-id sentinel
   pl->key_bits = bits < 1 ? 1 : bits;
   pl->ntiles = (int32_t)((Tc + HP_TILE - 1) / HP_TILE);
   pl->key[0] = (uint32_t*)take(4 * Tc);
@@ -888,8 +906,8 @@ int build_plan(DedupPlan& pl, const int64_t* ids, const int32_t* owner,
   k_heads<<<g, 256, 0, st>>>(pl, skey);
   int rc = device_scan(pl.segidx, pl.T, nullptr, pl.scan_bsum, &pl.counters[C_UNIQ], st);
   if (rc) return rc;
-  k_heads_write<<<g, 256, 0, st>>>(pl, skey, n_uniq);
-  k_first_u<<<grid_for(pl.P + 1, 256, 1024), 256, 0, st>>>(pl);
+  k_heads_write<<<g, 256, 0, st>>>(pl, skey);
+  k_first_u<<<grid_for(pl.P + 1, 256, 1024), 256, 0, st>>>(pl, n_uniq);
   k_part_base<<<1, 1024, 0, st>>>(pl, owner, dest_counts);
   k_seg_counts<<<g, 256, 0, st>>>(pl, dst_pb, send_ids, counts);
   HP_LAUNCHED(5, "dedup metadata");

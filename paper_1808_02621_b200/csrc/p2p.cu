@@ -215,7 +215,9 @@ k_owner_apply(PeerTable peers, void* my_win, WinLayout L, const int64_t* __restr
   const unsigned epoch = (unsigned)*sig.epoch;
   const int lane = threadIdx.x & 31, q = threadIdx.x % TPI;
   constexpr int GPB = 256 / TPI;
-  const int64_t total = (int64_t)n * L.cap;
+  // after a push wait timed out (error bit 4) nothing is merged (see k_owner_scan)
+  const int64_t total =
+      (*reinterpret_cast<volatile int*>(sig.err) & 4) ? 0 : (int64_t)n * L.cap;
   for (int64_t e = (int64_t)blockIdx.x * GPB + threadIdx.x / TPI; e < total;
        e += (int64_t)gridDim.x * GPB) {
     const int s = (int)(e / L.cap);
@@ -357,7 +359,7 @@ k_owner_stream(PeerTable peers, void* my_win, WinLayout L, const int64_t* __rest
     s_pre[n] = a;
   }
   __syncthreads();
-  const int E = s_pre[n];
+  const int E = (*reinterpret_cast<volatile int*>(sig.err) & 4) ? 0 : s_pre[n];
   const int NW = gridDim.x * 4, gw = blockIdx.x * 4 + wid;
   const int Q = (E + NW - 1) / NW;
   const int fb0 = min(E, gw * Q), fe = min(E, fb0 + Q);
@@ -554,6 +556,9 @@ k_owner_scan(void* my_win, WinLayout L, const int64_t* __restrict__ part_base, R
   int2* items = reinterpret_cast<int2*>(win + L.items_off);
   int* cidx = reinterpret_cast<int*>(win + L.cidx_off);
   const int n = L.n;
+  // a push wait that timed out (error bit 4) leaves partially written inboxes:
+  // merge nothing (0 items) rather than apply them; the runner raises
+  if (*reinterpret_cast<volatile int*>(sig.err) & 4) return;
   if (threadIdx.x == 0) {
     int a = 0;
     for (int q = 0; q < n; ++q) {
@@ -721,16 +726,19 @@ __global__ void k_applied(PeerTable peers, void* my_win, WinLayout L) {
   HP_SPAN_END(SP_APPLIED);
 }
 
-// Spin-wait budget (cycles) before a wait gives up and raises an error bit.
+}  // namespace
+
+// Spin-wait budget (cycles) before a wait gives up and raises an error bit:
+// hp_debug_set_wait_timeout (> 0), else HP_WAIT_TIMEOUT_CYCLES, else ~2 s.
+long long g_wait_cycles = 0;
 long long wait_budget() {
+  if (g_wait_cycles > 0) return g_wait_cycles;
   static long long v = [] {
     const char* e = getenv("HP_WAIT_TIMEOUT_CYCLES");
     return e ? atoll(e) : 4000000000LL;  // ~2 s at 1.9 GHz
   }();
   return v;
 }
-
-}  // namespace
 
 HP_SPAN_SETTER(set_spans_p2p)
 
@@ -744,6 +752,7 @@ struct hp_xchg_s {
   int64_t rows_cap, bytes;
   void* win;          // own window
   PeerTable peers;    // mapped windows (own = win)
+  uint64_t ipc_mask;  // peers mapped with cudaIpcOpenMemHandle (closed on destroy)
 };
 
 extern "C" {
@@ -804,13 +813,31 @@ int hp_xchg_open_peer(hp_xchg_t x, int32_t rank, const void* ipc_handle) {
   void* p = nullptr;
   HP_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
   x->peers.base[rank] = p;
+  x->ipc_mask |= 1ull << rank;
+  return HP_OK;
+}
+
+// Single-process emulation of n ranks (tests on one GPU): the windows are
+// plain device allocations of this process, so a peer is set from its raw
+// window address instead of a cudaIpc handle. Same kernels, same protocol.
+int hp_xchg_window_ptr(hp_xchg_t x, void** out) {
+  HP_REQUIRE(x && out, "NULL argument");
+  *out = x->win;
+  return HP_OK;
+}
+
+int hp_xchg_set_peer_ptr(hp_xchg_t x, int32_t rank, void* window) {
+  HP_REQUIRE(x && rank >= 0 && rank < x->L.n && window, "bad peer args");
+  if (rank == x->L.me) return HP_OK;
+  HP_REQUIRE(!((x->ipc_mask >> rank) & 1ull), "peer already mapped by IPC");
+  x->peers.base[rank] = window;
   return HP_OK;
 }
 
 int hp_xchg_destroy(hp_xchg_t x) {
   if (!x) return HP_OK;
   for (int r = 0; r < x->L.n; ++r)
-    if (r != x->L.me && x->peers.base[r]) cudaIpcCloseMemHandle(x->peers.base[r]);
+    if (r != x->L.me && ((x->ipc_mask >> r) & 1ull)) cudaIpcCloseMemHandle(x->peers.base[r]);
   cudaFree(x->win);
   delete x;
   return HP_OK;
@@ -994,6 +1021,13 @@ int hp_xchg_recv_counts(hp_xchg_t x, int32_t* out_dev, void* stream) {
   return HP_OK;
 }
 
+// Device address of the exchange's error word (for hp_err_collect).
+int hp_xchg_err_ptr(hp_xchg_t x, const int32_t** out) {
+  HP_REQUIRE(x && out, "NULL argument");
+  *out = SigView(x->win).err;
+  return HP_OK;
+}
+
 // Error bits of the exchange (4: push wait timed out, 8: apply wait timed out,
 // 16: a received id is not homed here). Synchronises the stream.
 int hp_xchg_status(hp_xchg_t x, int32_t* out_err, void* stream) {
@@ -1035,7 +1069,6 @@ struct ArLayout {
 // blockIdx.y = destination chunk; 4 float4 in flight per thread; no division.
 __global__ void __launch_bounds__(256)
 k_ar_scatter(PeerTable peers, void* my_win, ArLayout A, const float4* __restrict__ grad) {
-  __shared__ bool s_last;
   HP_ENTRY(SP_AR_SCATTER);
   const int c = blockIdx.y;
   const int64_t b4 = A.off4[c], c4 = A.off4[c + 1] - b4, real4 = A.S_real >> 2;
@@ -1057,25 +1090,8 @@ k_ar_scatter(PeerTable peers, void* my_win, ArLayout A, const float4* __restrict
       if (j < c4) dst[j] = v[u];
     }
   }
-  __syncthreads();
-  SigView sig(my_win);
-  const int nblocks = gridDim.x * gridDim.y;
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    s_last = atomicAdd(&sig.done[2], 1) == nblocks - 1;
-  }
-  __syncthreads();
-  if (s_last) {
-    __threadfence_system();
-    const int e = *sig.epoch + 1;
-    for (int r = threadIdx.x; r < A.n; r += blockDim.x)
-      st_release_sys(&SigView(peers.base[r]).push_flag[A.me], e);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      *sig.epoch = e;
-      sig.done[2] = 0;
-    }
-  }
+  // no per-block fence: k_signal (next in the stream) fences once at system
+  // scope, cumulatively over every peer store of this kernel, then publishes
   HP_SPAN_END(SP_AR_SCATTER);
 }
 
@@ -1097,7 +1113,6 @@ __device__ __forceinline__ void put4<__nv_bfloat16>(void* base, int64_t i4, floa
 template <typename OutT>
 __global__ void __launch_bounds__(256)
 k_ar_reduce_gather(PeerTable peers, void* my_win, ArLayout A, float scale) {
-  __shared__ bool s_last;
   HP_ENTRY(SP_AR_RG);
   const int64_t b4 = A.off4[A.me], c4 = A.off4[A.me + 1] - b4;
   const float4* slots =
@@ -1126,21 +1141,7 @@ k_ar_reduce_gather(PeerTable peers, void* my_win, ArLayout A, float scale) {
         put4<OutT>(static_cast<char*>(peers.base[r]) + A.out_off, o4, v);
     }
   }
-  __syncthreads();
-  SigView sig(my_win);
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    s_last = atomicAdd(&sig.done[3], 1) == (int)gridDim.x - 1;
-  }
-  __syncthreads();
-  if (s_last) {
-    __threadfence_system();
-    const int e = *sig.epoch;
-    for (int r = threadIdx.x; r < A.n; r += blockDim.x)
-      st_release_sys(&SigView(peers.base[r]).applied_flag[A.me], e);
-    if (threadIdx.x == 0) sig.done[3] = 0;
-  }
-  HP_SPAN_END(SP_AR_RG);
+  HP_SPAN_END(SP_AR_RG);  // published by k_signal(1), next in the stream
 }
 
 
@@ -1341,10 +1342,25 @@ struct hp_dar_s {
   PeerTable peers;
   int64_t arrive_off, queue_off;  // HP_DAR_PIPE: piece arrival counters, work queue
   bool weighted;                  // hp_dar_set_split gave a non-uniform split
+  uint64_t ipc_mask;              // peers mapped with cudaIpcOpenMemHandle
   int mode;                  // HP_DAR_SM | HP_DAR_CE | HP_DAR_PIPE
   cudaStream_t side[4];      // CE mode: copies to different peers run concurrently
   cudaEvent_t fork, join[4];
+  bool side_ready;           // side streams / events created (CE mode only)
 };
+
+// CE mode's side streams, created once on first use (SM / pipelined modes never
+// hold extra streams: fewer streams per rank share the device's hardware queues)
+static int dar_side_streams(hp_dar_s* d) {
+  if (d->side_ready) return HP_OK;
+  for (int k = 0; k < 4; ++k) {
+    HP_CUDA(cudaStreamCreateWithFlags(&d->side[k], cudaStreamNonBlocking));
+    HP_CUDA(cudaEventCreateWithFlags(&d->join[k], cudaEventDisableTiming));
+  }
+  HP_CUDA(cudaEventCreateWithFlags(&d->fork, cudaEventDisableTiming));
+  d->side_ready = true;
+  return HP_OK;
+}
 
 extern "C" {
 
@@ -1381,12 +1397,7 @@ int hp_dar_create(hp_dar_t* out, int32_t n, int32_t me, int64_t S_real, int32_t 
     return cuda_fail(e, "cudaMalloc(dense window)");
   }
   HP_CUDA(cudaMemset(d->win, 0, bytes));  // slot padding must read as zeros
-  d->mode = HP_DAR_CE;
-  for (int k = 0; k < 4; ++k) {
-    HP_CUDA(cudaStreamCreateWithFlags(&d->side[k], cudaStreamNonBlocking));
-    HP_CUDA(cudaEventCreateWithFlags(&d->join[k], cudaEventDisableTiming));
-  }
-  HP_CUDA(cudaEventCreateWithFlags(&d->fork, cudaEventDisableTiming));
+  d->mode = HP_DAR_CE;  // side streams for the copies: created on first CE use
   cudaIpcMemHandle_t h;
   HP_CUDA(cudaIpcGetMemHandle(&h, d->win));
   memcpy(ipc_handle_out, &h, sizeof(h));
@@ -1405,18 +1416,36 @@ int hp_dar_open_peer(hp_dar_t d, int32_t rank, const void* ipc_handle) {
   void* p = nullptr;
   HP_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
   d->peers.base[rank] = p;
+  d->ipc_mask |= 1ull << rank;
+  return HP_OK;
+}
+
+// Single-process emulation (see hp_xchg_set_peer_ptr).
+int hp_dar_window_ptr(hp_dar_t d, void** out) {
+  HP_REQUIRE(d && out, "NULL argument");
+  *out = d->win;
+  return HP_OK;
+}
+
+int hp_dar_set_peer_ptr(hp_dar_t d, int32_t rank, void* window) {
+  HP_REQUIRE(d && rank >= 0 && rank < d->A.n && window, "bad peer args");
+  if (rank == d->A.me) return HP_OK;
+  HP_REQUIRE(!((d->ipc_mask >> rank) & 1ull), "peer already mapped by IPC");
+  d->peers.base[rank] = window;
   return HP_OK;
 }
 
 int hp_dar_destroy(hp_dar_t d) {
   if (!d) return HP_OK;
   for (int r = 0; r < d->A.n; ++r)
-    if (r != d->A.me && d->peers.base[r]) cudaIpcCloseMemHandle(d->peers.base[r]);
-  for (int k = 0; k < 4; ++k) {
-    cudaStreamDestroy(d->side[k]);
-    cudaEventDestroy(d->join[k]);
+    if (r != d->A.me && ((d->ipc_mask >> r) & 1ull)) cudaIpcCloseMemHandle(d->peers.base[r]);
+  if (d->side_ready) {
+    for (int k = 0; k < 4; ++k) {
+      cudaStreamDestroy(d->side[k]);
+      cudaEventDestroy(d->join[k]);
+    }
+    cudaEventDestroy(d->fork);
   }
-  cudaEventDestroy(d->fork);
   cudaFree(d->win);
   delete d;
   return HP_OK;
@@ -1457,11 +1486,12 @@ int hp_dar_set_mode(hp_dar_t d, int32_t mode) {
   HP_REQUIRE(d && (mode == HP_DAR_SM || mode == HP_DAR_CE || mode == HP_DAR_PIPE),
              "mode must be HP_DAR_SM, HP_DAR_CE or HP_DAR_PIPE");
   d->mode = mode;
-  return HP_OK;
+  return mode == HP_DAR_CE ? dar_side_streams(d) : HP_OK;
 }
 
 // CE mode: chunk copies to every peer, fanned out over the side streams.
 static int dar_copies(hp_dar_t d, cudaStream_t st, bool gather, const float* grad) {
+  if (int rc = dar_side_streams(d)) return rc;
   const ArLayout& A = d->A;
   const int npeer = A.n - 1;
   const int ns = npeer < 4 ? npeer : 4;
@@ -1540,14 +1570,22 @@ int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream) {
   const int bx = std::max(1, std::min(grid_for(maxc / 16, 256, sms), sms / d->A.n));
   launch_k(k_ar_scatter, dim3(bx, d->A.n), dim3(256), 0, st, d->peers, d->win, d->A,
                                                 reinterpret_cast<const float4*>(grad));
+  launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 0);
   launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 0, d->A.n, wait_budget(), SP_AR_WAIT0);
   const int brg = grid_for(std::max<int64_t>(myc, 8) / 8, 256, sms * 2);
   if (d->A.out_bytes == 4)
     launch_k(k_ar_reduce_gather<float>, dim3(brg), dim3(256), 0, st, d->peers, d->win, d->A, scale);
   else
     launch_k(k_ar_reduce_gather<__nv_bfloat16>, dim3(brg), dim3(256), 0, st, d->peers, d->win, d->A, scale);
+  launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 1);
   launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 1, d->A.n, wait_budget(), SP_AR_WAIT1);
-  HP_LAUNCHED(4, "dense p2p allreduce");
+  HP_LAUNCHED(6, "dense p2p allreduce");
+  return HP_OK;
+}
+
+int hp_dar_err_ptr(hp_dar_t d, const int32_t** out) {
+  HP_REQUIRE(d && out, "NULL argument");
+  *out = SigView(d->win).err;
   return HP_OK;
 }
 

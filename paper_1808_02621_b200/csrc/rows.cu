@@ -12,14 +12,16 @@
 namespace hp {
 namespace {
 
-struct SrcSlab {  // row of a global id in this rank's slab (nullptr if not homed)
+struct SrcSlab {  // row of a global id in this rank's slab (nullptr: not homed / dropped id)
   const float4* w;
   const int64_t* part_base;
   const int64_t* ids;
   Router route;
+  int64_t V;
   int D4;
   __device__ __forceinline__ const float4* operator()(int64_t i) const {
     const int64_t id = ids[i];
+    if (id < 0 || id >= V) return nullptr;  // out-of-range id: a zero row (never clamped)
     const int p = route.part(id);
     const int64_t b = part_base[p];
     return b < 0 ? nullptr : w + (b + (id - route.lo(p))) * D4;
@@ -31,7 +33,8 @@ struct SrcInv {
   const int32_t* inv;
   int D4;
   __device__ __forceinline__ const float4* operator()(int64_t t) const {
-    return rows + (int64_t)inv[t] * D4;
+    const int32_t k = inv[t];
+    return k < 0 ? nullptr : rows + (int64_t)k * D4;  // inv -1: a dropped id -> zero row
   }
 };
 
@@ -202,7 +205,7 @@ int hp_gather_rows(hp_slab slab, const int64_t* ids, int64_t n, const int32_t* n
   HP_REQUIRE(slab.D >= 4 && slab.D % 4 == 0 && slab.D <= 2048, "D must be a multiple of 4");
   HP_REQUIRE(n == 0 || (ids && out && slab.w && slab.part_base), "NULL argument");
   SrcSlab src{reinterpret_cast<const float4*>(slab.w), slab.part_base, ids, Router(slab.V, slab.P),
-              slab.D >> 2};
+              slab.V, slab.D >> 2};
   return launch_copy(src, n, n_dev, out, slab.D, static_cast<cudaStream_t>(stream));
 }
 

@@ -47,6 +47,7 @@ class Workspace:
     def get(self, nbytes: int) -> torch.Tensor:
         if self.buf.numel() < nbytes:
             self.buf = torch.empty(int(nbytes * 1.25) + 4096, dtype=torch.uint8, device=self.device)
+            self.buf[:256].zero_()  # the plan counters (incl. the error word) start clean
         return self.buf
 
     @property
@@ -56,6 +57,47 @@ class Workspace:
     @property
     def nbytes(self) -> int:
         return self.buf.numel()
+
+
+class ErrorWords:
+    """Pinned, device-mapped host words that device error bits are collected into
+    (``hp_err_collect``): reading them never synchronises the GPU."""
+
+    def __init__(self, n: int):
+        h, d = C.c_void_p(), C.c_void_p()
+        call("hp_err_host_alloc", n, C.byref(h), C.byref(d))
+        self.n, self._host, self._dev = n, h.value, d.value
+        self.words = (C.c_int32 * n).from_address(self._host)
+
+    def collect(self, slot: int, sources, stream=None) -> None:
+        """OR ``(device word pointer, shift)`` sources into host word ``slot``."""
+        sources = [(p, sh) for p, sh in sources if p]
+        if not sources:
+            return
+        ptrs = (C.c_void_p * len(sources))(*[p for p, _ in sources])
+        shifts = (C.c_int32 * len(sources))(*[sh for _, sh in sources])
+        call("hp_err_collect", ptrs, shifts, len(sources), self._dev + 4 * slot, _stream(stream))
+
+    def read(self) -> list:
+        return [int(self.words[i]) for i in range(self.n)]
+
+    def clear(self) -> None:
+        for i in range(self.n):
+            self.words[i] = 0
+
+    def close(self) -> None:
+        if self._host:
+            call("hp_err_host_free", self._host)
+            self._host = None
+
+
+def plan_err_ptr(ws: "Workspace") -> int | None:
+    """Device address of the error word of the plan in ``ws`` (None if unsized)."""
+    if ws.nbytes == 0:
+        return None
+    out = C.c_void_p()
+    call("hp_plan_err_ptr", ws.ptr, C.byref(out))
+    return out.value
 
 
 def dedup_ws_bytes(T: int, D: int, P: int, nranks: int = 1) -> int:

@@ -146,6 +146,11 @@ class HybridRunner:
         if self.dense_exchange not in ("p2p", "p2p-sm", "p2p-pipe", "nvls", "nccl", "local"):
             raise ValueError("dense_exchange must be 'p2p' (copy engines), 'p2p-sm', "
                              "'p2p-pipe', 'nvls' or 'nccl'")
+        self._world = getattr(comm, "world", None)  # emulated ranks (emulate.LocalWorld)
+        if self._world is not None and (self.exchange != "p2p" or self.dense_exchange in
+                                        ("nccl", "nvls")):
+            raise ValueError("emulated ranks (LocalWorld) run the peer-memory transports only: "
+                             "exchange='p2p', dense_exchange in ('p2p', 'p2p-sm', 'p2p-pipe')")
         self.dar: dict = {}
         self.dense_weights = None  # reduction share per rank of the peer dense exchange
         self.xchg: dict = {}
@@ -178,7 +183,8 @@ class HybridRunner:
 
                     self.dar[var.name] = DenseExchange(
                         world_size, rank, var.elements, dense_dtype, self.device,
-                        mode={"p2p": "ce", "p2p-sm": "sm", "p2p-pipe": "pipe"}[self.dense_exchange])
+                        mode={"p2p": "ce", "p2p-sm": "sm", "p2p-pipe": "pipe"}[self.dense_exchange],
+                        world=self._world)
                     w = self._dense_split_weights(dense_split)
                     if w is not None:
                         self.dar[var.name].set_split(w)
@@ -206,6 +212,7 @@ class HybridRunner:
             for tab in self.tables.values():
                 tab.step_dev = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.dense_out: dict[str, torch.Tensor] = {}
+        self._dense_bufs: dict[str, dict] = {}
         self.outputs: dict[str, torch.Tensor] = {}
         self.step_count = 0
         self.last_counts: dict = {}
@@ -230,6 +237,10 @@ class HybridRunner:
                               for n in self.tables}
         self._pending_counts: dict = {}
         self.concurrent_tables = True
+        # device error bits -> pinned host words (one per table stream + dense),
+        # collected on the streams that own them, read at the next step()
+        self._err = ops.ErrorWords(len(self.tables) + 1)
+        self._err_slot = {n: i for i, n in enumerate(self.tables)}
 
     def _dense_split_weights(self, dense_split):
         """Reduction share per rank for the peer-memory dense exchange.
@@ -268,9 +279,13 @@ class HybridRunner:
 
         D = var.elem_bytes // 4
         bounds = partition_bounds(var.elements, P)
-        _, _, rows = slab_layout(bounds, owner, self.rank)
         cap = int(max_ids or var.touched_elements)
-        x = PeerExchange(self.world_size, self.rank, D, cap, max(rows, 1), self.device)
+        # the window layout must be identical on every rank (peers address each
+        # other's inboxes with their own offsets): size the slab region for the
+        # largest slab of any rank (P not a multiple of n gives unequal slabs)
+        rows_cap = max(max(slab_layout(bounds, owner, r)[2] for r in range(self.world_size)), 1)
+        x = PeerExchange(self.world_size, self.rank, D, cap, rows_cap, self.device,
+                         world=self._world)
         self.xchg[var.name] = x
         gb = np.zeros(P, dtype=np.int64)
         for r in range(self.world_size):
@@ -323,6 +338,10 @@ class HybridRunner:
             x.close()
         self.xchg.clear()
         self.dar.clear()
+        if self._err is not None:
+            torch.cuda.synchronize(self.device)
+            self._err.close()
+            self._err = None
 
     # ------------------------------------------------------------------ step
     def _buf(self, name: str, key: str, shape, dtype) -> torch.Tensor:
@@ -342,13 +361,61 @@ class HybridRunner:
         e.record(torch.cuda.current_stream())
         self.kernel_events.setdefault(key, []).append(e)
 
+    # bit layout of the runner's error words
+    ERR_BITS = {1: "an id outside [0, V) was dropped (no row updated, zero row pulled)",
+                2: "a row id is not homed on this rank",
+                4: "a sparse push wait timed out (the owner merged nothing)",
+                8: "a sparse apply wait timed out (pulled rows are stale)",
+                16: "a received row id is not homed on its owner",
+                4 << 8: "a dense-exchange scatter wait timed out",
+                8 << 8: "a dense-exchange gather wait timed out"}
+
+    def _collect_errors(self, tab: ShardedTable, slot: int) -> None:
+        """Enqueue (current stream) the error words of plan slot ``slot`` and of
+        the table's exchange into the table's host word."""
+        src = [(ops.plan_err_ptr(tab.wss[slot]), 0)]
+        if tab.name in self.xchg:
+            src.append((self.xchg[tab.name].err_ptr(), 0))
+        self._err.collect(self._err_slot[tab.name], src)
+
+    def _collect_dense_errors(self) -> None:
+        src = [(d.err_ptr(), 8) for d in self.dar.values()]
+        self._err.collect(len(self.tables), src)
+
+    def check_errors(self, sync: bool = False) -> None:
+        """Raise :class:`HybridPathError` if any device error bit reached the host.
+
+        ``step()`` calls this first (no synchronisation), so a failure in step i
+        raises from step i+1 at the latest one step after it completed.
+        ``sync=True`` collects every word now and waits for the GPU (end of a
+        run, or after graph replays)."""
+        from ._lib import HybridPathError
+
+        if sync:
+            for tab in self.tables.values():
+                for slot in (0, 1):
+                    self._collect_errors(tab, slot)
+            self._collect_dense_errors()
+            torch.cuda.synchronize(self.device)
+        words = self._err.read()
+        if not any(words):
+            return
+        self._err.clear()
+        names = list(self.tables) + ["dense"]
+        msgs = [f"{names[i]}: {text}" for i, w in enumerate(words) for bit, text in
+                self.ERR_BITS.items() if w & bit]
+        raise HybridPathError(f"rank {self.rank}: device error bits {words}: " + "; ".join(msgs))
+
     def _plan(self, tab: ShardedTable, ids, slot: int) -> None:
-        """Index half of the step (dedup + route) into plan slot ``slot``."""
+        """Index half of the step (dedup + route) into plan slot ``slot``, then
+        its error word (a dropped id is known as soon as the plan exists) and the
+        table's sticky exchange word (the steps before) go to the host word."""
         if self.world_size == 1:
             ops.apply_plan_build(ids, tab.slab(), tab.wss[slot])
         else:
             self.xchg[tab.name].plan(ids, tab.V, tab.P, tab.owner_dev, self.glob_base[tab.name],
                                      self._p2p_bufs(tab, slot), tab.wss[slot])
+        self._collect_errors(tab, slot)
 
     def _p2p_bufs(self, tab: ShardedTable, slot: int) -> dict:
         bufs = self._scratch[tab.name].tensors
@@ -389,6 +456,7 @@ class HybridRunner:
         ops.allgather(comm, vals.contiguous(), vals_all)
         slab = tab.slab()
         ops.apply_plan_build(ids_all, slab, tab.wss[0])
+        self._collect_errors(tab, 0)
         self._kev(f"k4:{tab.name}", True)
         ops.apply_plan(vals_all, n * T, slab, opt, tab.wss[0])
         self._kev(f"k4:{tab.name}", False)
@@ -401,6 +469,7 @@ class HybridRunner:
         name = tab.name
         r = ops.sort_dedup_route(ids, vals, tab.V, tab.P, tab.owner_dev, n, tab.ws,
                                  out=self._scratch[name].tensors.setdefault("k1", {}))
+        self._collect_errors(tab, 0)
         recv_counts = self._buf(name, "recv_counts", (n,), torch.int32)
         self.comm.alltoall_counts(r["dest_counts"], recv_counts)
         both = torch.cat([r["dest_counts"], recv_counts]).cpu()  # host counts for NCCL a2a-v
@@ -438,6 +507,7 @@ class HybridRunner:
         while this step applies, into the other plan slot; the following
         ``step(next_batch)`` then skips its dedup. Results are identical.
         """
+        self.check_errors()
         self.step_count += 1
         stream = torch.cuda.current_stream()
         phases = {"compute": 0.0, "network": 0.0, "intra": 0.0, "update": 0.0}
@@ -465,6 +535,7 @@ class HybridRunner:
             if self.dense:
                 self._dense_stream.wait_stream(stream)
                 with torch.cuda.stream(self._dense_stream):
+                    self._collect_dense_errors()  # the previous step's (sticky) words
                     self._dense(batch)
                 joins.append(self._dense_stream)
             for name, tab in self.tables.items():
@@ -491,10 +562,16 @@ class HybridRunner:
             ev("network" if self.world_size > 1 else "update")
         else:
             if self.dense:
+                self._collect_dense_errors()
                 self._dense(batch)
                 ev("network")
             for name, tab in self.tables.items():
                 self.outputs[name] = self._sparse(tab, batch[name], ev)
+            if next_batch is not None and self.pipelined:  # next plans, same stream
+                for name, tab in self.tables.items():
+                    nxt = tab.last_slot ^ 1
+                    self._plan(tab, next_batch[name][0], nxt)
+                    tab.ready, tab.ready_ids = nxt, next_batch[name][0]
         if timed:
             stream.synchronize()
             for name, (sc, rc) in self._pending_counts.items():
@@ -507,22 +584,58 @@ class HybridRunner:
         return IterationStats(iter_us, self._bytes_report(), phases, self._trace(),
                               {"step": self.step_count})
 
+    def _dense_buf(self, var: VariableSpec, key: str, shape, dtype) -> torch.Tensor:
+        """Runner-owned persistent buffer of one dense Weight (never a caller tensor)."""
+        bufs = self._dense_bufs.setdefault(var.name, {})
+        t = bufs.get(key)
+        if t is None or tuple(t.shape) != tuple(shape) or t.dtype != dtype:
+            t = torch.empty(shape, dtype=dtype, device=self.device)
+            bufs[key] = t
+        return t
+
+    def dense_is_noop(self) -> bool:
+        """K7 does no work at all: one replica, fp32 output, scale 1 ('mean' over
+        one rank): the averaged gradient IS this step's gradient."""
+        return (self.world_size == 1 and self.dense_dtype == torch.float32
+                and np.float32(self.scale) == np.float32(1.0))
+
     def _dense(self, batch: dict) -> None:
+        """K7 for every dense Weight. The result lands in ``dense_out[name]``:
+        a runner-owned buffer (or the exchange window), so the caller's gradient
+        tensors are only read; at n=1 with fp32 and scale 1 nothing is launched
+        and ``dense_out[name]`` is this step's gradient itself."""
         for var in self.dense:
             g = batch[var.name]
-            out = self.dense_out.get(var.name)
-            if out is None or out.numel() != g.numel() or out.dtype != self.dense_dtype:
-                out = g if self.dense_dtype == torch.float32 else torch.empty(
-                    g.shape, dtype=self.dense_dtype, device=self.device)
+            ops._need(g, torch.float32, f"dense gradient {var.name!r}")
+            if g.numel() != var.elements:
+                raise SpecError(f"dense Weight {var.name!r}: gradient has {g.numel()} elements, "
+                                f"the graph declares {var.elements}")
+            if self.dense_is_noop():
+                self.dense_out[var.name] = g
+                continue
             self._kev(f"k7:{var.name}", True)
-            if var.name in self.dense_ps:
-                self.dense_out[var.name] = ops.dense_reduce_bcast(
-                    self.comm.ptr, g, out, self.scale, self.dense_ps[var.name])
-            elif var.name in self.dar:
+            if var.name in self.dar:
                 self.dense_out[var.name] = self.dar[var.name].allreduce(g, self.scale)
+            elif var.name in self.dense_ps:
+                out = self._dense_buf(var, "out", (g.numel(),), self.dense_dtype).view(g.shape)
+                src = g
+                if self.dense_dtype != torch.float32:  # the owner reduces into its input
+                    src = self._dense_buf(var, "red", (g.numel(),), torch.float32).view(g.shape)
+                    src.copy_(g)
+                self.dense_out[var.name] = ops.dense_reduce_bcast(
+                    self.comm.ptr, src, out, self.scale, self.dense_ps[var.name])
             else:
-                self.dense_out[var.name] = ops.dense_allreduce_scale_cast(
-                    self.comm.ptr if self.comm else None, g, out, self.scale)
+                out = self._dense_buf(var, "out", (g.numel(),), self.dense_dtype).view(g.shape)
+                comm = self.comm.ptr if self.comm is not None else None
+                if self.world_size > 1 and self.dense_dtype != torch.float32:
+                    # NCCL reduces fp32 with the scale folded in (PreMulSum) into a
+                    # runner buffer; the cast then runs as its own epilogue
+                    red = self._dense_buf(var, "red", (g.numel(),), torch.float32).view(g.shape)
+                    ops.dense_allreduce_scale_cast(comm, g, red, self.scale)
+                    ops.dense_allreduce_scale_cast(None, red, out, 1.0)
+                else:
+                    ops.dense_allreduce_scale_cast(comm, g, out, self.scale)
+                self.dense_out[var.name] = out
             self._kev(f"k7:{var.name}", False)
 
     def _sparse(self, tab: ShardedTable, ids_vals, ev=None) -> torch.Tensor:
@@ -559,6 +672,35 @@ class HybridRunner:
         return ((self.world_size == 1 or self.exchange == "p2p") and not self.ar_tables
                 and not self.dense_ps)
 
+    def reserve(self, batch: dict) -> None:
+        """Allocate every buffer a step on ``batch``'s shapes uses (both plan
+        slots, exchange scratch, outputs) without launching the step. After it,
+        steps of these shapes never call the device allocator, which matters
+        when several ranks' steps share one GPU (:mod:`.emulate`): an
+        allocation is an implicit synchronisation point that would wait on the
+        other ranks' spinning exchange waits."""
+        n = self.world_size
+        for name, tab in self.tables.items():
+            T = batch[name][0].numel()
+            Tw = T * n if name in self.ar_tables else T
+            for ws in tab.wss:
+                ws.get(ops.dedup_ws_bytes(Tw, tab.D, tab.P, n))
+            self._buf(name, "out", (T, tab.D), torch.float32)
+            if name in self.ar_tables:
+                self._buf(name, "ar_ids", (n * T,), torch.int64)
+                self._buf(name, "ar_vals", (n * T, tab.D), torch.float32)
+            elif n > 1 and self.exchange == "p2p":
+                for slot in (0, 1):
+                    self._p2p_bufs(tab, slot)
+                self._buf(name, "recv_counts", (n,), torch.int32)
+        for var in self.dense:
+            if self.dense_is_noop() or var.name in self.dar:
+                continue
+            self._dense_buf(var, "out", (var.elements,), self.dense_dtype)
+            if self.dense_dtype != torch.float32 and (n > 1 or var.name in self.dense_ps):
+                self._dense_buf(var, "red", (var.elements,), torch.float32)
+        torch.cuda.synchronize(self.device)
+
     def prefetch(self, batch: dict) -> None:
         """Build the plans of ``batch`` now (stream-ordered) so its step skips dedup."""
         if not self.pipelined:
@@ -567,6 +709,13 @@ class HybridRunner:
             ids = batch[name][0]
             self._plan(tab, ids, 0)
             tab.ready, tab.ready_ids = 0, ids
+
+    def predicted_transfer(self) -> TransferReport:
+        """The reference's closed-form per-GPU bytes of this plan
+        (:func:`transfer.transfer_model`), to print beside the measured ones."""
+        from .transfer import transfer_model
+
+        return transfer_model(self.graph, self.plan, self.cluster)
 
     def _bytes_report(self) -> TransferReport:
         n = self.world_size
@@ -619,7 +768,8 @@ class HybridRunner:
             self.step(batch, timed=False)
         return g
 
-    def capture_pipelined(self, batches: list, steps_per_graph: int = 1) -> list:
+    def capture_pipelined(self, batches: list, steps_per_graph: int = 1,
+                          warm: bool = True) -> list:
         """CUDA graphs over a rotation of batches: graph r applies batches[r]
         with the plan built by the step before and builds the plan of
         batches[r+1]. With ``steps_per_graph`` = G > 1 one graph holds G
@@ -628,7 +778,9 @@ class HybridRunner:
 
         Replay them in order, repeatedly. ``len(batches)`` must be even (the
         plan slots alternate) and a multiple of G. The first plan is built
-        eagerly here.
+        eagerly here, followed by one eager rotation that sizes every buffer;
+        ``warm=False`` skips both (the caller ran them, e.g. every emulated rank
+        of :mod:`.emulate` interleaved, since their waits depend on each other).
         """
         R = len(batches)
         G = steps_per_graph
@@ -640,10 +792,11 @@ class HybridRunner:
             raise NotImplementedError("the NCCL a2a-v path reads counts on the host")
         # (the AR-sparse / PS-dense baselines are not pipelined: each graph then
         # plans its own batch; prefetch() and next_batch are no-ops for them)
-        self.prefetch(batches[0])
-        for r in range(R):  # eager warm-up rotation (sizes every buffer)
-            self.step(batches[r], timed=False, next_batch=batches[(r + 1) % R])
-        torch.cuda.synchronize()
+        if warm:
+            self.prefetch(batches[0])
+            for r in range(R):  # eager warm-up rotation (sizes every buffer)
+                self.step(batches[r], timed=False, next_batch=batches[(r + 1) % R])
+            torch.cuda.synchronize()
         graphs = []
         for r in range(0, R, G):
             g = torch.cuda.CUDAGraph()
@@ -712,6 +865,31 @@ class HybridRunner:
             dist.all_reduce(x, op=dist.ReduceOp.MAX)
             t = float(x.item())
         return t
+
+
+def simulate_training(plan: DistributedPlan, graph: GraphSpec, cluster: ClusterSpec,
+                      profile=None, iterations: int = 100, warmup_inflation: float = 1.5,
+                      seed: int = 0, *, rank: int = 0, world_size: int = 1, comm=None,
+                      optimizer: OptimizerConfig | None = None, device=None, **kw) -> float:
+    """Device counterpart of the reference's ``simulate_training``
+    (`sparseplan/simulate.py:380-402`, same signature): the mean time (us) of
+    ``iterations`` REAL hybrid steps of ``plan`` on synthetic inputs of the
+    graph's shapes (:func:`synth.graph_batches`), the first half discarded
+    (`PAPER.md:485`), max over ranks, plus the profile's serialized compute
+    time. ``warmup_inflation`` only pins the interface: the discarded warm-up
+    half is measured, not modelled. One process per GPU (``comm`` for n > 1)."""
+    from .synth import graph_batches
+
+    if iterations < 2:
+        raise SpecError(f"iterations must be >= 2, got {iterations}")
+    dev = torch.device(device if device is not None else torch.cuda.current_device())
+    runner = HybridRunner(plan, graph, cluster, rank=rank, world_size=world_size, comm=comm,
+                          optimizer=optimizer, device=dev, seed=seed, **kw)
+    try:
+        t = runner.measure_graphs(graph_batches(graph, seed, rank, 2, dev), iterations)
+    finally:
+        runner.close()
+    return t + (profile.compute_us_per_gpu if profile is not None else 0.0)
 
 
 def device_evaluator(graph: GraphSpec, cluster: ClusterSpec, make_batch, *, rank: int = 0,

@@ -72,6 +72,26 @@ class TransferReport:
 
 
 @dataclass(frozen=True)
+class ComputeProfile:
+    """Non-network costs of one iteration (reference `simulate.py:58-68`, same
+    fields and validation). On the device the aggregation / partition terms are
+    measured, not modelled; ``compute_us_per_gpu`` (the model's forward /
+    backward, which this path does not run) is added to measured step times by
+    :func:`~paper_1808_02621_b200.tuning.tune` and
+    :func:`~paper_1808_02621_b200.runner.simulate_training`."""
+
+    compute_us_per_gpu: float = 0.0
+    partition_overhead_us: float = 0.0
+    agg_us_per_mb: float = 0.0
+
+    def __post_init__(self) -> None:
+        from .model import SpecError
+
+        if min(self.compute_us_per_gpu, self.partition_overhead_us, self.agg_us_per_mb) < 0:
+            raise SpecError("compute profile fields must be >= 0")
+
+
+@dataclass(frozen=True)
 class IterationStats:
     """Measured counterpart of the reference's ``IterationStats`` (`simulate.py:71-79`)."""
 

@@ -107,3 +107,26 @@ def make_batch(w: Workload, seed: int, rank: int, dense: bool = True) -> dict:
         for name, n in w.dense.items():
             out[name] = rng.standard_normal(n, dtype=np.float32)
     return out
+
+
+def graph_batches(graph, seed: int, rank: int, count: int, device) -> list:
+    """Device batches shaped by a planner GraphSpec (the reference's inputs):
+    a sparse Weight gets ceil-rounded alpha * V Zipf(1.1) ids of its row width,
+    a dense Weight a standard-normal gradient of its element count."""
+    import torch
+
+    out = []
+    for i in range(count):
+        rng = np.random.default_rng((seed + i) * 1000 + rank)
+        b = {}
+        for v in graph.variables:
+            if v.kind == "sparse":
+                D = v.elem_bytes // 4
+                T = max(1, int(round(v.alpha * v.elements)))
+                ids = zipf_ids(rng, v.elements, T)
+                vals = rng.standard_normal((T, D), dtype=np.float32)
+                b[v.name] = (torch.from_numpy(ids).to(device), torch.from_numpy(vals).to(device))
+            else:
+                b[v.name] = torch.from_numpy(rng.standard_normal(v.elements, dtype=np.float32)).to(device)
+        out.append(b)
+    return out

@@ -23,24 +23,54 @@ class _DevPtr:
                                          "data": (ptr, False), "version": 3, "strides": None}
 
 
-class PeerExchange:
-    def __init__(self, n: int, rank: int, D: int, cap: int, rows_cap: int, device, group=None):
-        import torch.distributed as dist
+def _connect(x, prefix: str, ipc, group, world) -> None:
+    """Map the other ranks' windows: by cudaIpc handle (one process per GPU), or
+    by address through ``world`` (n emulated ranks in one process). Peers
+    address each other's windows with their own offsets, so the window shape
+    (``x.shape``) must be identical on every rank: checked here."""
+    if world is not None:
+        world.register(x.KIND, x.rank, x)
+        return
+    import torch.distributed as dist
 
+    handles = [None] * x.n
+    dist.all_gather_object(handles, (bytes(ipc), x.shape), group=group)
+    shapes = {h[1] for h in handles}
+    if len(shapes) != 1:
+        raise ValueError(f"{prefix}: window shapes differ across ranks: {sorted(shapes)}")
+    for r, (h, _) in enumerate(handles):
+        if r != x.rank:
+            buf = (C.c_ubyte * 64).from_buffer_copy(h)
+            call(f"{prefix}_open_peer", x.handle, r, C.addressof(buf))
+
+
+class PeerExchange:
+    """``world``: a :class:`~paper_1808_02621_b200.emulate.LocalWorld` links the
+    windows of n emulated ranks of THIS process by address (one-GPU parity
+    tests); otherwise cudaIpc handles are swapped over ``torch.distributed``."""
+
+    KIND = "xchg"
+
+    def __init__(self, n: int, rank: int, D: int, cap: int, rows_cap: int, device, group=None,
+                 world=None):
         load()
         self.n, self.rank, self.D, self.cap = n, rank, D, cap
+        self.shape = (n, D, cap, rows_cap)
         self.handle = C.c_void_p()
         ipc = (C.c_ubyte * 64)()
         wptr = C.c_void_p()
         call("hp_xchg_create", C.byref(self.handle), n, rank, D, cap, rows_cap, C.addressof(ipc),
              C.byref(wptr))
-        handles = [None] * n
-        dist.all_gather_object(handles, bytes(ipc), group=group)
-        for r, h in enumerate(handles):
-            if r != rank:
-                buf = (C.c_ubyte * 64).from_buffer_copy(h)
-                call("hp_xchg_open_peer", self.handle, r, C.addressof(buf))
         self.w = torch.as_tensor(_DevPtr(wptr.value, (rows_cap, D)), device=device)
+        _connect(self, "hp_xchg", ipc, group, world)
+
+    def window_ptr(self) -> int:
+        out = C.c_void_p()
+        call("hp_xchg_window_ptr", self.handle, C.byref(out))
+        return out.value
+
+    def link_peer(self, rank: int, window: int) -> None:
+        call("hp_xchg_set_peer_ptr", self.handle, rank, window)
 
     def push(self, ids, vals, V: int, P: int, owner, glob_base, out: dict, ws) -> dict:
         """Fused dedup + route + NVLink push; fills out[send_ids, inv, dest_counts, n_uniq]."""
@@ -98,6 +128,11 @@ class PeerExchange:
                 "applied_flag": v[128:128 + self.n], "epoch": v[192], "err": v[193],
                 "done": v[196:200], "push_off": v[256:256 + self.n]}
 
+    def err_ptr(self) -> int:
+        out = C.c_void_p()
+        call("hp_xchg_err_ptr", self.handle, C.byref(out))
+        return out.value
+
     def status(self) -> int:
         err = C.c_int32(0)
         call("hp_xchg_status", self.handle, C.addressof(err), torch.cuda.current_stream().cuda_stream)
@@ -116,11 +151,10 @@ class DenseExchange:
     cast(scale * sum_r grad_r) (summed in rank order) in ``self.out`` on every rank."""
 
     MODES = {"sm": 0, "ce": 1, "pipe": 2}  # HP_DAR_SM / _CE / _PIPE (include/hybridpath.h)
+    KIND = "dar"
 
     def __init__(self, n: int, rank: int, numel: int, out_dtype, device, group=None,
-                 mode: str = "ce"):
-        import torch.distributed as dist
-
+                 mode: str = "ce", world=None):
         from ._lib import HP_DTYPE
 
         if numel % 4:
@@ -130,18 +164,22 @@ class DenseExchange:
         ipc = (C.c_ubyte * 64)()
         optr = C.c_void_p()
         code = HP_DTYPE[str(out_dtype).split(".")[1]]
+        self.shape = (n, numel, code)
         call("hp_dar_create", C.byref(self.handle), n, rank, numel, code, C.addressof(ipc),
              C.byref(optr))
-        handles = [None] * n
-        dist.all_gather_object(handles, bytes(ipc), group=group)
-        for r, h in enumerate(handles):
-            if r != rank:
-                buf = (C.c_ubyte * 64).from_buffer_copy(h)
-                call("hp_dar_open_peer", self.handle, r, C.addressof(buf))
+        _connect(self, "hp_dar", ipc, group, world)
         call("hp_dar_set_mode", self.handle, self.MODES[mode])
         typestr = "<f4" if code == 0 else "<u2"
         t = torch.as_tensor(_DevPtr(optr.value, (numel,), typestr), device=device)
         self.out = t if code == 0 else t.view(torch.bfloat16)
+
+    def window_ptr(self) -> int:
+        out = C.c_void_p()
+        call("hp_dar_window_ptr", self.handle, C.byref(out))
+        return out.value
+
+    def link_peer(self, rank: int, window: int) -> None:
+        call("hp_dar_set_peer_ptr", self.handle, rank, window)
 
     def set_split(self, weights) -> None:
         """Share of the reduction per rank (hp_dar_set_split); identical on every rank."""
@@ -149,9 +187,20 @@ class DenseExchange:
         call("hp_dar_set_split", self.handle, C.addressof(w))
 
     def allreduce(self, grad, scale: float) -> torch.Tensor:
+        from .ops import _need
+
+        _need(grad, torch.float32, "grad")
+        if grad.numel() != self.numel:
+            raise ValueError(f"grad has {grad.numel()} elements, the exchange was built for "
+                             f"{self.numel}")
         call("hp_dar_allreduce", self.handle, grad.data_ptr(), scale,
              torch.cuda.current_stream().cuda_stream)
         return self.out
+
+    def err_ptr(self) -> int:
+        out = C.c_void_p()
+        call("hp_dar_err_ptr", self.handle, C.byref(out))
+        return out.value
 
     def status(self) -> int:
         err = C.c_int32(0)
@@ -202,11 +251,16 @@ class NvlsExchange:
         self.out = self.outbuf[:numel]
 
     def allreduce(self, grad, scale: float) -> torch.Tensor:
+        if grad.dtype != torch.float32 or grad.numel() != self.numel or not grad.is_cuda:
+            raise ValueError(f"grad must be a CUDA float32 tensor of {self.numel} elements")
         self.inp[:self.numel].copy_(grad.reshape(-1))
         call("hp_nvls_allreduce", self.mc_in, self.mc_out, self.S, self.n, self.rank, self.code,
              scale, self.pads.data_ptr(), self.state.data_ptr(),
              torch.cuda.current_stream().cuda_stream)
         return self.out
+
+    def err_ptr(self) -> int:
+        return self.state.data_ptr() + 4  # {epoch, error bits}
 
     def status(self) -> int:
         return int(self.state[1].item())

@@ -5,6 +5,14 @@ from pathlib import Path
 import pytest
 
 ROOT = Path(__file__).resolve().parent.parent
+# The one-GPU emulated multi-rank tests (test_gpu_emulated.py) keep several
+# ranks' spinning exchange waits in flight at once; a lazily loaded kernel's
+# first launch synchronises the context and would wait on them (measured:
+# every wait times out on the first step). Load modules eagerly, before the
+# first CUDA call of the test process.
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+# ... and give the emulated ranks' streams distinct hardware queues
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 

@@ -153,3 +153,39 @@ def test_ar_sparse_step_is_one_worker_step_over_the_concatenation():
         assert np.array_equal(a[k], b[k])
     for r, (i, _) in enumerate(batches):
         assert np.array_equal(res[r]["out"], b["w"][i])
+
+
+def test_out_of_range_ids_are_dropped_numpy_and_c():
+    """Ids outside [0, V) update nothing, pull a zero row and get inv = -1, in
+    both oracles (the device drops them the same way, never clamps)."""
+    from oracle import coracle
+
+    rng = np.random.default_rng(9)
+    V, D, P, n, T = 1000, 8, 4, 2, 600
+    ids = rng.integers(0, V, T)
+    bad = rng.choice(T, 40, replace=False)
+    ids[bad[:20]] = V + rng.integers(0, 5, 20)
+    ids[bad[20:]] = -1 - rng.integers(0, 5, 20)
+    vals = rng.standard_normal((T, D), dtype=F32)
+    owner = orc.owner_table("embedding", P, n)
+    ok = (ids >= 0) & (ids < V)
+    a = orc.sort_dedup_route(ids, vals, V, P, owner, n)
+    b = coracle.sort_dedup_route(ids, vals, V, P, owner, n)
+    ref = orc.sort_dedup_route(ids[ok], vals[ok], V, P, owner, n)
+    for r in (a, b):
+        assert r["n_uniq"] == ref["n_uniq"]
+        assert np.array_equal(r["send_ids"], ref["send_ids"])
+        assert np.array_equal(r["send_rows"], ref["send_rows"])
+        assert np.array_equal(r["inv"][ok], ref["inv"])
+        assert np.all(r["inv"][~ok] == -1)
+        assert np.array_equal(r["dest_counts"], ref["dest_counts"])
+    states = [orc.init_state("adagrad", V, D, 3) for _ in range(3)]
+    hpar = {"lr": 0.1}
+    r1 = orc.sparse_step(states[0], "adagrad", hpar, 1, [(ids, vals)], V, P, np.zeros(P, np.int32))
+    r2 = coracle.sparse_step(states[1], "adagrad", hpar, 1, [(ids, vals)], V, P, np.zeros(P, np.int32))
+    r3 = orc.sparse_step(states[2], "adagrad", hpar, 1, [(ids[ok], vals[ok])], V, P, np.zeros(P, np.int32))
+    assert np.array_equal(states[0]["w"], states[2]["w"])
+    assert np.array_equal(states[1]["w"], states[2]["w"])
+    for r in (r1, r2):
+        assert np.array_equal(r[0]["out"][ok], r3[0]["out"])
+        assert not r[0]["out"][~ok].any()

@@ -227,3 +227,66 @@ def test_live_reference_parity(reference):
         a = hp.transform_hybrid(mine, hp.ClusterSpec(m, 1, 10.0), hp.MechanismPolicy(*pol), parts_)
         b = sp.transform_hybrid(ref, sp.ClusterSpec(m, 1, 10.0), sp.MechanismPolicy(*pol), parts_)
         assert hp.plan_to_dict(a) == sp.plan_to_dict(b)
+
+
+def test_transfer_model_golden(golden):
+    """Predicted per-GPU bytes (reference transfer_model) of the
+    one-box hybrid plans, against the reference's own outputs."""
+    assert golden["transfer"]
+    for case in golden["transfer"]:
+        g = _graph(golden, case["graph"])
+        c = hp.ClusterSpec(case["machines"], 1, 7200.0)
+        sparse = [v.name for v in g.variables if v.kind == "sparse"]
+        plan = hp.transform_hybrid(g, c, partitions={n: 8 for n in sparse})
+        assert hp.transfer_model(g, plan, c).to_rows() == case["rows"]
+
+
+def test_transfer_model_live(reference):
+    sp = reference
+    rng = np.random.default_rng(3)
+    for _ in range(100):
+        m, G = int(rng.integers(1, 7)), int(rng.integers(1, 3))
+        vs = []
+        for k in range(int(rng.integers(1, 5))):
+            kind = "dense" if rng.random() < 0.3 else "sparse"
+            alpha = 1.0 if kind == "dense" else float(rng.uniform(0.001, 1.0))
+            vs.append((f"v{k}", int(rng.integers(1, 5000)), int(rng.integers(1, 64)), alpha, kind,
+                       bool(rng.random() < 0.7)))
+        parts = {v[0]: int(rng.integers(1, min(v[1], 40) + 1)) for v in vs
+                 if v[5] and v[4] == "sparse"}
+        mine = hp.GraphSpec("g", tuple(hp.VariableSpec(*v) for v in vs), 0.0)
+        ref = sp.GraphSpec("g", tuple(sp.VariableSpec(*v) for v in vs), 0.0)
+        for arch in ("ar", "ps_naive", "ps_opt", "hybrid"):
+            cm, cr = hp.ClusterSpec(m, G, 10.0), sp.ClusterSpec(m, G, 10.0)
+            if arch == "ar":
+                a, b = hp.transform_ar(mine, cm), sp.transform_ar(ref, cr)
+            elif arch == "hybrid":
+                a, b = hp.transform_hybrid(mine, cm, None, parts), sp.transform_hybrid(ref, cr, None, parts)
+            else:
+                la = arch == "ps_opt"
+                a = hp.transform_ps(mine, cm, local_agg=la, partitions=parts)
+                b = sp.transform_ps(ref, cr, local_agg=la, partitions=parts)
+            got = hp.transfer_model(mine, a, cm).to_rows()
+            want = sp.transfer_model(ref, b, cr).to_rows()
+            assert np.allclose([[r["egress_bytes"], r["ingress_bytes"]] for r in got],
+                               [[r["egress_bytes"], r["ingress_bytes"]] for r in want], rtol=1e-12)
+
+
+def test_tune_reference_signature(golden):
+    """tune(graph, cluster, plan_builder, profile, threshold, iterations, seed):
+    the reference's positional form; the profile's compute time is added to
+    every measured sample (a constant: the argmin is unchanged)."""
+    g = _graph(golden, "lm")
+    c = hp.ClusterSpec.b200_box(8)
+
+    def measure(plan, iterations):
+        return 10 + 1000 / plan.partitions_of["embedding"] + 0.1 * plan.partitions_of["embedding"]
+
+    build = lambda p: hp.transform_hybrid(g, c, partitions={"embedding": p})  # noqa: E731
+    res = hp.tune(g, c, build, hp.ComputeProfile(compute_us_per_gpu=50.0), 0.10, 10, 0,
+                  measure=measure)
+    base = hp.tune(g, c, build, hp.ComputeProfile(), measure=measure)
+    assert res.best_p == base.best_p == 100
+    assert res.predicted_time == pytest.approx(base.predicted_time + 50.0)
+    with pytest.raises(hp.SpecError):
+        hp.ComputeProfile(compute_us_per_gpu=-1)
