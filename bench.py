@@ -244,10 +244,11 @@ def main():
         int(args.workload.split("_")[1]))
     if args.impl == "reference":
         return run_reference(args, wl)
-    if args.knob:
+    knobs = args.knob + [kv for kv in os.environ.get("HP_KNOBS", "").split(",") if kv]
+    if knobs:
         from paper_1808_02621_b200 import _lib
 
-        for kv in args.knob:
+        for kv in knobs:
             k, v = kv.split("=")
             getattr(_lib.load(), f"hp_debug_set_{k}")(int(v))
 

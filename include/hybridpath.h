@@ -113,6 +113,23 @@ void hp_debug_set_reduce_b(int b);
 /* Spin-wait budget (clock cycles) of every exchange wait before it gives up and
  * raises an error bit; <= 0 restores the default (HP_WAIT_TIMEOUT_CYCLES or ~2 s). */
 void hp_debug_set_wait_timeout(long long cycles);
+/* A/B: 1 (default) = long segments' chunks first, their upper tree levels fused
+ * into k_reduce (TMA-staged, last-arriver nodes); 0 = sorted item order and a
+ * separate k_combine. Takes effect for plans built afterwards. */
+void hp_debug_set_fuse_tree(int on);
+/* A/B: 1 (default) = chain kernels carry their stream's priority as a launch
+ * attribute (graph node priority); 0 = plain launches. */
+void hp_debug_set_launch_prio(int on);
+
+/* ---------------------------------------------------------------- CUDA graphs
+ * Instantiate a captured cudaGraph_t (e.g. torch.cuda.CUDAGraph(keep_graph=True)
+ * .raw_cuda_graph()) with cudaGraphInstantiateFlagUseNodePriority, so kernel
+ * nodes keep the priority of the stream they were captured from (every chain
+ * kernel carries it as a launch attribute): the step's plan building is
+ * dispatched ahead of the apply kernels. Launch on the caller's stream. */
+int hp_graph_instantiate(void* graph, int32_t use_node_priority, void** exec_out);
+int hp_graph_launch(void* exec, void* stream);
+int hp_graph_destroy(void* exec);
 
 /* ---------------------------------------------------------------- asynchronous errors
  * Device-side failures (an id outside [0, V), a row not homed here, an exchange

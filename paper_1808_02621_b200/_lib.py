@@ -100,6 +100,11 @@ SIGNATURES = {
     "hp_debug_fence_bench": (C.c_int, [vp, i32, i32, i32, i32, vp]),
     "hp_xchg_debug_sig": (C.c_int, [vp, vp, vp]),
     "hp_debug_set_wait_timeout": (None, [C.c_longlong]),
+    "hp_debug_set_fuse_tree": (None, [C.c_int]),
+    "hp_debug_set_launch_prio": (None, [C.c_int]),
+    "hp_graph_instantiate": (C.c_int, [vp, i32, C.POINTER(vp)]),
+    "hp_graph_launch": (C.c_int, [vp, vp]),
+    "hp_graph_destroy": (C.c_int, [vp]),
     "hp_err_host_alloc": (C.c_int, [i32, C.POINTER(vp), C.POINTER(vp)]),
     "hp_err_host_free": (C.c_int, [vp]),
     "hp_err_collect": (C.c_int, [vp, vp, i32, vp, vp]),

@@ -23,6 +23,8 @@ extern int g_dar_blocks;
 extern int g_owner_waves;
 extern int g_reduce_b;
 extern long long g_wait_cycles;
+extern int g_fuse_tree;
+int g_launch_prio = 1;
 int g_pdl = 0;  // PDL measured neutral at N=1, slower at N=2
 
 static thread_local std::string g_err;
@@ -114,6 +116,32 @@ int hp_plan_err_ptr(const void* ws, const int32_t** out) {
   return HP_OK;
 }
 
+// ---- CUDA graphs with per-node priorities (captured by the caller, e.g.
+// torch.cuda.CUDAGraph(keep_graph=True) -> raw_cuda_graph()).
+int hp_graph_instantiate(void* graph, int32_t use_node_priority, void** exec_out) {
+  HP_REQUIRE(graph && exec_out, "NULL argument");
+  cudaGraphExec_t ex = nullptr;
+  // use_node_priority: 0/1 = without/with cudaGraphInstantiateFlagUseNodePriority;
+  // > 1: raw cudaGraphInstantiate* flags (A/B)
+  const unsigned long long flags =
+      use_node_priority > 1 ? (unsigned long long)use_node_priority
+                            : (use_node_priority ? cudaGraphInstantiateFlagUseNodePriority : 0);
+  HP_CUDA(cudaGraphInstantiateWithFlags(&ex, static_cast<cudaGraph_t>(graph), flags));
+  *exec_out = ex;
+  return HP_OK;
+}
+
+int hp_graph_launch(void* exec, void* stream) {
+  HP_REQUIRE(exec, "NULL graph exec");
+  HP_CUDA(cudaGraphLaunch(static_cast<cudaGraphExec_t>(exec), static_cast<cudaStream_t>(stream)));
+  return HP_OK;
+}
+
+int hp_graph_destroy(void* exec) {
+  if (exec) HP_CUDA(cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(exec)));
+  return HP_OK;
+}
+
 int hp_version(void) { return 100; /* 0.1.0 */ }
 
 const char* hp_last_error(void) { return hp::g_err.c_str(); }
@@ -147,5 +175,7 @@ void hp_debug_set_dar_blocks(int n) { hp::g_dar_blocks = n < 0 ? 0 : n; }
 void hp_debug_set_owner_waves(int on) { hp::g_owner_waves = on ? 1 : 0; }
 void hp_debug_set_reduce_b(int b) { hp::g_reduce_b = b; }
 void hp_debug_set_wait_timeout(long long cycles) { hp::g_wait_cycles = cycles; }
+void hp_debug_set_fuse_tree(int on) { hp::g_fuse_tree = on ? 1 : 0; }
+void hp_debug_set_launch_prio(int on) { hp::g_launch_prio = on ? 1 : 0; }
 
 }  // extern "C"

@@ -166,18 +166,30 @@ __device__ __forceinline__ void emit_bounds(const DedupPlan& pl, int it, int r, 
   }
 }
 
+// Item order (no row stream, pl.nw == 0): the chunks of every long segment
+// come FIRST, at item index = their partial slot (bp + k), so the hot ids'
+// chunks run in k_reduce's first wave and the fused upper levels of their
+// trees (combine_up, the last arriver of each group) finish early instead of
+// in a separate k_combine at the tail. Long chunks carry w = -(long index + 1);
+// short items (w = 1) follow at tot_p + (short items before). With the row
+// stream (pl.nw > 0) items stay in sorted-row order (w = 0 for long chunks,
+// k_combine runs the upper levels).
 __device__ __forceinline__ void emit_items(const DedupPlan& pl, int u, int j0, int L, int dst,
-                                           int bi, int bp, int bl, int pos0) {
+                                           int bi, int bp, int bl, int pos0, int tot_p) {
   const int n0 = (L + HP_CHUNK - 1) / HP_CHUNK;
   const bool lg = L > HP_CHUNK;
+  const bool reorder = pl.fused != 0;
+  const int si = reorder ? tot_p + (bi - bp) : bi;  // index of a short segment's item
   if (L == 1) {
-    pl.items[bi] = make_int4(-(pos0 + 1), 1, dst, 1);
+    pl.items[si] = make_int4(-(pos0 + 1), 1, dst, 1);
     emit_bounds(pl, bi, j0, 1);
     return;
   }
   for (int k = 0; k < n0; ++k) {
     const int n = min(HP_CHUNK, L - k * HP_CHUNK);
-    pl.items[bi + k] = make_int4(j0 + k * HP_CHUNK, n, lg ? bp + k : dst, lg ? 0 : 1);
+    const int idx = !lg ? si + k : (reorder ? bp + k : bi + k);
+    pl.items[idx] = make_int4(j0 + k * HP_CHUNK, n, lg ? bp + k : dst,
+                              lg ? (reorder ? -(bl + 1) : 0) : 1);
     emit_bounds(pl, bi + k, j0 + k * HP_CHUNK, n);
   }
   if (lg) pl.longs[bl] = make_int4(bp, n0, dst, u);
@@ -405,7 +417,7 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
       dst = seg_dst(id, p, slot, dst_pb, route, &pl.counters[C_ERR]);
     }
     s_sig[sidx] = slot;
-    emit_items(pl, u, c * S + li, L, dst, bi_, bp_, bl_, (int)s_buf[li].y);
+    emit_items(pl, u, c * S + li, L, dst, bi_, bp_, bl_, (int)s_buf[li].y, tot_p);
     const int n0 = (L + HP_CHUNK - 1) / HP_CHUNK;
     bi_ += n0;
     if (L > HP_CHUNK) { bp_ += n0; ++bl_; }
@@ -692,7 +704,7 @@ __global__ void k_items(DedupPlan pl) {
   for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x) {
     const int j0 = pl.seg_start[u];
     emit_items(pl, u, j0, pl.seg_start[u + 1] - j0, pl.dst[u], pl.item_off[u], pl.part_off[u],
-               pl.long_tmp[u], pl.sorted_pos[j0]);
+               pl.long_tmp[u], pl.sorted_pos[j0], pl.counters[C_PARTIALS]);
   }
 }
 
@@ -714,6 +726,7 @@ size_t dedup_ws_bytes(int64_t T, int32_t D, int32_t P) {
   const int64_t nscan = (Tc + HP_SCAN_TILE - 1) / HP_SCAN_TILE + 2;
   const int64_t prow = 2 * Tc / HP_CHUNK + 2;
   size_t s = align256(4 * C_NCOUNTERS);
+  s += align256(4 * (size_t)CMB_LV * (2 * Tc / HP_CHUNK + 2));  // fused-combine arrival counters
   s += 4 * align256(4 * Tc);          // key[2], pos[2]
   s += 3 * align256(4 * (Tc + 1));    // uniq_key, seg_start, item_off
   s += 5 * align256(4 * Tc);          // segidx, sigma, part_off, dst, long_tmp
@@ -763,6 +776,8 @@ int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, i
   char* p = static_cast<char*>(ws);
   auto take = [&](size_t bytes) { void* r = p; p += align256(bytes); return r; };
   pl->counters = (int32_t*)take(4 * C_NCOUNTERS);  // first: fixed offset (hp_plan_status)
+  // right after the counters, so ONE memset per plan build clears both
+  pl->comb_ctr = (int32_t*)take(4 * (size_t)CMB_LV * (2 * Tc / HP_CHUNK + 2));
   pl->T = T;
   pl->D = D;
   pl->P = P;
@@ -798,6 +813,7 @@ int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, i
   pl->wb_row = (int32_t*)take(4 * (HP_RS_MAX_WARPS + 1));
   pl->send_info = (int4*)take(16 * Tc);
   pl->nw = g_rowstream_off ? 0 : rs_warps(D);
+  pl->fused = pl->nw <= 0 && g_fuse_tree;
   pl->sorted_pos = pl->pos[0];
   pl->prof = g_prof;
   return HP_OK;
@@ -830,6 +846,7 @@ int g_combine_blocks = 0;  // 0: one CTA per long segment up to the SM count
 int g_dar_blocks = 0;     // HP_DAR_PIPE grid (0 = one block per SM)
 int g_owner_waves = 1;    // peer-store kernels run many waves (no per-block fences)
 int g_reduce_b = 2;
+int g_fuse_tree = 1;
 HP_SPAN_SETTER(set_spans_dedup)
 
 template <int CS>
@@ -864,7 +881,11 @@ void restore_sorted_pos(DedupPlan& pl) {
 int build_plan(DedupPlan& pl, const int64_t* ids, const int32_t* owner,
                const int64_t* dst_pb, int64_t* send_ids, int32_t* counts, int32_t* inv,
                int32_t* dest_counts, int32_t* n_uniq, cudaStream_t st) {
-  HP_CUDA(cudaMemsetAsync(pl.counters, 0, 4 * C_NCOUNTERS, st));
+  // counters + the fused-combine arrival counters (contiguous, carve_plan)
+  HP_CUDA(cudaMemsetAsync(pl.counters, 0,
+                          reinterpret_cast<char*>(pl.comb_ctr) - reinterpret_cast<char*>(pl.counters) +
+                              4 * (size_t)CMB_LV * pl.partial_rows,
+                          st));
   if (pl.T == 0) {
     if (dest_counts) HP_CUDA(cudaMemsetAsync(dest_counts, 0, 4 * (size_t)pl.nranks, st));
     if (n_uniq) HP_CUDA(cudaMemsetAsync(n_uniq, 0, 4, st));

@@ -134,24 +134,38 @@ inline int grid_for(int64_t work, int per_block, int max_blocks) {
 int sm_count();
 
 extern int g_pdl;  // programmatic dependent launch on/off (hp_debug_set_pdl)
+extern int g_launch_prio;  // stream priority as a launch attribute (hp_debug_set_launch_prio)
 
+// Chain kernels are launched with cudaLaunchKernelEx carrying the launching
+// stream's priority as a per-launch attribute: captured into a CUDA graph it
+// becomes the kernel NODE's priority, which a graph instantiated with
+// cudaGraphInstantiateFlagUseNodePriority (hp_graph_instantiate) schedules by.
+// So the next step's plan (cluster dedup, highest-priority plan stream) is
+// dispatched before the table's reduce floods the SMs, instead of waiting for
+// it to drain (measured: the dedup started 16 us into the step). Plus PDL when
+// hp_debug_set_pdl(1).
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                      Args... args) {
-  if (!g_pdl) {
-    kern<<<grid, block, smem, st>>>(static_cast<KArgs>(args)...);
-    return;
-  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute at[2];
+  int na = 0, prio = 0;
+  if (g_launch_prio && cudaStreamGetPriority(st, &prio) == cudaSuccess && prio != 0) {
+    at[na].id = cudaLaunchAttributePriority;
+    at[na].val.priority = prio;
+    ++na;
+  }
+  if (g_pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = na;
   cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 

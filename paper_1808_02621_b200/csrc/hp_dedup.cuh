@@ -43,8 +43,13 @@ struct DedupPlan {
   // sorted rows [w*R, (w+1)*R), R = ceil(T / nw); wb_item[w] / wb_row[w] are
   // its first item and that item's first sorted row. nw == 0: not used.
   int32_t nw;
+  int32_t fused;        // 1: long chunks first + fused tree in k_reduce (no k_combine)
   int32_t* wb_item;     // [HP_RS_MAX_WARPS + 1]
   int32_t* wb_row;      // [HP_RS_MAX_WARPS + 1]
+  // fused upper levels of long segments (combine_up): one arrival counter per
+  // (tree node slot, level), [partial_rows][CMB_LV], zeroed with the counters
+  // at every plan build and reset by each node's last arriver
+  int32_t* comb_ctr;
   // p2p send plans: per send slot u {inbox index at its owner, owner rank,
   // slab row at the owner, 0}, filled on the plan stream (k_send_info) so the
   // push epilogue's destination is one independent 16-byte load
@@ -52,6 +57,7 @@ struct DedupPlan {
 };
 
 constexpr int HP_RS_MAX_WARPS = 4096;
+constexpr int CMB_LV = 7;  // tree levels above the chunks (n0 <= 16^7 chunks: T < 2^31)
 
 // Row-stream geometry for a row width of D floats: stages per warp (0 = the
 // row stream does not handle this width) and warps per plan.
@@ -65,6 +71,7 @@ extern int g_combine_blocks;  // k_combine grid cap for peer-store epilogues (0:
 extern int g_dar_blocks;      // HP_DAR_PIPE grid (0: one block per SM)
 extern int g_owner_waves;     // peer-store kernels: many waves (1) or one resident wave (0)
 extern int g_reduce_b;        // k_reduce rows in flight at VPT=2 (2, 4, 8)
+extern int g_fuse_tree;       // 1 (default): fused tree (long_chunk) when the row stream is off
 
 size_t dedup_ws_bytes(int64_t T, int32_t D, int32_t P);
 int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, int64_t V,

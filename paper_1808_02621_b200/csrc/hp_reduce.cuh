@@ -110,6 +110,164 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// ---- TMA bulk copies (cp.async.bulk, SASS UBLKCP) into shared memory,
+// completed on an mbarrier (transaction bytes).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "HP_MBAR_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra HP_MBAR_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared, `bytes` (multiple of 16, both 16-byte aligned), completing on bar
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// generic-proxy writes (this thread's, and those acquired from other SMs)
+// before async-proxy (TMA) reads of global memory
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Staging buffer of the long chunks (TMA): static, 16 KB, shared with the
+// short items' epilogue prefetch (s_pre), so k_reduce's shared memory per CTA
+// does not grow (the next step's cluster dedup runs beside it on the same SMs).
+constexpr int STAGE_F4 = 1024;
+// Rows staged per TMA batch: 8 rows of 2 KB at D = 512 (a chunk = 2 batches).
+__host__ __device__ constexpr int stage_rows(int D) {
+  return STAGE_F4 * 4 / D >= HP_CHUNK ? HP_CHUNK : (STAGE_F4 * 4 / D > 0 ? STAGE_F4 * 4 / D : 1);
+}
+
+// One node of a long segment's summation tree, whole CTA: rows src[0..n) (row
+// pointers from `row_of(j)`) are TMA-copied into s_stage (batches of SR rows,
+// one elected lane per row), then every column is summed in row order from
+// +0.0 and handed to `out(c4, acc)`. Callers __syncthreads() before reusing
+// s_stage. Returns the next mbarrier parity.
+template <int CPT, class RowOf, class Out>
+__device__ __forceinline__ uint32_t cta_stage_sum(float4* s_stage, uint64_t* bar, uint32_t parity,
+                                                  int n, int D4, int SR, RowOf row_of, Out out,
+                                                  bool proxy_fence) {
+  const int tid = threadIdx.x;
+  const uint32_t rowbytes = (uint32_t)D4 * 16u;
+  // (SR == HP_CHUNK for D <= 1024: one batch; wider rows take several)
+  float4 acc[CPT];  // CPT = columns per thread (D4 <= 256 * CPT)
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int j0 = 0; j0 < n; j0 += SR) {
+    const int nb = min(SR, n - j0);
+    if (tid < 32) {
+      if (proxy_fence) fence_proxy_async_global();
+      if (tid == 0) mbar_expect_tx(bar, rowbytes * (uint32_t)nb);
+      __syncwarp();
+      for (int j = tid; j < nb; j += 32) bulk_g2s(s_stage + (size_t)j * D4, row_of(j0 + j), rowbytes, bar);
+    }
+    mbar_wait(bar, parity);
+    parity ^= 1u;
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+      const int c4 = tid + k * 256;
+      if (c4 < D4)
+        for (int j = 0; j < nb; ++j) acc[k] = f4_add(acc[k], s_stage[(size_t)j * D4 + c4]);
+    }
+    if (j0 + nb < n) __syncthreads();  // the batch is consumed before the next lands
+  }
+#pragma unroll
+  for (int k = 0; k < CPT; ++k)
+    if (tid + k * 256 < D4) out(k, tid + k * 256, acc[k]);
+  return parity;
+}
+
+// A long segment's chunk, the whole CTA (level 0 + the fused upper levels).
+// The chunk's n <= 16 gradient rows are TMA-copied into shared memory in one
+// batch and summed per column in row order (one DRAM round trip instead of
+// n/B); the partial row goes to its slot. The CTA then arrives at its tree node:
+// level-l node g sums level-(l-1) items [16g, 16g+16) in order; level-l item g
+// lives in the slot of its first child (partial slot bp + g*16^l, rewritten
+// only after every child was read, by the node's last arriver), so no extra
+// storage. Each node's arrival counter is one atomic (stores; __syncthreads;
+// fence + atomic by thread 0; last arriver: fence, then TMA reads of the
+// children from L2). The node whose level holds <= 16 items is the root: its
+// last arriver applies the epilogue (optimizer update / push). Same tree as
+// oracle.tree_sum (sequential groups of 16 from +0.0, then again on the group
+// sums) and as k_combine. Long chunks are the first items (dedup.cu
+// emit_items), so the hot ids' trees close in k_reduce's first wave.
+template <int CPT, class Epi>
+__device__ __forceinline__ uint32_t long_chunk(const DedupPlan& pl, const float4* vals, const Epi& epi,
+                                               int lit, float4* s_stage, uint64_t* bar,
+                                               uint32_t parity, int* s_bc) {
+  float4* partials = reinterpret_cast<float4*>(pl.partials);
+  const int D4 = pl.D >> 2;
+  const int SR = stage_rows(pl.D);
+  const int tid = threadIdx.x;
+  const int4 item = pl.items[lit];
+  const int j0 = item.x, slot = item.z;
+  const int4 d = pl.longs[-item.w - 1];  // {bp, n0, dst, u}
+  const int64_t bp = d.x;
+  parity = cta_stage_sum<CPT>(
+      s_stage, bar, parity, item.y, D4, SR,
+      [&](int j) { return vals + (int64_t)pl.sorted_pos[j0 + j] * D4; },
+      [&](int, int c4, float4 a) { partials[(int64_t)slot * D4 + c4] = a; }, false);
+  int i = slot - d.x, n_prev = d.y, lev = 1;
+#pragma unroll 1
+  while (true) {
+    const bool root = n_prev <= HP_CHUNK;
+    const int g = root ? 0 : i / HP_CHUNK;
+    const int first = g * HP_CHUNK, nch = min(HP_CHUNK, n_prev - first);
+    const int64_t node = bp + ((int64_t)g << (4 * lev));  // this node's item slot
+    int* ctr = pl.comb_ctr + node * CMB_LV + (lev - 1);
+    __syncthreads();  // every partial store of the CTA issued; s_stage consumed
+    if (tid == 0) {
+      __threadfence();
+      s_bc[0] = atomicAdd(ctr, 1) == nch - 1;
+    }
+    __syncthreads();
+    if (!s_bc[0]) break;
+    __threadfence();
+    const int64_t cs = (int64_t)1 << (4 * (lev - 1));  // child stride in slots
+    typename Epi::Pre pre[CPT];
+    if (root && d.z >= 0) {
+#pragma unroll
+      for (int k = 0; k < CPT; ++k)
+        if (tid + k * 256 < D4) pre[k] = epi.load(d.z, tid + k * 256);
+    }
+    parity = cta_stage_sum<CPT>(
+        s_stage, bar, parity, nch, D4, SR,
+        [&](int j) { return partials + (bp + (int64_t)(first + j) * cs) * D4; },
+        [&](int k, int c4, float4 a) {
+          if (!root)
+            partials[node * D4 + c4] = a;
+          else if (d.z >= 0)
+            epi.store(d.z, c4, a, pre[k]);
+        },
+        true);
+    if (tid == 0) *ctr = 0;  // every arrival is in: reset for the plan's next apply
+    if (root) break;
+    i = g;
+    n_prev = (n_prev + HP_CHUNK - 1) / HP_CHUNK;
+    ++lev;
+  }
+  __syncthreads();  // s_stage / s_bc free for the next chunk
+  return parity;
+}
+
 // Level 0 of the summation tree. A group of TPI threads owns an item
 // {j0, n <= HP_CHUNK, dst, final}; each thread owns VPT float4 columns
 // (c4 = lane-in-group + k*TPI). Row positions are loaded once per warp and
@@ -139,13 +297,19 @@ k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
   // columns) instead of registers: ~16 fewer registers per thread at LM shapes.
   constexpr int KP = Epi::kPre;
   constexpr bool SP = reduce_smem_pre<TPI, VPT, Epi>();
-  __shared__ float4 s_pre[SP ? GPB * KP * VPT * TPI : 1];
+  constexpr int NPRE = SP ? GPB * KP * VPT * TPI : 1;
+  // long chunks: [stage_rows][D4] TMA staging; then the short items' s_pre
+  __shared__ __align__(128) float4 s_buf[NPRE > STAGE_F4 ? NPRE : STAGE_F4];
+  float4* s_pre = s_buf;
+  float4* s_stage = s_buf;
+  __shared__ uint64_t s_bar;
+  __shared__ int s_bc[1];
   float4* my_pre = s_pre + (threadIdx.x / TPI) * KP * VPT * TPI + q;  // [g][k][v][TPI]
   const int n_items = pl.counters[C_ITEMS];
-  for (int it = blockIdx.x * GPB + threadIdx.x / TPI; it < n_items; it += gridDim.x * GPB) {
+  auto process = [&](int it) -> int4 {
     const int4 item = pl.items[it];
     const int j0 = item.x, n = item.y, dst = item.z;
-    const bool fin = item.w != 0;
+    const bool fin = item.w > 0;  // < 0: chunk of long segment -w-1 (fused combine)
     typename Epi::Pre pre[SP ? 1 : VPT];
     if (fin && dst >= 0) {
       if constexpr (SP) {
@@ -204,7 +368,26 @@ k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
         partials[(int64_t)dst * D4 + c4] = acc[v];
       }
     }
+    return item;
+  };
+  // Items come long-chunks-first (pl.nw == 0, dedup.cu emit_items): the
+  // CTAs first take the long chunks, one per CTA at a time (long_chunk: TMA
+  // staging + the fused tree), then every group takes short items. Two loops
+  // keep the tree's registers out of the short-item loop, which runs spill-free.
+  const int n_long_items = pl.fused ? pl.counters[C_PARTIALS] : 0;
+  if (n_long_items > (int)blockIdx.x) {  // CTA-uniform
+    if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+    __syncthreads();
+    uint32_t parity = 0;
+#pragma unroll 1
+    for (int lit = blockIdx.x; lit < n_long_items; lit += gridDim.x)
+      parity = long_chunk<(TPI * VPT + 255) / 256>(pl, vals, epi, lit, s_stage, &s_bar, parity, s_bc);
+    __syncthreads();  // s_buf becomes s_pre
   }
+  const int stride = gridDim.x * GPB;
+#pragma unroll 1
+  for (int it = n_long_items + blockIdx.x * GPB + threadIdx.x / TPI; it < n_items; it += stride)
+    process(it);
   HP_SPAN_END(SP_REDUCE);
 }
 
@@ -490,6 +673,12 @@ void launch_rowstream(const DedupPlan& pl, const float* vals, const Epi& epi, cu
   launch_k(kern, dim3(pl.nw / 4), dim3(128), smem, st, pl, vals, epi);
 }
 
+template <int TPI, int VPT, int B, class Epi>
+void launch_k_reduce_b(const DedupPlan& pl, const float* vals, const Epi& epi, cudaStream_t st,
+                       int blocks) {
+  launch_k(k_reduce<TPI, VPT, B, Epi>, dim3(blocks), dim3(256), 0, st, pl, vals, epi);
+}
+
 template <int TPI, int VPT, class Epi>
 void launch_k_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaStream_t st) {
   // rows in flight per batch: most items hold 1-2 rows, so a small batch keeps
@@ -499,11 +688,11 @@ void launch_k_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cud
   // stores to peers; hp_debug_set_owner_waves(0) keeps those in one resident wave)
   const int blocks = grid_for(pl.T, 256 / TPI, sm_count() * (Epi::kRemote && !g_owner_waves ? 3 : 16));
   if (VPT == 2 && g_reduce_b == 4)
-    launch_k(k_reduce<TPI, VPT, 4, Epi>, dim3(blocks), dim3(256), 0, st, pl, vals, epi);
+    launch_k_reduce_b<TPI, VPT, 4>(pl, vals, epi, st, blocks);
   else if (VPT == 2 && g_reduce_b == 8)
-    launch_k(k_reduce<TPI, VPT, 8, Epi>, dim3(blocks), dim3(256), 0, st, pl, vals, epi);
+    launch_k_reduce_b<TPI, VPT, 8>(pl, vals, epi, st, blocks);
   else
-    launch_k(k_reduce<TPI, VPT, B, Epi>, dim3(blocks), dim3(256), 0, st, pl, vals, epi);
+    launch_k_reduce_b<TPI, VPT, B>(pl, vals, epi, st, blocks);
 }
 
 template <class Epi>
@@ -526,7 +715,16 @@ int launch_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaSt
     else launch_k_reduce<128, 4>(pl, vals, epi, st);
     HP_LAUNCHED(1, "k_reduce");
   }
-  // one CTA per long segment (<= T/17); hp_debug_set_combine_blocks caps it for peer epilogues
+  // fused tree (items in long-first order, pl.nw == 0): k_reduce closed every
+  // long segment itself (long_chunk); otherwise one CTA per long segment
+  if (pl.fused) {
+    if constexpr (Epi::kRemote) {
+      launch_k(k_publish<Epi>, dim3(1), dim3(64), 0, st, epi);
+      HP_LAUNCHED(1, "k_publish");
+    }
+    return HP_OK;
+  }
+  // hp_debug_set_combine_blocks caps the k_combine grid for peer epilogues
   const int cblocks = grid_for(pl.T / (HP_CHUNK + 1) + 1, 1,
                                Epi::kRemote && g_combine_blocks > 0 ? g_combine_blocks : sm_count());
   const size_t csmem = (size_t)HP_CHUNK * std::min(D4, CMB_D4) * sizeof(float4);

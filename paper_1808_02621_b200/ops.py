@@ -91,6 +91,59 @@ class ErrorWords:
             self._host = None
 
 
+class StepGraph:
+    """A CUDA graph captured with torch (``torch.cuda.CUDAGraph(keep_graph=True)``,
+    so torch's private memory pool and stream bookkeeping apply) and
+    instantiated by the library with per-node priorities
+    (``hp_graph_instantiate``): each kernel node keeps the priority of the
+    stream it was captured on, so the plan streams' dedup is dispatched ahead
+    of the tables' reduce instead of after it drains. ``node_priority=False``
+    instantiates without the flag (A/B). ``replay()`` launches on the current stream."""
+
+    def __init__(self, node_priority: bool = True):
+        import os
+
+        # HP_STEPGRAPH=0 (default): torch instantiates and replays (measured:
+        # launching through the library's own runtime made every replay ~15 us
+        # slower, r2m); 1: library instantiate with node priorities; 2: torch
+        # instantiate, library launch; F > 2: raw instantiate flags F (A/B)
+        self.mode = int(os.environ.get("HP_STEPGRAPH", "0"))
+        self.torch_replay = self.mode == 0
+        self.graph = torch.cuda.CUDAGraph(keep_graph=not self.torch_replay)
+        self.node_priority = node_priority
+        self._exec = None
+        self._owned = True
+
+    def capture(self):
+        return torch.cuda.graph(self.graph)
+
+    def _instantiate(self) -> None:
+        if self.mode == 2:
+            self.graph.instantiate()
+            self._exec, self._owned = self.graph.raw_cuda_graph_exec(), False
+            return
+        ex = C.c_void_p()
+        flags = self.mode if self.mode > 2 else int(self.node_priority)
+        call("hp_graph_instantiate", self.graph.raw_cuda_graph(), flags, C.byref(ex))
+        self._exec = ex.value
+
+    def replay(self) -> None:
+        if self.torch_replay:
+            self.graph.replay()
+            return
+        if self._exec is None:
+            self._instantiate()
+        call("hp_graph_launch", self._exec, _stream())
+
+    def __del__(self):
+        if getattr(self, "_exec", None) and getattr(self, "_owned", False):
+            try:
+                load().hp_graph_destroy(self._exec)
+            except Exception:  # interpreter teardown
+                pass
+            self._exec = None
+
+
 def plan_err_ptr(ws: "Workspace") -> int | None:
     """Device address of the error word of the plan in ``ws`` (None if unsized)."""
     if ws.nbytes == 0:

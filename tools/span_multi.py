@@ -34,6 +34,9 @@ comm = hp.Comm.from_torch_distributed()
 graph = hp.load_graph_spec(json.dumps(wl.graph_json()))
 cluster = hp.ClusterSpec.b200_box(world)
 plan = hp.transform_hybrid(graph, cluster, partitions={t.name: 8 for t in wl.tables})
+for kv in filter(None, os.environ.get("HP_KNOBS", "").split(",")):  # before the first plan
+    k, v = kv.split("=")
+    getattr(_lib.load(), f"hp_debug_set_{k}")(int(v))
 runner = hp.HybridRunner(plan, graph, cluster, rank=rank, world_size=world, comm=comm,
                          optimizer=hp.OptimizerConfig(**wl.optimizer), device=dev)
 bs = []
@@ -42,6 +45,9 @@ for s in (1, 2):
     bs.append({k: ((torch.from_numpy(v[0]).to(dev), torch.from_numpy(v[1]).to(dev))
                    if isinstance(v, tuple) else torch.from_numpy(v).to(dev)) for k, v in b.items()})
 lib = _lib.load()
+for kv in filter(None, os.environ.get("HP_KNOBS", "").split(",")):  # A/B switches
+    k, v = kv.split("=")
+    getattr(lib, f"hp_debug_set_{k}")(int(v))
 span = torch.zeros(32, dtype=torch.int64, device=dev)
 graphs = None
 if use_graph:
