@@ -75,7 +75,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rotations", type=int, default=0, help="distinct resident batches")
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--steps-per-graph", type=int, default=2,
+    ap.add_argument("--steps-per-graph", type=int, default=3,
                     help="consecutive steps captured in one CUDA graph (divides the rotation)")
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
@@ -292,7 +292,9 @@ def main():
     per_batch = sum(v[0].nbytes + v[1].nbytes if isinstance(v, tuple) else v.nbytes
                     for v in host[0].values())
     R = args.rotations or max(2, int(np.ceil(2 * 126e6 / max(per_batch, 1))))
-    R = min(R + (R % 2), 16)  # even: the pipelined graphs alternate two plan slots
+    # the pipelined graphs rotate lookahead + 1 plan slots (plans built 2 steps
+    # ahead: 3 slots) and the rotation must be even: a multiple of 6
+    R = min(-(-R // 6) * 6, 18) if not args.rotations else R
     host += [make_batch(wl, seed=1 + i, rank=rank) for i in range(1, R)]
 
     def to_dev(b):

@@ -79,7 +79,8 @@ class LocalComm:
         pass
 
 
-def step_all(runners: list, streams: list, batches: list, next_batches: list | None = None) -> None:
+def step_all(runners: list, streams: list, batches: list, next_batches: list | None = None,
+             upcoming: list | None = None) -> None:
     """One hybrid step of every emulated rank, each on its own stream (the
     ranks' device waits depend on each other, so all are enqueued before any
     is waited for), then a device synchronisation."""
@@ -90,7 +91,8 @@ def step_all(runners: list, streams: list, batches: list, next_batches: list | N
     for r, (run, s) in enumerate(zip(runners, streams)):
         with torch.cuda.stream(s):
             run.step(batches[r], timed=False,
-                     next_batch=None if next_batches is None else next_batches[r])
+                     next_batch=None if next_batches is None else next_batches[r],
+                     upcoming=None if upcoming is None else upcoming[r])
     torch.cuda.synchronize()
 
 
@@ -103,10 +105,17 @@ def capture_pipelined_all(runners: list, streams: list, batches: list,
     import torch
 
     R = len(batches[0])
+    L = runners[0].lookahead
+    while L > 1 and R % (L + 1):
+        L -= 1
     for run, b in zip(runners, batches):
+        run.lookahead = L
+        for tab in run.tables.values():
+            tab.pending.clear()
         run.prefetch(b[0])
     for r in range(R):
-        step_all(runners, streams, [b[r] for b in batches], [b[(r + 1) % R] for b in batches])
+        step_all(runners, streams, [b[r] for b in batches],
+                 upcoming=[[b[(r + 1 + i) % R] for i in range(L)] for b in batches])
     torch.cuda.synchronize()
     return [run.capture_pipelined(b, steps_per_graph, warm=False) for run, b in zip(runners, batches)]
 

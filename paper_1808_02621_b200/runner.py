@@ -40,7 +40,7 @@ class ShardedTable:
 
     def __init__(self, var: VariableSpec, partitions: int, owner: np.ndarray, rank: int,
                  optimizer: OptimizerConfig, device, seed: int = 0, init_scale: float = 0.05,
-                 w_storage=None):
+                 w_storage=None, plan_slots: int = 3):
         if var.elem_bytes % 16:
             raise SpecError(f"table {var.name!r}: row bytes must be a multiple of 16 (D % 4 == 0)")
         self.var = var
@@ -71,10 +71,12 @@ class ShardedTable:
         elif optimizer.kind == "adam":
             for s in self.state:
                 s.zero_()
-        # two plan workspaces: the plan of step i+1 is built while step i applies
-        self.wss = [Workspace(self.device), Workspace(self.device)]
-        self.ready = None       # slot holding a prefetched plan, or None
-        self.ready_ids = None   # the ids tensor that plan was built from
+        # plan workspaces (HybridRunner.lookahead + 1): the plans of the next
+        # steps are built while this one applies; step k's plan lives in slot
+        # k % (lookahead + 1)
+        self.wss = [Workspace(self.device) for _ in range(max(plan_slots, 2))]
+        self.applied = 0        # number of this table's next step
+        self.pending: dict = {}  # step number -> (ids tensor, slot, event | None)
         self.step_count = 0
 
     @property
@@ -203,7 +205,7 @@ class HybridRunner:
                 storage = self._make_window(var, P, owner, (max_ids or {}).get(var.name))
             self.tables[var.name] = ShardedTable(var, P, owner, rank, self.optimizer,
                                                  self.device, seed=seed * 1000 + i,
-                                                 w_storage=storage)
+                                                 w_storage=storage, plan_slots=3)
         self._scratch: dict[str, _Scratch] = {n: _Scratch() for n in self.tables}
         if self.optimizer.kind == "adam":  # step size read on the device: graph-safe
             steps = np.arange(1 << 16, dtype=np.float64)
@@ -236,7 +238,13 @@ class HybridRunner:
         self._plan_streams = {n: torch.cuda.Stream(device=self.device, priority=pp)
                               for n in self.tables}
         self._pending_counts: dict = {}
+        self._ps_used: set = set()  # plan streams forked since the last join
         self.concurrent_tables = True
+        # Plans built ahead (pipelined steps): with lookahead L the dedup of step
+        # k + L runs on the plan streams during step k, so a step never waits for
+        # the next plan (the latency-bound cluster sort, ~28 us at LM1B shapes,
+        # was the N=1 step's critical path with L = 1). Slots: L + 1 <= 3.
+        self.lookahead = min(max(int(os.environ.get("HP_LOOKAHEAD", "2")), 1), 2)
         # captured steps run with per-node priorities (ops.StepGraph)
         self.graph_node_priority = os.environ.get("HP_GRAPH_NODE_PRIORITY", "1") != "0"
         # device error bits -> pinned host words (one per table stream + dense),
@@ -496,7 +504,8 @@ class HybridRunner:
         self.last_counts[name] = {"send": send_c, "recv": recv_c}
         return out
 
-    def step(self, batch: dict, timed: bool = True, next_batch: dict | None = None) -> IterationStats:
+    def step(self, batch: dict, timed: bool = True, next_batch: dict | None = None,
+             upcoming: list | None = None) -> IterationStats:
         """One synchronous hybrid step.
 
         ``batch[name]`` is ``(ids int64[T], vals f32[T, D])`` for a sparse Weight
@@ -504,11 +513,15 @@ class HybridRunner:
         rows land in ``self.outputs[name]``; averaged dense gradients in
         ``self.dense_out[name]``.
 
-        ``next_batch`` (optional): the batch of the following step. Its dedup /
-        routing plan (which depends only on its ids) is built on a side stream
-        while this step applies, into the other plan slot; the following
-        ``step(next_batch)`` then skips its dedup. Results are identical.
+        ``next_batch`` (optional): the batch of the following step, or
+        ``upcoming``: the batches of the following steps, in order. Their dedup
+        / routing plans (which depend only on their ids) are built on the plan
+        streams while this step applies, up to ``lookahead`` steps ahead, each
+        into its own plan slot; those steps then skip their dedup. Results are
+        identical.
         """
+        ahead = list(upcoming) if upcoming is not None else (
+            [next_batch] if next_batch is not None else [])
         self.check_errors()
         self.step_count += 1
         stream = torch.cuda.current_stream()
@@ -534,23 +547,10 @@ class HybridRunner:
             # The reference serialises these phases; overlap
             # is its named extension point.
             joins = []
-            # The next step's plans first (enqueue order = node order in a
-            # captured graph): their cluster dedup is latency-bound and on the
-            # step's critical path; enqueued after the tables' reduce it was
-            # dispatched only once the reduce drained from the SMs (spans:
-            # dedup [16.7, 43.4] us of a 43 us step). The slot it writes was
-            # last read by the previous step, which the main stream has joined.
-            nxt_slot = {}
-            if next_batch is not None and self.pipelined:
-                for name, tab in self.tables.items():
-                    ids = batch[name][0]
-                    use = tab.ready if (tab.ready is not None and tab.ready_ids is ids) else 0
-                    ps = self._plan_streams[name]
-                    ps.wait_stream(stream)
-                    with torch.cuda.stream(ps):
-                        self._plan(tab, next_batch[name][0], use ^ 1)
-                    nxt_slot[name] = use ^ 1
-                    joins.append(ps)
+            # Plans of the upcoming steps first (enqueue order = node order in a
+            # captured graph; the cluster dedup is latency-bound). Each is
+            # waited for by the step that applies it (an event), not joined here.
+            self._plan_ahead(ahead, stream)
             if self.dense:
                 self._dense_stream.wait_stream(stream)
                 with torch.cuda.stream(self._dense_stream):
@@ -560,11 +560,12 @@ class HybridRunner:
             for name, tab in self.tables.items():
                 side = self._streams[name]
                 side.wait_stream(stream)
+                slot, planned, evt = self._take_plan(tab, batch[name][0])
+                if evt is not None:
+                    side.wait_event(evt)
                 with torch.cuda.stream(side):
-                    self.outputs[name] = self._sparse(tab, batch[name])
+                    self.outputs[name] = self._sparse(tab, batch[name], None, slot, planned)
                 joins.append(side)
-                if name in nxt_slot:
-                    tab.ready, tab.ready_ids = nxt_slot[name], next_batch[name][0]
             for side in joins:
                 stream.wait_stream(side)
             ev("network" if self.world_size > 1 else "update")
@@ -574,12 +575,9 @@ class HybridRunner:
                 self._dense(batch)
                 ev("network")
             for name, tab in self.tables.items():
-                self.outputs[name] = self._sparse(tab, batch[name], ev)
-            if next_batch is not None and self.pipelined:  # next plans, same stream
-                for name, tab in self.tables.items():
-                    nxt = tab.last_slot ^ 1
-                    self._plan(tab, next_batch[name][0], nxt)
-                    tab.ready, tab.ready_ids = nxt, next_batch[name][0]
+                slot, planned, _ = self._take_plan(tab, batch[name][0])
+                self.outputs[name] = self._sparse(tab, batch[name], ev, slot, planned)
+            self._plan_ahead(ahead, None)  # same stream, after the tables
         if timed:
             stream.synchronize()
             for name, (sc, rc) in self._pending_counts.items():
@@ -646,7 +644,8 @@ class HybridRunner:
                 self.dense_out[var.name] = out
             self._kev(f"k7:{var.name}", False)
 
-    def _sparse(self, tab: ShardedTable, ids_vals, ev=None) -> torch.Tensor:
+    def _sparse(self, tab: ShardedTable, ids_vals, ev=None, slot: int = 0,
+                planned: bool = False) -> torch.Tensor:
         ids, vals = ids_vals
         tab.step_count += 1
         if self.optimizer.kind == "adam":
@@ -655,9 +654,6 @@ class HybridRunner:
                                           tab.step_dev)
         else:
             opt = self.optimizer.c_struct(tab.step_count, self.scale)
-        planned = tab.ready is not None and tab.ready_ids is ids
-        slot = tab.ready if planned else 0
-        tab.ready = tab.ready_ids = None
         if self.world_size == 1:
             out = self._sparse_local(tab, ids, vals, opt, slot, planned)
             if ev:
@@ -672,8 +668,59 @@ class HybridRunner:
                 ev("network")
         else:
             out = self._sparse_exchange(tab, ids, vals, opt, ev or (lambda _p: None))
-        tab.last_slot = slot
         return out
+
+    @property
+    def plan_slots(self) -> int:
+        return self.lookahead + 1
+
+    def _take_plan(self, tab: ShardedTable, ids):
+        """(slot, planned, event) of this table's current step; advances its step
+        number. A plan built ahead for different ids is discarded."""
+        k = tab.applied
+        tab.applied += 1
+        ent = tab.pending.pop(k, None)
+        if ent is not None and ent[0] is ids:
+            return ent[1], True, ent[2]
+        return k % self.plan_slots, False, None
+
+    def _plan_ahead(self, ahead: list, stream) -> None:
+        """Build the plans of the next ``lookahead`` steps that are not built yet,
+        on each table's plan stream (``stream`` given: after it, with an event
+        for the consumer) or on the current stream (``stream`` None)."""
+        if not ahead or not self.pipelined:
+            return
+        for name, tab in self.tables.items():
+            k = tab.applied
+            waited = False
+            for i, b in enumerate(ahead[:self.lookahead]):
+                sn, ids = k + 1 + i, b[name][0]
+                ent = tab.pending.get(sn)
+                if ent is not None and ent[0] is ids:
+                    continue
+                slot = sn % self.plan_slots  # last read by step sn - slots < k: done
+                if stream is None:
+                    self._plan(tab, ids, slot)
+                    tab.pending[sn] = (ids, slot, None)
+                    continue
+                ps = self._plan_streams[name]
+                if not waited:
+                    ps.wait_stream(stream)
+                    waited = True
+                    self._ps_used.add(name)
+                with torch.cuda.stream(ps):
+                    self._plan(tab, ids, slot)
+                e = torch.cuda.Event()
+                e.record(ps)
+                tab.pending[sn] = (ids, slot, e)
+
+    def _join_plan_streams(self) -> None:
+        """The current stream waits for the plan streams used since the last
+        join (end of a capture: only streams forked into it may be joined)."""
+        cur = torch.cuda.current_stream()
+        for name in sorted(self._ps_used):
+            cur.wait_stream(self._plan_streams[name])
+        self._ps_used.clear()
 
     @property
     def pipelined(self) -> bool:
@@ -698,7 +745,7 @@ class HybridRunner:
                 self._buf(name, "ar_ids", (n * T,), torch.int64)
                 self._buf(name, "ar_vals", (n * T, tab.D), torch.float32)
             elif n > 1 and self.exchange == "p2p":
-                for slot in (0, 1):
+                for slot in range(len(tab.wss)):
                     self._p2p_bufs(tab, slot)
                 self._buf(name, "recv_counts", (n,), torch.int32)
         for var in self.dense:
@@ -710,13 +757,14 @@ class HybridRunner:
         torch.cuda.synchronize(self.device)
 
     def prefetch(self, batch: dict) -> None:
-        """Build the plans of ``batch`` now (stream-ordered) so its step skips dedup."""
+        """Build the plans of ``batch`` (the next step's) now, on the current
+        stream, so its step skips dedup."""
         if not self.pipelined:
             return
         for name, tab in self.tables.items():
-            ids = batch[name][0]
-            self._plan(tab, ids, 0)
-            tab.ready, tab.ready_ids = 0, ids
+            ids, k = batch[name][0], tab.applied
+            self._plan(tab, ids, k % self.plan_slots)
+            tab.pending[k] = (ids, k % self.plan_slots, None)
 
     def predicted_transfer(self) -> TransferReport:
         """The reference's closed-form per-GPU bytes of this plan
@@ -763,7 +811,7 @@ class HybridRunner:
         if self.world_size > 1 and self.exchange != "p2p":
             raise NotImplementedError("the NCCL a2a-v path reads counts on the host")
         for tab in self.tables.values():
-            tab.ready = tab.ready_ids = None
+            tab.pending.clear()
         cur = torch.cuda.current_stream()
         side = torch.cuda.Stream(device=self.device)
         side.wait_stream(cur)
@@ -784,8 +832,11 @@ class HybridRunner:
         consecutive steps (batches[G·r … G·r+G-1]), so the step boundary inside
         it is a dependency edge instead of a graph launch.
 
-        Replay them in order, repeatedly. ``len(batches)`` must be even (the
-        plan slots alternate) and a multiple of G. The first plan is built
+        Replay them in order, repeatedly (and only replay them: the runner's
+        host-side plan bookkeeping then describes the replays, not eager
+        steps). ``len(batches)`` must be even and a multiple of G; the plan
+        lookahead is the deepest L <= ``lookahead`` whose L + 1 slots divide it
+        (6 batches: 2 steps ahead). The first plan is built
         eagerly here, followed by one eager rotation that sizes every buffer;
         ``warm=False`` skips both (the caller ran them, e.g. every emulated rank
         of :mod:`.emulate` interleaved, since their waits depend on each other).
@@ -796,21 +847,43 @@ class HybridRunner:
             raise ValueError("capture_pipelined needs an even number (>= 2) of batches")
         if G < 1 or R % G:
             raise ValueError("steps_per_graph must divide the number of batches")
+        # slot of step k = k % (L + 1) must be periodic in the rotation: the
+        # deepest lookahead L <= self.lookahead with R % (L + 1) == 0
+        L = self.lookahead
+        while L > 1 and R % (L + 1):
+            L -= 1
+        if L != self.lookahead:
+            if not warm:
+                raise ValueError(f"{R} batches do not rotate {self.lookahead + 1} plan slots")
+            self.lookahead = L
+
+        def ahead(j):
+            return [batches[(j + 1 + i) % R] for i in range(L)]
+
         if self.world_size > 1 and self.exchange != "p2p":
             raise NotImplementedError("the NCCL a2a-v path reads counts on the host")
         # (the AR-sparse / PS-dense baselines are not pipelined: each graph then
         # plans its own batch; prefetch() and next_batch are no-ops for them)
         if warm:
+            for tab in self.tables.values():
+                tab.pending.clear()
             self.prefetch(batches[0])
             for r in range(R):  # eager warm-up rotation (sizes every buffer)
-                self.step(batches[r], timed=False, next_batch=batches[(r + 1) % R])
+                self.step(batches[r], timed=False, upcoming=ahead(r))
             torch.cuda.synchronize()
         graphs = []
         for r in range(0, R, G):
+            # plans pending from before this capture: built by the eager warm-up
+            # (synchronised) or by the previous graph (which precedes this one in
+            # stream order at replay): no event to wait for inside the capture
+            for tab in self.tables.values():
+                tab.pending = {k: (ids, slot, None) for k, (ids, slot, _) in tab.pending.items()}
             g = ops.StepGraph(self.graph_node_priority)
+            self._ps_used = set()
             with g.capture():
                 for j in range(r, r + G):
-                    self.step(batches[j], timed=False, next_batch=batches[(j + 1) % R])
+                    self.step(batches[j], timed=False, upcoming=ahead(j))
+                self._join_plan_streams()  # a capture ends with every stream joined
             graphs.append(g)
         return graphs
 

@@ -24,10 +24,11 @@ def test_bench_config_bit_exact(cuda, workload):
     plan = hp.transform_hybrid(graph, cluster, partitions={t.name: wl.partitions for t in wl.tables})
     runner = hp.HybridRunner(plan, graph, cluster, optimizer=hp.OptimizerConfig(**wl.optimizer),
                              device=cuda, seed=0)
-    host = [make_batch(wl, seed=1 + i, rank=0) for i in range(4)]
+    host = [make_batch(wl, seed=1 + i, rank=0) for i in range(6)]  # 3 plan slots: 2 ahead
     dev = [{k: ((torch.from_numpy(v[0]).to(cuda), torch.from_numpy(v[1]).to(cuda))
                 if isinstance(v, tuple) else torch.from_numpy(v).to(cuda)) for k, v in b.items()}
            for b in host]
-    out = check_runner_n1(runner, wl, host, dev, steps_per_graph=2, replays=2)
+    out = check_runner_n1(runner, wl, host, dev, steps_per_graph=2, replays=1)
+    assert runner.lookahead == 2
     assert out["steps"] == 12 and all(v > 1000 for v in out["rows"].values())
     runner.close()

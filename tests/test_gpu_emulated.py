@@ -235,31 +235,34 @@ def test_emulated_empty_rank_and_bf16_dense(cuda):
         emu.close()
 
 
-@pytest.mark.parametrize("n", [2, 4])
-def test_emulated_graph_replays_bit_exact(cuda, n):
+@pytest.mark.parametrize("n,R", [(2, 2), (4, 2), (2, 6)])
+def test_emulated_graph_replays_bit_exact(cuda, n, R):
     """The pipelined CUDA-graph rotation (bench.py's timed path) of every rank,
-    replayed concurrently, with 1 and 2 steps per graph."""
+    replayed concurrently, with 1 and 2 steps per graph; R = 6 batches run
+    the plans 2 steps ahead (3 plan slots), R = 2 one step ahead."""
     from paper_1808_02621_b200.emulate import capture_pipelined_all, replay_all
 
     emu = Emu(cuda, n, _small_tables(), {"lstm": 100_000}, "adagrad", "p2p-sm",
               concurrent=n == 2)
     try:
-        data = [emu.batches(s) for s in (11, 12)]
+        data = [emu.batches(s) for s in range(11, 11 + R)]
         emu.init_oracle([b for h, _ in data for b in h])
-        rot = [[data[k][1][r] for k in range(2)] for r in range(n)]
-        graphs = capture_pipelined_all(emu.runners, emu.streams, rot)  # eager: batch 0, 1
-        emu.oracle_step(data[0][0])
-        emu.oracle_step(data[1][0])
+        rot = [[data[k][1][r] for k in range(R)] for r in range(n)]
+        graphs = capture_pipelined_all(emu.runners, emu.streams, rot)  # eager rotation
+        assert emu.runners[0].lookahead == (2 if R == 6 else 1)
+        for k in range(R):
+            emu.oracle_step(data[k][0])
         for _ in range(2):
-            for k in range(2):
+            for k in range(R):
                 replay_all(graphs, emu.streams, k)
                 emu.check_outputs(emu.oracle_step(data[k][0]))
         multi = capture_pipelined_all(emu.runners, emu.streams, rot, steps_per_graph=2)
-        emu.oracle_step(data[0][0])
-        emu.oracle_step(data[1][0])
-        replay_all(multi, emu.streams, 0)
-        emu.oracle_step(data[0][0])
-        emu.check_outputs(emu.oracle_step(data[1][0]))
+        for k in range(R):
+            emu.oracle_step(data[k][0])
+        for g in range(R // 2):
+            replay_all(multi, emu.streams, g)
+            emu.oracle_step(data[2 * g][0])
+            emu.check_outputs(emu.oracle_step(data[2 * g + 1][0]))
         emu.check_tables()
         emu.errors()
         del graphs, multi

@@ -8,4 +8,4 @@ run() {  # name env...
   python -c "
 import json; d=json.loads(open('gpurun_out/${T}_$name.json').read().strip().splitlines()[-1]); print('$name', round(d['ms_per_step']*1e3,2), {k:round(v,1) for k,v in d['kernels_us'].items()})" || tail -3 gpurun_out/${T}_$name.err
 }
-for spec in "$@"; do name=${spec%%:*}; envs=${spec#*:}; run $name $envs; done
+for spec in "$@"; do name=${spec%%:*}; envs=${spec#*:}; run $name ${envs//+/ }; done
