@@ -105,8 +105,9 @@ def peaks() -> dict:
 def k4_traffic(workload: str, table: str):
     """DRAM bytes (read + write) per K4 launch pair from the committed ncu capture
     (profiles/r1b_k4_traffic.json), for the workload/table it was taken on."""
-    p = ROOT / "profiles" / "r1b_k4_traffic.json"
-    if not p.exists():
+    p = next((q for q in (ROOT / "profiles" / "r2_k4_traffic.json",
+                          ROOT / "profiles" / "r1b_k4_traffic.json") if q.exists()), None)
+    if p is None:
         return None
     d = json.loads(p.read_text())
     if d.get("workload") != workload or d.get("table") != table:
@@ -404,18 +405,26 @@ def main():
         ops.apply_plan_build(batches[0][big.name][0], tab.slab(), tab.ws)
         U = int(tab.ws.buf[:4].view(torch.int32).item())
         k = 1 + opt.n_state
+        # K4 + K5 (world 1: apply with the pull fused, hp_apply_plan_pull): gradient
+        # rows + positions read, each unique row's state read + written (k tensors),
+        # every position's pulled row written. Other worlds: K4 alone.
+        fused_pull = world == 1
         algo = T * (4 + 4 * big.D) + U * (4 + 4 * big.D * 2 * k)
+        if fused_pull:
+            algo += T * 4 * big.D
         us = kern[f"k4:{big.name}"]
         achieved = algo / (us * 1e-6) / 1e9
-        roof = {"kernel": f"K4 merge+apply ({big.name}, k_reduce+k_combine)", "bound": "hbm",
+        roof = {"kernel": (f"K4+K5 merge+apply+pull ({big.name}: k_reduce with the fused tree and "
+                           "pull, k_bcast_rows for the long segments)" if fused_pull else
+                           f"K4 merge+apply ({big.name})"), "bound": "hbm",
                 "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"], "traffic": k4_traffic(wl.name, big.name),
                 "algorithmic_bytes": algo, "launch_us": us, "peak_src": pk["src"],
                 "unique_rows": U, "T": T,
                 "step_share": us / (t_dev / args.steps * 1e6)}
         gk = f"k5:{big.name}"
-        if gk in kern:
-            g_algo = T * 8 + U * 4 * big.D + T * 4 * big.D
+        if gk in kern:  # the pull through the plan: positions + unique rows read + rows written
+            g_algo = T * 4 + U * 4 * big.D + T * 4 * big.D
             roof["gather"] = {"launch_us": kern[gk], "algorithmic_bytes": g_algo,
                               "achieved": g_algo / (kern[gk] * 1e-6) / 1e9}
         # the whole step against HBM: every kernel's algorithmic bytes once
@@ -427,8 +436,7 @@ def main():
             Tt = t.T + t.sampled
             ops.apply_plan_build(batches[0][t.name][0], tb.slab(), tb.ws)
             Ut = int(tb.ws.buf[:4].view(torch.int32).item())
-            step_bytes += Tt * (4 + 4 * t.D) + Ut * (4 + 4 * t.D * 2 * k)
-            step_bytes += Tt * 8 + Ut * 4 * t.D + Tt * 4 * t.D
+            step_bytes += Tt * (4 + 4 * t.D) + Ut * (4 + 4 * t.D * 2 * k) + Tt * 4 * t.D
         step_us = t_dev / args.steps * 1e6
         roof["step"] = {"algorithmic_bytes": step_bytes, "us": step_us,
                         "achieved": step_bytes / (step_us * 1e-6) / 1e9,

@@ -120,6 +120,8 @@ void hp_debug_set_fuse_tree(int on);
 /* A/B: 1 (default) = chain kernels carry their stream's priority as a launch
  * attribute (graph node priority); 0 = plain launches. */
 void hp_debug_set_launch_prio(int on);
+/* A/B: hp_plan_stitch through TMA bulk copies (1, default) or registers (0). */
+void hp_debug_set_bcast_tma(int on);
 
 /* ---------------------------------------------------------------- CUDA graphs
  * Instantiate a captured cudaGraph_t (e.g. torch.cuda.CUDAGraph(keep_graph=True)
@@ -208,6 +210,16 @@ int hp_apply_plan_build(const int64_t* ids, int64_t R, hp_slab slab, void* ws, s
 int hp_apply_plan(const float* rows, int64_t R, hp_slab slab, hp_optim opt, void* ws,
                   size_t ws_bytes, void* stream);
 
+/* K4 + K5 fused (n == 1): hp_apply_plan, and out[t] (t < R) = the updated row of
+ * position t's id (a zero row for a dropped id). With the default plans (long
+ * segments first, fused tree) the apply epilogue writes every position itself
+ * — short segments from registers, long ones by TMA bulk stores of the root —
+ * so the pull costs no kernel, no re-read of the updated rows and no routing;
+ * otherwise hp_plan_stitch runs after the apply. Replaces: update + pull
+ * (`simulate.py:195-199,294-323`). */
+int hp_apply_plan_pull(const float* rows, int64_t R, hp_slab slab, hp_optim opt, float* out,
+                       void* ws, size_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------- K5 / K6
  * Gather: out[i] = slab row of global id ids[i], i < n (coalesced row copy); a
  * zero row for an id outside [0, V) or not homed on this rank.
@@ -221,6 +233,15 @@ int hp_gather_rows(hp_slab slab, const int64_t* ids, int64_t n, const int32_t* n
  * (`PAPER.md:473`, `simulate.py:317-323` "stitch" term). */
 int hp_stitch(const float* rows, const int32_t* inv, int64_t T, int32_t D, float* out,
               void* stream);
+
+/* K5 / K6 from the step's dedup plan (ws, built for the same T, D, V, P):
+ * out[t] = rows[d(t)], d(t) = the plan destination of position t's segment —
+ * a slab row for an apply plan (rows = the slab: the pull), a send slot for a
+ * send plan (rows = the returned rows: the stitch); a zero row for a dropped id.
+ * Each unique row is read once per plan item and broadcast to its positions by
+ * TMA bulk copies. Replaces: PS pull + stitch (`simulate.py:195-199`). */
+int hp_plan_stitch(const void* ws, size_t ws_bytes, int64_t T, int32_t D, int64_t V, int32_t P,
+                   const float* rows, float* out, void* stream);
 
 /* Deterministic table init: rows [row_lo, row_lo+nrows) of a D-wide table,
  * uniform[-scale, scale) from a counter hash of (seed, row, col). */
@@ -329,6 +350,8 @@ int hp_xchg_recv_counts(hp_xchg_t x, int32_t* out_dev, void* stream);
 int hp_xchg_status(hp_xchg_t x, int32_t* out_err, void* stream);
 /* Device address of the exchange's error word (for hp_err_collect). */
 int hp_xchg_err_ptr(hp_xchg_t x, const int32_t** out);
+/* Device address of the return rows [cap][D] (indexed by this rank's send slot). */
+int hp_xchg_ret_ptr(hp_xchg_t x, float** out);
 /* Single-process emulation of n ranks (parity tests on ONE GPU): instead of
  * cudaIpc handles, peers are set from the raw window addresses of the other
  * emulated ranks' exchanges in this process. Same kernels and protocol. */

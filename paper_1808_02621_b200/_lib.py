@@ -102,7 +102,11 @@ SIGNATURES = {
     "hp_debug_set_wait_timeout": (None, [C.c_longlong]),
     "hp_debug_set_fuse_tree": (None, [C.c_int]),
     "hp_debug_set_launch_prio": (None, [C.c_int]),
+    "hp_debug_set_bcast_tma": (None, [C.c_int]),
     "hp_graph_instantiate": (C.c_int, [vp, i32, C.POINTER(vp)]),
+    "hp_plan_stitch": (C.c_int, [vp, sz, i64, i32, i64, i32, vp, vp, vp]),
+    "hp_apply_plan_pull": (C.c_int, [vp, i64, Slab, Optim, vp, vp, sz, vp]),
+    "hp_xchg_ret_ptr": (C.c_int, [vp, C.POINTER(vp)]),
     "hp_graph_launch": (C.c_int, [vp, vp]),
     "hp_graph_destroy": (C.c_int, [vp]),
     "hp_err_host_alloc": (C.c_int, [i32, C.POINTER(vp), C.POINTER(vp)]),

@@ -171,9 +171,10 @@ __device__ __forceinline__ void emit_bounds(const DedupPlan& pl, int it, int r, 
 // chunks run in k_reduce's first wave and the fused upper levels of their
 // trees (combine_up, the last arriver of each group) finish early instead of
 // in a separate k_combine at the tail. Long chunks carry w = -(long index + 1);
-// short items (w = 1) follow at tot_p + (short items before). With the row
-// stream (pl.nw > 0) items stay in sorted-row order (w = 0 for long chunks,
-// k_combine runs the upper levels).
+// short items (w = 1) follow at tot_p + (short items before). Without the
+// fused tree (pl.fused == 0) items stay in sorted-row order (long chunks not final,
+// k_combine runs the upper levels). Every long chunk carries its segment's
+// long index (w = -(li+1)): the stitch (k_bcast_rows) finds the segment's row.
 __device__ __forceinline__ void emit_items(const DedupPlan& pl, int u, int j0, int L, int dst,
                                            int bi, int bp, int bl, int pos0, int tot_p) {
   const int n0 = (L + HP_CHUNK - 1) / HP_CHUNK;
@@ -188,11 +189,10 @@ __device__ __forceinline__ void emit_items(const DedupPlan& pl, int u, int j0, i
   for (int k = 0; k < n0; ++k) {
     const int n = min(HP_CHUNK, L - k * HP_CHUNK);
     const int idx = !lg ? si + k : (reorder ? bp + k : bi + k);
-    pl.items[idx] = make_int4(j0 + k * HP_CHUNK, n, lg ? bp + k : dst,
-                              lg ? (reorder ? -(bl + 1) : 0) : 1);
+    pl.items[idx] = make_int4(j0 + k * HP_CHUNK, n, lg ? bp + k : dst, lg ? -(bl + 1) : 1);
     emit_bounds(pl, bi + k, j0 + k * HP_CHUNK, n);
   }
-  if (lg) pl.longs[bl] = make_int4(bp, n0, dst, u);
+  if (lg) pl.longs[bl] = make_int4(bp, n0, dst, L);  // {partial slot, chunks, dst, rows}
 }
 
 // ------------------------------------------------------------------ cluster path

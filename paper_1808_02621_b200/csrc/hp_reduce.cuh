@@ -19,6 +19,7 @@ namespace hp {
 // only depends on the item), store(dst, c4, g, pre) consumes the summed float4.
 struct EpiSend {
   static constexpr bool kRemote = false;
+  static constexpr bool kOut = false;  // fused pull: the new row also goes to the positions
   static constexpr int kPre = 0;  // table rows the epilogue reads (row stream stages them)
   __device__ __forceinline__ const float4* pre_row(int, int) const { return nullptr; }
   float4* rows;
@@ -47,12 +48,14 @@ __device__ __forceinline__ void set_pre(Pre& p, int k, float4 v) {
 template <int OPT>
 struct EpiApply {
   static constexpr bool kRemote = false;
+  static constexpr bool kOut = true;
   static constexpr int kPre = OPT == HP_OPT_SGD ? 1 : (OPT == HP_OPT_ADAGRAD ? 2 : 3);
   float4* w;
   float4* s0;
   float4* s1;
   hp_optim o;
   int D4;
+  float4* out;  // fused pull (n = 1 steps): out[t] = new row, for every position t; or nullptr
   using Pre = ApplyPre<OPT>;
 
   __device__ __forceinline__ const float4* pre_row(int k, int dst) const {
@@ -83,7 +86,8 @@ struct EpiApply {
     }
   }
 
-  __device__ __forceinline__ void store(int dst, int c4, float4 g, Pre p) const {
+  // returns the new table row (for the fused pull)
+  __device__ __forceinline__ float4 store(int dst, int c4, float4 g, Pre p) const {
     float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
     if constexpr (OPT != HP_OPT_SGD) a = p.a;
     if constexpr (OPT == HP_OPT_ADAM) b = p.b;
@@ -95,8 +99,24 @@ struct EpiApply {
     w[off] = p.w;
     if constexpr (OPT != HP_OPT_SGD) s0[off] = a;
     if constexpr (OPT == HP_OPT_ADAM) s1[off] = b;
+    return p.w;
   }
 };
+
+// Fused pull of a short item (n <= 16 rows of one id): the new row (or zeros
+// for a dropped id) goes to each of the item's positions; lane j of each warp
+// of the group holds position j (myp).
+template <class Epi>
+__device__ __forceinline__ void pull_store(const Epi& epi, int n, int myp, int c4, float4 v,
+                                           int D4) {
+  if constexpr (Epi::kOut) {
+    if (epi.out == nullptr) return;
+    for (int j = 0; j < n; ++j) {
+      const int64_t p = __shfl_sync(0xffffffffu, myp, j);
+      if (c4 < D4) epi.out[p * D4 + c4] = v;
+    }
+  }
+}
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -108,43 +128,6 @@ __device__ __forceinline__ void cp_async_commit() {
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-
-// ---- TMA bulk copies (cp.async.bulk, SASS UBLKCP) into shared memory,
-// completed on an mbarrier (transaction bytes).
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "HP_MBAR_WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra HP_MBAR_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// global -> shared, `bytes` (multiple of 16, both 16-byte aligned), completing on bar
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-// generic-proxy writes (this thread's, and those acquired from other SMs)
-// before async-proxy (TMA) reads of global memory
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // Staging buffer of the long chunks (TMA): static, 16 KB, shared with the
@@ -352,21 +335,25 @@ k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
 #pragma unroll
     for (int v = 0; v < VPT; ++v) {
       const int c4 = q + v * TPI;
-      if (c4 >= D4) continue;
-      if (fin) {
-        if (dst >= 0) {
-          if constexpr (SP) {
+      float4 nw = make_float4(0.f, 0.f, 0.f, 0.f);  // the pulled row (zeros: dropped id)
+      if (c4 < D4) {
+        if (fin) {
+          if (dst >= 0) {
             typename Epi::Pre p;
+            if constexpr (SP) {
 #pragma unroll
-            for (int k = 0; k < KP; ++k) set_pre(p, k, my_pre[(k * VPT + v) * TPI]);
-            epi.store(dst, c4, acc[v], p);
-          } else {
-            epi.store(dst, c4, acc[v], pre[v]);
+              for (int k = 0; k < KP; ++k) set_pre(p, k, my_pre[(k * VPT + v) * TPI]);
+            } else {
+              p = pre[v];
+            }
+            if constexpr (Epi::kOut) nw = epi.store(dst, c4, acc[v], p);
+            else epi.store(dst, c4, acc[v], p);
           }
+        } else {
+          partials[(int64_t)dst * D4 + c4] = acc[v];
         }
-      } else {
-        partials[(int64_t)dst * D4 + c4] = acc[v];
       }
+      if (fin) pull_store(epi, n, myp, c4, nw, D4);  // group-uniform: every lane shuffles
     }
     return item;
   };
@@ -568,7 +555,7 @@ __global__ void __launch_bounds__(128) k_rowstream(DedupPlan pl, const float* __
     const int k = pi - dbase;
     pn = __shfl_sync(0xffffffffu, dcur.y, k);
     pdst = __shfl_sync(0xffffffffu, dcur.z, k);
-    pfin = __shfl_sync(0xffffffffu, dcur.w, k);
+    pfin = __shfl_sync(0xffffffffu, dcur.w, k) > 0;  // < 0: chunk of a long segment
     pnpre = (pfin && pdst >= 0) ? Epi::kPre : 0;
   };
   if (pi < ie) fetch_item();

@@ -88,6 +88,7 @@ struct WinLayout {
 // loads only and the item's row loads are not held behind an index chain.
 struct EpiPush {
   static constexpr bool kRemote = true;
+  static constexpr bool kOut = false;
   static constexpr int kPre = 0;
   __device__ __forceinline__ const float4* pre_row(int, int) const { return nullptr; }
   PeerTable peers;
@@ -1018,6 +1019,12 @@ int hp_xchg_recv_counts(hp_xchg_t x, int32_t* out_dev, void* stream) {
   SigView sig(x->win);
   HP_CUDA(cudaMemcpyAsync(out_dev, sig.push_count, 4 * (size_t)x->L.n, cudaMemcpyDeviceToDevice,
                           static_cast<cudaStream_t>(stream)));
+  return HP_OK;
+}
+
+int hp_xchg_ret_ptr(hp_xchg_t x, float** out) {
+  HP_REQUIRE(x && out, "NULL argument");
+  *out = reinterpret_cast<float*>(static_cast<char*>(x->win) + x->L.ret_off);
   return HP_OK;
 }
 

@@ -15,6 +15,8 @@
 #include "hp_reduce.cuh"
 
 namespace hp {
+int plan_stitch(const void* ws, size_t ws_bytes, int64_t T, int32_t D, int64_t V, int32_t P,
+                const float* rows, float* out, cudaStream_t stream, int long_only);
 namespace {
 
 int check_slab(const hp_slab& s, int opt) {
@@ -27,18 +29,19 @@ int check_slab(const hp_slab& s, int opt) {
 }
 
 template <int OPT>
-EpiApply<OPT> make_apply(const hp_slab& s, const hp_optim& o) {
+EpiApply<OPT> make_apply(const hp_slab& s, const hp_optim& o, float* out) {
   EpiApply<OPT> e{reinterpret_cast<float4*>(s.w), reinterpret_cast<float4*>(s.s0),
-                  reinterpret_cast<float4*>(s.s1), o, s.D >> 2};
+                  reinterpret_cast<float4*>(s.s1), o, s.D >> 2, reinterpret_cast<float4*>(out)};
   return e;
 }
 
+// out (nullable): the fused pull (the plan's items in long-first order only).
 int apply_plan(const DedupPlan& pl, const float* vals, const hp_slab& s, const hp_optim& o,
-               cudaStream_t st) {
+               cudaStream_t st, float* out = nullptr) {
   switch (o.kind) {
-    case HP_OPT_SGD: return launch_reduce(pl, vals, make_apply<HP_OPT_SGD>(s, o), st);
-    case HP_OPT_ADAGRAD: return launch_reduce(pl, vals, make_apply<HP_OPT_ADAGRAD>(s, o), st);
-    default: return launch_reduce(pl, vals, make_apply<HP_OPT_ADAM>(s, o), st);
+    case HP_OPT_SGD: return launch_reduce(pl, vals, make_apply<HP_OPT_SGD>(s, o, out), st);
+    case HP_OPT_ADAGRAD: return launch_reduce(pl, vals, make_apply<HP_OPT_ADAGRAD>(s, o, out), st);
+    default: return launch_reduce(pl, vals, make_apply<HP_OPT_ADAM>(s, o, out), st);
   }
 }
 
@@ -131,6 +134,28 @@ int hp_apply_plan(const float* rows, int64_t R, hp_slab slab, hp_optim opt, void
 
 // Error word of the last plan built in ws (bit 0: id out of range, bit 1: row
 // not homed on this rank). Synchronises the stream.
+// K4 + K5 fused (n = 1): reduce + apply with the plan in ws, and out[t] = the
+// updated row of position t's id (zero row for a dropped id). With a fused-
+// tree plan the apply epilogue writes the positions itself (long segments: the
+// root's TMA bulk stores); otherwise the pull runs after it (hp_plan_stitch).
+int hp_apply_plan_pull(const float* rows, int64_t R, hp_slab slab, hp_optim opt, float* out,
+                       void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_slab(slab, opt.kind);
+  if (rc) return rc;
+  HP_REQUIRE(R == 0 || (rows != nullptr && out != nullptr), "rows / out is NULL");
+  HP_REQUIRE(((uintptr_t)out & 15) == 0, "out must be 16-byte aligned");
+  DedupPlan pl;
+  if ((rc = carve_plan(&pl, ws, ws_bytes, R, slab.D, slab.V, slab.P, 1))) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  restore_sorted_pos(pl);
+  if (pl.fused) {  // short segments pulled by the apply epilogue, long ones after it
+    if ((rc = apply_plan(pl, rows, slab, opt, st, out))) return rc;
+    return plan_stitch(ws, ws_bytes, R, slab.D, slab.V, slab.P, slab.w, out, st, 1);
+  }
+  if ((rc = apply_plan(pl, rows, slab, opt, st))) return rc;
+  return plan_stitch(ws, ws_bytes, R, slab.D, slab.V, slab.P, slab.w, out, st, 0);
+}
+
 int hp_plan_status(const void* ws, int32_t* out_err, void* stream) {
   HP_REQUIRE(ws != nullptr && out_err != nullptr, "NULL argument");
   const int32_t* counters = static_cast<const int32_t*>(ws);  // carved first

@@ -7,7 +7,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
-#include "hp_common.cuh"
+#include "hp_dedup.cuh"
 
 namespace hp {
 namespace {
@@ -94,6 +94,97 @@ int launch_copy(const Src& src, int64_t n, const int32_t* n_dev, float* out, int
   return HP_OK;
 }
 
+// ---- K5 / K6 through the plan, on TMA: out[t] = row of position t's segment.
+// One warp per plan item (a segment, or a 16-row chunk of a long one): lane 0
+// bulk-copies the segment's row (slab row of an apply plan / return row of a
+// send plan: the item's destination, or its long segment's) global -> shared
+// (cp.async.bulk, mbarrier), then lane j bulk-stores it shared -> global to the
+// item's j-th position (cp.async.bulk.global.shared). Each unique row is read
+// once per item instead of once per position, no id -> partition -> slab-row
+// chain is walked (the plan already holds the destination), and the copies
+// run on the TMA units (SASS UBLKCP) instead of 2 rows per warp through
+// registers. Dropped ids (destination -1) get zero rows.
+__global__ void __launch_bounds__(256)
+k_bcast_rows(DedupPlan pl, const float4* __restrict__ rows, float4* __restrict__ out, int D4,
+             int long_only) {
+  extern __shared__ __align__(128) float4 s_rows[];  // [8 warps][D4]
+  __shared__ uint64_t s_bar[8];
+  HP_ENTRY(SP_COPY);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float4* my = s_rows + (size_t)w * D4;
+  if (lane == 0) mbar_init(&s_bar[w], 1);
+  __syncwarp();
+  const uint32_t bytes = (uint32_t)D4 * 16u;
+  // long_only: the items of long segments (first in a fused-tree plan), whose
+  // rows the fused apply+pull left to this kernel
+  const int n_items = long_only ? pl.counters[C_PARTIALS] : pl.counters[C_ITEMS];
+  uint32_t parity = 0;
+  bool stored = false;
+  for (int it = blockIdx.x * 8 + w; it < n_items; it += gridDim.x * 8) {
+    const int4 item = pl.items[it];
+    const int n = item.y;
+    const int dst = item.w < 0 ? pl.longs[-item.w - 1].z : item.z;
+    const int pos = item.x < 0 ? -item.x - 1 : (lane < n ? pl.sorted_pos[item.x + lane] : 0);
+    if (dst < 0) {  // dropped ids: zero rows, plain stores
+      for (int j = 0; j < n; ++j) {
+        const int64_t p = __shfl_sync(0xffffffffu, pos, j);
+        for (int c = lane; c < D4; c += 32) out[p * D4 + c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      continue;
+    }
+    if (stored) {  // this warp's previous stores have read the shared row
+      if (lane < 32) bulk_wait_read0();
+      __syncwarp();
+    }
+    if (lane == 0) {
+      mbar_expect_tx(&s_bar[w], bytes);
+      bulk_g2s(my, rows + (int64_t)dst * D4, bytes, &s_bar[w]);
+    }
+    mbar_wait(&s_bar[w], parity);
+    parity ^= 1u;
+    if (lane < n) {
+      bulk_s2g(out + (int64_t)pos * D4, my, bytes);
+      bulk_commit();
+    }
+    stored = true;
+  }
+  bulk_wait_read0();  // shared memory stays valid until every bulk store has read it
+  HP_SPAN_END(SP_COPY);
+}
+
+// Register variant of k_bcast_rows (A/B, hp_debug_set_bcast_tma(0)): the warp
+// loads the segment's row into registers (VPL float4 per lane) and stores it to
+// each of the item's positions; no TMA round trip through shared memory.
+template <int VPL>
+__global__ void __launch_bounds__(256)
+k_bcast_rows_reg(DedupPlan pl, const float4* __restrict__ rows, float4* __restrict__ out, int D4) {
+  HP_ENTRY(SP_COPY);
+  const int lane = threadIdx.x & 31;
+  const int n_items = pl.counters[C_ITEMS];
+  for (int it = (blockIdx.x * 256 + threadIdx.x) >> 5; it < n_items; it += (gridDim.x * 256) >> 5) {
+    const int4 item = pl.items[it];
+    const int n = item.y;
+    const int dst = item.w < 0 ? pl.longs[-item.w - 1].z : item.z;
+    const int pos = item.x < 0 ? -item.x - 1 : (lane < n ? pl.sorted_pos[item.x + lane] : 0);
+    float4 x[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      const int c = lane + 32 * v;
+      x[v] = (dst >= 0 && c < D4) ? ldg_stream(rows + (int64_t)dst * D4 + c)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int j = 0; j < n; ++j) {
+      const int64_t p = __shfl_sync(0xffffffffu, pos, j);
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        const int c = lane + 32 * v;
+        if (c < D4) out[p * D4 + c] = x[v];
+      }
+    }
+  }
+  HP_SPAN_END(SP_COPY);
+}
+
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   uint64_t z = x + 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -167,6 +258,7 @@ k_scale_cast(const float* __restrict__ in, OutT* __restrict__ out, int64_t n, fl
 }  // namespace
 
 HP_SPAN_SETTER(set_spans_rows)
+int g_bcast_tma = 1;  // hp_debug_set_bcast_tma
 
 int scale_cast(const float* in, void* out, int64_t count, int32_t out_dtype, float scale,
                cudaStream_t st) {
@@ -194,6 +286,47 @@ int scale_cast(const float* in, void* out, int64_t count, int32_t out_dtype, flo
   return HP_OK;
 }
 
+// K5 / K6 from a dedup plan in ws (built for the same T, D, V, P):
+// out[t] = rows[destination of position t's segment] (see k_bcast_rows).
+// hp_plan_stitch over all items, or (long_only) over the long segments' chunks
+// of a fused-tree plan (the rest was pulled by the apply epilogue)
+int plan_stitch(const void* ws, size_t ws_bytes, int64_t T, int32_t D, int64_t V, int32_t P,
+                const float* rows, float* out, cudaStream_t stream, int long_only) {
+  HP_REQUIRE(D >= 4 && D % 4 == 0 && D <= 2048, "D must be a multiple of 4 in [4, 2048]");
+  HP_REQUIRE(T == 0 || (rows && out), "NULL argument");
+  HP_REQUIRE(((uintptr_t)rows & 15) == 0 && ((uintptr_t)out & 15) == 0, "rows / out must be 16-byte aligned");
+  if (T == 0) return HP_OK;
+  DedupPlan pl;
+  int rc = carve_plan(&pl, const_cast<void*>(ws), ws_bytes, T, D, V, P, 1);
+  if (rc) return rc;
+  restore_sorted_pos(pl);
+  const int D4 = D >> 2;
+  cudaStream_t st = stream;
+  if (!g_bcast_tma && !long_only) {
+    const int g = grid_for(T + T / HP_CHUNK + 1, 8, sm_count() * 8);
+    const float4* r4 = reinterpret_cast<const float4*>(rows);
+    float4* o4 = reinterpret_cast<float4*>(out);
+    if (D4 <= 32) launch_k(k_bcast_rows_reg<1>, dim3(g), dim3(256), 0, st, pl, r4, o4, D4);
+    else if (D4 <= 64) launch_k(k_bcast_rows_reg<2>, dim3(g), dim3(256), 0, st, pl, r4, o4, D4);
+    else if (D4 <= 128) launch_k(k_bcast_rows_reg<4>, dim3(g), dim3(256), 0, st, pl, r4, o4, D4);
+    else if (D4 <= 256) launch_k(k_bcast_rows_reg<8>, dim3(g), dim3(256), 0, st, pl, r4, o4, D4);
+    else launch_k(k_bcast_rows_reg<16>, dim3(g), dim3(256), 0, st, pl, r4, o4, D4);
+    HP_LAUNCHED(1, "k_bcast_rows_reg");
+    return HP_OK;
+  }
+  const size_t smem = (size_t)8 * D4 * 16;
+  static bool configured = false;
+  if (!configured) {
+    HP_CUDA(cudaFuncSetAttribute(k_bcast_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 8 * 512 * 16));
+    configured = true;
+  }
+  const int64_t work = long_only ? T / HP_CHUNK + 2 : T + T / HP_CHUNK + 1;
+  launch_k(k_bcast_rows, dim3(grid_for(work, 8, sm_count() * 8)), dim3(256), smem, st, pl,
+           reinterpret_cast<const float4*>(rows), reinterpret_cast<float4*>(out), D4, long_only);
+  HP_LAUNCHED(1, "k_bcast_rows");
+  return HP_OK;
+}
 }  // namespace hp
 
 using namespace hp;
@@ -215,6 +348,12 @@ int hp_stitch(const float* rows, const int32_t* inv, int64_t T, int32_t D, float
   HP_REQUIRE(T == 0 || (rows && inv && out), "NULL argument");
   SrcInv src{reinterpret_cast<const float4*>(rows), inv, D >> 2};
   return launch_copy(src, T, nullptr, out, D, static_cast<cudaStream_t>(stream));
+}
+
+
+extern "C" int hp_plan_stitch(const void* ws, size_t ws_bytes, int64_t T, int32_t D, int64_t V,
+                              int32_t P, const float* rows, float* out, void* stream) {
+  return plan_stitch(ws, ws_bytes, T, D, V, P, rows, out, static_cast<cudaStream_t>(stream), 0);
 }
 
 int hp_init_rows(float* w, int64_t row_lo, int64_t nrows, int32_t D, uint64_t seed, float scale,

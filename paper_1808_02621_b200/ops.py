@@ -288,6 +288,18 @@ def apply_plan(rows: torch.Tensor, n: int, slab: Slab, opt: Optim, ws: Workspace
     call("hp_apply_plan", _p(rows), n, slab, opt, ws.ptr, ws.nbytes, _stream(stream))
 
 
+def apply_plan_pull(rows: torch.Tensor, n: int, slab: Slab, opt: Optim, out: torch.Tensor,
+                    ws: Workspace, stream=None) -> torch.Tensor:
+    """K4 + K5 fused (n = 1): reduce + apply with the plan in ``ws`` and
+    out[t] = the updated row of position t's id (``hp_apply_plan_pull``)."""
+    _need(rows, torch.float32, "rows", 2)
+    _need(out, torch.float32, "out", 2)
+    if out.shape[0] < n or out.shape[1] != slab.D:
+        raise ValueError(f"out must be at least [{n}, {slab.D}]")
+    call("hp_apply_plan_pull", _p(rows), n, slab, opt, _p(out), ws.ptr, ws.nbytes, _stream(stream))
+    return out
+
+
 def step_counter_inc(ctr: torch.Tensor, stream=None) -> None:
     """++ctr on the device (the Adam step of graph-captured steps)."""
     call("hp_step_counter_inc", _p(ctr), _stream(stream))
@@ -305,6 +317,18 @@ def gather_rows(slab: Slab, ids: torch.Tensor, out: torch.Tensor, n: int | None 
     _need(out, torch.float32, "out", 2)
     n = ids.numel() if n is None else n
     call("hp_gather_rows", slab, _p(ids), n, _p(n_dev), _p(out), _stream(stream))
+    return out
+
+
+def plan_stitch(ws: Workspace, T: int, D: int, V: int, P: int, rows_ptr: int,
+                out: torch.Tensor, stream=None) -> torch.Tensor:
+    """K5 / K6 from the dedup plan in ``ws``: out[t] = rows[plan destination of
+    position t] (slab rows of an apply plan / return rows of a send plan),
+    TMA-broadcast once per unique row (``hp_plan_stitch``)."""
+    _need(out, torch.float32, "out", 2)
+    if out.shape[0] < T or out.shape[1] != D:
+        raise ValueError(f"out must be at least [{T}, {D}]")
+    call("hp_plan_stitch", ws.ptr, ws.nbytes, T, D, V, P, rows_ptr, _p(out), _stream(stream))
     return out
 
 

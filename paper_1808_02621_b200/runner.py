@@ -332,7 +332,7 @@ class HybridRunner:
         x.wait(1)
         k(f"wait_applied:{name}", False)
         k(f"stitch:{name}", True)
-        x.stitch(r["inv"][:T], out, wait=False)
+        ops.plan_stitch(tab.wss[slot], T, D, tab.V, tab.P, x.ret_ptr, out)
         k(f"stitch:{name}", False)
         self._pending_counts[name] = (r["dest_counts"], rc)
         return out
@@ -444,13 +444,10 @@ class HybridRunner:
         slab = tab.slab()
         if not planned:
             self._plan(tab, ids, slot)
-        self._kev(f"k4:{tab.name}", True)
-        ops.apply_plan(vals, T, slab, opt, tab.wss[slot])
-        self._kev(f"k4:{tab.name}", False)
         out = self._buf(tab.name, "out", (T, tab.D), torch.float32)
-        self._kev(f"k5:{tab.name}", True)
-        ops.gather_rows(slab, ids, out)
-        self._kev(f"k5:{tab.name}", False)
+        self._kev(f"k4:{tab.name}", True)  # K4 + K5: apply, and the pull fused into it
+        ops.apply_plan_pull(vals, T, slab, opt, out, tab.wss[slot])
+        self._kev(f"k4:{tab.name}", False)
         return out
 
     def _sparse_ar(self, tab: ShardedTable, ids, vals, opt) -> torch.Tensor:

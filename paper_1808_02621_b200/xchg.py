@@ -69,6 +69,13 @@ class PeerExchange:
         call("hp_xchg_window_ptr", self.handle, C.byref(out))
         return out.value
 
+    @property
+    def ret_ptr(self) -> int:
+        """Device address of the returned rows [cap][D] (by send slot)."""
+        out = C.c_void_p()
+        call("hp_xchg_ret_ptr", self.handle, C.byref(out))
+        return out.value
+
     def link_peer(self, rank: int, window: int) -> None:
         call("hp_xchg_set_peer_ptr", self.handle, rank, window)
 
