@@ -379,23 +379,63 @@ def main():
         ups = float(t_u.item())
     value = ups * args.steps / t_dev
 
-    # ---- per-kernel timing (eager steps, events around K4 / K5 launches)
+    # ---- per-kernel timing (eager steps, events around each phase's launches)
     kern = {}
-    if world == 1:
+    if world == 1 or runner.exchange == "p2p":
         # Eager steps, tables one after another, each step queued behind a GPU
-        # sleep so the CPU enqueue cost never shows up between an event pair.
+        # sleep so the CPU enqueue cost never shows up between an event pair;
+        # with several ranks every step starts after a barrier (same sleep on
+        # every GPU) and each phase reports the max over ranks.
         runner.kernel_events = {}
         runner.concurrent_tables = False
         kt = min(args.steps, 20)
         for i in range(kt):
+            if world > 1:
+                barrier()
+                torch.cuda.synchronize()
             torch.cuda._sleep(20_000_000)
             runner.step(batches[i % R], timed=False)
         torch.cuda.synchronize()
         runner.concurrent_tables = True
-        for key, evs in runner.kernel_events.items():
+        for key, evs in sorted(runner.kernel_events.items()):
             d = [a.elapsed_time(b) * 1e3 for a, b in zip(evs[0::2], evs[1::2])]
-            kern[key] = float(np.mean(d))
+            kern[key] = max_over_ranks(float(np.mean(d)))
         runner.kernel_events = None
+
+    # ---- N > 1: the sparse exchange's NVLink bytes (measured from the device
+    # send / receive counts of one timed step) against the push / apply kernel
+    # times above, and the reference's predicted per-GPU bytes beside them
+    sparse_x = None
+    if world > 1 and wl.tables and runner.exchange == "p2p":
+        st_ = runner.step(batches[0], timed=True)
+        mine = torch.tensor(list(st_.per_machine_bytes.per_machine[rank]), dtype=torch.float64,
+                            device=dev)
+        allb = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allb, mine)
+        measured = [[float(x) for x in t.tolist()] for t in allb]
+        pred = runner.predicted_transfer().per_machine
+        push_b, ret_b = 0.0, 0.0
+        for name, c in runner.last_counts.items():
+            D = runner.tables[name].D
+            push_b += sum(c["send"][o] * (8 + 4 * D) for o in range(world) if o != rank)
+            ret_b += sum(c["recv"][s_] * 4 * D for s_ in range(world) if s_ != rank)
+        push_max = max_over_ranks(push_b)
+        ret_max = max_over_ranks(ret_b)
+        t_push = sum(v for k_, v in kern.items() if k_.startswith("push:"))
+        t_apply = sum(v for k_, v in kern.items() if k_.startswith("apply:"))
+        sparse_x = {
+            "push_bytes_max_rank": push_max, "push_us": t_push,
+            "push_egress_gbs": push_max / (t_push * 1e-6) / 1e9 if t_push else None,
+            "return_bytes_max_rank": ret_max, "apply_return_us": t_apply,
+            "return_egress_gbs": ret_max / (t_apply * 1e-6) / 1e9 if t_apply else None,
+            "nvlink_peak_gbs": 770.0,
+            "note": "push = reduce + NVLink stores (k_reduce EpiPush + k_publish); return = owner "
+                    "merge + apply + stores back (k_owner_scan/rows + k_applied): each kernel also "
+                    "reads HBM, so egress/t is a lower bound of the link rate",
+            "measured_bytes_per_gpu": measured,
+            "predicted_bytes_per_gpu_transfer_model": [list(r) for r in pred],
+            "predicted_note": "reference transfer_model (uniform alpha, rows only, dense 2(n-1)/n S); "
+                              "measured counts ids + rows of the actual Zipf batch: reported, not asserted"}
     pk = peaks()
     roof = None
     big = max(wl.tables, key=lambda t: (t.T + t.sampled) * t.D) if wl.tables else None
@@ -545,6 +585,7 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "launches_per_step": launches_per_step,
             "roofline": roof, "kernels_us": kern, "cpu_baseline": cpu,
+            "sparse_exchange": sparse_x,
             "clocks": clk.summary(),
         }
         if check is not None:

@@ -44,14 +44,23 @@ def main():
     for kv in filter(None, os.environ.get("HP_CHECK_KNOBS", "").split(",")):
         k, v = kv.split("=")
         getattr(_lib.load(), f"hp_debug_set_{k}")(int(v))
-    wl = Workload("check", [TableShape("embedding", 60_000, 128, 2560),
-                            TableShape("softmax", 60_000, 256, 2560, sampled=3000)],
-                  {"lstm": int(os.environ.get("HP_CHECK_DENSE_ELEMS", "50000"))}, {"kind": opt_kind, "lr": 0.1, "init_acc": 0.1}, 2560,
-                  partitions=8)
+    lm1b = os.environ.get("HP_CHECK_SHAPE") == "lm1b"
+    if lm1b:  # BASELINE configs[1]: 2 x 800k x 512, T = 2560 / 2560 + 8192, 9.4M dense, P = 8
+        from paper_1808_02621_b200.synth import WORKLOADS
+
+        base = WORKLOADS["lm1b"]
+        wl = Workload("check_lm1b", base.tables, dict(base.dense),
+                      {"kind": opt_kind, "lr": 0.1, "init_acc": 0.1}, 2560, partitions=8)
+        parts = {"embedding": 8, "softmax": 8}
+    else:
+        wl = Workload("check", [TableShape("embedding", 60_000, 128, 2560),
+                                TableShape("softmax", 60_000, 256, 2560, sampled=3000)],
+                      {"lstm": int(os.environ.get("HP_CHECK_DENSE_ELEMS", "50000"))},
+                      {"kind": opt_kind, "lr": 0.1, "init_acc": 0.1}, 2560, partitions=8)
+        parts = {"embedding": 8, "softmax": 12}
     graph = hp.load_graph_spec(json.dumps(wl.graph_json()))
     cluster = hp.ClusterSpec.b200_box(world)
     arch = os.environ.get("HP_CHECK_ARCH", "hybrid")
-    parts = {"embedding": 8, "softmax": 12}
     if arch == "ar":  # SURVEY §8f baselines: every Weight AR / every Weight PS
         plan = hp.transform_ar(graph, cluster)
     elif arch == "ps":
@@ -60,24 +69,9 @@ def main():
         plan = hp.transform_hybrid(graph, cluster, partitions=parts)
     runner = hp.HybridRunner(plan, graph, cluster, rank=rank, world_size=world, comm=comm,
                              optimizer=hp.OptimizerConfig(kind=opt_kind, lr=0.1), device=dev,
-                             seed=5, exchange=xmode, dense_exchange=dmode,
+                             seed=5, exchange=xmode, dense_exchange=None if dmode == "default" else dmode,
                              dense_split=_split(os.environ.get("HP_CHECK_SPLIT", "auto"), world))
     hpar = {"lr": 0.1, "beta1": 0.9, "beta2": 0.999, "eps": 1e-8}
-    states = {t.name: orc.init_state(opt_kind, t.V, t.D, 5 * 1000 + i + 1, 0.1)
-              for i, t in enumerate(wl.tables)}
-    ok, why = True, []
-
-    def oracle_step(name, step, tb):
-        if name in runner.ar_tables:
-            orc.ar_sparse_step(states[name], opt_kind, hpar, step, tb)
-        else:
-            V = next(t.V for t in wl.tables if t.name == name)
-            orc.sparse_step(states[name], opt_kind, hpar, step, tb, V, plan.partitions_of[name],
-                            plan.owner_table(name))
-    def to_dev(b):
-        return {k: ((torch.from_numpy(v[0]).to(dev), torch.from_numpy(v[1]).to(dev))
-                    if isinstance(v, tuple) else torch.from_numpy(v).to(dev)) for k, v in b.items()}
-
     empty = os.environ.get("HP_CHECK_EMPTY") == "1"
 
     def batch_of(step, r):
@@ -88,6 +82,31 @@ def main():
             ids, vals = b["embedding"]
             b["embedding"] = (ids[:0].copy(), vals[:0].copy())
         return b
+
+    names = [v.name for v in graph.variables]
+    if lm1b:  # lazily paged full tables, initialised at every row the steps touch
+        from oracle import coracle
+
+        touched = {t.name: np.concatenate([batch_of(s, r)[t.name][0] for s in (1, 2, 3, 4)
+                                           for r in range(world)]) for t in wl.tables}
+        states = {t.name: orc.lazy_state(opt_kind, t.V, t.D, 5 * 1000 + names.index(t.name),
+                                         touched[t.name], 0.1) for t in wl.tables}
+    else:
+        states = {t.name: orc.init_state(opt_kind, t.V, t.D, 5 * 1000 + i + 1, 0.1)
+                  for i, t in enumerate(wl.tables)}
+    ok, why = True, []
+
+    def oracle_step(name, step, tb):
+        if name in runner.ar_tables:
+            orc.ar_sparse_step(states[name], opt_kind, hpar, step, tb)
+        else:
+            V = next(t.V for t in wl.tables if t.name == name)
+            (coracle if lm1b else orc).sparse_step(states[name], opt_kind, hpar, step, tb, V,
+                                                   plan.partitions_of[name],
+                                                   plan.owner_table(name))
+    def to_dev(b):
+        return {k: ((torch.from_numpy(v[0]).to(dev), torch.from_numpy(v[1]).to(dev))
+                    if isinstance(v, tuple) else torch.from_numpy(v).to(dev)) for k, v in b.items()}
 
     staged = {s: to_dev(batch_of(s, rank)) for s in (1, 2, 3)}
     if xmode == "p2p":
@@ -100,10 +119,20 @@ def main():
         for t in wl.tables:
             oracle_step(t.name, step, [b[t.name] for b in batches])
             got = runner.outputs[t.name].cpu().numpy()
-            if not np.array_equal(got, states[t.name]["w"][mine[t.name][0]]):
+            if not np.array_equal(got, orc.pull_rows(states[t.name]["w"], mine[t.name][0])):
                 ok = False
                 why.append(f"step {step} {t.name}: pulled rows differ")
             tab = runner.tables[t.name]
+            if lm1b:  # the touched rows this rank homes (the oracle's other rows are lazy zeros)
+                rows = np.unique(touched[t.name])
+                p = np.searchsorted(tab.bounds, rows, side="right") - 1
+                sel = tab.part_base_host[p] >= 0
+                srow = tab.part_base_host[p[sel]] + rows[sel] - tab.bounds[p[sel]]
+                got_w = tab.w[torch.from_numpy(srow).to(dev)].cpu().numpy()
+                if not np.array_equal(got_w, states[t.name]["w"][rows[sel]]):
+                    ok = False
+                    why.append(f"step {step} {t.name} homed touched rows differ")
+                continue
             w = tab.w.cpu().numpy()
             for p in tab.owned:
                 lo, hi = int(tab.bounds[p]), int(tab.bounds[p + 1])
@@ -151,11 +180,12 @@ def main():
             if True:  # Adam's step size comes from the device step counter
                 for t in wl.tables:
                     got = runner.outputs[t.name].cpu().numpy()
-                    if not np.array_equal(got, states[t.name]["w"][mine[t.name][0]]):
+                    if not np.array_equal(got, orc.pull_rows(states[t.name]["w"], mine[t.name][0])):
                         ok = False
                         why.append(f"graph replay {t.name}: pulled rows differ")
         runner.close()
-    print(f"DIST_CHECK rank {rank}/{world} opt={opt_kind} xchg={xmode}: "
+    print(f"DIST_CHECK rank {rank}/{world} opt={opt_kind} xchg={xmode} dense={runner.dense_exchange} "
+          f"shape={'lm1b' if lm1b else 'small'}: "
           f"{'PASS' if ok else 'FAIL'} {why[:4]}", flush=True)
     flag = torch.tensor([0 if ok else 1], device=dev)
     dist.all_reduce(flag)

@@ -19,6 +19,8 @@ def _ngpu():
 
 
 @pytest.mark.parametrize("opt,xchg,dense,knobs,arch", [
+    # BASELINE configs[1] shapes with the default transports (the bench's path)
+    ("adagrad", "p2p", "default", "shape=lm1b", "hybrid"),
     ("adagrad", "p2p", "p2p", "", "hybrid"),
     # weighted reduction split (rank 0 takes no chunk), SM stores and copy engines
     ("adagrad", "p2p", "p2p-sm", "split=first0", "hybrid"),
@@ -38,14 +40,16 @@ def test_multi_gpu_step_matches_oracle(opt, xchg, dense, knobs, arch):
     n = min(_ngpu(), 8)
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
-    split, empty = "auto", "0"
+    split, empty, shape = "auto", "0", "small"
+    if knobs.startswith("shape="):
+        shape, knobs = knobs.split("=", 1)[1], ""
     if knobs.startswith("split="):
         split, knobs = knobs.split("=", 1)[1], ""
     if knobs.startswith("empty="):
         empty, knobs = knobs.split("=", 1)[1], ""
     env = dict(os.environ, HP_CHECK_OPT=opt, HP_CHECK_XCHG=xchg, HP_CHECK_DENSE=dense,
                HP_CHECK_KNOBS=knobs, HP_CHECK_ARCH=arch, HP_CHECK_SPLIT=split,
-               HP_CHECK_EMPTY=empty,
+               HP_CHECK_EMPTY=empty, HP_CHECK_SHAPE=shape,
                # the pipelined dense exchange cuts each chunk into 64 KB pieces: many of them
                HP_CHECK_DENSE_ELEMS="1000004" if dense == "p2p-pipe" else "50000")
     import socket
