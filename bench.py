@@ -237,6 +237,14 @@ def config(args, wl):
 
 
 # ------------------------------------------------------------------ GPU arm
+_T0 = time.time()
+
+
+def _mark(msg: str) -> None:
+    """Wall-clock progress on stderr (where a multi-minute run spends its time)."""
+    print(f"[bench {time.time() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def main():
     args = parse()
     from paper_1808_02621_b200.synth import WORKLOADS, micro_workload
@@ -304,6 +312,7 @@ def main():
                 for k, v in b.items()}
 
     batches = [to_dev(b) for b in host]
+    _mark("inputs resident")
     use_graph = (world == 1 or args.exchange == "p2p") and not args.no_graph
     stream = torch.cuda.current_stream()
     check = None
@@ -324,6 +333,7 @@ def main():
     # Graph r applies batch r with the plan graph r-1 built, and builds batch r+1's
     # plan on a side stream meanwhile (plans depend only on the ids).
     graphs = runner.capture_pipelined(batches) if use_graph else None
+    _mark("graphs captured")
     G = args.steps_per_graph if graphs and R % max(args.steps_per_graph, 1) == 0 else 1
     # G > 1: graphs of G consecutive steps (same rotation and plan-slot order as
     # the single-step graphs), so K steps replay as K // G launches (+ singles)
@@ -371,6 +381,7 @@ def main():
         barrier()
         torch.cuda.synchronize()
     t_dev = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    _mark("timed region done")
     metric, unit = metric_for(wl, world)
     ups = units_per_step(wl, world, host, rank)
     if wl.tables and not wl.words_per_worker and world > 1:  # exact sum of unique rows
@@ -516,6 +527,7 @@ def main():
                 "peak_src": "fallback: measured peer copy 770 GB/s per direction (B200_PROFILING.md)",
                 "step_share": us / (t_dev / args.steps * 1e6)}
 
+    _mark("kernel timing / roofline done")
     # ---- e2e through the public API: pinned host inputs -> step -> result to host
     pinned = []
     for b in host:
@@ -560,6 +572,7 @@ def main():
     t_e2e = max_over_ranks(a.elapsed_time(b) / 1e3)
     e2e_value = ups * ke / t_e2e
 
+    _mark("e2e done")
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -279,6 +279,9 @@ int hp_nccl_get_unique_id(void* out /* hp_nccl_unique_id_bytes() bytes */);
 int hp_comm_init(hp_comm_t* out, int32_t nranks, int32_t rank, const void* unique_id);
 int hp_comm_destroy(hp_comm_t comm);
 int hp_comm_size(hp_comm_t comm);
+/* Asynchronous NCCL error (ncclCommGetAsyncError; host-only, never synchronises):
+ * *out = ncclResult_t, 0 = success. HybridRunner polls it before every step. */
+int hp_comm_status(hp_comm_t comm, int32_t* out);
 
 /* all-to-all of one int32 per peer (device counts), graph-capturable. */
 int hp_alltoall_counts(hp_comm_t comm, const int32_t* send, int32_t* recv, void* stream);
@@ -350,6 +353,14 @@ int hp_xchg_recv_counts(hp_xchg_t x, int32_t* out_dev, void* stream);
 int hp_xchg_status(hp_xchg_t x, int32_t* out_err, void* stream);
 /* Device address of the exchange's error word (for hp_err_collect). */
 int hp_xchg_err_ptr(hp_xchg_t x, const int32_t** out);
+/* Forward pull (a lookup before the step): out[t] = the CURRENT row of global id
+ * ids[t], read straight from its owner's slab over NVLink (peer loads; zero row
+ * for an id outside [0, V)). owner / glob_base as in hp_xchg_plan. Call it after
+ * this rank's previous step completed its stitch (every owner applied) and
+ * before its next push. Replaces: the PS pull of the forward pass
+ * (`simulate.py:195-199`; the reference's compute phase, `simulate.py:62`). */
+int hp_xchg_pull(hp_xchg_t x, const int64_t* ids, int64_t T, int64_t V, int32_t P,
+                 const int32_t* owner, const int64_t* glob_base, float* out, void* stream);
 /* Device address of the return rows [cap][D] (indexed by this rank's send slot). */
 int hp_xchg_ret_ptr(hp_xchg_t x, float** out);
 /* Single-process emulation of n ranks (parity tests on ONE GPU): instead of

@@ -73,6 +73,7 @@ SIGNATURES = {
     "hp_comm_init": (C.c_int, [C.POINTER(vp), i32, i32, vp]),
     "hp_comm_destroy": (C.c_int, [vp]),
     "hp_comm_size": (C.c_int, [vp]),
+    "hp_comm_status": (C.c_int, [vp, vp]),
     "hp_alltoall_counts": (C.c_int, [vp, vp, vp, vp]),
     "hp_exchange_push": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, i32, vp]),
     "hp_exchange_pull": (C.c_int, [vp, vp, vp, vp, vp, i32, vp]),
@@ -107,6 +108,7 @@ SIGNATURES = {
     "hp_plan_stitch": (C.c_int, [vp, sz, i64, i32, i64, i32, vp, vp, vp]),
     "hp_apply_plan_pull": (C.c_int, [vp, i64, Slab, Optim, vp, vp, sz, vp]),
     "hp_xchg_ret_ptr": (C.c_int, [vp, C.POINTER(vp)]),
+    "hp_xchg_pull": (C.c_int, [vp, vp, i64, i64, i32, vp, vp, vp, vp]),
     "hp_graph_launch": (C.c_int, [vp, vp]),
     "hp_graph_destroy": (C.c_int, [vp]),
     "hp_err_host_alloc": (C.c_int, [i32, C.POINTER(vp), C.POINTER(vp)]),

@@ -204,8 +204,15 @@ def _cmd_tune(args, graph, cluster, dv) -> dict:
                          max_p=max_p)
     final = ev(res.best_p)
     doc = res.to_dict()
+    # the reference's rule (Eq. 1 fit, argmin clamped to the sampled range) can
+    # return a sampled point that measured slower than another one when the fit
+    # is flat (both slopes clamp to 0): report the best MEASURED point beside it
+    sampled = [(p, t) for p, t in log[:-1]]
+    best_p, best_t = min(sampled, key=lambda s: s[1]) if sampled else (res.best_p, final)
     doc.update({"final_mean_iter_time_us": final,
                 "final_throughput_items_per_sec": _throughput(graph, cluster, final),
+                "best_sampled_p": best_p, "best_sampled_time_us": best_t,
+                "samples_us": [[p, t] for p, t in sampled],
                 "backend": "device", "n_gpus": dv.world})
     return doc
 

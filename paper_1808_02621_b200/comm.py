@@ -58,6 +58,12 @@ class Comm:
         call("hp_exchange_pull", self.handle, owner_rows.data_ptr(), oc, worker_rows.data_ptr(),
              wc, D, torch.cuda.current_stream().cuda_stream)
 
+    def status(self) -> int:
+        """ncclCommGetAsyncError of the communicator (0 = success; host-only)."""
+        r = C.c_int32(0)
+        call("hp_comm_status", self.handle, C.addressof(r))
+        return r.value
+
     def close(self) -> None:
         if self.handle:
             call("hp_comm_destroy", self.handle)

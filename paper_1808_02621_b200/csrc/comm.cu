@@ -68,6 +68,16 @@ int hp_comm_destroy(hp_comm_t comm) {
 
 int hp_comm_size(hp_comm_t comm) { return comm ? comm->nranks : 1; }
 
+// Asynchronous NCCL error of the communicator (ncclCommGetAsyncError, host-only,
+// no synchronisation): *out = the ncclResult_t (0 = ncclSuccess, 7 = in progress).
+int hp_comm_status(hp_comm_t comm, int32_t* out) {
+  HP_REQUIRE(comm && out, "NULL argument");
+  ncclResult_t r = ncclSuccess;
+  HP_NCCL(ncclCommGetAsyncError(comm->comm, &r));
+  *out = (int32_t)r;
+  return HP_OK;
+}
+
 int hp_alltoall_counts(hp_comm_t comm, const int32_t* send, int32_t* recv, void* stream) {
   HP_REQUIRE(comm && send && recv, "NULL argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -698,8 +698,10 @@ int launch_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaSt
     if (D4 <= 32) launch_k_reduce<32, 1>(pl, vals, epi, st);
     else if (D4 <= 64) launch_k_reduce<32, 2>(pl, vals, epi, st);
     else if (D4 <= 128) launch_k_reduce<64, 2>(pl, vals, epi, st);
-    else if (D4 <= 256) launch_k_reduce<64, 4>(pl, vals, epi, st);
-    else launch_k_reduce<128, 4>(pl, vals, epi, st);
+    // wide rows (NMT D = 1024, D = 2048): wider groups at 2 float4 columns per
+    // thread keep the kernel spill-free (4 columns spilled 300-700 B per thread)
+    else if (D4 <= 256) launch_k_reduce<128, 2>(pl, vals, epi, st);
+    else launch_k_reduce<256, 2>(pl, vals, epi, st);
     HP_LAUNCHED(1, "k_reduce");
   }
   // fused tree (items in long-first order, pl.nw == 0): k_reduce closed every

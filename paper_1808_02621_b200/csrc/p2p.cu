@@ -729,6 +729,47 @@ __global__ void k_applied(PeerTable peers, void* my_win, WinLayout L) {
 
 }  // namespace
 
+// ---- forward pull (a worker's lookup of rows homed anywhere): one warp per id
+// reads the row straight out of its owner's slab over NVLink (every slab lives
+// in its rank's peer-mapped window) — no owner participation. Dropped ids give
+// zero rows. Callers order it after the previous step's "applied" (the stitch
+// waited for every owner) and before their own next push, so no owner can be
+// updating the rows being read (an owner applies step i+1 only after every
+// source, this one included, pushed step i+1).
+__global__ void __launch_bounds__(256)
+k_peer_pull(PeerTable peers, WinLayout L, const int64_t* __restrict__ ids, int64_t T, Router route,
+            int64_t V, const int32_t* __restrict__ owner, const int64_t* __restrict__ glob_base,
+            float4* __restrict__ out) {
+  HP_ENTRY(SP_COPY);
+  const int lane = threadIdx.x & 31;
+  const int D4 = L.D4;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < T;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t id = ids[r];
+    const float4* src = nullptr;
+    if (id >= 0 && id < V) {
+      const int p = route.part(id);
+      const int64_t row = glob_base[p] + (id - route.lo(p));
+      src = reinterpret_cast<const float4*>(static_cast<const char*>(peers.base[owner[p]]) + L.w_off) +
+            row * D4;
+    }
+    for (int c0 = lane; c0 < D4; c0 += 32 * 4) {
+      float4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + 32 * u;
+        x[u] = (src && c < D4) ? src[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + 32 * u;
+        if (c < D4) out[r * D4 + c] = x[u];
+      }
+    }
+  }
+  HP_SPAN_END(SP_COPY);
+}
+
 // Spin-wait budget (cycles) before a wait gives up and raises an error bit:
 // hp_debug_set_wait_timeout (> 0), else HP_WAIT_TIMEOUT_CYCLES, else ~2 s.
 long long g_wait_cycles = 0;
@@ -950,8 +991,8 @@ void dispatch_owner_apply(const hp_xchg_s* x, const hp_slab& slab, const hp_opti
     if (D4 <= 32) launch_owner_rows<OPT, 32, 1>(x, slab, opt, st);
     else if (D4 <= 64) launch_owner_rows<OPT, 32, 2>(x, slab, opt, st);
     else if (D4 <= 128) launch_owner_rows<OPT, 64, 2>(x, slab, opt, st);
-    else if (D4 <= 256) launch_owner_rows<OPT, 64, 4>(x, slab, opt, st);
-    else launch_owner_rows<OPT, 128, 4>(x, slab, opt, st);
+    else if (D4 <= 256) launch_owner_rows<OPT, 128, 2>(x, slab, opt, st);  // spill-free at D = 1024
+    else launch_owner_rows<OPT, 256, 2>(x, slab, opt, st);
     return;
   }
   if (g_owner_stream == 1) {
@@ -1019,6 +1060,19 @@ int hp_xchg_recv_counts(hp_xchg_t x, int32_t* out_dev, void* stream) {
   SigView sig(x->win);
   HP_CUDA(cudaMemcpyAsync(out_dev, sig.push_count, 4 * (size_t)x->L.n, cudaMemcpyDeviceToDevice,
                           static_cast<cudaStream_t>(stream)));
+  return HP_OK;
+}
+
+int hp_xchg_pull(hp_xchg_t x, const int64_t* ids, int64_t T, int64_t V, int32_t P,
+                 const int32_t* owner, const int64_t* glob_base, float* out, void* stream) {
+  HP_REQUIRE(x && owner && glob_base && (T == 0 || (ids && out)), "NULL argument");
+  HP_REQUIRE(V >= 1 && V < (int64_t(1) << 31) && P >= 1 && P <= V, "bad V / P");
+  if (T == 0) return HP_OK;
+  for (int r = 0; r < x->L.n; ++r) HP_REQUIRE(x->peers.base[r], "a peer window is not mapped");
+  launch_k(k_peer_pull, dim3(grid_for(T, 8, sm_count() * 8)), dim3(256), 0,
+           static_cast<cudaStream_t>(stream), x->peers, x->L, ids, T, Router(V, P), V, owner,
+           glob_base, reinterpret_cast<float4*>(out));
+  HP_LAUNCHED(1, "k_peer_pull");
   return HP_OK;
 }
 

@@ -2,12 +2,13 @@
 language model whose embedding and sampled-softmax tables are the sharded
 sparse Weights and whose LSTM is the dense Weight.
 
-One training step on this GPU (one worker; N=1, where every partition is
-local — the reference marks all Weights AR at one machine,
-`placement.py:111`):
+One training step of one worker (one process per GPU; N=1 keeps every
+partition local — the reference marks all Weights AR at one machine,
+`placement.py:111` — N>1 shards the tables across the box):
 
 1. pull: the token rows and the softmax rows (targets + shared log-uniform
-   samples) are gathered from the table slabs (K5, `hp_gather_rows`);
+   samples) are looked up with :meth:`HybridRunner.pull` — a local gather at
+   N=1, NVLink reads from each row's owner slab at N>1 (`hp_xchg_pull`);
 2. compute: embedding rows → LSTM (cuDNN, PyTorch plumbing) → sampled softmax
    cross entropy; backward gives IndexedSlices for both tables (one gradient
    row per looked-up position) and dense LSTM gradients;
@@ -35,7 +36,8 @@ from .synth import log_uniform_ids, zipf_ids
 class HybridLM:
     def __init__(self, V: int = 800_000, D: int = 512, hidden: int = 1024, batch: int = 128,
                  seq: int = 20, samples: int = 8192, partitions: int = 8, lr: float = 0.2,
-                 dense_lr: float = 0.05, device="cuda", seed: int = 0):
+                 dense_lr: float = 0.05, device="cuda", seed: int = 0, rank: int = 0,
+                 world_size: int = 1, comm=None):
         from .runner import HybridRunner
 
         self.V, self.D, self.batch, self.seq, self.samples = V, D, batch, seq, samples
@@ -56,13 +58,14 @@ class HybridLM:
                  "alpha": min(1.0, T / V), "kind": "sparse", "partitionable": True},
                 {"name": "softmax", "elements": V, "elem_bytes": 4 * D,
                  "alpha": min(1.0, (T + samples) / V), "kind": "sparse", "partitionable": True}]}))
-        cluster = ClusterSpec.b200_box(1)
+        cluster = ClusterSpec.b200_box(world_size)
         plan = transform_hybrid(graph, cluster,
                                 partitions={"embedding": partitions, "softmax": partitions})
         self.runner = HybridRunner(plan, graph, cluster, device=self.device, seed=seed,
+                                   rank=rank, world_size=world_size, comm=comm,
                                    optimizer=ops.OptimizerConfig("adagrad", lr=lr))
         self.dense_lr = dense_lr
-        self.rng = np.random.default_rng(seed)
+        self.rng = np.random.default_rng(seed * 1000 + rank)  # each worker its own data
         self._flat = torch.zeros(self.n_dense, device=self.device)
 
     def batch_ids(self):
@@ -73,9 +76,7 @@ class HybridLM:
         return (torch.from_numpy(toks).to(self.device), torch.from_numpy(samp).to(self.device))
 
     def _pull(self, name: str, ids: torch.Tensor) -> torch.Tensor:
-        tab = self.runner.tables[name]
-        out = torch.empty(ids.numel(), self.D, device=self.device)
-        return ops.gather_rows(tab.slab(), ids.contiguous(), out)
+        return self.runner.pull(name, ids.contiguous())
 
     def step(self, toks: torch.Tensor, samp: torch.Tensor) -> float:
         inp, tgt = toks[:, :-1].reshape(-1), toks[:, 1:].reshape(-1)

@@ -239,6 +239,8 @@ class HybridRunner:
                               for n in self.tables}
         self._pending_counts: dict = {}
         self._ps_used: set = set()  # plan streams forked since the last join
+        # NVTX ranges around the step and its phases (HP_NVTX=1; ncu --nvtx filters)
+        self.nvtx = os.environ.get("HP_NVTX", "0") == "1"
         self.concurrent_tables = True
         # Plans built ahead (pipelined steps): with lookahead L the dedup of step
         # k + L runs on the plan streams during step k, so a step never waits for
@@ -401,6 +403,10 @@ class HybridRunner:
         run, or after graph replays)."""
         from ._lib import HybridPathError
 
+        if self.comm is not None and getattr(self.comm, "ptr", None) and hasattr(self.comm, "status"):
+            rc = self.comm.status()  # NCCL asynchronous error (host-only poll)
+            if rc not in (0, 7):     # ncclSuccess, ncclInProgress
+                raise HybridPathError(f"rank {self.rank}: NCCL asynchronous error {rc}")
         if sync:
             for tab in self.tables.values():
                 for slot in (0, 1):
@@ -521,6 +527,8 @@ class HybridRunner:
             [next_batch] if next_batch is not None else [])
         self.check_errors()
         self.step_count += 1
+        if self.nvtx:
+            torch.cuda.nvtx.range_push(f"hp.step {self.step_count}")
         stream = torch.cuda.current_stream()
         phases = {"compute": 0.0, "network": 0.0, "intra": 0.0, "update": 0.0}
         marks = []
@@ -575,6 +583,8 @@ class HybridRunner:
                 slot, planned, _ = self._take_plan(tab, batch[name][0])
                 self.outputs[name] = self._sparse(tab, batch[name], ev, slot, planned)
             self._plan_ahead(ahead, None)  # same stream, after the tables
+        if self.nvtx:
+            torch.cuda.nvtx.range_pop()
         if timed:
             stream.synchronize()
             for name, (sc, rc) in self._pending_counts.items():
@@ -603,6 +613,15 @@ class HybridRunner:
                 and np.float32(self.scale) == np.float32(1.0))
 
     def _dense(self, batch: dict) -> None:
+        if self.nvtx:
+            torch.cuda.nvtx.range_push("hp.dense")
+        try:
+            self._dense_body(batch)
+        finally:
+            if self.nvtx:
+                torch.cuda.nvtx.range_pop()
+
+    def _dense_body(self, batch: dict) -> None:
         """K7 for every dense Weight. The result lands in ``dense_out[name]``:
         a runner-owned buffer (or the exchange window), so the caller's gradient
         tensors are only read; at n=1 with fp32 and scale 1 nothing is launched
@@ -643,6 +662,15 @@ class HybridRunner:
 
     def _sparse(self, tab: ShardedTable, ids_vals, ev=None, slot: int = 0,
                 planned: bool = False) -> torch.Tensor:
+        if self.nvtx:
+            torch.cuda.nvtx.range_push(f"hp.sparse {tab.name}")
+        try:
+            return self._sparse_body(tab, ids_vals, ev, slot, planned)
+        finally:
+            if self.nvtx:
+                torch.cuda.nvtx.range_pop()
+
+    def _sparse_body(self, tab: ShardedTable, ids_vals, ev, slot: int, planned: bool) -> torch.Tensor:
         ids, vals = ids_vals
         tab.step_count += 1
         if self.optimizer.kind == "adam":
@@ -665,6 +693,29 @@ class HybridRunner:
                 ev("network")
         else:
             out = self._sparse_exchange(tab, ids, vals, opt, ev or (lambda _p: None))
+        return out
+
+    def pull(self, name: str, ids: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Forward lookup of a sparse Weight: out[t] = its current row ids[t]
+        (zero row for an id outside [0, V)), on the current stream.
+
+        One GPU (or a replicated AR table): a local gather. Several GPUs (p2p
+        exchange): each row is read straight from its owner's slab over NVLink
+        (``hp_xchg_pull``); call it between steps — after the previous step's
+        stitch has waited for every owner, before the next step's push."""
+        tab = self.tables[name]
+        ops._need(ids, torch.int64, "ids", 1)
+        if out is None:
+            out = torch.empty(ids.numel(), tab.D, dtype=torch.float32, device=self.device)
+        ops._need(out, torch.float32, "out", 2)
+        if out.shape[0] < ids.numel() or out.shape[1] != tab.D:
+            raise ValueError(f"out must be at least [{ids.numel()}, {tab.D}]")
+        if self.world_size == 1 or name in self.ar_tables:
+            return ops.gather_rows(tab.slab(), ids, out)
+        if name not in self.xchg:
+            raise NotImplementedError("the forward pull reads owners' slabs over peer memory "
+                                      "(exchange='p2p')")
+        self.xchg[name].pull(ids, tab.V, tab.P, tab.owner_dev, self.glob_base[name], out)
         return out
 
     @property

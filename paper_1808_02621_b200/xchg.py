@@ -69,6 +69,11 @@ class PeerExchange:
         call("hp_xchg_window_ptr", self.handle, C.byref(out))
         return out.value
 
+    def pull(self, ids, V: int, P: int, owner, glob_base, out) -> None:
+        """out[t] = the current row of ids[t], read from its owner's slab (NVLink)."""
+        call("hp_xchg_pull", self.handle, ids.data_ptr(), ids.numel(), V, P, owner.data_ptr(),
+             glob_base.data_ptr(), out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+
     @property
     def ret_ptr(self) -> int:
         """Device address of the returned rows [cap][D] (by send slot)."""

@@ -213,6 +213,28 @@ def test_emulated_hybrid_steps_bit_exact(cuda, knobs, n, dense_exchange, opt, co
         emu.close()
 
 
+def test_emulated_forward_pull_reads_owner_slabs(cuda):
+    """HybridRunner.pull at n > 1 (hp_xchg_pull): after hybrid steps every rank
+    reads the current rows of any ids — homed anywhere — straight from the
+    owners' slabs (peer loads); dropped ids give zero rows."""
+    emu = Emu(cuda, 4, _small_tables(), {"lstm": 40_000}, "adagrad", "p2p-sm")
+    try:
+        _eager_pipelined(emu, [21, 22])
+        rng = np.random.default_rng(5)
+        for t in emu.wl.tables:
+            pool = emu.touched[t.name]
+            ids = rng.choice(pool, 3000)
+            ids[:7] = [-1, t.V, t.V + 5, -9, 0, 1, 2]
+            ref = orc.pull_rows(emu.states[t.name]["w"], ids)
+            ref[4:7] = emu.table_rows(t.name, np.array([0, 1, 2]))  # untouched rows: device init
+            for r, run in enumerate(emu.runners):
+                got = run.pull(t.name, _t(ids, emu.dev)).cpu().numpy()
+                ok = np.isin(ids, pool) | (ids < 0) | (ids >= t.V) | (ids <= 2)
+                assert np.array_equal(got[ok], ref[ok]), (t.name, r)
+    finally:
+        emu.close()
+
+
 @pytest.mark.parametrize("owner_kernel", [0, 1])
 def test_emulated_alternative_owner_kernels(cuda, knobs, owner_kernel):
     """k_owner_apply (0) and k_owner_stream (1) instead of the two-pass default."""
