@@ -80,7 +80,8 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"])
-    ap.add_argument("--dense-exchange", default=None, choices=["p2p", "p2p-sm", "p2p-pipe", "nvls", "nccl"])
+    ap.add_argument("--dense-exchange", default=None,
+                    choices=["p2p", "p2p-sm", "p2p-pipe", "p2p-pull", "nvls", "nccl"])
     ap.add_argument("--dense-split", default="auto",
                     help="peer-memory dense exchange: reduction share per rank "
                          "('auto', 'uniform' or comma-separated weights)")
@@ -500,7 +501,10 @@ def main():
     if world > 1 and wl.dense and not runner.dense_ps:
         S = sum(v.elements for v in runner.dense) * 4
         w = runner.dense_weights or [1.0] * world
-        if runner.dense_exchange in ("p2p", "p2p-sm", "p2p-pipe"):
+        if runner.dense_exchange == "p2p-pull":
+            egress = (world - 1) * S
+            how = "each rank reads every peer's copy: (n-1) S per rank (ingress)"
+        elif runner.dense_exchange in ("p2p", "p2p-sm", "p2p-pipe"):
             c = [x / sum(w) * S for x in w]
             egress = max((S - c[r]) + (world - 1) * c[r] for r in range(world))
             how = "max over ranks of (S - chunk_r) + (n-1) chunk_r"

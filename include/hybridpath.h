@@ -113,9 +113,10 @@ void hp_debug_set_reduce_b(int b);
 /* Spin-wait budget (clock cycles) of every exchange wait before it gives up and
  * raises an error bit; <= 0 restores the default (HP_WAIT_TIMEOUT_CYCLES or ~2 s). */
 void hp_debug_set_wait_timeout(long long cycles);
-/* A/B: 1 (default) = long segments' chunks first, their upper tree levels fused
- * into k_reduce (TMA-staged, last-arriver nodes); 0 = sorted item order and a
- * separate k_combine. Takes effect for plans built afterwards. */
+/* A/B: 1 = long segments' chunks first, their upper tree levels fused into
+ * k_reduce (TMA-staged, last-arriver nodes); 0 (default, measured faster in the
+ * step and at scale) = sorted item order and a separate k_combine. Takes effect
+ * for plans built afterwards. */
 void hp_debug_set_fuse_tree(int on);
 /* A/B: 1 (default) = chain kernels carry their stream's priority as a launch
  * attribute (graph node priority); 0 = plain launches. */
@@ -211,11 +212,11 @@ int hp_apply_plan(const float* rows, int64_t R, hp_slab slab, hp_optim opt, void
                   size_t ws_bytes, void* stream);
 
 /* K4 + K5 fused (n == 1): hp_apply_plan, and out[t] (t < R) = the updated row of
- * position t's id (a zero row for a dropped id). With the default plans (long
- * segments first, fused tree) the apply epilogue writes every position itself
- * — short segments from registers, long ones by TMA bulk stores of the root —
- * so the pull costs no kernel, no re-read of the updated rows and no routing;
- * otherwise hp_plan_stitch runs after the apply. Replaces: update + pull
+ * position t's id (a zero row for a dropped id). The apply epilogue writes the
+ * positions of every short segment (<= 16 rows of one id) from its registers,
+ * so the pull re-reads no updated row and walks no routing; the long (hot)
+ * segments' positions get one TMA broadcast kernel after the apply (with the
+ * row stream on: hp_plan_stitch after it). Replaces: update + pull
  * (`simulate.py:195-199,294-323`). */
 int hp_apply_plan_pull(const float* rows, int64_t R, hp_slab slab, hp_optim opt, float* out,
                        void* ws, size_t ws_bytes, void* stream);
@@ -387,6 +388,7 @@ int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream);
 #define HP_DAR_SM 0
 #define HP_DAR_CE 1
 #define HP_DAR_PIPE 2 /* one persistent kernel; scatter and reduce-gather pipelined by 64 KB pieces */
+#define HP_DAR_PULL 3 /* one-shot: copy in, publish, read every peer's copy and sum (n <= 8; n = 2 default) */
 int hp_dar_set_mode(hp_dar_t d, int32_t mode);
 /* Split of the reduction between ranks: rank r reduces a share of S
  * proportional to weights[n] (double, >= 0, identical on every rank; default

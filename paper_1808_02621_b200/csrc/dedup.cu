@@ -846,7 +846,11 @@ int g_combine_blocks = 0;  // 0: one CTA per long segment up to the SM count
 int g_dar_blocks = 0;     // HP_DAR_PIPE grid (0 = one block per SM)
 int g_owner_waves = 1;    // peer-store kernels run many waves (no per-block fences)
 int g_reduce_b = 2;
-int g_fuse_tree = 1;
+// fused tree: default OFF by measurement (r2x / r2mic): K4 alone at LM1B
+// 24.3 vs 25.4 us, but the step no faster and 1.8x slower at the micro
+// config's 16M draws (one CTA per long chunk holds 4-8x fewer chunks in flight
+// than k_reduce's thread groups)
+int g_fuse_tree = 0;
 HP_SPAN_SETTER(set_spans_dedup)
 
 template <int CS>

@@ -1264,6 +1264,74 @@ k_ar_reduce_local(void* my_win, ArLayout A, const float4* __restrict__ grad, flo
   HP_SPAN_END(SP_AR_RG);
 }
 
+// ---- one-shot pull variant (HP_DAR_PULL, the default at n = 2): every rank
+// copies its gradient into its own window (slot [me]), publishes it, and then
+// reads every peer's whole copy over NVLink and sums all n in rank order (own
+// contribution from grad) -> scale -> cast -> its own output. One NVLink phase
+// (each rank reads (n-1) S: at n = 2 the same bytes per direction as the two
+// store phases, with one exchange of flags fewer and no second kernel on the
+// peer's links); "applied" then tells each peer its copy may be overwritten by
+// the next step (checked before the next copy).
+__global__ void __launch_bounds__(256)
+k_ar_copy_in(void* my_win, ArLayout A, const float4* __restrict__ grad) {
+  HP_ENTRY(SP_AR_SCATTER);
+  float4* in = reinterpret_cast<float4*>(static_cast<char*>(my_win) + A.slots_off) +
+               (int64_t)A.me * A.sstride4;
+  const int64_t n4 = A.S_real >> 2, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < n4; j0 += 4 * stride) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t j = j0 + u * stride;
+      if (j < n4) v[u] = ldg_stream(grad + j);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t j = j0 + u * stride;
+      if (j < n4) in[j] = v[u];
+    }
+  }
+  HP_SPAN_END(SP_AR_SCATTER);
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(256)
+k_ar_pull_sum(PeerTable peers, void* my_win, ArLayout A, const float4* __restrict__ grad, float scale) {
+  HP_ENTRY(SP_AR_RG);
+  const int64_t n4 = A.S_real >> 2, stride = (int64_t)gridDim.x * blockDim.x;
+  char* out = static_cast<char*>(my_win) + A.out_off;
+  for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < n4; j0 += 2 * stride) {
+    float4 x[2][AR_MAXN > 8 ? 8 : AR_MAXN];
+    // issue every contribution's loads first (NVLink latency), then sum in rank order
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t j = j0 + u * stride;
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        if (s >= A.n || j >= n4) continue;
+        x[u][s] = s == A.me ? ldg_stream(grad + j)
+                            : reinterpret_cast<const float4*>(static_cast<const char*>(peers.base[s]) +
+                                                              A.slots_off)[(int64_t)s * A.sstride4 + j];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t j = j0 + u * stride;
+      if (j >= n4) continue;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+        if (s < A.n) v = f4_add(v, x[u][s]);
+      v.x = __fmul_rn(v.x, scale);
+      v.y = __fmul_rn(v.y, scale);
+      v.z = __fmul_rn(v.z, scale);
+      v.w = __fmul_rn(v.w, scale);
+      put4<OutT>(out, j, v);
+    }
+  }
+  HP_SPAN_END(SP_AR_RG);
+}
+
 // ---- pipelined variant (HP_DAR_PIPE): ONE persistent kernel per rank. Every
 // chunk is cut into pieces of AR_PIECE4 float4; the work items are, in queue
 // order, (a) "scatter piece k of chunk c to rank c" for every peer c, then
@@ -1544,8 +1612,10 @@ int hp_dar_set_split(hp_dar_t d, const double* weights) {
 }
 
 int hp_dar_set_mode(hp_dar_t d, int32_t mode) {
-  HP_REQUIRE(d && (mode == HP_DAR_SM || mode == HP_DAR_CE || mode == HP_DAR_PIPE),
-             "mode must be HP_DAR_SM, HP_DAR_CE or HP_DAR_PIPE");
+  HP_REQUIRE(d && (mode == HP_DAR_SM || mode == HP_DAR_CE || mode == HP_DAR_PIPE ||
+                  mode == HP_DAR_PULL),
+             "mode must be HP_DAR_SM, HP_DAR_CE, HP_DAR_PIPE or HP_DAR_PULL");
+  HP_REQUIRE(mode != HP_DAR_PULL || d->A.n <= 8, "the pull exchange sums at most 8 ranks");
   d->mode = mode;
   return mode == HP_DAR_CE ? dar_side_streams(d) : HP_OK;
 }
@@ -1607,6 +1677,24 @@ int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream) {
     launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 1);
     launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 1, d->A.n, wait_budget(), SP_AR_WAIT1);
     HP_LAUNCHED(5, "dense p2p allreduce (copy engines)");
+    return HP_OK;
+  }
+  if (d->mode == HP_DAR_PULL) {
+    // the peers finished reading my previous copy (their "applied" of my epoch)
+    launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 1, d->A.n, wait_budget(), SP_AR_WAIT1);
+    const int bc = grid_for(d->A.S_real / 16, 256, sms * 4);
+    launch_k(k_ar_copy_in, dim3(bc), dim3(256), 0, st, d->win, d->A, reinterpret_cast<const float4*>(grad));
+    launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 0);
+    launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 0, d->A.n, wait_budget(), SP_AR_WAIT0);
+    const int bp = grid_for(d->A.S_real / 8, 256, sms * 4);
+    if (d->A.out_bytes == 4)
+      launch_k(k_ar_pull_sum<float>, dim3(bp), dim3(256), 0, st, d->peers, d->win, d->A,
+               reinterpret_cast<const float4*>(grad), scale);
+    else
+      launch_k(k_ar_pull_sum<__nv_bfloat16>, dim3(bp), dim3(256), 0, st, d->peers, d->win, d->A,
+               reinterpret_cast<const float4*>(grad), scale);
+    launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 1);
+    HP_LAUNCHED(6, "dense p2p allreduce (one-shot pull)");
     return HP_OK;
   }
   if (d->mode == HP_DAR_PIPE) {

@@ -148,7 +148,8 @@ int hp_apply_plan_pull(const float* rows, int64_t R, hp_slab slab, hp_optim opt,
   if ((rc = carve_plan(&pl, ws, ws_bytes, R, slab.D, slab.V, slab.P, 1))) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   restore_sorted_pos(pl);
-  if (pl.fused) {  // short segments pulled by the apply epilogue, long ones after it
+  const bool rowstream = pl.nw > 0 && rs_stages(pl.D) > 0 && !g_rowstream_off;
+  if (!rowstream) {  // short segments pulled by the k_reduce epilogue, long ones after it
     if ((rc = apply_plan(pl, rows, slab, opt, st, out))) return rc;
     return plan_stitch(ws, ws_bytes, R, slab.D, slab.V, slab.P, slab.w, out, st, 1);
   }

@@ -115,13 +115,14 @@ k_bcast_rows(DedupPlan pl, const float4* __restrict__ rows, float4* __restrict__
   if (lane == 0) mbar_init(&s_bar[w], 1);
   __syncwarp();
   const uint32_t bytes = (uint32_t)D4 * 16u;
-  // long_only: the items of long segments (first in a fused-tree plan), whose
-  // rows the fused apply+pull left to this kernel
-  const int n_items = long_only ? pl.counters[C_PARTIALS] : pl.counters[C_ITEMS];
+  // long_only: the chunks of long segments (w < 0; the first items of a fused-
+  // tree plan), whose rows the apply+pull epilogue left to this kernel
+  const int n_items = long_only && pl.fused ? pl.counters[C_PARTIALS] : pl.counters[C_ITEMS];
   uint32_t parity = 0;
   bool stored = false;
   for (int it = blockIdx.x * 8 + w; it < n_items; it += gridDim.x * 8) {
     const int4 item = pl.items[it];
+    if (long_only && item.w >= 0) continue;  // a short segment: pulled by the apply epilogue
     const int n = item.y;
     const int dst = item.w < 0 ? pl.longs[-item.w - 1].z : item.z;
     const int pos = item.x < 0 ? -item.x - 1 : (lane < n ? pl.sorted_pos[item.x + lane] : 0);
@@ -321,7 +322,7 @@ int plan_stitch(const void* ws, size_t ws_bytes, int64_t T, int32_t D, int64_t V
                                  8 * 512 * 16));
     configured = true;
   }
-  const int64_t work = long_only ? T / HP_CHUNK + 2 : T + T / HP_CHUNK + 1;
+  const int64_t work = long_only && pl.fused ? T / HP_CHUNK + 2 : T + T / HP_CHUNK + 1;
   launch_k(k_bcast_rows, dim3(grid_for(work, 8, sm_count() * 8)), dim3(256), smem, st, pl,
            reinterpret_cast<const float4*>(rows), reinterpret_cast<float4*>(out), D4, long_only);
   HP_LAUNCHED(1, "k_bcast_rows");

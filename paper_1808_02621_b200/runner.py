@@ -145,14 +145,16 @@ class HybridRunner:
         # keeps the hot sparse partitions' owners out of the reduce/gather
         default_dense = ("nccl" if world_size == 2 else "p2p-sm") if exchange == "p2p" else exchange
         self.dense_exchange = (dense_exchange or default_dense) if world_size > 1 else "local"
-        if self.dense_exchange not in ("p2p", "p2p-sm", "p2p-pipe", "nvls", "nccl", "local"):
+        if self.dense_exchange not in ("p2p", "p2p-sm", "p2p-pipe", "p2p-pull", "nvls", "nccl",
+                                       "local"):
             raise ValueError("dense_exchange must be 'p2p' (copy engines), 'p2p-sm', "
-                             "'p2p-pipe', 'nvls' or 'nccl'")
+                             "'p2p-pipe', 'p2p-pull', 'nvls' or 'nccl'")
         self._world = getattr(comm, "world", None)  # emulated ranks (emulate.LocalWorld)
         if self._world is not None and (self.exchange != "p2p" or self.dense_exchange in
                                         ("nccl", "nvls")):
             raise ValueError("emulated ranks (LocalWorld) run the peer-memory transports only: "
-                             "exchange='p2p', dense_exchange in ('p2p', 'p2p-sm', 'p2p-pipe')")
+                             "exchange='p2p', dense_exchange in ('p2p', 'p2p-sm', 'p2p-pipe', "
+                             "'p2p-pull')")
         self.dar: dict = {}
         self.dense_weights = None  # reduction share per rank of the peer dense exchange
         self.xchg: dict = {}
@@ -180,12 +182,13 @@ class HybridRunner:
 
                     self.dar[var.name] = NvlsExchange(world_size, rank, var.elements,
                                                       dense_dtype, self.device)
-                elif self.dense_exchange in ("p2p", "p2p-sm", "p2p-pipe"):
+                elif self.dense_exchange in ("p2p", "p2p-sm", "p2p-pipe", "p2p-pull"):
                     from .xchg import DenseExchange
 
                     self.dar[var.name] = DenseExchange(
                         world_size, rank, var.elements, dense_dtype, self.device,
-                        mode={"p2p": "ce", "p2p-sm": "sm", "p2p-pipe": "pipe"}[self.dense_exchange],
+                        mode={"p2p": "ce", "p2p-sm": "sm", "p2p-pipe": "pipe",
+                              "p2p-pull": "pull"}[self.dense_exchange],
                         world=self._world)
                     w = self._dense_split_weights(dense_split)
                     if w is not None:
@@ -269,7 +272,7 @@ class HybridRunner:
             if len(dense_split) != n:
                 raise ValueError(f"dense_split needs {n} weights")
             return list(dense_split)
-        if dense_split in (None, "uniform") or self.dense_exchange == "p2p-pipe" or n < 4:
+        if dense_split in (None, "uniform") or self.dense_exchange in ("p2p-pipe", "p2p-pull") or n < 4:
             return None
         if dense_split != "auto":
             raise ValueError("dense_split: 'auto', 'uniform' or a list of weights")

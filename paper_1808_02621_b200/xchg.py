@@ -162,7 +162,7 @@ class DenseExchange:
     reduce slots and the output; ``allreduce(grad, scale)`` leaves
     cast(scale * sum_r grad_r) (summed in rank order) in ``self.out`` on every rank."""
 
-    MODES = {"sm": 0, "ce": 1, "pipe": 2}  # HP_DAR_SM / _CE / _PIPE (include/hybridpath.h)
+    MODES = {"sm": 0, "ce": 1, "pipe": 2, "pull": 3}  # HP_DAR_* (include/hybridpath.h)
     KIND = "dar"
 
     def __init__(self, n: int, rank: int, numel: int, out_dtype, device, group=None,

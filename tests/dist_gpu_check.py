@@ -145,7 +145,7 @@ def main():
         if not np.allclose(got, ref, rtol=1e-5, atol=1e-6):
             ok = False
             why.append(f"step {step} dense differs (max {np.abs(got - ref).max():.3g})")
-        if runner.dense_exchange in ("p2p", "p2p-sm", "p2p-pipe") and not runner.dense_ps:  # rank order
+        if runner.dense_exchange in ("p2p", "p2p-sm", "p2p-pipe", "p2p-pull") and not runner.dense_ps:  # rank order
             seq = np.zeros_like(batches[0]["lstm"])
             for b in batches:
                 seq = seq + b["lstm"]

@@ -199,6 +199,8 @@ def _eager_pipelined(emu, seeds, empty=()):
                           (4, "p2p-sm", "adagrad", False),   # weighted split
                           (3, "p2p", "sgd", False),          # copy engines
                           (2, "p2p-pipe", "adam", True),
+                          (2, "p2p-pull", "adagrad", True),  # one-shot pull (n = 2 default)
+                          (3, "p2p-pull", "sgd", False),
                           (4, "p2p-pipe", "adagrad", False)])
 def test_emulated_hybrid_steps_bit_exact(cuda, knobs, n, dense_exchange, opt, concurrent):
     if dense_exchange == "p2p-pipe":

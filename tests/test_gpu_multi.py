@@ -30,6 +30,7 @@ def _ngpu():
     ("adam", "p2p", "nccl", "", "hybrid"),
     ("adagrad", "p2p", "nvls", "", "hybrid"),
     ("adagrad", "p2p", "p2p-pipe", "", "hybrid"),
+    ("adam", "p2p", "p2p-pull", "", "hybrid"),
     # the alternative kernels behind the instrumentation knobs stay parity-checked
     ("adagrad", "p2p", "p2p-sm", "owner_stream=0,rowstream=1,pdl=1", "hybrid"),
     ("sgd", "nccl", "nccl", "", "hybrid"),
