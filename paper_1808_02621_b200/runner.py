@@ -936,6 +936,10 @@ class HybridRunner:
                     self.step(batches[j], timed=False, upcoming=ahead(j))
                 self._join_plan_streams()  # a capture ends with every stream joined
             graphs.append(g)
+        # the plans left pending were only captured (built at replay time, with
+        # captured events): an eager step after this plans inline instead
+        for tab in self.tables.values():
+            tab.pending.clear()
         return graphs
 
     # ------------------------------------------------------------------ timing / P search

@@ -66,3 +66,22 @@ def test_multi_gpu_step_matches_oracle(opt, xchg, dense, knobs, arch):
              if ln.startswith("DIST_CHECK") and ("PASS" in ln or "FAIL" in ln)]
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     assert len(lines) == n and all("PASS" in ln for ln in lines), lines
+
+
+def test_multi_gpu_lm_consumer():
+    """HybridLM across the box's GPUs (forward pull from owners over NVLink)."""
+    n = min(_ngpu(), 8)
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node",
+           str(n), "--master-addr", "127.0.0.1", "--master-port", str(port),
+           str(ROOT / "tests" / "dist_lm_check.py")]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("DIST_LM")]
+    assert res.returncode == 0 and len(lines) == n and all("PASS" in ln for ln in lines), (
+        res.stdout[-3000:] + res.stderr[-3000:])
