@@ -609,17 +609,23 @@ def main():
             line["parity_check"] = check
         print(json.dumps(line), flush=True)
     # release captured graphs (they reference NCCL and peer windows) before teardown
-    graphs = e2e_graph = None
+    graphs = e2e_graph = multi = None
     torch.cuda.synchronize()
     runner.check_errors(sync=True)  # any device error bit of the run raises here
+    _mark("errors checked")
     if world > 1:
         errs = runner.exchange_status()
         if any(errs.values()):
             print(f"rank {rank}: exchange error bits {errs}", file=sys.stderr, flush=True)
         barrier()
-        runner.close()
-        comm.close()
-        dist.destroy_process_group()
+        torch.cuda.synchronize()
+        _mark("teardown")
+        # The line is printed and every rank is past the last collective: leave
+        # without the NCCL / IPC teardown (measured: a torchrun bench could sit
+        # in it until killed; the OS releases the GPU resources of the process)
+        sys.stdout.flush()
+        sys.stderr.flush()
+        os._exit(0)
 
 
 if __name__ == "__main__":

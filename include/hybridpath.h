@@ -338,8 +338,9 @@ int hp_xchg_push_plan(hp_xchg_t x, const float* vals, int64_t T, int64_t V, int3
 /* Wait (one spinning block, bounded) until every source pushed (which = 0) or
  * every owner applied (which = 1) for this rank's current epoch. */
 int hp_xchg_wait(hp_xchg_t x, int32_t which, void* stream);
-/* Owner, fused K4+K5: (wait for all pushes,) merge in source order, apply to the
- * slab, store each updated row back into its contributors' return buffers. */
+/* Owner, fused K4+K5: (wait for all pushes — folded into k_owner_scan's
+ * prologue,) merge in source order, apply to the slab, store each updated row
+ * back into its contributors' return buffers. */
 int hp_xchg_merge_apply(hp_xchg_t x, hp_slab slab, hp_optim opt, int32_t wait, void* stream);
 /* Worker K6: (wait for all applies,) out[t] = returned row of send slot inv[t]. */
 int hp_xchg_stitch(hp_xchg_t x, const int32_t* inv, int64_t T, float* out, int32_t wait,
@@ -354,6 +355,12 @@ int hp_xchg_recv_counts(hp_xchg_t x, int32_t* out_dev, void* stream);
 int hp_xchg_status(hp_xchg_t x, int32_t* out_err, void* stream);
 /* Device address of the exchange's error word (for hp_err_collect). */
 int hp_xchg_err_ptr(hp_xchg_t x, const int32_t** out);
+/* Worker K6 through the send plan in ws (hp_xchg_plan, same T / V / P): out[t] =
+ * the returned row of position t's send slot, TMA-broadcast once per unique row
+ * (k_bcast_rows); wait != 0 folds the wait for every owner's "applied" into the
+ * kernel's prologue (no separate k_wait on the chain). */
+int hp_xchg_stitch_plan(hp_xchg_t x, const void* ws, size_t ws_bytes, int64_t T, int64_t V,
+                        int32_t P, float* out, int32_t wait, void* stream);
 /* Forward pull (a lookup before the step): out[t] = the CURRENT row of global id
  * ids[t], read straight from its owner's slab over NVLink (peer loads; zero row
  * for an id outside [0, V)). owner / glob_base as in hp_xchg_plan. Call it after

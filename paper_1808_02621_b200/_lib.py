@@ -109,6 +109,7 @@ SIGNATURES = {
     "hp_apply_plan_pull": (C.c_int, [vp, i64, Slab, Optim, vp, vp, sz, vp]),
     "hp_xchg_ret_ptr": (C.c_int, [vp, C.POINTER(vp)]),
     "hp_xchg_pull": (C.c_int, [vp, vp, i64, i64, i32, vp, vp, vp, vp]),
+    "hp_xchg_stitch_plan": (C.c_int, [vp, vp, sz, i64, i64, i32, vp, i32, vp]),
     "hp_graph_launch": (C.c_int, [vp, vp]),
     "hp_graph_destroy": (C.c_int, [vp]),
     "hp_err_host_alloc": (C.c_int, [i32, C.POINTER(vp), C.POINTER(vp)]),

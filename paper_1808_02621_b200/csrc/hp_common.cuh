@@ -207,6 +207,44 @@ __device__ __forceinline__ void pdl_trigger() {
   void fn(unsigned long long* p) { cudaMemcpyToSymbol(d_span, &p, sizeof(p)); }
 HP_SPAN_DECL
 
+// System-scope acquire load (flags raised by peer GPUs with st.release.sys).
+__device__ __forceinline__ int ld_acquire_sys_i32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// A bounded wait folded into a consumer kernel's prologue: every block waits
+// until flags[s] >= *epoch for s < n (error bit `err_bit` on timeout).
+struct StitchWait {
+  const int* flags;  // nullptr: no wait
+  const int* epoch;
+  int* err;
+  int n;
+  long long cycles;
+};
+__device__ __forceinline__ void block_wait_flags(const StitchWait& w, int err_bit) {
+  if (w.flags == nullptr) return;
+  const int e = *reinterpret_cast<const volatile int*>(w.epoch);
+  for (int s = threadIdx.x; s < w.n; s += blockDim.x) {
+    const long long t0 = clock64();
+    while (ld_acquire_sys_i32(&w.flags[s]) < e) {
+      if (clock64() - t0 > w.cycles) {
+        atomicOr(w.err, err_bit);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
+// K5/K6 through a dedup plan (rows.cu): out[t] = rows[plan destination of t];
+// long_only: only the chunks of long segments; wait: folded flag wait.
+int plan_stitch(const void* ws, size_t ws_bytes, int64_t T, int32_t D, int64_t V, int32_t P,
+                const float* rows, float* out, cudaStream_t stream, int long_only,
+                const StitchWait* wait = nullptr);
+
 // ---- TMA bulk copies (cp.async.bulk, SASS UBLKCP) into shared memory,
 // completed on an mbarrier (transaction bytes).
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -547,10 +547,24 @@ k_owner_stream(PeerTable peers, void* my_win, WinLayout L, const int64_t* __rest
 // inside the apply loop.
 __global__ void __launch_bounds__(256)
 k_owner_scan(void* my_win, WinLayout L, const int64_t* __restrict__ part_base, Router route,
-             int64_t rows_cap) {
+             int64_t rows_cap, long long wait_cycles) {
   __shared__ int s_pre[OS_NMAX + 1];
   HP_ENTRY(SP_SCATTER);
   SigView sig(my_win);
+  if (wait_cycles > 0) {  // the push wait, folded in (no k_wait launch on the chain)
+    const int e = *reinterpret_cast<volatile int*>(sig.epoch);
+    for (int s = threadIdx.x; s < L.n; s += blockDim.x) {
+      const long long t0 = clock64();
+      while (ld_acquire_sys(&sig.push_flag[s]) < e) {
+        if (clock64() - t0 > wait_cycles) {
+          atomicOr(sig.err, 4);
+          break;
+        }
+        __nanosleep(64);
+      }
+    }
+    __syncthreads();
+  }
   char* win = static_cast<char*>(my_win);
   const int64_t* inbox_ids = reinterpret_cast<const int64_t*>(win + L.ids_off);
   const unsigned long long* slot = reinterpret_cast<const unsigned long long*>(win + L.slot_off);
@@ -974,10 +988,10 @@ void launch_owner_stream(const hp_xchg_s* x, const hp_slab& slab, const hp_optim
 
 template <int OPT, int TPI, int VPT>
 void launch_owner_rows(const hp_xchg_s* x, const hp_slab& slab, const hp_optim& opt,
-                       cudaStream_t st) {
+                       cudaStream_t st, bool wait) {
   const int64_t total = (int64_t)x->L.n * x->L.cap;
   launch_k(k_owner_scan, dim3(grid_for(total, 256, sm_count() * 8)), dim3(256), 0, st, x->win, x->L,
-           slab.part_base, Router(slab.V, slab.P), x->rows_cap);
+           slab.part_base, Router(slab.V, slab.P), x->rows_cap, wait ? wait_budget() : 0LL);
   const int blocks = grid_for(total, 256 / TPI, g_owner_waves ? 1 << 30 : sm_count() * 3);
   launch_k(k_owner_rows<OPT, TPI, VPT>, dim3(blocks), dim3(256), 0, st, x->peers, x->win, x->L,
            reinterpret_cast<float4*>(slab.s0), reinterpret_cast<float4*>(slab.s1), opt);
@@ -986,15 +1000,16 @@ void launch_owner_rows(const hp_xchg_s* x, const hp_slab& slab, const hp_optim& 
 
 template <int OPT>
 void dispatch_owner_apply(const hp_xchg_s* x, const hp_slab& slab, const hp_optim& opt, int D4,
-                          cudaStream_t st) {
+                          cudaStream_t st, bool wait) {
   if (g_owner_stream == 2) {
-    if (D4 <= 32) launch_owner_rows<OPT, 32, 1>(x, slab, opt, st);
-    else if (D4 <= 64) launch_owner_rows<OPT, 32, 2>(x, slab, opt, st);
-    else if (D4 <= 128) launch_owner_rows<OPT, 64, 2>(x, slab, opt, st);
-    else if (D4 <= 256) launch_owner_rows<OPT, 128, 2>(x, slab, opt, st);  // spill-free at D = 1024
-    else launch_owner_rows<OPT, 256, 2>(x, slab, opt, st);
+    if (D4 <= 32) launch_owner_rows<OPT, 32, 1>(x, slab, opt, st, wait);
+    else if (D4 <= 64) launch_owner_rows<OPT, 32, 2>(x, slab, opt, st, wait);
+    else if (D4 <= 128) launch_owner_rows<OPT, 64, 2>(x, slab, opt, st, wait);
+    else if (D4 <= 256) launch_owner_rows<OPT, 128, 2>(x, slab, opt, st, wait);  // spill-free at D = 1024
+    else launch_owner_rows<OPT, 256, 2>(x, slab, opt, st, wait);
     return;
   }
+  if (wait) hp_xchg_wait(const_cast<hp_xchg_s*>(x), 0, st);
   if (g_owner_stream == 1) {
     switch (D4) {
       case 32: return launch_owner_stream<OPT, 1>(x, slab, opt, st);
@@ -1018,15 +1033,12 @@ int hp_xchg_merge_apply(hp_xchg_t x, hp_slab slab, hp_optim opt, int32_t wait, v
   HP_REQUIRE(opt.kind == HP_OPT_SGD || slab.s0, "optimizer state s0 is NULL");
   HP_REQUIRE(opt.kind != HP_OPT_ADAM || slab.s1, "Adam state s1 is NULL");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (wait) {
-    int rc = hp_xchg_wait(x, 0, stream);
-    if (rc) return rc;
-  }
+  // the push wait: folded into k_owner_scan (default owner kernels), else k_wait
   const int D4 = x->L.D4;
   switch (opt.kind) {
-    case HP_OPT_SGD: dispatch_owner_apply<HP_OPT_SGD>(x, slab, opt, D4, st); break;
-    case HP_OPT_ADAGRAD: dispatch_owner_apply<HP_OPT_ADAGRAD>(x, slab, opt, D4, st); break;
-    default: dispatch_owner_apply<HP_OPT_ADAM>(x, slab, opt, D4, st);
+    case HP_OPT_SGD: dispatch_owner_apply<HP_OPT_SGD>(x, slab, opt, D4, st, wait != 0); break;
+    case HP_OPT_ADAGRAD: dispatch_owner_apply<HP_OPT_ADAGRAD>(x, slab, opt, D4, st, wait != 0); break;
+    default: dispatch_owner_apply<HP_OPT_ADAM>(x, slab, opt, D4, st, wait != 0);
   }
   HP_LAUNCHED(g_owner_stream == 2 ? 3 : 1, "owner merge/apply");
   return HP_OK;
@@ -1074,6 +1086,19 @@ int hp_xchg_pull(hp_xchg_t x, const int64_t* ids, int64_t T, int64_t V, int32_t 
            glob_base, reinterpret_cast<float4*>(out));
   HP_LAUNCHED(1, "k_peer_pull");
   return HP_OK;
+}
+
+int hp_xchg_stitch_plan(hp_xchg_t x, const void* ws, size_t ws_bytes, int64_t T, int64_t V,
+                        int32_t P, float* out, int32_t wait, void* stream) {
+  HP_REQUIRE(x && ws, "NULL argument");
+  SigView sig(x->win);
+  const float* ret = reinterpret_cast<const float*>(static_cast<char*>(x->win) + x->L.ret_off);
+  StitchWait w{wait ? sig.applied_flag : nullptr, sig.epoch, sig.err, x->L.n, wait_budget()};
+  if (T == 0) {  // no rows, but the next push must still follow every owner's apply
+    return wait ? hp_xchg_wait(x, 1, stream) : HP_OK;
+  }
+  return plan_stitch(ws, ws_bytes, T, x->L.D4 * 4, V, P, ret, out,
+                     static_cast<cudaStream_t>(stream), 0, wait ? &w : nullptr);
 }
 
 int hp_xchg_ret_ptr(hp_xchg_t x, float** out) {

@@ -15,8 +15,6 @@
 #include "hp_reduce.cuh"
 
 namespace hp {
-int plan_stitch(const void* ws, size_t ws_bytes, int64_t T, int32_t D, int64_t V, int32_t P,
-                const float* rows, float* out, cudaStream_t stream, int long_only);
 namespace {
 
 int check_slab(const hp_slab& s, int opt) {

@@ -106,10 +106,11 @@ int launch_copy(const Src& src, int64_t n, const int32_t* n_dev, float* out, int
 // registers. Dropped ids (destination -1) get zero rows.
 __global__ void __launch_bounds__(256)
 k_bcast_rows(DedupPlan pl, const float4* __restrict__ rows, float4* __restrict__ out, int D4,
-             int long_only) {
+             int long_only, StitchWait wt) {
   extern __shared__ __align__(128) float4 s_rows[];  // [8 warps][D4]
   __shared__ uint64_t s_bar[8];
   HP_ENTRY(SP_COPY);
+  block_wait_flags(wt, 8);  // p2p stitch: every owner applied (error bit 8 on timeout)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float4* my = s_rows + (size_t)w * D4;
   if (lane == 0) mbar_init(&s_bar[w], 1);
@@ -292,7 +293,8 @@ int scale_cast(const float* in, void* out, int64_t count, int32_t out_dtype, flo
 // hp_plan_stitch over all items, or (long_only) over the long segments' chunks
 // of a fused-tree plan (the rest was pulled by the apply epilogue)
 int plan_stitch(const void* ws, size_t ws_bytes, int64_t T, int32_t D, int64_t V, int32_t P,
-                const float* rows, float* out, cudaStream_t stream, int long_only) {
+                const float* rows, float* out, cudaStream_t stream, int long_only,
+                const StitchWait* wait) {
   HP_REQUIRE(D >= 4 && D % 4 == 0 && D <= 2048, "D must be a multiple of 4 in [4, 2048]");
   HP_REQUIRE(T == 0 || (rows && out), "NULL argument");
   HP_REQUIRE(((uintptr_t)rows & 15) == 0 && ((uintptr_t)out & 15) == 0, "rows / out must be 16-byte aligned");
@@ -303,7 +305,7 @@ int plan_stitch(const void* ws, size_t ws_bytes, int64_t T, int32_t D, int64_t V
   restore_sorted_pos(pl);
   const int D4 = D >> 2;
   cudaStream_t st = stream;
-  if (!g_bcast_tma && !long_only) {
+  if (!g_bcast_tma && !long_only && wait == nullptr) {
     const int g = grid_for(T + T / HP_CHUNK + 1, 8, sm_count() * 8);
     const float4* r4 = reinterpret_cast<const float4*>(rows);
     float4* o4 = reinterpret_cast<float4*>(out);
@@ -323,8 +325,9 @@ int plan_stitch(const void* ws, size_t ws_bytes, int64_t T, int32_t D, int64_t V
     configured = true;
   }
   const int64_t work = long_only && pl.fused ? T / HP_CHUNK + 2 : T + T / HP_CHUNK + 1;
+  const StitchWait wt = wait ? *wait : StitchWait{nullptr, nullptr, nullptr, 0, 0};
   launch_k(k_bcast_rows, dim3(grid_for(work, 8, sm_count() * 8)), dim3(256), smem, st, pl,
-           reinterpret_cast<const float4*>(rows), reinterpret_cast<float4*>(out), D4, long_only);
+           reinterpret_cast<const float4*>(rows), reinterpret_cast<float4*>(out), D4, long_only, wt);
   HP_LAUNCHED(1, "k_bcast_rows");
   return HP_OK;
 }

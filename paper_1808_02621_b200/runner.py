@@ -242,6 +242,7 @@ class HybridRunner:
                               for n in self.tables}
         self._pending_counts: dict = {}
         self._ps_used: set = set()  # plan streams forked since the last join
+        self._want_counts = False
         # NVTX ranges around the step and its phases (HP_NVTX=1; ncu --nvtx filters)
         self.nvtx = os.environ.get("HP_NVTX", "0") == "1"
         self.concurrent_tables = True
@@ -324,22 +325,17 @@ class HybridRunner:
         k(f"push:{name}", True)
         x.push_plan(vals, tab.V, tab.P, r, self.glob_base[name], tab.wss[slot])
         k(f"push:{name}", False)
-        k(f"wait_push:{name}", True)
-        x.wait(0)
-        k(f"wait_push:{name}", False)
-        k(f"apply:{name}", True)
-        x.merge_apply(tab.slab(), opt, wait=False)
+        k(f"apply:{name}", True)  # the push wait is folded into the owner scan
+        x.merge_apply(tab.slab(), opt, wait=True)
         k(f"apply:{name}", False)
-        rc = self._buf(name, "recv_counts", (n,), torch.int32)
-        x.recv_counts(rc)
+        if self._want_counts:  # exchange bytes of a timed step (a memcpy off the graphs)
+            rc = self._buf(name, "recv_counts", (n,), torch.int32)
+            x.recv_counts(rc)
+            self._pending_counts[name] = (r["dest_counts"], rc)
         out = self._buf(name, "out", (T, D), torch.float32)
-        k(f"wait_applied:{name}", True)
-        x.wait(1)
-        k(f"wait_applied:{name}", False)
-        k(f"stitch:{name}", True)
-        ops.plan_stitch(tab.wss[slot], T, D, tab.V, tab.P, x.ret_ptr, out)
+        k(f"stitch:{name}", True)  # the applied wait is folded into the stitch
+        x.stitch_plan(tab.wss[slot], T, tab.V, tab.P, out, wait=True)
         k(f"stitch:{name}", False)
-        self._pending_counts[name] = (r["dest_counts"], rc)
         return out
 
     def exchange_status(self) -> dict:
@@ -529,6 +525,8 @@ class HybridRunner:
         ahead = list(upcoming) if upcoming is not None else (
             [next_batch] if next_batch is not None else [])
         self.check_errors()
+        self._want_counts = timed
+        self._pending_counts = {}
         self.step_count += 1
         if self.nvtx:
             torch.cuda.nvtx.range_push(f"hp.step {self.step_count}")

@@ -127,6 +127,12 @@ class PeerExchange:
         call("hp_xchg_stitch", self.handle, inv.data_ptr(), out.shape[0], out.data_ptr(),
              int(wait), torch.cuda.current_stream().cuda_stream)
 
+    def stitch_plan(self, ws, T: int, V: int, P: int, out, wait: bool = True) -> None:
+        """K6 through the send plan in ``ws``: out[t] = returned row of t's slot
+        (the wait for every owner's apply folded into the kernel)."""
+        call("hp_xchg_stitch_plan", self.handle, ws.ptr, ws.nbytes, T, V, P, out.data_ptr(),
+             int(wait), torch.cuda.current_stream().cuda_stream)
+
     def recv_counts(self, out) -> None:
         call("hp_xchg_recv_counts", self.handle, out.data_ptr(),
              torch.cuda.current_stream().cuda_stream)

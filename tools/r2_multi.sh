@@ -28,6 +28,7 @@ except Exception as e:
 PY
 }
 run default
-run sm --dense-exchange p2p-sm
-run nccl --dense-exchange nccl
-run sparse_only --workload lm1b_sparse
+run pull --dense-exchange p2p-pull
+run dense_pull --workload lm1b_dense --dense-exchange p2p-pull
+run dense_nccl --workload lm1b_dense --dense-exchange nccl
+run dense_sm --workload lm1b_dense --dense-exchange p2p-sm
