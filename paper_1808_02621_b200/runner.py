@@ -325,16 +325,26 @@ class HybridRunner:
         k(f"push:{name}", True)
         x.push_plan(vals, tab.V, tab.P, r, self.glob_base[name], tab.wss[slot])
         k(f"push:{name}", False)
-        k(f"apply:{name}", True)  # the push wait is folded into the owner scan
-        x.merge_apply(tab.slab(), opt, wait=True)
+        # Waits stay one-block kernels (k_wait): folded into the prologue of the
+        # owner scan / stitch, every block of those grids spun, holding SMs the
+        # other tables' concurrent chains need (and deadlocking the one-GPU
+        # emulation of 4 ranks, whose waits then outnumber the SM slots)
+        k(f"wait_push:{name}", True)
+        x.wait(0)
+        k(f"wait_push:{name}", False)
+        k(f"apply:{name}", True)
+        x.merge_apply(tab.slab(), opt, wait=False)
         k(f"apply:{name}", False)
         if self._want_counts:  # exchange bytes of a timed step (a memcpy off the graphs)
             rc = self._buf(name, "recv_counts", (n,), torch.int32)
             x.recv_counts(rc)
             self._pending_counts[name] = (r["dest_counts"], rc)
         out = self._buf(name, "out", (T, D), torch.float32)
-        k(f"stitch:{name}", True)  # the applied wait is folded into the stitch
-        x.stitch_plan(tab.wss[slot], T, tab.V, tab.P, out, wait=True)
+        k(f"wait_applied:{name}", True)
+        x.wait(1)
+        k(f"wait_applied:{name}", False)
+        k(f"stitch:{name}", True)
+        x.stitch_plan(tab.wss[slot], T, tab.V, tab.P, out, wait=False)
         k(f"stitch:{name}", False)
         return out
 
