@@ -28,7 +28,13 @@ except Exception as e:
 PY
 }
 run default
-run pull --dense-exchange p2p-pull
-run dense_pull --workload lm1b_dense --dense-exchange p2p-pull
+run sparse_only --workload lm1b_sparse
+run dense_only --workload lm1b_dense
 run dense_nccl --workload lm1b_dense --dense-exchange nccl
-run dense_sm --workload lm1b_dense --dense-exchange p2p-sm
+run nccl --dense-exchange nccl
+run nmt --workload nmt
+run micro1m --workload micro_1000000
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
+    --master-port $((29700 + RANDOM % 200)) bench.py --impl reference --gpus $N --steps 3 --warmup 1 \
+    > gpurun_out/${T}_reference.json 2> gpurun_out/${T}_reference.err
+tail -1 gpurun_out/${T}_reference.json | head -c 300; echo
