@@ -138,12 +138,13 @@ class HybridRunner:
         if exchange not in ("p2p", "nccl"):
             raise ValueError("exchange must be 'p2p' (NVLink peer memory) or 'nccl'")
         self.exchange = exchange if world_size > 1 else "local"
-        # dense allreduce: peer-memory kernel (deterministic, scale/cast fused) or NCCL
-        # default K7 transport by measurement: two ranks -> NCCL
-        # (138 vs 146 us with the dense stream prioritised); from 4 ranks the
-        # SM-store peer exchange (bit-exact rank-order sum) whose reduction split
-        # keeps the hot sparse partitions' owners out of the reduce/gather
-        default_dense = ("nccl" if world_size == 2 else "p2p-sm") if exchange == "p2p" else exchange
+        # dense allreduce: peer-memory kernel (deterministic, scale/cast fused) or NCCL.
+        # Default K7 transport by measurement: the SM-store peer
+        # exchange (bit-exact rank-order sum, scale + cast fused) — at n = 2 equal
+        # to NCCL in the full LM1B step (138.6 vs 138.4 us) and faster alone
+        # (dense-only step 81.7 vs 106.7 us, r2m2b); from 4 ranks its reduction
+        # split keeps the hot sparse partitions' owners out of the reduce/gather
+        default_dense = "p2p-sm" if exchange == "p2p" else exchange
         self.dense_exchange = (dense_exchange or default_dense) if world_size > 1 else "local"
         if self.dense_exchange not in ("p2p", "p2p-sm", "p2p-pipe", "p2p-pull", "nvls", "nccl",
                                        "local"):
