@@ -17,7 +17,7 @@
 // for the next step).
 #include <cuda_bf16.h>
 
-#include "hp_common.cuh"
+#include "hp_dedup.cuh"
 
 namespace hp {
 namespace {
@@ -78,22 +78,23 @@ __global__ void k_nvls_barrier(int* const* pads, int n, int me, int* state, int 
   HP_SPAN_END(which ? SP_AR_WAIT1 : SP_AR_WAIT0);
 }
 
-// 4 vectors in flight per thread; chunk = S / n elements (S padded to 4n).
-template <typename OutT>
+// U vectors in flight per thread (switch reductions are long-latency: 8 by
+// default); chunk = S / n elements (S padded to 4n).
+template <typename OutT, int U>
 __global__ void __launch_bounds__(256)
 k_nvls_reduce(const float* mc_in, OutT* mc_out, int64_t chunk, int me, float scale) {
   HP_ENTRY(SP_AR_RG);
   const int64_t c4 = chunk >> 2, base4 = (int64_t)me * c4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < c4; j0 += 4 * stride) {
-    float4 v[4];
+  for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < c4; j0 += U * stride) {
+    float4 v[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t j = j0 + u * stride;
       if (j < c4) v[u] = mm_ld_reduce_f32x4(mc_in + (base4 + j) * 4);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t j = j0 + u * stride;
       if (j >= c4) continue;
       float4 x = v[u];
@@ -140,12 +141,12 @@ int hp_nvls_allreduce(const float* mc_in, void* mc_out, int64_t S, int32_t n, in
   const int64_t chunk = S / n;
   launch_k(k_nvls_barrier, dim3(1), dim3(32), 0, st, pads_dev, n, me, state_dev, 0,
            nvls_wait_budget());
-  const int blocks = grid_for(chunk / 16, 256, sm_count() * 2);
+  const int blocks = grid_for(chunk / 32, 256, g_dar_blocks > 0 ? g_dar_blocks : sm_count() * 4);
   if (out_dtype == HP_DTYPE_F32)
-    launch_k(k_nvls_reduce<float>, dim3(blocks), dim3(256), 0, st, mc_in,
+    launch_k(k_nvls_reduce<float, 8>, dim3(blocks), dim3(256), 0, st, mc_in,
              static_cast<float*>(mc_out), chunk, me, scale);
   else
-    launch_k(k_nvls_reduce<__nv_bfloat16>, dim3(blocks), dim3(256), 0, st, mc_in,
+    launch_k(k_nvls_reduce<__nv_bfloat16, 8>, dim3(blocks), dim3(256), 0, st, mc_in,
              static_cast<__nv_bfloat16*>(mc_out), chunk, me, scale);
   launch_k(k_nvls_barrier, dim3(1), dim3(32), 0, st, pads_dev, n, me, state_dev, 1,
            nvls_wait_budget());

@@ -1741,7 +1741,10 @@ int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream) {
   }
   // ~half the SMs: NVLink saturates well below full occupancy, and the sparse
   // tables' latency-bound kernels run concurrently on the rest
-  const int bx = std::max(1, std::min(grid_for(maxc / 16, 256, sms), sms / d->A.n));
+  // scatter grid: ~half the SMs (the sparse tables' kernels run beside it);
+  // hp_debug_set_dar_blocks(b > 0) sets b blocks in total (A/B)
+  const int bx = g_dar_blocks > 0 ? std::max(1, g_dar_blocks / d->A.n)
+                                  : std::max(1, std::min(grid_for(maxc / 16, 256, sms), sms / d->A.n));
   launch_k(k_ar_scatter, dim3(bx, d->A.n), dim3(256), 0, st, d->peers, d->win, d->A,
                                                 reinterpret_cast<const float4*>(grad));
   launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 0);
