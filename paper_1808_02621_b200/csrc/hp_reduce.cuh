@@ -266,7 +266,7 @@ __host__ __device__ constexpr bool reduce_smem_pre() {
 }
 
 template <int TPI, int VPT, int B, class Epi>
-__global__ void __launch_bounds__(256, reduce_smem_pre<TPI, VPT, Epi>() ? 4 : 3)
+__global__ void __launch_bounds__(256, reduce_smem_pre<TPI, VPT, Epi>() && Epi::kPre < 3 ? 4 : 3)
 k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
   const float4* __restrict__ vals = reinterpret_cast<const float4*>(vals_f);
   float4* partials = reinterpret_cast<float4*>(pl.partials);
@@ -670,7 +670,9 @@ template <int TPI, int VPT, class Epi>
 void launch_k_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaStream_t st) {
   // rows in flight per batch: most items hold 1-2 rows, so a small batch keeps
   // registers (and so resident items per SM) up without costing the hot chunks much
-  constexpr int B = VPT >= 2 ? 2 : 8;  // measured: B=2 beats 4 and 8 at VPT=2
+  // measured: B=2 beats 4 and 8 at VPT=2; B=4 at VPT=1 (D <= 128)
+  // keeps the default variant spill-free (B=8 spilled 16-52 B)
+  constexpr int B = VPT >= 2 ? 2 : 4;
   // <= one group per item, many waves (each block fences once if its epilogue
   // stores to peers; hp_debug_set_owner_waves(0) keeps those in one resident wave)
   const int blocks = grid_for(pl.T, 256 / TPI, sm_count() * (Epi::kRemote && !g_owner_waves ? 3 : 16));
