@@ -197,6 +197,7 @@ def _eager_pipelined(emu, seeds, empty=()):
                          [(2, "p2p-sm", "adagrad", True),    # the multi-stream step
                           (2, "p2p-sm", "adagrad", False),
                           (4, "p2p-sm", "adagrad", False),   # weighted split
+                          (8, "p2p-sm", "adagrad", False),   # a full box (the driver's N=8 run)
                           (3, "p2p", "sgd", False),          # copy engines
                           (2, "p2p-pipe", "adam", True),
                           (2, "p2p-pull", "adagrad", True),  # one-shot pull (n = 2 default)
