@@ -2,6 +2,8 @@
 // peer-memory (p2p.cu) paths; see reduce.cu for the summation tree.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "hp_dedup.cuh"
 
 namespace hp {
@@ -409,7 +411,10 @@ __global__ void __launch_bounds__(CMB_NT) k_combine(DedupPlan pl, Epi epi) {
   HP_ENTRY(SP_COMBINE);
   const int D4 = pl.D >> 2;
   const int n_long = pl.counters[C_LONG];
-  const int4 d_first = pl.longs[blockIdx.x];
+  // (speculative: the capacity is T/16 + 2 descriptors; a cooperative grid of
+  // one CTA per SM may be larger)
+  const int4 d_first = (int64_t)blockIdx.x < pl.T / HP_CHUNK + 2 ? pl.longs[blockIdx.x]
+                                                                   : make_int4(0, 0, 0, 0);
   float4* partials = reinterpret_cast<float4*>(pl.partials);
 #pragma unroll 1
   for (int li = blockIdx.x; li < n_long; li += gridDim.x) {
