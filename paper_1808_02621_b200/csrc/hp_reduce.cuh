@@ -411,8 +411,7 @@ __global__ void __launch_bounds__(CMB_NT) k_combine(DedupPlan pl, Epi epi) {
   HP_ENTRY(SP_COMBINE);
   const int D4 = pl.D >> 2;
   const int n_long = pl.counters[C_LONG];
-  // (speculative: the capacity is T/16 + 2 descriptors; a cooperative grid of
-  // one CTA per SM may be larger)
+  // (speculative read guarded by the capacity, T/16 + 2 descriptors)
   const int4 d_first = (int64_t)blockIdx.x < pl.T / HP_CHUNK + 2 ? pl.longs[blockIdx.x]
                                                                    : make_int4(0, 0, 0, 0);
   float4* partials = reinterpret_cast<float4*>(pl.partials);

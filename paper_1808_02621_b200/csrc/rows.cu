@@ -94,6 +94,31 @@ int launch_copy(const Src& src, int64_t n, const int32_t* n_dev, float* out, int
   return HP_OK;
 }
 
+// Work unit `it` of a plan broadcast: (rows n, destination dst, this lane's
+// position). long_only: `it` is a long segment's chunk (a partial slot) — its
+// segment found by binary search over the descriptors' slot bases; else a
+// plan item.
+__device__ __forceinline__ void bcast_unit(const DedupPlan& pl, int it, bool long_only, int n_long,
+                                           int lane, int& n, int& dst, int& pos) {
+  if (long_only) {
+    int lo = 0, hi = n_long - 1;  // last li with longs[li].x <= it
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (pl.longs[mid].x <= it) lo = mid; else hi = mid - 1;
+    }
+    const int4 d = pl.longs[lo];
+    const int k = it - d.x;  // chunk index
+    n = min(HP_CHUNK, d.w - k * HP_CHUNK);
+    dst = d.z;
+    pos = lane < n ? pl.sorted_pos[pl.long_j0[lo] + k * HP_CHUNK + lane] : 0;
+  } else {
+    const int4 item = pl.items[it];
+    n = item.y;
+    dst = item.w < 0 ? pl.longs[-item.w - 1].z : item.z;
+    pos = item.x < 0 ? -item.x - 1 : (lane < n ? pl.sorted_pos[item.x + lane] : 0);
+  }
+}
+
 // ---- K5 / K6 through the plan, on TMA: out[t] = row of position t's segment.
 // One warp per plan item (a segment, or a 16-row chunk of a long one): lane 0
 // bulk-copies the segment's row (slab row of an apply plan / return row of a
@@ -116,17 +141,16 @@ k_bcast_rows(DedupPlan pl, const float4* __restrict__ rows, float4* __restrict__
   if (lane == 0) mbar_init(&s_bar[w], 1);
   __syncwarp();
   const uint32_t bytes = (uint32_t)D4 * 16u;
-  // long_only: the chunks of long segments (w < 0; the first items of a fused-
-  // tree plan), whose rows the apply+pull epilogue left to this kernel
-  const int n_items = long_only && pl.fused ? pl.counters[C_PARTIALS] : pl.counters[C_ITEMS];
+  // long_only: the chunks of long segments only (their rows were left to this
+  // kernel by the apply + pull); work unit = a chunk = a partial slot f, whose
+  // long segment is found by binary search over the descriptors' slot bases
+  const int n_items = long_only ? pl.counters[C_PARTIALS] : pl.counters[C_ITEMS];
+  const int n_long = pl.counters[C_LONG];
   uint32_t parity = 0;
   bool stored = false;
   for (int it = blockIdx.x * 8 + w; it < n_items; it += gridDim.x * 8) {
-    const int4 item = pl.items[it];
-    if (long_only && item.w >= 0) continue;  // a short segment: pulled by the apply epilogue
-    const int n = item.y;
-    const int dst = item.w < 0 ? pl.longs[-item.w - 1].z : item.z;
-    const int pos = item.x < 0 ? -item.x - 1 : (lane < n ? pl.sorted_pos[item.x + lane] : 0);
+    int n, dst, pos;
+    bcast_unit(pl, it, long_only, n_long, lane, n, dst, pos);
     if (dst < 0) {  // dropped ids: zero rows, plain stores
       for (int j = 0; j < n; ++j) {
         const int64_t p = __shfl_sync(0xffffffffu, pos, j);
@@ -159,15 +183,15 @@ k_bcast_rows(DedupPlan pl, const float4* __restrict__ rows, float4* __restrict__
 // each of the item's positions; no TMA round trip through shared memory.
 template <int VPL>
 __global__ void __launch_bounds__(256)
-k_bcast_rows_reg(DedupPlan pl, const float4* __restrict__ rows, float4* __restrict__ out, int D4) {
+k_bcast_rows_reg(DedupPlan pl, const float4* __restrict__ rows, float4* __restrict__ out, int D4,
+                 int long_only) {
   HP_ENTRY(SP_COPY);
   const int lane = threadIdx.x & 31;
-  const int n_items = pl.counters[C_ITEMS];
+  const int n_items = long_only ? pl.counters[C_PARTIALS] : pl.counters[C_ITEMS];
+  const int n_long = pl.counters[C_LONG];
   for (int it = (blockIdx.x * 256 + threadIdx.x) >> 5; it < n_items; it += (gridDim.x * 256) >> 5) {
-    const int4 item = pl.items[it];
-    const int n = item.y;
-    const int dst = item.w < 0 ? pl.longs[-item.w - 1].z : item.z;
-    const int pos = item.x < 0 ? -item.x - 1 : (lane < n ? pl.sorted_pos[item.x + lane] : 0);
+    int n, dst, pos;
+    bcast_unit(pl, it, long_only, n_long, lane, n, dst, pos);
     float4 x[VPL];
 #pragma unroll
     for (int v = 0; v < VPL; ++v) {
@@ -305,15 +329,15 @@ int plan_stitch(const void* ws, size_t ws_bytes, int64_t T, int32_t D, int64_t V
   restore_sorted_pos(pl);
   const int D4 = D >> 2;
   cudaStream_t st = stream;
-  if (!g_bcast_tma && !long_only && wait == nullptr) {
-    const int g = grid_for(T + T / HP_CHUNK + 1, 8, sm_count() * 8);
+  if (!g_bcast_tma && wait == nullptr) {
+    const int g = grid_for(long_only ? T / HP_CHUNK + 2 : T + T / HP_CHUNK + 1, 8, sm_count() * 8);
     const float4* r4 = reinterpret_cast<const float4*>(rows);
     float4* o4 = reinterpret_cast<float4*>(out);
-    if (D4 <= 32) launch_k(k_bcast_rows_reg<1>, dim3(g), dim3(256), 0, st, pl, r4, o4, D4);
-    else if (D4 <= 64) launch_k(k_bcast_rows_reg<2>, dim3(g), dim3(256), 0, st, pl, r4, o4, D4);
-    else if (D4 <= 128) launch_k(k_bcast_rows_reg<4>, dim3(g), dim3(256), 0, st, pl, r4, o4, D4);
-    else if (D4 <= 256) launch_k(k_bcast_rows_reg<8>, dim3(g), dim3(256), 0, st, pl, r4, o4, D4);
-    else launch_k(k_bcast_rows_reg<16>, dim3(g), dim3(256), 0, st, pl, r4, o4, D4);
+    if (D4 <= 32) launch_k(k_bcast_rows_reg<1>, dim3(g), dim3(256), 0, st, pl, r4, o4, D4, long_only);
+    else if (D4 <= 64) launch_k(k_bcast_rows_reg<2>, dim3(g), dim3(256), 0, st, pl, r4, o4, D4, long_only);
+    else if (D4 <= 128) launch_k(k_bcast_rows_reg<4>, dim3(g), dim3(256), 0, st, pl, r4, o4, D4, long_only);
+    else if (D4 <= 256) launch_k(k_bcast_rows_reg<8>, dim3(g), dim3(256), 0, st, pl, r4, o4, D4, long_only);
+    else launch_k(k_bcast_rows_reg<16>, dim3(g), dim3(256), 0, st, pl, r4, o4, D4, long_only);
     HP_LAUNCHED(1, "k_bcast_rows_reg");
     return HP_OK;
   }
@@ -324,7 +348,7 @@ int plan_stitch(const void* ws, size_t ws_bytes, int64_t T, int32_t D, int64_t V
                                  8 * 512 * 16));
     configured = true;
   }
-  const int64_t work = long_only && pl.fused ? T / HP_CHUNK + 2 : T + T / HP_CHUNK + 1;
+  const int64_t work = long_only ? T / HP_CHUNK + 2 : T + T / HP_CHUNK + 1;
   const StitchWait wt = wait ? *wait : StitchWait{nullptr, nullptr, nullptr, 0, 0};
   launch_k(k_bcast_rows, dim3(grid_for(work, 8, sm_count() * 8)), dim3(256), smem, st, pl,
            reinterpret_cast<const float4*>(rows), reinterpret_cast<float4*>(out), D4, long_only, wt);
