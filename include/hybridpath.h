@@ -105,6 +105,9 @@ void hp_debug_set_owner_stream(int on);
 void hp_debug_set_combine_blocks(int n);
 /* Grid of the pipelined dense allreduce (HP_DAR_PIPE); 0 = one block per SM. */
 void hp_debug_set_dar_blocks(int n);
+/* HP_DAR_SM: buckets per step (pieces of every chunk; the phases of one bucket
+ * overlap the waits of the others), 1..16, default 2. */
+void hp_debug_set_dar_buckets(int n);
 /* Instrumentation: grids of the peer-store kernels (push reduce, owner rows):
  * 1 (default) = one group per item, many waves; 0 = one resident wave. */
 void hp_debug_set_owner_waves(int on);

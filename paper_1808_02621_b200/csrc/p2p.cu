@@ -157,12 +157,13 @@ __global__ void k_send_info(const int64_t* __restrict__ send_ids, const int32_t*
   }
 }
 
-// ---- wait until flags[s] >= epoch for every s (one block; bounded spin).
-__global__ void k_wait(void* my_win, int which, int n, long long timeout_cycles, int span) {
+// ---- wait until flags[s] >= epoch - lag for every s (one block; bounded
+// spin). lag > 0: an earlier bucket of a bucketed dense exchange.
+__global__ void k_wait(void* my_win, int which, int n, long long timeout_cycles, int span, int lag) {
   HP_ENTRY(span);
   SigView sig(my_win);
   const int* flags = which == 0 ? sig.push_flag : sig.applied_flag;
-  const int e = *sig.epoch;
+  const int e = *sig.epoch - lag;
   for (int s = threadIdx.x; s < n; s += blockDim.x) {
     const long long t0 = clock64();
     while (ld_acquire_sys(&flags[s]) < e) {
@@ -953,7 +954,7 @@ int hp_xchg_push(hp_xchg_t x, const int64_t* ids, const float* vals, int64_t T, 
 int hp_xchg_wait(hp_xchg_t x, int32_t which, void* stream) {
   HP_REQUIRE(x && (which == 0 || which == 1), "bad wait arguments");
   launch_k(k_wait, dim3(1), dim3(64), 0, static_cast<cudaStream_t>(stream), x->win, which, x->L.n, wait_budget(),
-                                                          which ? SP_WAIT_APPLIED : SP_WAIT_PUSH);
+           which ? SP_WAIT_APPLIED : SP_WAIT_PUSH, 0);
   HP_LAUNCHED(1, "k_wait");
   return HP_OK;
 }
@@ -1131,12 +1132,15 @@ int hp_xchg_status(hp_xchg_t x, int32_t* out_err, void* stream) {
 // K7 over peer memory: dense gradient allreduce fused with scale + cast.
 //
 // Rank r owns chunk r of the S elements. Phase 1 (k_ar_scatter): every rank
-// stores chunk c of its own gradient into rank c's reduce slot [me][*] (NVLink
-// stores; the gradient is read locally, in place, no staging copy). Phase 2
-// (k_ar_reduce_gather): rank c sums the n slots of its chunk in source-rank
-// order (deterministic, bit-reproducible), multiplies by scale, casts, and
-// stores the result into every rank's output. Each phase ends with a
-// last-block epoch flag; one-block k_wait kernels order the phases across GPUs.
+// stores chunk c != me of its own gradient into rank c's reduce slot [me][*]
+// (NVLink stores; the gradient is read locally, in place, no staging copy).
+// Phase 2 (k_ar_reduce_gather): rank c sums the n contributions of its chunk
+// in source-rank order (its own read from grad; deterministic,
+// bit-reproducible), multiplies by scale, casts, and stores the result into
+// every rank's output. Each phase is published by a one-block k_signal (one
+// system fence, cumulative over the stream's earlier kernels) and ordered
+// across GPUs by one-block k_wait kernels. Both phases run in nb buckets
+// (pieces of every chunk), so the waits of one bucket overlap the others.
 // Per rank NVLink bytes: (n-1)/n * S * (4 + out_bytes).
 // ============================================================================
 namespace hp {
@@ -1152,18 +1156,26 @@ struct ArLayout {
   int64_t off4[AR_MAXN + 1];
 };
 
-// blockIdx.y = destination chunk; 4 float4 in flight per thread; no division.
+// Bucket bk of nb: every chunk is cut into nb pieces, [c4*bk/nb, c4*(bk+1)/nb)
+// float4 of it; bucket bk's scatter, reduce and gather only touch piece bk.
+__host__ __device__ __forceinline__ int64_t ar_piece(int64_t c4, int bk, int nb) {
+  return c4 * bk / nb;
+}
+
+// blockIdx.y = destination peer (my own chunk is not copied: the reduce reads
+// my contribution straight from grad); 4 float4 in flight per thread.
 __global__ void __launch_bounds__(256)
-k_ar_scatter(PeerTable peers, void* my_win, ArLayout A, const float4* __restrict__ grad) {
+k_ar_scatter(PeerTable peers, ArLayout A, const float4* __restrict__ grad, int bk, int nb) {
   HP_ENTRY(SP_AR_SCATTER);
-  const int c = blockIdx.y;
+  const int c = (int)blockIdx.y < A.me ? (int)blockIdx.y : (int)blockIdx.y + 1;
   const int64_t b4 = A.off4[c], c4 = A.off4[c + 1] - b4, real4 = A.S_real >> 2;
+  const int64_t p0 = ar_piece(c4, bk, nb), p1 = ar_piece(c4, bk + 1, nb);
   const float4* src = grad + b4;
   float4* dst = reinterpret_cast<float4*>(static_cast<char*>(peers.base[c]) + A.slots_off) +
                 (int64_t)A.me * A.sstride4;
-  const int64_t lim = min(c4, max((int64_t)0, real4 - b4));  // real elements here
+  const int64_t lim = min(p1, max((int64_t)0, real4 - b4));  // real elements here
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < c4; j0 += 4 * stride) {
+  for (int64_t j0 = p0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < p1; j0 += 4 * stride) {
     float4 v[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -1173,7 +1185,7 @@ k_ar_scatter(PeerTable peers, void* my_win, ArLayout A, const float4* __restrict
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int64_t j = j0 + u * stride;
-      if (j < c4) dst[j] = v[u];
+      if (j < p1) dst[j] = v[u];
     }
   }
   // no per-block fence: k_signal (next in the stream) fences once at system
@@ -1198,25 +1210,34 @@ __device__ __forceinline__ void put4<__nv_bfloat16>(void* base, int64_t i4, floa
 
 template <typename OutT>
 __global__ void __launch_bounds__(256)
-k_ar_reduce_gather(PeerTable peers, void* my_win, ArLayout A, float scale) {
+k_ar_reduce_gather(PeerTable peers, void* my_win, ArLayout A, const float4* __restrict__ grad,
+                   float scale, int bk, int nb) {
   HP_ENTRY(SP_AR_RG);
   const int64_t b4 = A.off4[A.me], c4 = A.off4[A.me + 1] - b4;
+  const int64_t p0 = ar_piece(c4, bk, nb), p1 = ar_piece(c4, bk + 1, nb);
+  const int64_t own_lim = min(p1, max((int64_t)0, (A.S_real >> 2) - b4));
   const float4* slots =
       reinterpret_cast<const float4*>(static_cast<char*>(my_win) + A.slots_off);
+  const float4* mine = grad + b4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < c4; j0 += 2 * stride) {
+  for (int64_t j0 = p0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < p1; j0 += 2 * stride) {
     float4 acc[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int64_t j = j0 + u * stride;
       acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (j < c4)
-        for (int s = 0; s < A.n; ++s) acc[u] = f4_add(acc[u], ldg_stream(slots + (int64_t)s * A.sstride4 + j));
+      if (j < p1)
+        for (int s = 0; s < A.n; ++s) {  // source-rank order; my own from grad
+          const float4 x = s == A.me ? (j < own_lim ? ldg_stream(mine + j)
+                                                    : make_float4(0.f, 0.f, 0.f, 0.f))
+                                     : ldg_stream(slots + (int64_t)s * A.sstride4 + j);
+          acc[u] = f4_add(acc[u], x);
+        }
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int64_t j = j0 + u * stride;
-      if (j >= c4) continue;
+      if (j >= p1) continue;
       float4 v = acc[u];
       v.x = __fmul_rn(v.x, scale);
       v.y = __fmul_rn(v.y, scale);
@@ -1234,10 +1255,12 @@ k_ar_reduce_gather(PeerTable peers, void* my_win, ArLayout A, float scale) {
 // ---- copy-engine variant: the NVLink phases are cudaMemcpyAsync peer copies
 // (no SMs), flags are raised by one-warp kernels after the copies complete in
 // stream order; only the local source-order sum runs on the SMs.
-__global__ void k_signal(void* my_win, PeerTable peers, int n, int me, int which) {
+// which 0: epoch + 1 -> push_flag[me] at every rank (and my epoch); which 1:
+// epoch - lag -> applied_flag[me] (lag: buckets still to come this step).
+__global__ void k_signal(void* my_win, PeerTable peers, int n, int me, int which, int lag) {
   HP_ENTRY(which ? SP_AR_WAIT1 : SP_AR_WAIT0);
   SigView sig(my_win);
-  const int e = *sig.epoch + (which == 0 ? 1 : 0);
+  const int e = which == 0 ? *sig.epoch + 1 : *sig.epoch - lag;
   __threadfence_system();
   for (int r = threadIdx.x; r < n; r += blockDim.x) {
     SigView peer(peers.base[r]);
@@ -1689,8 +1712,8 @@ int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream) {
   if (d->mode == HP_DAR_CE) {
     int rc;
     if (d->A.n > 1 && (rc = dar_copies(d, st, false, grad))) return rc;
-    launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 0);
-    launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 0, d->A.n, wait_budget(), SP_AR_WAIT0);
+    launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 0, 0);
+    launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 0, d->A.n, wait_budget(), SP_AR_WAIT0, 0);
     const int brg = grid_for(myc / 8, 256, sms * 2);
     if (d->A.out_bytes == 4)
       launch_k(k_ar_reduce_local<float>, dim3(brg), dim3(256), 0, st, d->win, d->A,
@@ -1699,18 +1722,18 @@ int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream) {
       launch_k(k_ar_reduce_local<__nv_bfloat16>, dim3(brg), dim3(256), 0, st, d->win, d->A,
                reinterpret_cast<const float4*>(grad), scale);
     if (d->A.n > 1 && (rc = dar_copies(d, st, true, grad))) return rc;
-    launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 1);
-    launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 1, d->A.n, wait_budget(), SP_AR_WAIT1);
+    launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 1, 0);
+    launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 1, d->A.n, wait_budget(), SP_AR_WAIT1, 0);
     HP_LAUNCHED(5, "dense p2p allreduce (copy engines)");
     return HP_OK;
   }
   if (d->mode == HP_DAR_PULL) {
     // the peers finished reading my previous copy (their "applied" of my epoch)
-    launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 1, d->A.n, wait_budget(), SP_AR_WAIT1);
+    launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 1, d->A.n, wait_budget(), SP_AR_WAIT1, 0);
     const int bc = grid_for(d->A.S_real / 16, 256, sms * 4);
     launch_k(k_ar_copy_in, dim3(bc), dim3(256), 0, st, d->win, d->A, reinterpret_cast<const float4*>(grad));
-    launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 0);
-    launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 0, d->A.n, wait_budget(), SP_AR_WAIT0);
+    launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 0, 0);
+    launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 0, d->A.n, wait_budget(), SP_AR_WAIT0, 0);
     const int bp = grid_for(d->A.S_real / 8, 256, sms * 4);
     if (d->A.out_bytes == 4)
       launch_k(k_ar_pull_sum<float>, dim3(bp), dim3(256), 0, st, d->peers, d->win, d->A,
@@ -1718,7 +1741,7 @@ int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream) {
     else
       launch_k(k_ar_pull_sum<__nv_bfloat16>, dim3(bp), dim3(256), 0, st, d->peers, d->win, d->A,
                reinterpret_cast<const float4*>(grad), scale);
-    launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 1);
+    launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 1, 0);
     HP_LAUNCHED(6, "dense p2p allreduce (one-shot pull)");
     return HP_OK;
   }
@@ -1735,28 +1758,42 @@ int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream) {
     else
       launch_k(k_ar_pipe<__nv_bfloat16>, dim3(blocks), dim3(256), 0, st, d->peers, d->win, d->A,
                reinterpret_cast<const float4*>(grad), scale, arrive, queue, wait_budget());
-    launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 1, d->A.n, wait_budget(), SP_AR_WAIT1);
+    launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 1, d->A.n, wait_budget(), SP_AR_WAIT1, 0);
     HP_LAUNCHED(2, "dense p2p allreduce (pipelined)");
     return HP_OK;
   }
-  // ~half the SMs: NVLink saturates well below full occupancy, and the sparse
-  // tables' latency-bound kernels run concurrently on the rest
+  // SM stores in nb buckets (hp_debug_set_dar_buckets; default 2): every
+  // chunk is cut into nb pieces; all scatters go first (each published with
+  // its own epoch), then per bucket wait -> reduce/gather -> publish, so one
+  // bucket's cross-GPU wait overlaps the other buckets' link traffic and only
+  // the last gather's wait is exposed. Epochs advance by nb per step.
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(g_dar_buckets, std::max<int64_t>(1, maxc / 4096)));
   // scatter grid: ~half the SMs (the sparse tables' kernels run beside it);
-  // hp_debug_set_dar_blocks(b > 0) sets b blocks in total (A/B)
-  const int bx = g_dar_blocks > 0 ? std::max(1, g_dar_blocks / d->A.n)
-                                  : std::max(1, std::min(grid_for(maxc / 16, 256, sms), sms / d->A.n));
-  launch_k(k_ar_scatter, dim3(bx, d->A.n), dim3(256), 0, st, d->peers, d->win, d->A,
-                                                reinterpret_cast<const float4*>(grad));
-  launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 0);
-  launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 0, d->A.n, wait_budget(), SP_AR_WAIT0);
-  const int brg = grid_for(std::max<int64_t>(myc, 8) / 8, 256, sms * 2);
-  if (d->A.out_bytes == 4)
-    launch_k(k_ar_reduce_gather<float>, dim3(brg), dim3(256), 0, st, d->peers, d->win, d->A, scale);
-  else
-    launch_k(k_ar_reduce_gather<__nv_bfloat16>, dim3(brg), dim3(256), 0, st, d->peers, d->win, d->A, scale);
-  launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 1);
-  launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 1, d->A.n, wait_budget(), SP_AR_WAIT1);
-  HP_LAUNCHED(6, "dense p2p allreduce");
+  // hp_debug_set_dar_blocks(b > 0) sets b blocks per bucket in total (A/B)
+  const int np = d->A.n - 1;
+  const int bx = g_dar_blocks > 0 ? std::max(1, g_dar_blocks / std::max(1, np))
+                                  : std::max(1, std::min(grid_for(maxc / nb / 16, 256, sms),
+                                                         sms / std::max(1, np)));
+  const int brg = grid_for(std::max<int64_t>(myc / nb, 8) / 8, 256, sms * 2);
+  const float4* g4 = reinterpret_cast<const float4*>(grad);
+  for (int b = 0; b < nb; ++b) {
+    if (np > 0)
+      launch_k(k_ar_scatter, dim3(bx, np), dim3(256), 0, st, d->peers, d->A, g4, b, nb);
+    launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 0, 0);
+  }
+  for (int b = 0; b < nb; ++b) {
+    const int lag = nb - 1 - b;
+    launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 0, d->A.n, wait_budget(), SP_AR_WAIT0, lag);
+    if (d->A.out_bytes == 4)
+      launch_k(k_ar_reduce_gather<float>, dim3(brg), dim3(256), 0, st, d->peers, d->win, d->A, g4,
+               scale, b, nb);
+    else
+      launch_k(k_ar_reduce_gather<__nv_bfloat16>, dim3(brg), dim3(256), 0, st, d->peers, d->win,
+               d->A, g4, scale, b, nb);
+    launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 1, lag);
+  }
+  launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 1, d->A.n, wait_budget(), SP_AR_WAIT1, 0);
+  HP_LAUNCHED(nb * ((np > 0 ? 1 : 0) + 4) + 1, "dense p2p allreduce");
   return HP_OK;
 }
 

@@ -37,7 +37,7 @@ def knobs(cuda):
     from paper_1808_02621_b200 import _lib
 
     lib = _lib.load()
-    defaults = {"owner_stream": 2, "dar_blocks": 0, "wait_timeout": 0}
+    defaults = {"owner_stream": 2, "dar_blocks": 0, "dar_buckets": 2, "wait_timeout": 0}
 
     def set_(name, v):
         getattr(lib, f"hp_debug_set_{name}")(v)
@@ -191,6 +191,18 @@ def _eager_pipelined(emu, seeds, empty=()):
         emu.check_outputs(emu.oracle_step(data[i][0]))
     emu.check_tables()
     emu.errors()
+
+
+@pytest.mark.parametrize("n,buckets,opt", [(2, 1, "adagrad"), (3, 5, "sgd"), (4, 3, "adam")])
+def test_emulated_dense_buckets_bit_exact(cuda, knobs, n, buckets, opt):
+    """The SM-store dense exchange with its phases cut into `buckets` pieces per
+    chunk (per-bucket epochs): same rank-order sums as one bucket."""
+    knobs("dar_buckets", buckets)
+    emu = Emu(cuda, n, _small_tables(), {"lstm": 100_000}, opt, "p2p-sm")
+    try:
+        _eager_pipelined(emu, [1, 2, 3])
+    finally:
+        emu.close()
 
 
 @pytest.mark.parametrize("n,dense_exchange,opt,concurrent",
