@@ -103,10 +103,13 @@ void hp_debug_set_rs_ctas(int n);
 void hp_debug_set_owner_stream(int on);
 /* Instrumentation: k_combine grid cap when its epilogue stores to peers (0 = SM count, default). */
 void hp_debug_set_combine_blocks(int n);
-/* Grid of the pipelined dense allreduce (HP_DAR_PIPE); 0 = one block per SM. */
+/* Grid of the pipelined dense allreduce (HP_DAR_PIPE; 0 = one block per SM) and
+ * of the SM-store scatter (HP_DAR_SM; 0 = up to one block per SM). */
 void hp_debug_set_dar_blocks(int n);
+/* Grid of the SM-store reduce/gather kernel (HP_DAR_SM); 0 = two blocks per SM. */
+void hp_debug_set_dar_rg_blocks(int n);
 /* HP_DAR_SM: buckets per step (pieces of every chunk; the phases of one bucket
- * overlap the waits of the others), 1..16, default 2. */
+ * overlap the waits of the others), 1..16, default 1. */
 void hp_debug_set_dar_buckets(int n);
 /* Instrumentation: grids of the peer-store kernels (push reduce, owner rows):
  * 1 (default) = one group per item, many waves; 0 = one resident wave. */

@@ -1762,19 +1762,23 @@ int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream) {
     HP_LAUNCHED(2, "dense p2p allreduce (pipelined)");
     return HP_OK;
   }
-  // SM stores in nb buckets (hp_debug_set_dar_buckets; default 2): every
+  // SM stores in nb buckets (hp_debug_set_dar_buckets; default 1): every
   // chunk is cut into nb pieces; all scatters go first (each published with
   // its own epoch), then per bucket wait -> reduce/gather -> publish, so one
   // bucket's cross-GPU wait overlaps the other buckets' link traffic and only
   // the last gather's wait is exposed. Epochs advance by nb per step.
+  // Measured at N = 2 (LM1B dense): every extra bucket costs ~17 us of kernel
+  // boundaries (5 more dependent launches) for ~6 us of hidden wait, so 1.
   const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(g_dar_buckets, std::max<int64_t>(1, maxc / 4096)));
   // scatter grid: ~half the SMs (the sparse tables' kernels run beside it);
-  // hp_debug_set_dar_blocks(b > 0) sets b blocks per bucket in total (A/B)
+  // hp_debug_set_dar_blocks / _dar_rg_blocks (b > 0): b blocks in total per
+  // scatter / per reduce-gather (A/B)
   const int np = d->A.n - 1;
   const int bx = g_dar_blocks > 0 ? std::max(1, g_dar_blocks / std::max(1, np))
                                   : std::max(1, std::min(grid_for(maxc / nb / 16, 256, sms),
                                                          sms / std::max(1, np)));
-  const int brg = grid_for(std::max<int64_t>(myc / nb, 8) / 8, 256, sms * 2);
+  const int brg = g_dar_rg_blocks > 0 ? g_dar_rg_blocks
+                                      : grid_for(std::max<int64_t>(myc / nb, 8) / 8, 256, sms * 2);
   const float4* g4 = reinterpret_cast<const float4*>(grad);
   for (int b = 0; b < nb; ++b) {
     if (np > 0)

@@ -37,7 +37,7 @@ def knobs(cuda):
     from paper_1808_02621_b200 import _lib
 
     lib = _lib.load()
-    defaults = {"owner_stream": 2, "dar_blocks": 0, "dar_buckets": 2, "wait_timeout": 0}
+    defaults = {"owner_stream": 2, "dar_blocks": 0, "dar_buckets": 1, "dar_rg_blocks": 0, "wait_timeout": 0}
 
     def set_(name, v):
         getattr(lib, f"hp_debug_set_{name}")(v)
@@ -193,7 +193,7 @@ def _eager_pipelined(emu, seeds, empty=()):
     emu.errors()
 
 
-@pytest.mark.parametrize("n,buckets,opt", [(2, 1, "adagrad"), (3, 5, "sgd"), (4, 3, "adam")])
+@pytest.mark.parametrize("n,buckets,opt", [(2, 2, "adagrad"), (3, 5, "sgd"), (4, 3, "adam")])
 def test_emulated_dense_buckets_bit_exact(cuda, knobs, n, buckets, opt):
     """The SM-store dense exchange with its phases cut into `buckets` pieces per
     chunk (per-bucket epochs): same rank-order sums as one bucket."""

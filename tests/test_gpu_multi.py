@@ -24,8 +24,8 @@ def _ngpu():
     ("adagrad", "p2p", "p2p", "", "hybrid"),
     # weighted reduction split (rank 0 takes no chunk), SM stores and copy engines
     ("adagrad", "p2p", "p2p-sm", "split=first0", "hybrid"),
-    # the SM-store dense exchange in 1 and 5 buckets (default 2)
-    ("adagrad", "p2p", "p2p-sm", "dar_buckets=1", "hybrid"),
+    # the SM-store dense exchange in 2 and 5 buckets (default 1)
+    ("adagrad", "p2p", "p2p-sm", "dar_buckets=2", "hybrid"),
     ("sgd", "p2p", "p2p-sm", "dar_buckets=5", "hybrid"),
     # the last rank pushes an empty IndexedSlices for one table at step 2
     ("sgd", "p2p", "nccl", "empty=1", "hybrid"),
