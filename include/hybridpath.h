@@ -124,6 +124,9 @@ void hp_debug_set_wait_timeout(long long cycles);
  * step and at scale) = sorted item order and a separate k_combine. Takes effect
  * for plans built afterwards. */
 void hp_debug_set_fuse_tree(int on);
+/* Plans built after the call: 1 (default) = items long-chunks-first, so the
+ * n = 1 apply can run its short items on a side stream; 0 = build order. */
+void hp_debug_set_split_long(int on);
 /* A/B: 1 (default) = chain kernels carry their stream's priority as a launch
  * attribute (graph node priority); 0 = plain launches. */
 void hp_debug_set_launch_prio(int on);
@@ -222,10 +225,12 @@ int hp_apply_plan(const float* rows, int64_t R, hp_slab slab, hp_optim opt, void
  * positions of every short segment (<= 16 rows of one id) from its registers,
  * so the pull re-reads no updated row and walks no routing; the long (hot)
  * segments' positions get one TMA broadcast kernel after the apply (with the
- * row stream on: hp_plan_stitch after it). Replaces: update + pull
- * (`simulate.py:195-199,294-323`). */
+ * row stream on: hp_plan_stitch after it). side_stream (nullable): the short
+ * segments' reduce + apply + pull runs there, forked from and joined back into
+ * `stream`, beside the long segments' chain (their chunks -> k_combine ->
+ * broadcast) on `stream`. Replaces: update + pull (`simulate.py:195-199,294-323`). */
 int hp_apply_plan_pull(const float* rows, int64_t R, hp_slab slab, hp_optim opt, float* out,
-                       void* ws, size_t ws_bytes, void* stream);
+                       void* ws, size_t ws_bytes, void* stream, void* side_stream);
 
 /* ---------------------------------------------------------------- K5 / K6
  * Gather: out[i] = slab row of global id ids[i], i < n (coalesced row copy); a

@@ -104,11 +104,12 @@ SIGNATURES = {
     "hp_xchg_debug_sig": (C.c_int, [vp, vp, vp]),
     "hp_debug_set_wait_timeout": (None, [C.c_longlong]),
     "hp_debug_set_fuse_tree": (None, [C.c_int]),
+    "hp_debug_set_split_long": (None, [C.c_int]),
     "hp_debug_set_launch_prio": (None, [C.c_int]),
     "hp_debug_set_bcast_tma": (None, [C.c_int]),
     "hp_graph_instantiate": (C.c_int, [vp, i32, C.POINTER(vp)]),
     "hp_plan_stitch": (C.c_int, [vp, sz, i64, i32, i64, i32, vp, vp, vp]),
-    "hp_apply_plan_pull": (C.c_int, [vp, i64, Slab, Optim, vp, vp, sz, vp]),
+    "hp_apply_plan_pull": (C.c_int, [vp, i64, Slab, Optim, vp, vp, sz, vp, vp]),
     "hp_xchg_ret_ptr": (C.c_int, [vp, C.POINTER(vp)]),
     "hp_xchg_pull": (C.c_int, [vp, vp, i64, i64, i32, vp, vp, vp, vp]),
     "hp_xchg_stitch_plan": (C.c_int, [vp, vp, sz, i64, i64, i32, vp, i32, vp]),

@@ -179,7 +179,7 @@ __device__ __forceinline__ void emit_items(const DedupPlan& pl, int u, int j0, i
                                            int bi, int bp, int bl, int pos0, int tot_p) {
   const int n0 = (L + HP_CHUNK - 1) / HP_CHUNK;
   const bool lg = L > HP_CHUNK;
-  const bool reorder = pl.fused != 0;
+  const bool reorder = pl.reorder != 0;
   const int si = reorder ? tot_p + (bi - bp) : bi;  // index of a short segment's item
   if (L == 1) {
     pl.items[si] = make_int4(-(pos0 + 1), 1, dst, 1);
@@ -819,6 +819,8 @@ int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, i
   pl->send_info = (int4*)take(16 * Tc);
   pl->nw = g_rowstream_off ? 0 : rs_warps(D);
   pl->fused = pl->nw <= 0 && g_fuse_tree;
+  pl->reorder = pl->fused || (pl->nw <= 0 && g_split_long);
+  pl->part = 0;
   pl->sorted_pos = pl->pos[0];
   pl->prof = g_prof;
   return HP_OK;
@@ -859,6 +861,7 @@ int g_reduce_b = 2;
 // 24.3 vs 25.4 us, but the step no faster and 1.8x slower at the micro
 // config's 16M draws (one CTA per long chunk holds 4-8x fewer chunks in flight
 // than k_reduce's thread groups)
+int g_split_long = 1;
 int g_fuse_tree = 0;
 HP_SPAN_SETTER(set_spans_dedup)
 

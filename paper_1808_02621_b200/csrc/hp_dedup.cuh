@@ -45,6 +45,8 @@ struct DedupPlan {
   // its first item and that item's first sorted row. nw == 0: not used.
   int32_t nw;
   int32_t fused;        // 1: long chunks first + fused tree in k_reduce (no k_combine)
+  int32_t reorder;      // 1: items long-chunks-first ([0, C_PARTIALS) long chunks, then short)
+  int32_t part;         // per launch: 0 every item, 1 long chunks only, 2 short items only
   int32_t* wb_item;     // [HP_RS_MAX_WARPS + 1]
   int32_t* wb_row;      // [HP_RS_MAX_WARPS + 1]
   // fused upper levels of long segments (combine_up): one arrival counter per
@@ -74,6 +76,8 @@ extern int g_dar_rg_blocks;   // HP_DAR_SM reduce/gather grid (0: 2 per SM)
 extern int g_dar_buckets;     // HP_DAR_SM buckets per step
 extern int g_owner_waves;     // peer-store kernels: many waves (1) or one resident wave (0)
 extern int g_reduce_b;        // k_reduce rows in flight at VPT=2 (2, 4, 8)
+extern int g_split_long;      // 1 (default): long-first items; the n = 1 apply runs its short
+                              // items on a side stream beside the long chain
 extern int g_fuse_tree;       // 1 (default): fused tree (long_chunk) when the row stream is off
 
 size_t dedup_ws_bytes(int64_t T, int32_t D, int32_t P);

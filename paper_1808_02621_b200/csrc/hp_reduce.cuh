@@ -363,7 +363,11 @@ k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
   // CTAs first take the long chunks, one per CTA at a time (long_chunk: TMA
   // staging + the fused tree), then every group takes short items. Two loops
   // keep the tree's registers out of the short-item loop, which runs spill-free.
-  const int n_long_items = pl.fused ? pl.counters[C_PARTIALS] : 0;
+  const int n_part = pl.counters[C_PARTIALS];
+  const int n_long_items = pl.fused ? n_part : 0;
+  // pl.part (long-first items): 1 = the long chunks only, 2 = the short items only
+  const int it_lo = pl.part == 2 ? n_part : n_long_items;
+  const int it_hi = pl.part == 1 ? n_part : n_items;
   if (n_long_items > (int)blockIdx.x) {  // CTA-uniform
     if (threadIdx.x == 0) mbar_init(&s_bar, 1);
     __syncthreads();
@@ -375,7 +379,7 @@ k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
   }
   const int stride = gridDim.x * GPB;
 #pragma unroll 1
-  for (int it = n_long_items + blockIdx.x * GPB + threadIdx.x / TPI; it < n_items; it += stride)
+  for (int it = it_lo + blockIdx.x * GPB + threadIdx.x / TPI; it < it_hi; it += stride)
     process(it);
   HP_SPAN_END(SP_REDUCE);
 }
@@ -679,7 +683,8 @@ void launch_k_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cud
   constexpr int B = VPT >= 2 ? 2 : 4;
   // <= one group per item, many waves (each block fences once if its epilogue
   // stores to peers; hp_debug_set_owner_waves(0) keeps those in one resident wave)
-  const int blocks = grid_for(pl.T, 256 / TPI, sm_count() * (Epi::kRemote && !g_owner_waves ? 3 : 16));
+  const int blocks = grid_for(pl.part == 1 ? 2 * pl.T / HP_CHUNK + 2 : pl.T, 256 / TPI,
+                              sm_count() * (Epi::kRemote && !g_owner_waves ? 3 : 16));
   if (VPT == 2 && g_reduce_b == 4)
     launch_k_reduce_b<TPI, VPT, 4>(pl, vals, epi, st, blocks);
   else if (VPT == 2 && g_reduce_b == 8)
@@ -710,6 +715,7 @@ int launch_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaSt
     else launch_k_reduce<256, 2>(pl, vals, epi, st);
     HP_LAUNCHED(1, "k_reduce");
   }
+  if (pl.part == 2) return HP_OK;  // short items only: no long segment to close
   // fused tree (items in long-first order, pl.nw == 0): k_reduce closed every
   // long segment itself (long_chunk); otherwise one CTA per long segment
   if (pl.fused) {

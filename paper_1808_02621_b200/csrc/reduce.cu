@@ -33,6 +33,16 @@ EpiApply<OPT> make_apply(const hp_slab& s, const hp_optim& o, float* out) {
   return e;
 }
 
+// Fork / join events of the split apply (hp_apply_plan_pull with a side
+// stream), per device; recorded and waited on back to back, so two suffice.
+cudaEvent_t split_event(int k) {
+  static cudaEvent_t ev[64][2] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!ev[dev][k]) cudaEventCreateWithFlags(&ev[dev][k], cudaEventDisableTiming);
+  return ev[dev][k];
+}
+
 // out (nullable): the fused pull (the plan's items in long-first order only).
 int apply_plan(const DedupPlan& pl, const float* vals, const hp_slab& s, const hp_optim& o,
                cudaStream_t st, float* out = nullptr) {
@@ -137,7 +147,7 @@ int hp_apply_plan(const float* rows, int64_t R, hp_slab slab, hp_optim opt, void
 // tree plan the apply epilogue writes the positions itself (long segments: the
 // root's TMA bulk stores); otherwise the pull runs after it (hp_plan_stitch).
 int hp_apply_plan_pull(const float* rows, int64_t R, hp_slab slab, hp_optim opt, float* out,
-                       void* ws, size_t ws_bytes, void* stream) {
+                       void* ws, size_t ws_bytes, void* stream, void* side_stream) {
   int rc = check_slab(slab, opt.kind);
   if (rc) return rc;
   HP_REQUIRE(R == 0 || (rows != nullptr && out != nullptr), "rows / out is NULL");
@@ -151,6 +161,25 @@ int hp_apply_plan_pull(const float* rows, int64_t R, hp_slab slab, hp_optim opt,
   // broadcast after the apply. (Measured: doing the long ones in k_combine's
   // tail behind a grid barrier needs a cooperative launch, which waited for the
   // other table's concurrent kernels to drain: 43.6 -> 76 us per step.)
+  if (!rowstream && side_stream != nullptr && pl.reorder && !pl.fused && R > 0) {
+    // items are long-chunks-first: the short items (apply + pull from the
+    // epilogue) fork onto side_stream; the long chunks -> k_combine -> their
+    // broadcast stay on stream; one join. The long chain no longer waits for
+    // the short items' reduce.
+    cudaStream_t ss = static_cast<cudaStream_t>(side_stream);
+    cudaEvent_t fork = split_event(0), join = split_event(1);
+    HP_CUDA(cudaEventRecord(fork, st));
+    HP_CUDA(cudaStreamWaitEvent(ss, fork, 0));
+    DedupPlan ps = pl, pg = pl;
+    ps.part = 2;
+    pg.part = 1;
+    if ((rc = apply_plan(ps, rows, slab, opt, ss, out))) return rc;
+    HP_CUDA(cudaEventRecord(join, ss));
+    if ((rc = apply_plan(pg, rows, slab, opt, st, out))) return rc;
+    if ((rc = plan_stitch(ws, ws_bytes, R, slab.D, slab.V, slab.P, slab.w, out, st, 1))) return rc;
+    HP_CUDA(cudaStreamWaitEvent(st, join, 0));
+    return HP_OK;
+  }
   if (!rowstream) {
     if ((rc = apply_plan(pl, rows, slab, opt, st, out))) return rc;
     return plan_stitch(ws, ws_bytes, R, slab.D, slab.V, slab.P, slab.w, out, st, 1);

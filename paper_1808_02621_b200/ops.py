@@ -289,14 +289,16 @@ def apply_plan(rows: torch.Tensor, n: int, slab: Slab, opt: Optim, ws: Workspace
 
 
 def apply_plan_pull(rows: torch.Tensor, n: int, slab: Slab, opt: Optim, out: torch.Tensor,
-                    ws: Workspace, stream=None) -> torch.Tensor:
+                    ws: Workspace, stream=None, side_stream=None) -> torch.Tensor:
     """K4 + K5 fused (n = 1): reduce + apply with the plan in ``ws`` and
-    out[t] = the updated row of position t's id (``hp_apply_plan_pull``)."""
+    out[t] = the updated row of position t's id (``hp_apply_plan_pull``).
+    ``side_stream``: the short segments run there, beside the long ones' chain."""
     _need(rows, torch.float32, "rows", 2)
     _need(out, torch.float32, "out", 2)
     if out.shape[0] < n or out.shape[1] != slab.D:
         raise ValueError(f"out must be at least [{n}, {slab.D}]")
-    call("hp_apply_plan_pull", _p(rows), n, slab, opt, _p(out), ws.ptr, ws.nbytes, _stream(stream))
+    call("hp_apply_plan_pull", _p(rows), n, slab, opt, _p(out), ws.ptr, ws.nbytes, _stream(stream),
+         None if side_stream is None else _stream(side_stream))
     return out
 
 

@@ -239,6 +239,13 @@ class HybridRunner:
                                               else pt)
                          for n in self.tables}
         self._dense_stream = torch.cuda.Stream(device=self.device, priority=pd)
+        # n = 1: each table's short segments (reduce + apply + pull) run on a
+        # side stream beside its long segments' chain (hp_apply_plan_pull);
+        # one priority step below the chain. HP_SPLIT_LONG=0 keeps one stream.
+        self._short_streams = ({n: torch.cuda.Stream(device=self.device, priority=min(pt + 1, 0))
+                                for n in self.tables}
+                               if world_size == 1 and os.environ.get("HP_SPLIT_LONG", "1") == "1"
+                               else {})
         self._plan_streams = {n: torch.cuda.Stream(device=self.device, priority=pp)
                               for n in self.tables}
         self._pending_counts: dict = {}
@@ -462,7 +469,8 @@ class HybridRunner:
             self._plan(tab, ids, slot)
         out = self._buf(tab.name, "out", (T, tab.D), torch.float32)
         self._kev(f"k4:{tab.name}", True)  # K4 + K5: apply, and the pull fused into it
-        ops.apply_plan_pull(vals, T, slab, opt, out, tab.wss[slot])
+        ops.apply_plan_pull(vals, T, slab, opt, out, tab.wss[slot],
+                            side_stream=self._short_streams.get(tab.name))
         self._kev(f"k4:{tab.name}", False)
         return out
 

@@ -196,6 +196,40 @@ def test_local_apply_and_gather(cuda, level0, opt):
     assert np.array_equal(tab.w.cpu().numpy(), state["w"])
 
 
+@pytest.mark.parametrize("opt", ["adagrad", "adam"])
+@pytest.mark.parametrize("mode", ["side", "one_stream", "build_order"])
+def test_apply_plan_pull_split_bit_exact(cuda, opt, mode):
+    """K4 + K5 fused (hp_apply_plan_pull) at the LM1B softmax shape: the short
+    segments on a side stream beside the long chain (default), on one stream,
+    and with plans in build order (hp_debug_set_split_long(0)) == oracle."""
+    from paper_1808_02621_b200 import _lib, ops
+    from paper_1808_02621_b200.synth import log_uniform_ids, zipf_ids
+
+    V, D, P, T = 800_000, 512, 8, 2560
+    rng = np.random.default_rng(17)
+    owner = np.zeros(P, dtype=np.int32)
+    tab, state = _slab_for(V, D, P, owner, 0, opt, seed=5, dev=cuda)
+    hpar = {"lr": 0.1, "beta1": 0.9, "beta2": 0.999, "eps": 1e-8}
+    side = torch.cuda.Stream(device=cuda) if mode == "side" else None
+    _lib.load().hp_debug_set_split_long(0 if mode == "build_order" else 1)
+    try:
+        for step in (1, 2):
+            ids = np.concatenate([zipf_ids(rng, V, T), log_uniform_ids(rng, V, 8192)])
+            ids[::997] = V + 5  # dropped ids: zero rows, no update
+            vals = rng.standard_normal((ids.size, D), dtype=F32)
+            res = orc.sparse_step(state, opt, hpar, step, [(ids, vals)], V, P, owner)
+            o = tab.optimizer.c_struct(step, 1.0)
+            ops.apply_plan_build(_t(ids, cuda), tab.slab(), tab.ws)
+            out = torch.full((ids.size, D), float("nan"), device=cuda)
+            ops.apply_plan_pull(_t(vals, cuda), ids.size, tab.slab(), o, out, tab.ws,
+                                side_stream=side)
+            torch.cuda.synchronize()
+            assert np.array_equal(out.cpu().numpy(), res[0]["out"]), step
+        assert np.array_equal(tab.w.cpu().numpy(), state["w"])
+    finally:
+        _lib.load().hp_debug_set_split_long(1)
+
+
 def test_init_rows_bit_exact(cuda):
     from paper_1808_02621_b200 import ops
 
