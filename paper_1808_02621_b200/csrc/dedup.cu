@@ -190,6 +190,7 @@ __device__ __forceinline__ void emit_items(const DedupPlan& pl, int u, int j0, i
     const int n = min(HP_CHUNK, L - k * HP_CHUNK);
     const int idx = !lg ? si + k : (reorder ? bp + k : bi + k);
     pl.items[idx] = make_int4(j0 + k * HP_CHUNK, n, lg ? bp + k : dst, lg ? -(bl + 1) : 1);
+    if (lg) pl.part_desc[bp + k] = make_int4(j0 + k * HP_CHUNK, n, dst, bl);
     emit_bounds(pl, bi + k, j0 + k * HP_CHUNK, n);
   }
   if (lg) {
@@ -735,6 +736,7 @@ size_t dedup_ws_bytes(int64_t T, int32_t D, int32_t P) {
   s += 5 * align256(4 * Tc);          // segidx, sigma, part_off, dst, long_tmp
   s += align256(16 * Tc) + align256(16 * (Tc / HP_CHUNK + 2));  // items, longs
   s += align256(4 * (Tc / HP_CHUNK + 2));                         // long_j0
+  s += align256(16 * prow);                                       // part_desc
   s += align256(4 * ((size_t)P + 1)) + 2 * align256(4 * (size_t)P);
   s += align256(4 * HP_RADIX * ntiles) + align256(4 * HP_RADIX);
   s += align256(4 * nscan);
@@ -806,6 +808,7 @@ int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, i
   pl->items = (int4*)take(16 * Tc);
   pl->longs = (int4*)take(16 * (Tc / HP_CHUNK + 2));
   pl->long_j0 = (int32_t*)take(4 * (Tc / HP_CHUNK + 2));
+  pl->part_desc = (int4*)take(16 * (2 * Tc / HP_CHUNK + 2));
   pl->first_u = (int32_t*)take(4 * ((size_t)P + 1));
   pl->part_base = (int32_t*)take(4 * (size_t)P);
   pl->zero_owner = (int32_t*)take(4 * (size_t)P);

@@ -95,22 +95,16 @@ int launch_copy(const Src& src, int64_t n, const int32_t* n_dev, float* out, int
 }
 
 // Work unit `it` of a plan broadcast: (rows n, destination dst, this lane's
-// position). long_only: `it` is a long segment's chunk (a partial slot) — its
-// segment found by binary search over the descriptors' slot bases; else a
-// plan item.
+// position). long_only: `it` is a long segment's chunk (a partial slot), read
+// from its descriptor (one load, then the positions); else a plan item.
 __device__ __forceinline__ void bcast_unit(const DedupPlan& pl, int it, bool long_only, int n_long,
                                            int lane, int& n, int& dst, int& pos) {
   if (long_only) {
-    int lo = 0, hi = n_long - 1;  // last li with longs[li].x <= it
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (pl.longs[mid].x <= it) lo = mid; else hi = mid - 1;
-    }
-    const int4 d = pl.longs[lo];
-    const int k = it - d.x;  // chunk index
-    n = min(HP_CHUNK, d.w - k * HP_CHUNK);
+    (void)n_long;
+    const int4 d = pl.part_desc[it];
+    n = d.y;
     dst = d.z;
-    pos = lane < n ? pl.sorted_pos[pl.long_j0[lo] + k * HP_CHUNK + lane] : 0;
+    pos = lane < n ? pl.sorted_pos[d.x + lane] : 0;
   } else {
     const int4 item = pl.items[it];
     n = item.y;
