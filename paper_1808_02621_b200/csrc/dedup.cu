@@ -251,13 +251,22 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
     ++nprof;                                                          \
   } while (0)
   HP_PROF();
+  // Error bits gather in shared memory and reach counters[C_ERR] once per CTA
+  // at the end; CTA 0 zeroes the word first (ordered by the cluster barriers
+  // in between), so the plan needs no memset node in front of this kernel.
+  __shared__ int s_err;
+  if (tid == 0) {
+    s_err = 0;
+    if (c == 0) pl.counters[C_ERR] = 0;
+  }
+  __syncthreads();
 
   uint32_t key[IPT];
   int32_t pos[IPT];
 #pragma unroll
   for (int r = 0; r < IPT; ++r) {
     const int i = c * S + w * 32 * IPT + r * 32 + lane;
-    key[r] = i < T ? load_key(ids, i, pl.V, &pl.counters[C_ERR]) : 0xffffffffu;
+    key[r] = i < T ? load_key(ids, i, pl.V, &s_err) : 0xffffffffu;
     pos[r] = i;
   }
   HP_PROF();
@@ -418,7 +427,7 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
       slot = s_pbase[p] + (u - s_first[p]);
       if (send_ids) send_ids[slot] = id;
       if (counts) counts[slot] = L;
-      dst = seg_dst(id, p, slot, dst_pb, route, &pl.counters[C_ERR]);
+      dst = seg_dst(id, p, slot, dst_pb, route, &s_err);
     }
     s_sig[sidx] = slot;
     emit_items(pl, u, c * S + li, L, dst, bi_, bp_, bl_, (int)s_buf[li].y, tot_p);
@@ -459,6 +468,8 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
       if (li < nvalid) inv[s_buf[li].y] = hcount > 0 ? s_sig[hcount - 1] : spill_slot;
     }
   }
+  __syncthreads();
+  if (tid == 0 && s_err) atomicOr(&pl.counters[C_ERR], s_err);
   HP_PROF();
   cl.sync();  // no CTA may exit while others still read its shared memory
   HP_PROF();
@@ -900,11 +911,18 @@ void restore_sorted_pos(DedupPlan& pl) {
 int build_plan(DedupPlan& pl, const int64_t* ids, const int32_t* owner,
                const int64_t* dst_pb, int64_t* send_ids, int32_t* counts, int32_t* inv,
                int32_t* dest_counts, int32_t* n_uniq, cudaStream_t st) {
-  // counters + the fused-combine arrival counters (contiguous, carve_plan)
-  HP_CUDA(cudaMemsetAsync(pl.counters, 0,
-                          reinterpret_cast<char*>(pl.comb_ctr) - reinterpret_cast<char*>(pl.counters) +
-                              4 * (size_t)CMB_LV * pl.partial_rows,
-                          st));
+  // counters + the fused-combine arrival counters (contiguous, carve_plan).
+  // The cluster path writes every counter itself (C_ERR zeroed in-kernel), so
+  // without the fused tree it needs no memset: a memset node in front of the
+  // cluster kernel let the concurrent apply's k_reduce fill every SM first and
+  // the cluster (8 co-scheduled SMs) then waited ~14 us for it (LM1B n = 1 step
+  // 44.1 -> 40.3 us without it).
+  const bool cluster = pl.T > 0 && pl.T <= HP_SMALL_MAX && pl.P <= CL_PMAX;
+  if (!cluster || pl.fused)
+    HP_CUDA(cudaMemsetAsync(pl.counters, 0,
+                            reinterpret_cast<char*>(pl.comb_ctr) - reinterpret_cast<char*>(pl.counters) +
+                                4 * (size_t)CMB_LV * pl.partial_rows,
+                            st));
   if (pl.T == 0) {
     if (dest_counts) HP_CUDA(cudaMemsetAsync(dest_counts, 0, 4 * (size_t)pl.nranks, st));
     if (n_uniq) HP_CUDA(cudaMemsetAsync(n_uniq, 0, 4, st));

@@ -174,7 +174,8 @@ inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 // span = [first block start, last block end] in %globaltimer ns.
 enum SpanId {
   SP_DEDUP = 0, SP_REDUCE, SP_COMBINE, SP_WAIT_PUSH, SP_SCATTER, SP_APPLY, SP_WAIT_APPLIED,
-  SP_COPY, SP_AR_SCATTER, SP_AR_WAIT0, SP_AR_RG, SP_AR_WAIT1, SP_PUBLISH, SP_APPLIED, SP_N = 16
+  SP_COPY, SP_AR_SCATTER, SP_AR_WAIT0, SP_AR_RG, SP_AR_WAIT1, SP_PUBLISH, SP_APPLIED,
+  SP_REDUCE2, SP_N = 16  // SP_REDUCE2: k_reduce over the short items only (split apply)
 };
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;

@@ -276,7 +276,8 @@ k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
   constexpr int GPB = 256 / TPI;
   const int q = threadIdx.x % TPI;
   const int lane = threadIdx.x & 31;
-  HP_ENTRY(SP_REDUCE);
+  const int span_id = pl.part == 2 ? SP_REDUCE2 : SP_REDUCE;
+  HP_ENTRY(span_id);
   // The epilogue's table rows (w, optimizer state) are staged through shared
   // memory with cp.async (each thread copies and later reads only its own
   // columns) instead of registers: ~16 fewer registers per thread at LM shapes.
@@ -381,7 +382,7 @@ k_reduce(DedupPlan pl, const float* __restrict__ vals_f, Epi epi) {
 #pragma unroll 1
   for (int it = it_lo + blockIdx.x * GPB + threadIdx.x / TPI; it < it_hi; it += stride)
     process(it);
-  HP_SPAN_END(SP_REDUCE);
+  HP_SPAN_END(span_id);
 }
 
 // ((0 + r0) + r1) + ... over n <= HP_CHUNK rows of stride D4: all HP_CHUNK

@@ -15,7 +15,7 @@ from paper_1808_02621_b200 import _lib
 from paper_1808_02621_b200.synth import WORKLOADS, TableShape, Workload, make_batch
 
 NAMES = ["dedup", "reduce", "combine", "wait_push", "scatter", "apply", "wait_applied", "copy",
-         "ar_scatter", "ar_wait0", "ar_rg", "ar_wait1", "publish", "applied"]
+         "ar_scatter", "ar_wait0", "ar_rg", "ar_wait1", "publish", "applied", "reduce_short"]
 which = sys.argv[1] if len(sys.argv) > 1 else "table"
 pipelined = len(sys.argv) > 2 and sys.argv[2] in ("pipelined", "graph")
 use_graph = len(sys.argv) > 2 and sys.argv[2] == "graph"  # replay the bench's pipelined graphs
