@@ -127,6 +127,8 @@ void hp_debug_set_fuse_tree(int on);
 /* Plans built after the call: 1 (default) = items long-chunks-first, so the
  * n = 1 apply can run its short items on a side stream; 0 = build order. */
 void hp_debug_set_split_long(int on);
+/* A/B: 1 (default) = the long chunks' reduce (split apply) keeps 8 rows in flight per group. */
+void hp_debug_set_long_b8(int on);
 /* A/B: 1 (default) = chain kernels carry their stream's priority as a launch
  * attribute (graph node priority); 0 = plain launches. */
 void hp_debug_set_launch_prio(int on);

@@ -246,7 +246,11 @@ class HybridRunner:
                                 for n in self.tables}
                                if world_size == 1 and os.environ.get("HP_SPLIT_LONG", "1") == "1"
                                else {})
-        self._plan_streams = {n: torch.cuda.Stream(device=self.device, priority=pp)
+        # two plan streams per table, alternating by step: the dedup of step s+1
+        # may start before the one of step s has finished (each is a latency-
+        # bound cluster sort on a few SMs, about as long as a whole step)
+        self._plan_streams = {n: [torch.cuda.Stream(device=self.device, priority=pp)
+                                  for _ in range(2)]
                               for n in self.tables}
         self._pending_counts: dict = {}
         self._ps_used: set = set()  # plan streams forked since the last join
@@ -760,7 +764,7 @@ class HybridRunner:
             return
         for name, tab in self.tables.items():
             k = tab.applied
-            waited = False
+            waited = []
             for i, b in enumerate(ahead[:self.lookahead]):
                 sn, ids = k + 1 + i, b[name][0]
                 ent = tab.pending.get(sn)
@@ -771,11 +775,11 @@ class HybridRunner:
                     self._plan(tab, ids, slot)
                     tab.pending[sn] = (ids, slot, None)
                     continue
-                ps = self._plan_streams[name]
-                if not waited:
+                ps = self._plan_streams[name][sn % 2]
+                if ps not in waited:
                     ps.wait_stream(stream)
-                    waited = True
-                    self._ps_used.add(name)
+                    waited.append(ps)
+                    self._ps_used.add((name, sn % 2))
                 with torch.cuda.stream(ps):
                     self._plan(tab, ids, slot)
                 e = torch.cuda.Event()
@@ -786,8 +790,8 @@ class HybridRunner:
         """The current stream waits for the plan streams used since the last
         join (end of a capture: only streams forked into it may be joined)."""
         cur = torch.cuda.current_stream()
-        for name in sorted(self._ps_used):
-            cur.wait_stream(self._plan_streams[name])
+        for name, j in sorted(self._ps_used):
+            cur.wait_stream(self._plan_streams[name][j])
         self._ps_used.clear()
 
     @property
