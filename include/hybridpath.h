@@ -127,7 +127,11 @@ void hp_debug_set_fuse_tree(int on);
 /* Plans built after the call: 1 (default) = items long-chunks-first, so the
  * n = 1 apply can run its short items on a side stream; 0 = build order. */
 void hp_debug_set_split_long(int on);
-/* A/B: 1 (default) = the long chunks' reduce (split apply) keeps 8 rows in flight per group. */
+/* A/B: b > 0 = the long chunks' reduce (split apply) keeps 8 rows in flight per
+ * group, b blocks per SM at most; 0 (default) = the generic k_reduce. Measured:
+ * the kernel alone is faster (K4+K5 34.5 -> 31 us) but the LM1B step slower
+ * (38 -> 50 us): the long chain then reaches its TMA broadcast while the short
+ * items and the next plan's cluster sort still hold the SMs. */
 void hp_debug_set_long_b8(int on);
 /* A/B: 1 (default) = chain kernels carry their stream's priority as a launch
  * attribute (graph node priority); 0 = plain launches. */

@@ -694,20 +694,23 @@ void launch_k_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cud
     launch_k_reduce_b<TPI, VPT, B>(pl, vals, epi, st, blocks);
 }
 
-// The long segments' chunks alone (pl.part == 1): every item is a full
-// 16-row chunk, so each group keeps 8 rows in flight (2 round trips per chunk
-// instead of 8) on one float4 column per thread; few items, so occupancy is
-// not the limit here. Long chunks only write partial rows, so no epilogue is
+// The long segments' chunks alone (pl.part == 1, hp_debug_set_long_b8 > 0;
+// A/B, off by default: faster alone, slower in the step, see the header):
+// every item is a full 16-row chunk, so each group keeps 8 rows in flight (2
+// round trips per chunk instead of 8) on one float4 column per thread. Long chunks only write partial rows, so no epilogue is
 // compiled in (EpiSend, never called): one instantiation per width, spill-free.
 inline void launch_k_reduce_long(const DedupPlan& pl, const float* vals, cudaStream_t st) {
   const int D4 = pl.D >> 2;
   const EpiSend epi{nullptr, D4};
+  // the chunk count is on the device: at most one block per SM (g_long_b8
+  // blocks per SM when > 1), grid-striding over the chunks
   const int64_t items = 2 * pl.T / HP_CHUNK + 2;
-  if (D4 <= 32) launch_k_reduce_b<32, 1, 8>(pl, vals, epi, st, grid_for(items, 8, sm_count() * 16));
-  else if (D4 <= 64) launch_k_reduce_b<64, 1, 8>(pl, vals, epi, st, grid_for(items, 4, sm_count() * 16));
-  else if (D4 <= 128) launch_k_reduce_b<128, 1, 8>(pl, vals, epi, st, grid_for(items, 2, sm_count() * 16));
-  else if (D4 <= 256) launch_k_reduce_b<256, 1, 8>(pl, vals, epi, st, grid_for(items, 1, sm_count() * 16));
-  else launch_k_reduce_b<256, 2, 4>(pl, vals, epi, st, grid_for(items, 1, sm_count() * 16));
+  const int cap = sm_count() * std::max(1, g_long_b8);
+  if (D4 <= 32) launch_k_reduce_b<32, 1, 8>(pl, vals, epi, st, grid_for(items, 8, cap));
+  else if (D4 <= 64) launch_k_reduce_b<64, 1, 8>(pl, vals, epi, st, grid_for(items, 4, cap));
+  else if (D4 <= 128) launch_k_reduce_b<128, 1, 8>(pl, vals, epi, st, grid_for(items, 2, cap));
+  else if (D4 <= 256) launch_k_reduce_b<256, 1, 8>(pl, vals, epi, st, grid_for(items, 1, cap));
+  else launch_k_reduce_b<256, 2, 4>(pl, vals, epi, st, grid_for(items, 1, cap));
 }
 
 template <class Epi>

@@ -22,6 +22,9 @@ use_graph = len(sys.argv) > 2 and sys.argv[2] == "graph"  # replay the bench's p
 if which == "table":
     wl = Workload("t", [TableShape("softmax", 800_000, 512, 2560, sampled=8192)], {},
                   {"kind": "adagrad", "lr": 0.2, "init_acc": 0.1}, 2560)
+elif which == "table_emb":
+    wl = Workload("t", [TableShape("embedding", 800_000, 512, 2560)], {},
+                  {"kind": "adagrad", "lr": 0.2, "init_acc": 0.1}, 2560)
 elif which == "dense":
     wl = Workload("d", [], {"lstm": 9_400_000}, {"kind": "adagrad", "lr": 0.2}, 2560)
 else:
