@@ -197,11 +197,12 @@ def test_local_apply_and_gather(cuda, level0, opt):
 
 
 @pytest.mark.parametrize("opt", ["adagrad", "adam"])
-@pytest.mark.parametrize("mode", ["side", "one_stream", "build_order"])
+@pytest.mark.parametrize("mode", ["side", "side_b8", "one_stream", "build_order"])
 def test_apply_plan_pull_split_bit_exact(cuda, opt, mode):
     """K4 + K5 fused (hp_apply_plan_pull) at the LM1B softmax shape: the short
-    segments on a side stream beside the long chain (default), on one stream,
-    and with plans in build order (hp_debug_set_split_long(0)) == oracle."""
+    segments on a side stream beside the long chain (default; also with the
+    8-rows-in-flight long-chunk reduce), on one stream, and with plans in build
+    order (hp_debug_set_split_long(0)) == oracle."""
     from paper_1808_02621_b200 import _lib, ops
     from paper_1808_02621_b200.synth import log_uniform_ids, zipf_ids
 
@@ -210,8 +211,9 @@ def test_apply_plan_pull_split_bit_exact(cuda, opt, mode):
     owner = np.zeros(P, dtype=np.int32)
     tab, state = _slab_for(V, D, P, owner, 0, opt, seed=5, dev=cuda)
     hpar = {"lr": 0.1, "beta1": 0.9, "beta2": 0.999, "eps": 1e-8}
-    side = torch.cuda.Stream(device=cuda) if mode == "side" else None
+    side = torch.cuda.Stream(device=cuda) if mode.startswith("side") else None
     _lib.load().hp_debug_set_split_long(0 if mode == "build_order" else 1)
+    _lib.load().hp_debug_set_long_b8(1 if mode == "side_b8" else 0)
     try:
         for step in (1, 2):
             ids = np.concatenate([zipf_ids(rng, V, T), log_uniform_ids(rng, V, 8192)])
@@ -228,6 +230,7 @@ def test_apply_plan_pull_split_bit_exact(cuda, opt, mode):
         assert np.array_equal(tab.w.cpu().numpy(), state["w"])
     finally:
         _lib.load().hp_debug_set_split_long(1)
+        _lib.load().hp_debug_set_long_b8(0)
 
 
 def test_init_rows_bit_exact(cuda):
