@@ -570,14 +570,33 @@ def main():
               for x in (v if isinstance(v, tuple) else (v,)))
     d2h = res_host.numel() * 4
 
+    # the step's host->device copies spread over HP_E2E_STREAMS copy streams
+    # (largest tensors first, round robin), joined before the step
+    n_cs = int(os.environ.get("HP_E2E_STREAMS", "1"))
+    cstreams = [torch.cuda.Stream(device=dev) for _ in range(n_cs)] if n_cs > 1 else []
+
     def e2e_step(i):
         src = pinned[i % R]
+        pairs = []
         for k, v in src.items():
             if isinstance(v, tuple):
-                static[k][0].copy_(v[0], non_blocking=True)
-                static[k][1].copy_(v[1], non_blocking=True)
+                pairs += [(static[k][0], v[0]), (static[k][1], v[1])]
             else:
-                static[k].copy_(v, non_blocking=True)
+                pairs.append((static[k], v))
+        if cstreams:
+            cur = torch.cuda.current_stream()
+            pairs.sort(key=lambda p: -p[1].numel() * p[1].element_size())
+            for j, (d, s) in enumerate(pairs):
+                cs = cstreams[j % n_cs]
+                if j < n_cs:
+                    cs.wait_stream(cur)
+                with torch.cuda.stream(cs):
+                    d.copy_(s, non_blocking=True)
+            for cs in cstreams[:len(pairs)]:
+                cur.wait_stream(cs)
+        else:
+            for d, s in pairs:
+                d.copy_(s, non_blocking=True)
         if e2e_graph:
             e2e_graph.replay()
         else:
