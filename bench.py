@@ -554,6 +554,9 @@ def main():
                 "timing": "graph replay of the exchange alone (all ranks released together, "
                           "max over ranks, median of 10)" if us_graph is not None else "eager",
                 "peak_src": "fallback: measured peer copy 770 GB/s per direction (B200_PROFILING.md)",
+                # every rank storing to its peer at once (tools/nvlink_bidir.py, N = 2,
+                # profiles/r2_n2_k7_studies.txt): the rate both link directions sustain
+                "frac_of_bidir_measured": achieved / 680.0,
                 "step_share": us / (t_dev / args.steps * 1e6)}
 
     _mark("kernel timing / roofline done")
