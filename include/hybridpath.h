@@ -275,6 +275,13 @@ int hp_fill(float* x, int64_t n, float value, void* stream);
 typedef struct hp_comm_s* hp_comm_t;
 int hp_dense_allreduce_scale_cast(hp_comm_t comm, float* in, void* out, int64_t count,
                                   int32_t out_dtype, float scale, void* stream);
+/* Same with the input dtype explicit (SURVEY §8b's in_dtype): HP_DTYPE_F32
+ * (then == the call above, in place in `in` for a non-fp32 out) or
+ * HP_DTYPE_BF16: widened exactly into `scratch` (fp32 [count], 16-byte
+ * aligned; may be NULL when nranks == 1), reduced there, scaled, cast to out. */
+int hp_dense_allreduce_scale_cast_ex(hp_comm_t comm, const void* in, int32_t in_dtype, void* out,
+                                     int64_t count, int32_t out_dtype, float scale, float* scratch,
+                                     void* stream);
 
 /* ---------------------------------------------------------------- other mechanisms
  * (SURVEY §8f baselines: the same Weights under transform_ar / transform_ps.)
@@ -405,10 +412,17 @@ int hp_dar_create(hp_dar_t* out, int32_t n, int32_t me, int64_t S, int32_t out_d
                   void* ipc_handle_out, void** out_ptr);
 int hp_dar_open_peer(hp_dar_t d, int32_t rank, const void* ipc_handle);
 int hp_dar_destroy(hp_dar_t d);
-int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream);
-/* Transport of the two NVLink phases: HP_DAR_CE (default) = cudaMemcpyAsync
- * peer copies on the copy engines (no SMs; overlaps the sparse kernels),
- * HP_DAR_SM = peer stores from SM kernels. Same result bit for bit. */
+/* grad: [S] of the window's input dtype (fp32 unless hp_dar_set_in_dtype). */
+int hp_dar_allreduce(hp_dar_t d, const void* grad, float scale, void* stream);
+/* Input dtype of the gradients: HP_DTYPE_F32 (default) or HP_DTYPE_BF16 (SM
+ * mode only: bf16 travels over NVLink, half the bytes; every contribution is
+ * widened exactly to fp32 and summed in source-rank order, then scaled and
+ * cast to the output dtype). */
+int hp_dar_set_in_dtype(hp_dar_t d, int32_t in_dtype);
+/* Transport of the two NVLink phases: HP_DAR_SM = peer stores from SM kernels
+ * (the runner's default), HP_DAR_CE = cudaMemcpyAsync peer copies on the copy
+ * engines (the window's initial mode), pipelined, one-shot pull. Same result
+ * bit for bit. */
 #define HP_DAR_SM 0
 #define HP_DAR_CE 1
 #define HP_DAR_PIPE 2 /* one persistent kernel; scatter and reduce-gather pipelined by 64 KB pieces */

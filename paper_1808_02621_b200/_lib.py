@@ -70,6 +70,7 @@ SIGNATURES = {
     "hp_allgather": (C.c_int, [vp, vp, vp, i64, vp]),
     "hp_dense_reduce_bcast": (C.c_int, [vp, vp, vp, i64, i32, f32, i32, vp]),
     "hp_dense_allreduce_scale_cast": (C.c_int, [vp, vp, vp, i64, i32, f32, vp]),
+    "hp_dense_allreduce_scale_cast_ex": (C.c_int, [vp, vp, i32, vp, i64, i32, f32, vp, vp]),
     "hp_nccl_unique_id_bytes": (C.c_int, []),
     "hp_nccl_get_unique_id": (C.c_int, [vp]),
     "hp_comm_init": (C.c_int, [C.POINTER(vp), i32, i32, vp]),
@@ -95,6 +96,7 @@ SIGNATURES = {
     "hp_dar_open_peer": (C.c_int, [vp, i32, vp]),
     "hp_dar_destroy": (C.c_int, [vp]),
     "hp_dar_set_mode": (C.c_int, [vp, i32]),
+    "hp_dar_set_in_dtype": (C.c_int, [vp, i32]),
     "hp_dar_set_split": (C.c_int, [vp, vp]),
     "hp_nvls_allreduce": (C.c_int, [vp, vp, i64, i32, i32, i32, f32, vp, vp, vp]),
     "hp_dar_allreduce": (C.c_int, [vp, vp, f32, vp]),

@@ -20,6 +20,8 @@ namespace hp {
 
 int scale_cast(const float* in, void* out, int64_t count, int32_t out_dtype, float scale,
                cudaStream_t st);
+int scale_cast_bf16(const void* in, void* out, int64_t count, int32_t out_dtype, float scale,
+                    cudaStream_t st);
 
 static int nccl_fail(ncclResult_t r, const char* what) {
   set_error(std::string(what) + ": " + ncclGetErrorString(r));
@@ -148,6 +150,23 @@ int hp_dense_allreduce_scale_cast(hp_comm_t comm, float* in, void* out, int64_t 
     HP_NCCL(ncclAllReduce(in, in, count, ncclFloat32, ncclSum, comm->comm, st));
   }
   return scale_cast(in, out, count, out_dtype, scale, st);
+}
+
+// in_dtype explicit. bf16 input: one rank -> scale + cast in one
+// kernel; several -> exact widening into scratch, then the fp32 path above.
+int hp_dense_allreduce_scale_cast_ex(hp_comm_t comm, const void* in, int32_t in_dtype, void* out,
+                                     int64_t count, int32_t out_dtype, float scale, float* scratch,
+                                     void* stream) {
+  HP_REQUIRE(in_dtype == HP_DTYPE_F32 || in_dtype == HP_DTYPE_BF16, "in dtype f32 | bf16");
+  if (in_dtype == HP_DTYPE_F32)
+    return hp_dense_allreduce_scale_cast(comm, static_cast<float*>(const_cast<void*>(in)), out,
+                                         count, out_dtype, scale, stream);
+  HP_REQUIRE(count >= 0 && (count == 0 || (in && out)), "bad dense arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!(comm && comm->nranks > 1)) return scale_cast_bf16(in, out, count, out_dtype, scale, st);
+  HP_REQUIRE(scratch != nullptr, "bf16 input over NCCL needs an fp32 scratch of count elements");
+  if (int rc = scale_cast_bf16(in, scratch, count, HP_DTYPE_F32, 1.0f, st)) return rc;
+  return hp_dense_allreduce_scale_cast(comm, scratch, out, count, out_dtype, scale, stream);
 }
 
 // AR for a sparse Weight (reference AllGatherv, `simulate.py:138-180`): every

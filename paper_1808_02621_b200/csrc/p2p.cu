@@ -1150,6 +1150,7 @@ constexpr int AR_MAXN = 32;
 struct ArLayout {
   int64_t S, S_real, chunk, slots_off, out_off;  // S = S_real padded to a multiple of 4n
   int n, me, out_bytes;
+  int in_bytes;  // 4 = fp32 gradients, 2 = bf16 (SM mode; slots then hold bf16, half the NVLink bytes)
   // chunk of rank r = float4 range [off4[r], off4[r+1]) (uniform S/n unless
   // hp_dar_set_split weighted it); source s's slot at every rank starts at s * sstride4
   int64_t sstride4;
@@ -1162,25 +1163,53 @@ __host__ __device__ __forceinline__ int64_t ar_piece(int64_t c4, int bk, int nb)
   return c4 * bk / nb;
 }
 
+// Four gradient elements as one vector: float4 (fp32) or uint2 (4 x bf16).
+template <typename InT> struct Vec4;
+template <> struct Vec4<float> {
+  using T = float4;
+  static __device__ __forceinline__ T zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+  static __device__ __forceinline__ float4 f32(T v) { return v; }
+  static __device__ __forceinline__ T ld(const T* p) { return ldg_stream(p); }
+};
+template <> struct Vec4<__nv_bfloat16> {
+  using T = uint2;
+  static __device__ __forceinline__ T zero() { return make_uint2(0u, 0u); }
+  static __device__ __forceinline__ float4 f32(T v) {  // exact widening
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
+    return make_float4(a.x, a.y, b.x, b.y);
+  }
+  static __device__ __forceinline__ T ld(const T* p) {
+    T v;
+    asm volatile("ld.global.cs.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+  }
+};
+
 // blockIdx.y = destination peer (my own chunk is not copied: the reduce reads
-// my contribution straight from grad); 4 float4 in flight per thread.
+// my contribution straight from grad); 4 vectors in flight per thread. bf16
+// gradients travel as bf16 (slot s of a rank holds them at the same byte
+// offset as fp32 would, half of it used).
+template <typename InT>
 __global__ void __launch_bounds__(256)
-k_ar_scatter(PeerTable peers, ArLayout A, const float4* __restrict__ grad, int bk, int nb) {
+k_ar_scatter(PeerTable peers, ArLayout A, const void* __restrict__ grad_v, int bk, int nb) {
+  using V = Vec4<InT>;
+  using VT = typename V::T;
   HP_ENTRY(SP_AR_SCATTER);
   const int c = (int)blockIdx.y < A.me ? (int)blockIdx.y : (int)blockIdx.y + 1;
   const int64_t b4 = A.off4[c], c4 = A.off4[c + 1] - b4, real4 = A.S_real >> 2;
   const int64_t p0 = ar_piece(c4, bk, nb), p1 = ar_piece(c4, bk + 1, nb);
-  const float4* src = grad + b4;
-  float4* dst = reinterpret_cast<float4*>(static_cast<char*>(peers.base[c]) + A.slots_off) +
-                (int64_t)A.me * A.sstride4;
+  const VT* src = static_cast<const VT*>(grad_v) + b4;
+  VT* dst = reinterpret_cast<VT*>(static_cast<char*>(peers.base[c]) + A.slots_off +
+                                  (int64_t)A.me * A.sstride4 * 16);
   const int64_t lim = min(p1, max((int64_t)0, real4 - b4));  // real elements here
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t j0 = p0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < p1; j0 += 4 * stride) {
-    float4 v[4];
+    VT v[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int64_t j = j0 + u * stride;
-      v[u] = j < lim ? ldg_stream(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[u] = j < lim ? V::ld(src + j) : V::zero();
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -1208,17 +1237,18 @@ __device__ __forceinline__ void put4<__nv_bfloat16>(void* base, int64_t i4, floa
   reinterpret_cast<uint2*>(base)[i4] = u;
 }
 
-template <typename OutT>
+template <typename OutT, typename InT>
 __global__ void __launch_bounds__(256)
-k_ar_reduce_gather(PeerTable peers, void* my_win, ArLayout A, const float4* __restrict__ grad,
+k_ar_reduce_gather(PeerTable peers, void* my_win, ArLayout A, const void* __restrict__ grad_v,
                    float scale, int bk, int nb) {
+  using V = Vec4<InT>;
+  using VT = typename V::T;
   HP_ENTRY(SP_AR_RG);
   const int64_t b4 = A.off4[A.me], c4 = A.off4[A.me + 1] - b4;
   const int64_t p0 = ar_piece(c4, bk, nb), p1 = ar_piece(c4, bk + 1, nb);
   const int64_t own_lim = min(p1, max((int64_t)0, (A.S_real >> 2) - b4));
-  const float4* slots =
-      reinterpret_cast<const float4*>(static_cast<char*>(my_win) + A.slots_off);
-  const float4* mine = grad + b4;
+  const char* slots = static_cast<const char*>(my_win) + A.slots_off;
+  const VT* mine = static_cast<const VT*>(grad_v) + b4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t j0 = p0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < p1; j0 += 2 * stride) {
     float4 acc[2];
@@ -1227,10 +1257,10 @@ k_ar_reduce_gather(PeerTable peers, void* my_win, ArLayout A, const float4* __re
       const int64_t j = j0 + u * stride;
       acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (j < p1)
-        for (int s = 0; s < A.n; ++s) {  // source-rank order; my own from grad
-          const float4 x = s == A.me ? (j < own_lim ? ldg_stream(mine + j)
-                                                    : make_float4(0.f, 0.f, 0.f, 0.f))
-                                     : ldg_stream(slots + (int64_t)s * A.sstride4 + j);
+        for (int s = 0; s < A.n; ++s) {  // source-rank order; my own from grad (fp32 sums)
+          const float4 x =
+              s == A.me ? (j < own_lim ? V::f32(V::ld(mine + j)) : make_float4(0.f, 0.f, 0.f, 0.f))
+                        : V::f32(V::ld(reinterpret_cast<const VT*>(slots + (int64_t)s * A.sstride4 * 16) + j));
           acc[u] = f4_add(acc[u], x);
         }
     }
@@ -1560,6 +1590,7 @@ int hp_dar_create(hp_dar_t* out, int32_t n, int32_t me, int64_t S_real, int32_t 
   d->A.me = me;
   d->A.chunk = S / n;
   d->A.out_bytes = out_dtype == HP_DTYPE_F32 ? 4 : 2;
+  d->A.in_bytes = 4;
   // slots sized for any split (a chunk may be all of S): n sources x S
   d->A.sstride4 = S / 4;
   for (int r = 0; r <= n; ++r) d->A.off4[r] = (int64_t)r * (S / n) / 4;
@@ -1703,8 +1734,11 @@ static int dar_copies(hp_dar_t d, cudaStream_t st, bool gather, const float* gra
   return HP_OK;
 }
 
-int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream) {
-  HP_REQUIRE(d && grad && ((uintptr_t)grad & 15) == 0, "grad must be a 16-byte aligned buffer");
+int hp_dar_allreduce(hp_dar_t d, const void* grad_v, float scale, void* stream) {
+  HP_REQUIRE(d && grad_v && ((uintptr_t)grad_v & 15) == 0, "grad must be a 16-byte aligned buffer");
+  HP_REQUIRE(d->A.in_bytes == 4 || d->mode == HP_DAR_SM,
+             "bf16 gradients need the SM-store dense exchange (HP_DAR_SM)");
+  const float* grad = static_cast<const float*>(grad_v);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int sms = sm_count();
   int64_t maxc = 0, myc = (d->A.off4[d->A.me + 1] - d->A.off4[d->A.me]) * 4;
@@ -1779,25 +1813,42 @@ int hp_dar_allreduce(hp_dar_t d, const float* grad, float scale, void* stream) {
                                                          sms / std::max(1, np)));
   const int brg = g_dar_rg_blocks > 0 ? g_dar_rg_blocks
                                       : grid_for(std::max<int64_t>(myc / nb, 8) / 8, 256, sms * 2);
-  const float4* g4 = reinterpret_cast<const float4*>(grad);
+  const void* g = grad;
+  const bool bf_in = d->A.in_bytes == 2;
   for (int b = 0; b < nb; ++b) {
-    if (np > 0)
-      launch_k(k_ar_scatter, dim3(bx, np), dim3(256), 0, st, d->peers, d->A, g4, b, nb);
+    if (np > 0) {
+      if (bf_in)
+        launch_k(k_ar_scatter<__nv_bfloat16>, dim3(bx, np), dim3(256), 0, st, d->peers, d->A, g, b, nb);
+      else
+        launch_k(k_ar_scatter<float>, dim3(bx, np), dim3(256), 0, st, d->peers, d->A, g, b, nb);
+    }
     launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 0, 0);
   }
   for (int b = 0; b < nb; ++b) {
     const int lag = nb - 1 - b;
     launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 0, d->A.n, wait_budget(), SP_AR_WAIT0, lag);
-    if (d->A.out_bytes == 4)
-      launch_k(k_ar_reduce_gather<float>, dim3(brg), dim3(256), 0, st, d->peers, d->win, d->A, g4,
+    const dim3 G(brg), Bk(256);
+    if (d->A.out_bytes == 4 && !bf_in)
+      launch_k(k_ar_reduce_gather<float, float>, G, Bk, 0, st, d->peers, d->win, d->A, g, scale, b, nb);
+    else if (d->A.out_bytes == 4)
+      launch_k(k_ar_reduce_gather<float, __nv_bfloat16>, G, Bk, 0, st, d->peers, d->win, d->A, g,
+               scale, b, nb);
+    else if (!bf_in)
+      launch_k(k_ar_reduce_gather<__nv_bfloat16, float>, G, Bk, 0, st, d->peers, d->win, d->A, g,
                scale, b, nb);
     else
-      launch_k(k_ar_reduce_gather<__nv_bfloat16>, dim3(brg), dim3(256), 0, st, d->peers, d->win,
-               d->A, g4, scale, b, nb);
+      launch_k(k_ar_reduce_gather<__nv_bfloat16, __nv_bfloat16>, G, Bk, 0, st, d->peers, d->win,
+               d->A, g, scale, b, nb);
     launch_k(k_signal, dim3(1), dim3(32), 0, st, d->win, d->peers, d->A.n, d->A.me, 1, lag);
   }
   launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 1, d->A.n, wait_budget(), SP_AR_WAIT1, 0);
   HP_LAUNCHED(nb * ((np > 0 ? 1 : 0) + 4) + 1, "dense p2p allreduce");
+  return HP_OK;
+}
+
+int hp_dar_set_in_dtype(hp_dar_t d, int32_t in_dtype) {
+  HP_REQUIRE(d && (in_dtype == HP_DTYPE_F32 || in_dtype == HP_DTYPE_BF16), "in dtype f32 | bf16");
+  d->A.in_bytes = in_dtype == HP_DTYPE_F32 ? 4 : 2;
   return HP_OK;
 }
 

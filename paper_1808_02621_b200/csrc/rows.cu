@@ -275,10 +275,60 @@ k_scale_cast(const float* __restrict__ in, OutT* __restrict__ out, int64_t n, fl
   }
 }
 
+// bf16 -> OutT with scale: each element widened exactly to fp32, then x scale
+// (scale 1 and fp32 out: the exact widening alone).
+template <typename OutT>
+__global__ void __launch_bounds__(256)
+k_scale_cast_bf16(const __nv_bfloat16* __restrict__ in, OutT* __restrict__ out, int64_t n,
+                  float scale) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n4 = n >> 2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const uint2 u = reinterpret_cast<const uint2*>(in)[i];
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    float4 v = make_float4(__fmul_rn(a.x, scale), __fmul_rn(a.y, scale), __fmul_rn(b.x, scale),
+                           __fmul_rn(b.y, scale));
+    store4<OutT>(out, i, v);
+  }
+  for (int64_t i = (n4 << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float v = __fmul_rn(__bfloat162float(in[i]), scale);
+    if constexpr (sizeof(OutT) == 4) out[i] = v;
+    else if constexpr (std::is_same<OutT, __nv_bfloat16>::value) out[i] = __float2bfloat16_rn(v);
+    else out[i] = __float2half_rn(v);
+  }
+}
+
 }  // namespace
 
 HP_SPAN_SETTER(set_spans_rows)
 int g_bcast_tma = 1;  // hp_debug_set_bcast_tma
+
+int scale_cast_bf16(const void* in, void* out, int64_t count, int32_t out_dtype, float scale,
+                    cudaStream_t st) {
+  if (count <= 0) return HP_OK;
+  HP_REQUIRE(((uintptr_t)in & 15) == 0 && ((uintptr_t)out & 15) == 0,
+             "dense buffers must be 16-byte aligned");
+  const int g = grid_for((count >> 2) + 1, 256, sm_count() * 8);
+  const auto* x = static_cast<const __nv_bfloat16*>(in);
+  switch (out_dtype) {
+    case HP_DTYPE_F32:
+      k_scale_cast_bf16<float><<<g, 256, 0, st>>>(x, static_cast<float*>(out), count, scale);
+      break;
+    case HP_DTYPE_BF16:
+      k_scale_cast_bf16<__nv_bfloat16><<<g, 256, 0, st>>>(x, static_cast<__nv_bfloat16*>(out),
+                                                          count, scale);
+      break;
+    case HP_DTYPE_F16:
+      k_scale_cast_bf16<__half><<<g, 256, 0, st>>>(x, static_cast<__half*>(out), count, scale);
+      break;
+    default:
+      set_error("unknown out_dtype");
+      return HP_EINVAL;
+  }
+  HP_LAUNCHED(1, "k_scale_cast_bf16");
+  return HP_OK;
+}
 
 int scale_cast(const float* in, void* out, int64_t count, int32_t out_dtype, float scale,
                cudaStream_t st) {

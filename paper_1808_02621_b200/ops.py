@@ -355,16 +355,28 @@ def fill(x: torch.Tensor, value: float, stream=None) -> None:
 
 
 def dense_allreduce_scale_cast(comm, grad: torch.Tensor, out: torch.Tensor, scale: float,
-                               stream=None) -> torch.Tensor:
-    """K7: out = cast(scale * sum over ranks of grad); grad is reduced in place."""
-    _need(grad, torch.float32, "grad")
+                               stream=None, scratch: torch.Tensor | None = None) -> torch.Tensor:
+    """K7: out = cast(scale * sum over ranks of grad). fp32 grad: reduced in
+    place; bf16 grad (``hp_dense_allreduce_scale_cast_ex``): widened exactly to
+    fp32 (into ``scratch``, fp32 of grad's size, when there is more than one rank)."""
+    if grad.dtype not in (torch.float32, torch.bfloat16):
+        raise TypeError("grad must be float32 or bfloat16")
+    _need(grad, grad.dtype, "grad")
     if out.dtype not in (torch.float32, torch.bfloat16, torch.float16) or not out.is_contiguous():
         raise TypeError("out must be a contiguous float32/bfloat16/float16 tensor")
     if out.numel() != grad.numel():
         raise ValueError("grad and out sizes differ")
     code = _lib.HP_DTYPE[str(out.dtype).split(".")[1]]
-    call("hp_dense_allreduce_scale_cast", comm, _p(grad), _p(out), grad.numel(), code, scale,
-         _stream(stream))
+    if grad.dtype == torch.float32:
+        call("hp_dense_allreduce_scale_cast", comm, _p(grad), _p(out), grad.numel(), code, scale,
+             _stream(stream))
+        return out
+    if scratch is not None:
+        _need(scratch, torch.float32, "scratch")
+        if scratch.numel() < grad.numel():
+            raise ValueError("scratch must hold grad.numel() fp32 elements")
+    call("hp_dense_allreduce_scale_cast_ex", comm, _p(grad), _lib.HP_DTYPE["bfloat16"], _p(out),
+         grad.numel(), code, scale, None if scratch is None else _p(scratch), _stream(stream))
     return out
 
 

@@ -126,7 +126,8 @@ class HybridRunner:
                  optimizer: OptimizerConfig | None = None, aggregation: str = "mean",
                  dense_dtype: torch.dtype = torch.float32, device=None, seed: int = 0,
                  exchange: str = "p2p", max_ids: dict | None = None,
-                 dense_exchange: str | None = None, dense_split="auto"):
+                 dense_exchange: str | None = None, dense_split="auto",
+                 dense_in_dtype: torch.dtype = torch.float32):
         if aggregation not in ("mean", "sum"):
             raise ValueError("aggregation must be 'mean' or 'sum'")
         if cluster.total_gpus != world_size:
@@ -168,6 +169,15 @@ class HybridRunner:
         self.aggregation = aggregation
         self.scale = 1.0 / world_size if aggregation == "mean" else 1.0
         self.dense_dtype = dense_dtype
+        # dense gradients arrive in fp32 or bf16 (SURVEY §8b in_dtype): bf16 is
+        # widened exactly and summed in fp32; over peer memory it travels as
+        # bf16 (SM stores: half the NVLink bytes)
+        if dense_in_dtype not in (torch.float32, torch.bfloat16):
+            raise ValueError("dense_in_dtype must be torch.float32 or torch.bfloat16")
+        if dense_in_dtype == torch.bfloat16 and world_size > 1 and self.dense_exchange not in (
+                "p2p-sm", "nccl"):
+            raise ValueError("bf16 dense gradients run over dense_exchange 'p2p-sm' or 'nccl'")
+        self.dense_in_dtype = dense_in_dtype
         self.device = torch.device(device if device is not None else torch.cuda.current_device())
         self.seed = seed
         self.tables: dict[str, ShardedTable] = {}
@@ -177,6 +187,8 @@ class HybridRunner:
             if var.kind == "dense":
                 self.dense.append(var)
                 if mech is Mechanism.PS and world_size > 1:  # reduce at the owner + broadcast
+                    if dense_in_dtype != torch.float32:
+                        raise ValueError("a dense Weight under PS takes fp32 gradients")
                     self.dense_ps[var.name] = plan.owner_of(var.name, 0)
                 elif self.dense_exchange == "nvls":
                     from .xchg import NvlsExchange
@@ -190,7 +202,7 @@ class HybridRunner:
                         world_size, rank, var.elements, dense_dtype, self.device,
                         mode={"p2p": "ce", "p2p-sm": "sm", "p2p-pipe": "pipe",
                               "p2p-pull": "pull"}[self.dense_exchange],
-                        world=self._world)
+                        world=self._world, in_dtype=dense_in_dtype)
                     w = self._dense_split_weights(dense_split)
                     if w is not None:
                         self.dar[var.name].set_split(w)
@@ -634,6 +646,7 @@ class HybridRunner:
         """K7 does no work at all: one replica, fp32 output, scale 1 ('mean' over
         one rank): the averaged gradient IS this step's gradient."""
         return (self.world_size == 1 and self.dense_dtype == torch.float32
+                and self.dense_in_dtype == torch.float32
                 and np.float32(self.scale) == np.float32(1.0))
 
     def _dense(self, batch: dict) -> None:
@@ -652,7 +665,7 @@ class HybridRunner:
         and ``dense_out[name]`` is this step's gradient itself."""
         for var in self.dense:
             g = batch[var.name]
-            ops._need(g, torch.float32, f"dense gradient {var.name!r}")
+            ops._need(g, self.dense_in_dtype, f"dense gradient {var.name!r}")
             if g.numel() != var.elements:
                 raise SpecError(f"dense Weight {var.name!r}: gradient has {g.numel()} elements, "
                                 f"the graph declares {var.elements}")
@@ -670,6 +683,13 @@ class HybridRunner:
                     src.copy_(g)
                 self.dense_out[var.name] = ops.dense_reduce_bcast(
                     self.comm.ptr, src, out, self.scale, self.dense_ps[var.name])
+            elif self.dense_in_dtype != torch.float32:  # bf16 in: widened into fp32 scratch
+                out = self._dense_buf(var, "out", (g.numel(),), self.dense_dtype).view(g.shape)
+                comm = self.comm.ptr if self.comm is not None else None
+                red = (self._dense_buf(var, "red", (g.numel(),), torch.float32)
+                       if self.world_size > 1 else None)
+                ops.dense_allreduce_scale_cast(comm, g, out, self.scale, scratch=red)
+                self.dense_out[var.name] = out
             else:
                 out = self._dense_buf(var, "out", (g.numel(),), self.dense_dtype).view(g.shape)
                 comm = self.comm.ptr if self.comm is not None else None
@@ -824,7 +844,8 @@ class HybridRunner:
             if self.dense_is_noop() or var.name in self.dar:
                 continue
             self._dense_buf(var, "out", (var.elements,), self.dense_dtype)
-            if self.dense_dtype != torch.float32 and (n > 1 or var.name in self.dense_ps):
+            if (self.dense_dtype != torch.float32 or self.dense_in_dtype != torch.float32) and (
+                    n > 1 or var.name in self.dense_ps):
                 self._dense_buf(var, "red", (var.elements,), torch.float32)
         torch.cuda.synchronize(self.device)
 

@@ -172,7 +172,7 @@ class DenseExchange:
     KIND = "dar"
 
     def __init__(self, n: int, rank: int, numel: int, out_dtype, device, group=None,
-                 mode: str = "ce", world=None):
+                 mode: str = "ce", world=None, in_dtype=torch.float32):
         from ._lib import HP_DTYPE
 
         if numel % 4:
@@ -187,6 +187,12 @@ class DenseExchange:
              C.byref(optr))
         _connect(self, "hp_dar", ipc, group, world)
         call("hp_dar_set_mode", self.handle, self.MODES[mode])
+        if in_dtype not in (torch.float32, torch.bfloat16):
+            raise TypeError("dense exchange input: float32 | bfloat16")
+        if in_dtype == torch.bfloat16 and mode != "sm":
+            raise ValueError("bf16 dense gradients need the SM-store exchange (mode 'sm')")
+        self.in_dtype = in_dtype
+        call("hp_dar_set_in_dtype", self.handle, HP_DTYPE[str(in_dtype).split(".")[1]])
         typestr = "<f4" if code == 0 else "<u2"
         t = torch.as_tensor(_DevPtr(optr.value, (numel,), typestr), device=device)
         self.out = t if code == 0 else t.view(torch.bfloat16)
@@ -207,7 +213,7 @@ class DenseExchange:
     def allreduce(self, grad, scale: float) -> torch.Tensor:
         from .ops import _need
 
-        _need(grad, torch.float32, "grad")
+        _need(grad, self.in_dtype, "grad")
         if grad.numel() != self.numel:
             raise ValueError(f"grad has {grad.numel()} elements, the exchange was built for "
                              f"{self.numel}")

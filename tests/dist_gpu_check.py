@@ -67,10 +67,13 @@ def main():
         plan = hp.transform_ps(graph, cluster, local_agg=True, partitions=parts)
     else:
         plan = hp.transform_hybrid(graph, cluster, partitions=parts)
+    # HP_CHECK_DENSE_IN=bf16: the dense gradients arrive in bf16 (in_dtype)
+    dense_in = torch.bfloat16 if os.environ.get("HP_CHECK_DENSE_IN") == "bf16" else torch.float32
     runner = hp.HybridRunner(plan, graph, cluster, rank=rank, world_size=world, comm=comm,
                              optimizer=hp.OptimizerConfig(kind=opt_kind, lr=0.1), device=dev,
                              seed=5, exchange=xmode, dense_exchange=None if dmode == "default" else dmode,
-                             dense_split=_split(os.environ.get("HP_CHECK_SPLIT", "auto"), world))
+                             dense_split=_split(os.environ.get("HP_CHECK_SPLIT", "auto"), world),
+                             dense_in_dtype=dense_in)
     hpar = {"lr": 0.1, "beta1": 0.9, "beta2": 0.999, "eps": 1e-8}
     empty = os.environ.get("HP_CHECK_EMPTY") == "1"
 
@@ -81,6 +84,8 @@ def main():
         if empty and step == 2 and r == world - 1:
             ids, vals = b["embedding"]
             b["embedding"] = (ids[:0].copy(), vals[:0].copy())
+        if dense_in == torch.bfloat16:  # the oracle sees the bf16 values, widened
+            b["lstm"] = torch.from_numpy(b["lstm"]).to(torch.bfloat16).float().numpy()
         return b
 
     names = [v.name for v in graph.variables]
@@ -106,7 +111,8 @@ def main():
                                                    plan.owner_table(name))
     def to_dev(b):
         return {k: ((torch.from_numpy(v[0]).to(dev), torch.from_numpy(v[1]).to(dev))
-                    if isinstance(v, tuple) else torch.from_numpy(v).to(dev)) for k, v in b.items()}
+                    if isinstance(v, tuple) else torch.from_numpy(v).to(dense_in).to(dev))
+                for k, v in b.items()}
 
     staged = {s: to_dev(batch_of(s, rank)) for s in (1, 2, 3)}
     if xmode == "p2p":

@@ -52,7 +52,7 @@ class Emu:
     plus the oracle state of every table."""
 
     def __init__(self, cuda, n, tables, dense, opt, dense_exchange, P=8, dense_dtype=torch.float32,
-                 seed=3, concurrent=False):
+                 seed=3, concurrent=False, dense_in_dtype=torch.float32):
         import paper_1808_02621_b200 as hp
         from paper_1808_02621_b200.emulate import LocalWorld
         from paper_1808_02621_b200.synth import Workload
@@ -67,8 +67,10 @@ class Emu:
         optc = hp.OptimizerConfig(kind=opt, lr=HPAR["lr"], init_acc=0.1)
         self.runners = [hp.HybridRunner(self.plan, self.graph, cluster, rank=r, world_size=n,
                                         comm=world.comm(r), optimizer=optc, device=cuda, seed=seed,
-                                        dense_exchange=dense_exchange, dense_dtype=dense_dtype)
+                                        dense_exchange=dense_exchange, dense_dtype=dense_dtype,
+                                        dense_in_dtype=dense_in_dtype)
                         for r in range(n)]
+        self.dense_in_dtype = dense_in_dtype
         if not concurrent:  # one stream per rank (emulate.LocalWorld.serialize)
             for run in self.runners:
                 LocalWorld.serialize(run)
@@ -90,6 +92,12 @@ class Emu:
             host.append(b)
         dev = [{k: ((_t(v[0], self.dev), _t(v[1], self.dev)) if isinstance(v, tuple)
                     else _t(v, self.dev)) for k, v in b.items()} for b in host]
+        if self.dense_in_dtype == torch.bfloat16:  # bf16 gradients; the oracle sees their fp32 value
+            for b, d in zip(host, dev):
+                for name in self.wl.dense:
+                    g16 = torch.from_numpy(b[name]).to(torch.bfloat16)
+                    b[name] = g16.float().numpy()
+                    d[name] = g16.to(self.dev)
         return host, dev
 
     def init_oracle(self, host_batches_all):
@@ -191,6 +199,18 @@ def _eager_pipelined(emu, seeds, empty=()):
         emu.check_outputs(emu.oracle_step(data[i][0]))
     emu.check_tables()
     emu.errors()
+
+
+@pytest.mark.parametrize("n,out_dtype", [(2, torch.float32), (3, torch.bfloat16)])
+def test_emulated_bf16_dense_gradients_bit_exact(cuda, n, out_dtype):
+    """bf16 dense gradients (in_dtype) over the SM-store exchange: bf16 on the
+    links, widened exactly, summed in rank order in fp32, scaled, cast."""
+    emu = Emu(cuda, n, _small_tables(), {"lstm": 100_000}, "adagrad", "p2p-sm",
+              dense_dtype=out_dtype, dense_in_dtype=torch.bfloat16)
+    try:
+        _eager_pipelined(emu, [1, 2, 3])
+    finally:
+        emu.close()
 
 
 @pytest.mark.parametrize("n,buckets,opt", [(2, 2, "adagrad"), (3, 5, "sgd"), (4, 3, "adam")])

@@ -24,6 +24,9 @@ def _ngpu():
     ("adagrad", "p2p", "p2p", "", "hybrid"),
     # weighted reduction split (rank 0 takes no chunk), SM stores and copy engines
     ("adagrad", "p2p", "p2p-sm", "split=first0", "hybrid"),
+    # bf16 dense gradients (in_dtype): SM stores (bf16 on the links) and NCCL (widened first)
+    ("adagrad", "p2p", "p2p-sm", "dense_in=bf16", "hybrid"),
+    ("sgd", "p2p", "nccl", "dense_in=bf16", "hybrid"),
     # the SM-store dense exchange in 2 and 5 buckets (default 1)
     ("adagrad", "p2p", "p2p-sm", "dar_buckets=2", "hybrid"),
     ("sgd", "p2p", "p2p-sm", "dar_buckets=5", "hybrid"),
@@ -51,9 +54,12 @@ def test_multi_gpu_step_matches_oracle(opt, xchg, dense, knobs, arch):
         split, knobs = knobs.split("=", 1)[1], ""
     if knobs.startswith("empty="):
         empty, knobs = knobs.split("=", 1)[1], ""
+    dense_in = "f32"
+    if knobs.startswith("dense_in="):
+        dense_in, knobs = knobs.split("=", 1)[1], ""
     env = dict(os.environ, HP_CHECK_OPT=opt, HP_CHECK_XCHG=xchg, HP_CHECK_DENSE=dense,
                HP_CHECK_KNOBS=knobs, HP_CHECK_ARCH=arch, HP_CHECK_SPLIT=split,
-               HP_CHECK_EMPTY=empty, HP_CHECK_SHAPE=shape,
+               HP_CHECK_EMPTY=empty, HP_CHECK_SHAPE=shape, HP_CHECK_DENSE_IN=dense_in,
                # the pipelined dense exchange cuts each chunk into 64 KB pieces: many of them
                HP_CHECK_DENSE_ELEMS="1000004" if dense == "p2p-pipe" else "50000")
     import socket

@@ -265,6 +265,20 @@ def test_dense_scale_cast_single_rank(cuda, dtype):
     assert torch.equal(out.cpu(), ref)
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float16])
+def test_dense_bf16_input_scale_cast(cuda, dtype):
+    """K7 with bf16 gradients (in_dtype) at n = 1: exact widening, scale, cast;
+    odd size (vector body + scalar tail)."""
+    from paper_1808_02621_b200 import ops
+
+    rng = np.random.default_rng(9)
+    g16 = torch.from_numpy(rng.standard_normal(100_003, dtype=F32)).to(torch.bfloat16)
+    out = torch.empty(g16.numel(), dtype=dtype, device=cuda)
+    ops.dense_allreduce_scale_cast(None, g16.to(cuda), out, 0.25)
+    ref = torch.from_numpy(g16.float().numpy() * F32(0.25)).to(dtype)
+    assert torch.equal(out.cpu(), ref)
+
+
 def test_runner_single_gpu_matches_oracle(cuda):
     """HybridRunner at n=1 on a reduced LM graph: pulled rows, tables and dense."""
     import paper_1808_02621_b200 as hp
