@@ -172,9 +172,7 @@ def main():
             step = 4
             batches = [batch_of(step, r) for r in range(world)]
             mine = batches[rank]
-            static = {k: ((torch.from_numpy(v[0]).to(dev), torch.from_numpy(v[1]).to(dev))
-                          if isinstance(v, tuple) else torch.from_numpy(v).to(dev))
-                      for k, v in mine.items()}
+            static = to_dev(mine)
             g = runner.capture(static, warmup=1)  # runs step 4 eagerly, records one step
             g.replay()                            # executes step 5
             torch.cuda.synchronize()
