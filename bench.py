@@ -82,6 +82,9 @@ def parse():
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"])
     ap.add_argument("--dense-exchange", default=None,
                     choices=["p2p", "p2p-sm", "p2p-pipe", "p2p-pull", "nvls", "nccl"])
+    ap.add_argument("--dense-in", default="f32", choices=["f32", "bf16"],
+                    help="dtype the dense gradients arrive in (not BASELINE's config: an "
+                         "in_dtype data point; bf16 travels as bf16 over the SM-store exchange)")
     ap.add_argument("--dense-split", default="auto",
                     help="peer-memory dense exchange: reduction share per rank "
                          "('auto', 'uniform' or comma-separated weights)")
@@ -295,7 +298,10 @@ def main():
                              optimizer=opt, device=dev, seed=0, exchange=args.exchange,
                              dense_exchange=args.dense_exchange,
                              dense_split=(args.dense_split if args.dense_split in ("auto", "uniform")
-                                          else [float(x) for x in args.dense_split.split(",")]))
+                                          else [float(x) for x in args.dense_split.split(",")]),
+                             dense_in_dtype=torch.bfloat16 if args.dense_in == "bf16" else torch.float32)
+    if args.dense_in == "bf16" and args.check:
+        raise SystemExit("--check runs the BASELINE config (fp32 dense gradients)")
 
     # resident batches, rotated so their total exceeds 2x L2 (126 MB)
     host = [make_batch(wl, seed=1 + i, rank=rank) for i in range(1)]
@@ -307,9 +313,11 @@ def main():
     R = min(-(-R // 6) * 6, 18) if not args.rotations else R
     host += [make_batch(wl, seed=1 + i, rank=rank) for i in range(1, R)]
 
+    din = runner.dense_in_dtype
+
     def to_dev(b):
         return {k: ((torch.from_numpy(v[0]).to(dev), torch.from_numpy(v[1]).to(dev))
-                    if isinstance(v, tuple) else torch.from_numpy(v).to(dev))
+                    if isinstance(v, tuple) else torch.from_numpy(v).to(din).to(dev))
                 for k, v in b.items()}
 
     batches = [to_dev(b) for b in host]
@@ -506,8 +514,11 @@ def main():
             how = "each rank reads every peer's copy: (n-1) S per rank (ingress)"
         elif runner.dense_exchange in ("p2p", "p2p-sm", "p2p-pipe"):
             c = [x / sum(w) * S for x in w]
-            egress = max((S - c[r]) + (world - 1) * c[r] for r in range(world))
-            how = "max over ranks of (S - chunk_r) + (n-1) chunk_r"
+            ib = 0.5 if runner.dense_in_dtype == torch.bfloat16 else 1.0  # bf16 scatter: half
+            ob = runner.dense_dtype.itemsize / 4
+            egress = max((S - c[r]) * ib + (world - 1) * c[r] * ob for r in range(world))
+            how = ("max over ranks of (S - chunk_r) * in_bytes/4 + (n-1) chunk_r * out_bytes/4 "
+                   "(S, chunks in fp32 bytes)")
         else:
             egress = 2.0 * (world - 1) / world * S
             how = "ring-equivalent bus bytes 2(n-1)/n S"
@@ -643,7 +654,8 @@ def main():
                                           "steps_per_graph": G,
                                           "exchange": runner.exchange,
                                           "dense_exchange": runner.dense_exchange,
-                                          "dense_split": runner.dense_weights or "uniform"},
+                                          "dense_split": runner.dense_weights or "uniform"}
+                      | ({"dense_in": "bf16"} if args.dense_in == "bf16" else {}),
             "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": ke},
             "gpu_launches": launches_per_step * args.steps,
