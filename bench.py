@@ -75,8 +75,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rotations", type=int, default=0, help="distinct resident batches")
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--steps-per-graph", type=int, default=3,
-                    help="consecutive steps captured in one CUDA graph (divides the rotation)")
+    ap.add_argument("--steps-per-graph", type=int, default=6,
+                    help="consecutive steps captured in one CUDA graph (divides the rotation); "
+                         "graphs of 3 and 2 steps cover the remainder")
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"])
@@ -345,8 +346,15 @@ def main():
     _mark("graphs captured")
     G = args.steps_per_graph if graphs and R % max(args.steps_per_graph, 1) == 0 else 1
     # G > 1: graphs of G consecutive steps (same rotation and plan-slot order as
-    # the single-step graphs), so K steps replay as K // G launches (+ singles)
-    multi = runner.capture_pipelined(batches, steps_per_graph=G) if G > 1 else None
+    # the single-step graphs), so K steps replay as K // G launches; the
+    # remainder replays graphs of 3 / 2 steps where they divide the rotation,
+    # then single steps. (Measured LM1B N=1 per step: 1 step per graph 51.3 us,
+    # 2: 41, 3: 38.2, 6: 36.2 - each graph ends by joining the plan streams.)
+    multis = {}
+    rem = os.environ.get("HP_BENCH_REMAINDER", "1") == "1"
+    for g in sorted({G, 3, 2} if rem else {G}, reverse=True):
+        if G > 1 and 1 < g <= G and R % g == 0:
+            multis[g] = runner.capture_pipelined(batches, steps_per_graph=g)
     torch.cuda.synchronize()
     pos = [0]  # next step's index in the rotation
 
@@ -354,9 +362,10 @@ def main():
         done = 0
         while done < k:
             i = pos[0]
-            if multi and i % G == 0 and k - done >= G:
-                multi[(i % R) // G].replay()
-                n = G
+            g = next((g for g in multis if i % g == 0 and k - done >= g), 0)
+            if g:
+                multis[g][(i % R) // g].replay()
+                n = g
             elif graphs:
                 graphs[i % R].replay()
                 n = 1
@@ -377,6 +386,14 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    # setup (untimed, before the warm-up): every captured graph replayed once
+    # (a graph's first launch uploads it: ~0.1-0.2 ms that must not land in the
+    # timed region), each set over a whole rotation so the position stays 0;
+    # then align the rotation so the warm-up ends on a G-step graph boundary
+    for gs in list(multis.values()) + ([graphs] if graphs else []):
+        for gr in gs:
+            gr.replay()
+    run_steps((-max(args.warmup, 3)) % G)
     run_steps(max(args.warmup, 3))
     torch.cuda.synchronize()
     barrier()
@@ -668,7 +685,7 @@ def main():
             line["parity_check"] = check
         print(json.dumps(line), flush=True)
     # release captured graphs (they reference NCCL and peer windows) before teardown
-    graphs = e2e_graph = multi = None
+    graphs = e2e_graph = multis = None
     torch.cuda.synchronize()
     runner.check_errors(sync=True)  # any device error bit of the run raises here
     _mark("errors checked")
