@@ -195,7 +195,6 @@ __device__ __forceinline__ void emit_items(const DedupPlan& pl, int u, int j0, i
   }
   if (lg) {
     pl.longs[bl] = make_int4(bp, n0, dst, L);  // {partial slot, chunks, dst, rows}
-    pl.long_j0[bl] = j0;
   }
 }
 
@@ -746,7 +745,6 @@ size_t dedup_ws_bytes(int64_t T, int32_t D, int32_t P) {
   s += 3 * align256(4 * (Tc + 1));    // uniq_key, seg_start, item_off
   s += 5 * align256(4 * Tc);          // segidx, sigma, part_off, dst, long_tmp
   s += align256(16 * Tc) + align256(16 * (Tc / HP_CHUNK + 2));  // items, longs
-  s += align256(4 * (Tc / HP_CHUNK + 2));                         // long_j0
   s += align256(16 * prow);                                       // part_desc
   s += align256(4 * ((size_t)P + 1)) + 2 * align256(4 * (size_t)P);
   s += align256(4 * HP_RADIX * ntiles) + align256(4 * HP_RADIX);
@@ -818,7 +816,6 @@ int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, i
   pl->long_tmp = (int32_t*)take(4 * Tc);
   pl->items = (int4*)take(16 * Tc);
   pl->longs = (int4*)take(16 * (Tc / HP_CHUNK + 2));
-  pl->long_j0 = (int32_t*)take(4 * (Tc / HP_CHUNK + 2));
   pl->part_desc = (int4*)take(16 * (2 * Tc / HP_CHUNK + 2));
   pl->first_u = (int32_t*)take(4 * ((size_t)P + 1));
   pl->part_base = (int32_t*)take(4 * (size_t)P);

@@ -27,7 +27,6 @@ struct DedupPlan {
   int4* items;          // [T] reduce items {j0, n, dst, final}: rows sorted[j0, j0+n)
   int32_t* part_off;    // [T] partial-buffer slot of segment u (large-path scratch)
   int4* longs;          // [T/C+1] long segments {partial slot, n0 chunks, dst, L rows}
-  int32_t* long_j0;     // [T/C+1] first sorted row of each long segment
   int4* part_desc;      // [2T/C+2] per partial slot (long chunk): {first sorted row, rows, dst, long index}
   int32_t* dst;         // [T] destination row of segment u (send slot or slab row)
   int32_t* long_tmp;    // [T] large-path scratch

@@ -97,10 +97,9 @@ int launch_copy(const Src& src, int64_t n, const int32_t* n_dev, float* out, int
 // Work unit `it` of a plan broadcast: (rows n, destination dst, this lane's
 // position). long_only: `it` is a long segment's chunk (a partial slot), read
 // from its descriptor (one load, then the positions); else a plan item.
-__device__ __forceinline__ void bcast_unit(const DedupPlan& pl, int it, bool long_only, int n_long,
+__device__ __forceinline__ void bcast_unit(const DedupPlan& pl, int it, bool long_only,
                                            int lane, int& n, int& dst, int& pos) {
   if (long_only) {
-    (void)n_long;
     const int4 d = pl.part_desc[it];
     n = d.y;
     dst = d.z;
@@ -139,12 +138,11 @@ k_bcast_rows(DedupPlan pl, const float4* __restrict__ rows, float4* __restrict__
   // kernel by the apply + pull); work unit = a chunk = a partial slot f, whose
   // long segment is found by binary search over the descriptors' slot bases
   const int n_items = long_only ? pl.counters[C_PARTIALS] : pl.counters[C_ITEMS];
-  const int n_long = pl.counters[C_LONG];
   uint32_t parity = 0;
   bool stored = false;
   for (int it = blockIdx.x * 8 + w; it < n_items; it += gridDim.x * 8) {
     int n, dst, pos;
-    bcast_unit(pl, it, long_only, n_long, lane, n, dst, pos);
+    bcast_unit(pl, it, long_only, lane, n, dst, pos);
     if (dst < 0) {  // dropped ids: zero rows, plain stores
       for (int j = 0; j < n; ++j) {
         const int64_t p = __shfl_sync(0xffffffffu, pos, j);
@@ -182,10 +180,9 @@ k_bcast_rows_reg(DedupPlan pl, const float4* __restrict__ rows, float4* __restri
   HP_ENTRY(SP_COPY);
   const int lane = threadIdx.x & 31;
   const int n_items = long_only ? pl.counters[C_PARTIALS] : pl.counters[C_ITEMS];
-  const int n_long = pl.counters[C_LONG];
   for (int it = (blockIdx.x * 256 + threadIdx.x) >> 5; it < n_items; it += (gridDim.x * 256) >> 5) {
     int n, dst, pos;
-    bcast_unit(pl, it, long_only, n_long, lane, n, dst, pos);
+    bcast_unit(pl, it, long_only, lane, n, dst, pos);
     float4 x[VPL];
 #pragma unroll
     for (int v = 0; v < VPL; ++v) {
