@@ -133,6 +133,9 @@ void hp_debug_set_split_long(int on);
  * (38 -> 50 us): the long chain then reaches its TMA broadcast while the short
  * items and the next plan's cluster sort still hold the SMs. */
 void hp_debug_set_long_b8(int on);
+/* A/B: k_reduce (local epilogues) grid cap in blocks per SM (default 16: one
+ * group per item, many waves; 4 = one resident wave, groups loop over items). */
+void hp_debug_set_reduce_bps(int n);
 /* A/B: 1 (default) = chain kernels carry their stream's priority as a launch
  * attribute (graph node priority); 0 = plain launches. */
 void hp_debug_set_launch_prio(int on);

@@ -873,6 +873,7 @@ int g_reduce_b = 2;
 // config's 16M draws (one CTA per long chunk holds 4-8x fewer chunks in flight
 // than k_reduce's thread groups)
 int g_split_long = 1;
+int g_reduce_bps = 16;  // k_reduce grid cap in blocks per SM (hp_debug_set_reduce_bps)
 int g_long_b8 = 0;  // long-chunk reduce with 8 rows in flight (hp_debug_set_long_b8; A/B)
 int g_fuse_tree = 0;
 HP_SPAN_SETTER(set_spans_dedup)

@@ -76,6 +76,7 @@ extern int g_dar_rg_blocks;   // HP_DAR_SM reduce/gather grid (0: 2 per SM)
 extern int g_dar_buckets;     // HP_DAR_SM buckets per step
 extern int g_owner_waves;     // peer-store kernels: many waves (1) or one resident wave (0)
 extern int g_reduce_b;        // k_reduce rows in flight at VPT=2 (2, 4, 8)
+extern int g_reduce_bps;
 extern int g_long_b8;
 extern int g_split_long;      // 1 (default): long-first items; the n = 1 apply runs its short
                               // items on a side stream beside the long chain

@@ -685,7 +685,7 @@ void launch_k_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cud
   // <= one group per item, many waves (each block fences once if its epilogue
   // stores to peers; hp_debug_set_owner_waves(0) keeps those in one resident wave)
   const int blocks = grid_for(pl.part == 1 ? 2 * pl.T / HP_CHUNK + 2 : pl.T, 256 / TPI,
-                              sm_count() * (Epi::kRemote && !g_owner_waves ? 3 : 16));
+                              sm_count() * (Epi::kRemote && !g_owner_waves ? 3 : g_reduce_bps));
   if (VPT == 2 && g_reduce_b == 4)
     launch_k_reduce_b<TPI, VPT, 4>(pl, vals, epi, st, blocks);
   else if (VPT == 2 && g_reduce_b == 8)
