@@ -358,10 +358,14 @@ int hp_xchg_plan(hp_xchg_t x, const int64_t* ids, int64_t T, int64_t V, int32_t 
                  const int32_t* owner, const int64_t* glob_base, int64_t* send_ids, int32_t* inv,
                  int32_t* dest_counts, int32_t* n_uniq, void* ws, size_t ws_bytes, void* stream);
 /* (hp_xchg_push_plan takes the destinations hp_xchg_plan resolved from its
- * glob_base; the glob_base argument here is checked for non-NULL only.) */
+ * glob_base; the glob_base argument here is checked for non-NULL only.)
+ * side_stream (nullable): the short segments' reduce + stores run there,
+ * forked from and joined back into `stream`, beside the long segments' chunks
+ * -> k_combine; the publication follows the join. */
 int hp_xchg_push_plan(hp_xchg_t x, const float* vals, int64_t T, int64_t V, int32_t P,
                       const int64_t* send_ids, const int32_t* dest_counts,
-                      const int64_t* glob_base, void* ws, size_t ws_bytes, void* stream);
+                      const int64_t* glob_base, void* ws, size_t ws_bytes, void* stream,
+                      void* side_stream);
 /* Wait (one spinning block, bounded) until every source pushed (which = 0) or
  * every owner applied (which = 1) for this rank's current epoch. */
 int hp_xchg_wait(hp_xchg_t x, int32_t which, void* stream);

@@ -88,7 +88,7 @@ SIGNATURES = {
     "hp_xchg_merge_apply": (C.c_int, [vp, Slab, Optim, i32, vp]),
     "hp_xchg_wait": (C.c_int, [vp, i32, vp]),
     "hp_xchg_plan": (C.c_int, [vp, vp, i64, i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
-    "hp_xchg_push_plan": (C.c_int, [vp, vp, i64, i64, i32, vp, vp, vp, vp, sz, vp]),
+    "hp_xchg_push_plan": (C.c_int, [vp, vp, i64, i64, i32, vp, vp, vp, vp, sz, vp, vp]),
     "hp_xchg_stitch": (C.c_int, [vp, vp, i64, vp, i32, vp]),
     "hp_xchg_status": (C.c_int, [vp, vp, vp]),
     "hp_xchg_recv_counts": (C.c_int, [vp, vp, vp]),

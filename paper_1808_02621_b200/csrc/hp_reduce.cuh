@@ -738,7 +738,7 @@ int launch_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaSt
     else launch_k_reduce<256, 2>(pl, vals, epi, st);
     HP_LAUNCHED(1, "k_reduce");
   }
-  if (pl.part == 2) return HP_OK;  // short items only: no long segment to close
+  if (pl.part == 2) return HP_OK;  // short items only: no long segment to close (nor publish)
   // fused tree (items in long-first order, pl.nw == 0): k_reduce closed every
   // long segment itself (long_chunk); otherwise one CTA per long segment
   if (pl.fused) {
@@ -760,6 +760,7 @@ int launch_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaSt
   }
   launch_k(k_combine<Epi>, dim3(cblocks), dim3(CMB_NT), csmem, st, pl, epi);
   HP_LAUNCHED(1, "k_combine");
+  if (pl.part == 1) return HP_OK;  // split push: the caller publishes after the join
   if constexpr (Epi::kRemote) {
     launch_k(k_publish<Epi>, dim3(1), dim3(64), 0, st, epi);
     HP_LAUNCHED(1, "k_publish");

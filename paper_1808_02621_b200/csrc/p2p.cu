@@ -64,6 +64,16 @@ struct SigView {
   }
 };
 
+// Fork / join events of the split push (hp_xchg_push_plan with a side
+// stream), per device; recorded and waited on back to back, so two suffice.
+cudaEvent_t push_event(int k) {
+  static cudaEvent_t ev[64][2] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!ev[dev][k]) cudaEventCreateWithFlags(&ev[dev][k], cudaEventDisableTiming);
+  return ev[dev][k];
+}
+
 __device__ __forceinline__ void st_release_sys(int* p, int v) {
   asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -925,7 +935,8 @@ int hp_xchg_plan(hp_xchg_t x, const int64_t* ids, int64_t T, int64_t V, int32_t 
 // over NVLink; the last block publishes counts / offsets / epoch at every owner.
 int hp_xchg_push_plan(hp_xchg_t x, const float* vals, int64_t T, int64_t V, int32_t P,
                       const int64_t* send_ids, const int32_t* dest_counts,
-                      const int64_t* glob_base, void* ws, size_t ws_bytes, void* stream) {
+                      const int64_t* glob_base, void* ws, size_t ws_bytes, void* stream,
+                      void* side_stream) {
   HP_REQUIRE(x && send_ids && dest_counts && glob_base, "NULL argument");
   HP_REQUIRE(T == 0 || vals, "NULL vals");
   DedupPlan pl;
@@ -933,8 +944,28 @@ int hp_xchg_push_plan(hp_xchg_t x, const float* vals, int64_t T, int64_t V, int3
   if (rc) return rc;
   restore_sorted_pos(pl);
   EpiPush epi{x->peers, x->L, dest_counts, send_ids, pl.send_info, x->win};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (side_stream != nullptr && T > 0 && pl.reorder && !pl.fused && pl.nw <= 0) {
+    // long-first items: the short items' reduce + peer stores fork onto
+    // side_stream; the long chunks -> k_combine stay on stream; after the
+    // join one k_publish (its system fence covers both branches' stores)
+    cudaStream_t ss = static_cast<cudaStream_t>(side_stream);
+    cudaEvent_t fork = push_event(0), join = push_event(1);
+    HP_CUDA(cudaEventRecord(fork, st));
+    HP_CUDA(cudaStreamWaitEvent(ss, fork, 0));
+    DedupPlan ps = pl, pg = pl;
+    ps.part = 2;
+    pg.part = 1;
+    if ((rc = launch_reduce(ps, vals, epi, ss))) return rc;
+    HP_CUDA(cudaEventRecord(join, ss));
+    if ((rc = launch_reduce(pg, vals, epi, st))) return rc;  // no publication for part 1
+    HP_CUDA(cudaStreamWaitEvent(st, join, 0));
+    launch_k(k_publish<EpiPush>, dim3(1), dim3(64), 0, st, epi);
+    HP_LAUNCHED(1, "k_publish");
+    return HP_OK;
+  }
   pl.T = std::max<int64_t>(T, 1);  // launch even for T == 0: k_publish carries the publication
-  return launch_reduce(pl, vals, epi, static_cast<cudaStream_t>(stream));
+  return launch_reduce(pl, vals, epi, st);
 }
 
 // Worker, fused K1+K2+K3 = hp_xchg_plan + hp_xchg_push_plan.
@@ -946,7 +977,7 @@ int hp_xchg_push(hp_xchg_t x, const int64_t* ids, const float* vals, int64_t T, 
                         ws_bytes, stream);
   if (rc) return rc;
   return hp_xchg_push_plan(x, vals, T, V, P, send_ids, dest_counts, glob_base, ws, ws_bytes,
-                           stream);
+                           stream, nullptr);
 }
 
 // Owner: wait for every source's push, merge in source order, apply to the

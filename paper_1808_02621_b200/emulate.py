@@ -60,8 +60,10 @@ class LocalWorld:
         hardware queues only. With the concurrent multi-stream step, n ranks x
         (table, plan, dense) streams outnumber the device's connections and
         streams of different ranks share a queue: one rank's spinning wait then
-        blocks another rank's work queued behind it (measured: n >= 3 timed out)."""
+        blocks another rank's work queued behind it (measured: n >= 3 timed out).
+        The split push's side stream goes too, for the same reason."""
         runner.concurrent_tables = False
+        runner._short_streams = {}
 
     def comm(self, rank: int) -> "LocalComm":
         return LocalComm(self, rank)

@@ -251,13 +251,13 @@ class HybridRunner:
                                               else pt)
                          for n in self.tables}
         self._dense_stream = torch.cuda.Stream(device=self.device, priority=pd)
-        # n = 1: each table's short segments (reduce + apply + pull) run on a
-        # side stream beside its long segments' chain (hp_apply_plan_pull);
-        # one priority step below the chain. HP_SPLIT_LONG=0 keeps one stream.
+        # each table's short segments (n = 1: reduce + apply + pull,
+        # hp_apply_plan_pull; n > 1: reduce + peer stores, hp_xchg_push_plan)
+        # run on a side stream beside its long segments' chain; one priority
+        # step below the chain. HP_SPLIT_LONG=0 keeps one stream.
         self._short_streams = ({n: torch.cuda.Stream(device=self.device, priority=min(pt + 1, 0))
                                 for n in self.tables}
-                               if world_size == 1 and os.environ.get("HP_SPLIT_LONG", "1") == "1"
-                               else {})
+                               if os.environ.get("HP_SPLIT_LONG", "1") == "1" else {})
         # two plan streams per table, alternating by step: the dedup of step s+1
         # may start before the one of step s has finished (each is a latency-
         # bound cluster sort on a few SMs, about as long as a whole step)
@@ -347,7 +347,8 @@ class HybridRunner:
         if not planned:
             self._plan(tab, ids, slot)
         k(f"push:{name}", True)
-        x.push_plan(vals, tab.V, tab.P, r, self.glob_base[name], tab.wss[slot])
+        x.push_plan(vals, tab.V, tab.P, r, self.glob_base[name], tab.wss[slot],
+                    side_stream=self._short_streams.get(name))
         k(f"push:{name}", False)
         # Waits stay one-block kernels (k_wait): folded into the prologue of the
         # owner scan / stitch, every block of those grids spun, holding SMs the

@@ -109,11 +109,13 @@ class PeerExchange:
              out["n_uniq"].data_ptr(), ws.ptr, ws.nbytes, torch.cuda.current_stream().cuda_stream)
         return out
 
-    def push_plan(self, vals, V: int, P: int, out: dict, glob_base, ws) -> None:
-        """Value half of push: reduce with the plan in ``ws`` and store into owners' inboxes."""
+    def push_plan(self, vals, V: int, P: int, out: dict, glob_base, ws, side_stream=None) -> None:
+        """Value half of push: reduce with the plan in ``ws`` and store into owners'
+        inboxes (``side_stream``: the short segments there, beside the long ones)."""
         call("hp_xchg_push_plan", self.handle, vals.data_ptr(), vals.shape[0], V, P,
              out["send_ids"].data_ptr(), out["dest_counts"].data_ptr(), glob_base.data_ptr(),
-             ws.ptr, ws.nbytes, torch.cuda.current_stream().cuda_stream)
+             ws.ptr, ws.nbytes, torch.cuda.current_stream().cuda_stream,
+             None if side_stream is None else side_stream.cuda_stream)
 
     def wait(self, which: int) -> None:
         """0: until every source pushed; 1: until every owner applied."""
