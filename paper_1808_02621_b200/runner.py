@@ -254,10 +254,14 @@ class HybridRunner:
         # each table's short segments (n = 1: reduce + apply + pull,
         # hp_apply_plan_pull; n > 1: reduce + peer stores, hp_xchg_push_plan)
         # run on a side stream beside its long segments' chain; one priority
-        # step below the chain. HP_SPLIT_LONG=0 keeps one stream.
+        # step below the chain. Default at n = 1 (HP_SPLIT_LONG=0: one stream);
+        # at n > 1 only with HP_SPLIT_PUSH=1 (measured neutral at N = 2: full
+        # step 134.0 vs 136.6 us, sparse-only 96.6 vs 92.9 us, the push alone
+        # 42 vs 38 us)
+        split = (os.environ.get("HP_SPLIT_LONG", "1") == "1" if world_size == 1
+                 else os.environ.get("HP_SPLIT_PUSH", "0") == "1")
         self._short_streams = ({n: torch.cuda.Stream(device=self.device, priority=min(pt + 1, 0))
-                                for n in self.tables}
-                               if os.environ.get("HP_SPLIT_LONG", "1") == "1" else {})
+                                for n in self.tables} if split else {})
         # two plan streams per table, alternating by step: the dedup of step s+1
         # may start before the one of step s has finished (each is a latency-
         # bound cluster sort on a few SMs, about as long as a whole step)
