@@ -27,6 +27,8 @@ def _ngpu():
     # bf16 dense gradients (in_dtype): SM stores (bf16 on the links) and NCCL (widened first)
     ("adagrad", "p2p", "p2p-sm", "dense_in=bf16", "hybrid"),
     ("sgd", "p2p", "nccl", "dense_in=bf16", "hybrid"),
+    # the split push (short items on a side stream; HP_SPLIT_PUSH=1)
+    ("adam", "p2p", "p2p-sm", "split_push=1", "hybrid"),
     # the SM-store dense exchange in 2 and 5 buckets (default 1)
     ("adagrad", "p2p", "p2p-sm", "dar_buckets=2", "hybrid"),
     ("sgd", "p2p", "p2p-sm", "dar_buckets=5", "hybrid"),
@@ -57,9 +59,13 @@ def test_multi_gpu_step_matches_oracle(opt, xchg, dense, knobs, arch):
     dense_in = "f32"
     if knobs.startswith("dense_in="):
         dense_in, knobs = knobs.split("=", 1)[1], ""
+    split_push = "0"
+    if knobs.startswith("split_push="):
+        split_push, knobs = knobs.split("=", 1)[1], ""
     env = dict(os.environ, HP_CHECK_OPT=opt, HP_CHECK_XCHG=xchg, HP_CHECK_DENSE=dense,
                HP_CHECK_KNOBS=knobs, HP_CHECK_ARCH=arch, HP_CHECK_SPLIT=split,
                HP_CHECK_EMPTY=empty, HP_CHECK_SHAPE=shape, HP_CHECK_DENSE_IN=dense_in,
+               HP_SPLIT_PUSH=split_push,
                # the pipelined dense exchange cuts each chunk into 64 KB pieces: many of them
                HP_CHECK_DENSE_ELEMS="1000004" if dense == "p2p-pipe" else "50000")
     import socket
