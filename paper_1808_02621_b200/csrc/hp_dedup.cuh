@@ -76,11 +76,11 @@ extern int g_dar_rg_blocks;   // HP_DAR_SM reduce/gather grid (0: 2 per SM)
 extern int g_dar_buckets;     // HP_DAR_SM buckets per step
 extern int g_owner_waves;     // peer-store kernels: many waves (1) or one resident wave (0)
 extern int g_reduce_b;        // k_reduce rows in flight at VPT=2 (2, 4, 8)
-extern int g_reduce_bps;
-extern int g_long_b8;
-extern int g_split_long;      // 1 (default): long-first items; the n = 1 apply runs its short
+extern int g_reduce_bps;      // k_reduce grid cap, blocks per SM (local epilogues; default 16)
+extern int g_long_b8;         // > 0: long chunks reduced with 8 rows in flight (A/B; default 0)
+extern int g_split_long;      // 1 (default): long-first items; the split apply / push runs the short
                               // items on a side stream beside the long chain
-extern int g_fuse_tree;       // 1 (default): fused tree (long_chunk) when the row stream is off
+extern int g_fuse_tree;       // 1: fused tree (long_chunk) when the row stream is off; 0 (default)
 
 size_t dedup_ws_bytes(int64_t T, int32_t D, int32_t P);
 int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, int64_t V,
