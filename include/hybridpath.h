@@ -133,6 +133,9 @@ void hp_debug_set_split_long(int on);
  * (38 -> 50 us): the long chain then reaches its TMA broadcast while the short
  * items and the next plan's cluster sort still hold the SMs. */
 void hp_debug_set_long_b8(int on);
+/* A/B: 1 (default) = the split apply's long roots and the pull of their rows
+ * run as one work-queue kernel (k_combine_bcast); 0 = k_combine + k_bcast_rows. */
+void hp_debug_set_cbcast(int on);
 /* A/B: k_reduce (local epilogues) grid cap in blocks per SM (default 16: one
  * group per item, many waves; 4 = one resident wave, groups loop over items). */
 void hp_debug_set_reduce_bps(int n);

@@ -195,6 +195,7 @@ __device__ __forceinline__ void emit_items(const DedupPlan& pl, int u, int j0, i
   }
   if (lg) {
     pl.longs[bl] = make_int4(bp, n0, dst, L);  // {partial slot, chunks, dst, rows}
+    pl.long_flag[bl] = 0;
   }
 }
 
@@ -256,7 +257,12 @@ k_dedup_cluster(DedupPlan pl, const int64_t* __restrict__ ids, const int32_t* __
   __shared__ int s_err;
   if (tid == 0) {
     s_err = 0;
-    if (c == 0) pl.counters[C_ERR] = 0;
+    if (c == 0) {
+      pl.counters[C_ERR] = 0;
+      pl.counters[C_QUEUE] = 0;
+      pl.counters[C_DONE] = 0;
+      pl.counters[C_GEN] = 0;
+    }
   }
   __syncthreads();
 
@@ -746,6 +752,7 @@ size_t dedup_ws_bytes(int64_t T, int32_t D, int32_t P) {
   s += 5 * align256(4 * Tc);          // segidx, sigma, part_off, dst, long_tmp
   s += align256(16 * Tc) + align256(16 * (Tc / HP_CHUNK + 2));  // items, longs
   s += align256(16 * prow);                                       // part_desc
+  s += align256(4 * (Tc / HP_CHUNK + 2));                         // long_flag
   s += align256(4 * ((size_t)P + 1)) + 2 * align256(4 * (size_t)P);
   s += align256(4 * HP_RADIX * ntiles) + align256(4 * HP_RADIX);
   s += align256(4 * nscan);
@@ -817,6 +824,8 @@ int carve_plan(DedupPlan* pl, void* ws, size_t ws_bytes, int64_t T, int32_t D, i
   pl->items = (int4*)take(16 * Tc);
   pl->longs = (int4*)take(16 * (Tc / HP_CHUNK + 2));
   pl->part_desc = (int4*)take(16 * (2 * Tc / HP_CHUNK + 2));
+  pl->long_flag = (int32_t*)take(4 * (Tc / HP_CHUNK + 2));
+  pl->cbcast = 0;
   pl->first_u = (int32_t*)take(4 * ((size_t)P + 1));
   pl->part_base = (int32_t*)take(4 * (size_t)P);
   pl->zero_owner = (int32_t*)take(4 * (size_t)P);
@@ -874,6 +883,7 @@ int g_reduce_b = 2;
 // than k_reduce's thread groups)
 int g_split_long = 1;
 int g_reduce_bps = 16;  // k_reduce grid cap in blocks per SM (hp_debug_set_reduce_bps)
+int g_cbcast = 1;  // hp_debug_set_cbcast
 int g_long_b8 = 0;  // long-chunk reduce with 8 rows in flight (hp_debug_set_long_b8; A/B)
 int g_fuse_tree = 0;
 HP_SPAN_SETTER(set_spans_dedup)

@@ -6,7 +6,10 @@
 namespace hp {
 
 // Counter slots in DedupPlan::counters (device int32).
-enum { C_UNIQ = 0, C_ITEMS = 1, C_LONG = 2, C_PARTIALS = 3, C_ERR = 4, C_NCOUNTERS = 8 };
+// counters: C_QUEUE / C_DONE / C_GEN serve k_combine_bcast's work queue (zero
+// after a plan build; the kernel leaves QUEUE and DONE at zero and bumps GEN)
+enum { C_UNIQ = 0, C_ITEMS = 1, C_LONG = 2, C_PARTIALS = 3, C_ERR = 4, C_QUEUE = 5, C_DONE = 6,
+       C_GEN = 7, C_NCOUNTERS = 8 };
 
 // Views into the caller's workspace (all device pointers).
 struct DedupPlan {
@@ -47,6 +50,8 @@ struct DedupPlan {
   int32_t fused;        // 1: long chunks first + fused tree in k_reduce (no k_combine)
   int32_t reorder;      // 1: items long-chunks-first ([0, C_PARTIALS) long chunks, then short)
   int32_t part;         // per launch: 0 every item, 1 long chunks only, 2 short items only
+  int32_t cbcast;       // per launch (part 1, local apply with the pull): k_combine_bcast
+  int32_t* long_flag;   // [T/C+2] per long segment: generation its root finished (k_combine_bcast)
   int32_t* wb_item;     // [HP_RS_MAX_WARPS + 1]
   int32_t* wb_row;      // [HP_RS_MAX_WARPS + 1]
   // fused upper levels of long segments (combine_up): one arrival counter per
@@ -77,6 +82,7 @@ extern int g_dar_buckets;     // HP_DAR_SM buckets per step
 extern int g_owner_waves;     // peer-store kernels: many waves (1) or one resident wave (0)
 extern int g_reduce_b;        // k_reduce rows in flight at VPT=2 (2, 4, 8)
 extern int g_reduce_bps;      // k_reduce grid cap, blocks per SM (local epilogues; default 16)
+extern int g_cbcast;          // 1 (default): the split apply's long roots + their pull in one kernel
 extern int g_long_b8;         // > 0: long chunks reduced with 8 rows in flight (A/B; default 0)
 extern int g_split_long;      // 1 (default): long-first items; the split apply / push runs the short
                               // items on a side stream beside the long chain

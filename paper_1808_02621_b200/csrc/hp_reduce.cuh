@@ -410,85 +410,167 @@ static __device__ __noinline__ float4 seq_sum_rows(const float4* src, int n, int
 // +0, then the group sums sequentially (oracle.grouped_tree_sum).
 constexpr int CMB_D4 = 256;  // widest row (float4) of the shared-memory path
 constexpr int CMB_NT = 512;  // threads per long segment: one pass over <= 4 groups at D = 512
+// One long segment, by the whole CTA: its partial rows (k_reduce's level-0
+// chunk sums) summed up the tree in order, then the epilogue (apply) stores
+// the result. Ends with a __syncthreads.
+template <class Epi>
+__device__ __forceinline__ void combine_segment(const DedupPlan& pl, const Epi& epi, int4 d,
+                                                float4* s_grp) {
+  const int D4 = pl.D >> 2;
+  float4* partials = reinterpret_cast<float4*>(pl.partials);
+  int n = d.y;
+  float4* Pp = partials + (int64_t)d.x * D4;
+  constexpr int PV = (CMB_D4 + CMB_NT - 1) / CMB_NT;  // epilogue columns per thread (fast path)
+  typename Epi::Pre pre[PV];
+  const bool fast = n <= HP_CHUNK * HP_CHUNK && D4 <= CMB_D4;
+  if (fast) {
+#pragma unroll
+    for (int v = 0; v < PV; ++v) {
+      const int c4 = threadIdx.x + v * CMB_NT;
+      if (c4 < D4 && d.z >= 0) pre[v] = epi.load(d.z, c4);
+    }
+    const int ng = (n + HP_CHUNK - 1) / HP_CHUNK;
+    if (ng > 1) {
+#pragma unroll 1
+      for (int unit = threadIdx.x; unit < ng * D4; unit += blockDim.x) {
+        const int g = unit / D4, c4 = unit - g * D4;
+        const int e = min(HP_CHUNK, n - g * HP_CHUNK);
+        s_grp[g * D4 + c4] = seq_sum_rows(Pp + (int64_t)g * HP_CHUNK * D4 + c4, e, D4);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int v = 0; v < PV; ++v) {
+      const int c4 = threadIdx.x + v * CMB_NT;
+      if (c4 >= D4) continue;
+      float4 acc;
+      if (ng > 1) {
+        acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int g = 0; g < ng; ++g) acc = f4_add(acc, s_grp[g * D4 + c4]);
+      } else {
+        acc = seq_sum_rows(Pp + c4, n, D4);
+      }
+      if (d.z >= 0) epi.store(d.z, c4, acc, pre[v]);
+    }
+    __syncthreads();
+    return;
+  }
+#pragma unroll 1
+  while (n > HP_CHUNK) {
+    const int ng = (n + HP_CHUNK - 1) / HP_CHUNK;
+    const int units = ng * D4;
+#pragma unroll 1
+    for (int ub = 0; ub < units; ub += blockDim.x) {
+      const int unit = ub + threadIdx.x;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      int g = 0, c4 = 0;
+      if (unit < units) {
+        g = unit / D4;
+        c4 = unit - g * D4;
+        const int e = min(HP_CHUNK, n - g * HP_CHUNK);
+        acc = seq_sum_rows(Pp + (int64_t)g * HP_CHUNK * D4 + c4, e, D4);
+      }
+      __syncthreads();
+      if (unit < units) Pp[(int64_t)g * D4 + c4] = acc;
+      __syncthreads();
+    }
+    n = ng;
+  }
+#pragma unroll 1
+  for (int c4 = threadIdx.x; c4 < D4; c4 += blockDim.x) {
+    typename Epi::Pre p{};
+    if (d.z >= 0) p = epi.load(d.z, c4);
+    const float4 acc = seq_sum_rows(Pp + c4, n, D4);
+    if (d.z >= 0) epi.store(d.z, c4, acc, p);
+  }
+  __syncthreads();
+}
+
 template <class Epi>
 __global__ void __launch_bounds__(CMB_NT) k_combine(DedupPlan pl, Epi epi) {
   extern __shared__ __align__(16) float4 s_grp[];  // [HP_CHUNK][D4] group sums
   HP_ENTRY(SP_COMBINE);
-  const int D4 = pl.D >> 2;
   const int n_long = pl.counters[C_LONG];
   // (speculative read guarded by the capacity, T/16 + 2 descriptors)
   const int4 d_first = (int64_t)blockIdx.x < pl.T / HP_CHUNK + 2 ? pl.longs[blockIdx.x]
                                                                    : make_int4(0, 0, 0, 0);
-  float4* partials = reinterpret_cast<float4*>(pl.partials);
 #pragma unroll 1
-  for (int li = blockIdx.x; li < n_long; li += gridDim.x) {
-    const int4 d = li == (int)blockIdx.x ? d_first : pl.longs[li];
-    int n = d.y;
-    float4* Pp = partials + (int64_t)d.x * D4;
-    constexpr int PV = (CMB_D4 + CMB_NT - 1) / CMB_NT;  // epilogue columns per thread (fast path)
-    typename Epi::Pre pre[PV];
-    const bool fast = n <= HP_CHUNK * HP_CHUNK && D4 <= CMB_D4;
-    if (fast) {
-#pragma unroll
-      for (int v = 0; v < PV; ++v) {
-        const int c4 = threadIdx.x + v * CMB_NT;
-        if (c4 < D4 && d.z >= 0) pre[v] = epi.load(d.z, c4);
-      }
-      const int ng = (n + HP_CHUNK - 1) / HP_CHUNK;
-      if (ng > 1) {
+  for (int li = blockIdx.x; li < n_long; li += gridDim.x)
+    combine_segment(pl, epi, li == (int)blockIdx.x ? d_first : pl.longs[li], s_grp);
+  HP_SPAN_END(SP_COMBINE);
+}
+
+// n = 1 apply with the pull (the split apply's long chain): the long
+// segments' roots AND the copy of their updated rows to every position, in
+// ONE kernel. Work items come from a queue in order: first the n_long roots
+// (combine + apply, then a release flag per segment), then the long chunks
+// (wait for the segment's flag, copy its slab row to the chunk's <= 16
+// positions). A CTA only waits on a root an earlier ticket handed to a
+// running CTA: no deadlock at any residency. The queue / done counters and
+// the generation word are the plan's spare counters (zeroed with the plan);
+// the last CTA resets the queue and bumps the generation, so a plan may be
+// applied again.
+template <class Epi>
+__global__ void __launch_bounds__(CMB_NT) k_combine_bcast(DedupPlan pl, Epi epi) {
+  extern __shared__ __align__(16) float4 s_grp[];
+  __shared__ int s_item;
+  HP_ENTRY(SP_COMBINE);
+  const int D4 = pl.D >> 2;
+  const int n_long = pl.counters[C_LONG];
+  const int n_items = n_long + pl.counters[C_PARTIALS];
+  const int gen = *reinterpret_cast<volatile int*>(&pl.counters[C_GEN]) + 1;
+  int* queue = &pl.counters[C_QUEUE];
 #pragma unroll 1
-        for (int unit = threadIdx.x; unit < ng * D4; unit += blockDim.x) {
-          const int g = unit / D4, c4 = unit - g * D4;
-          const int e = min(HP_CHUNK, n - g * HP_CHUNK);
-          s_grp[g * D4 + c4] = seq_sum_rows(Pp + (int64_t)g * HP_CHUNK * D4 + c4, e, D4);
-        }
-        __syncthreads();
+  while (true) {
+    if (threadIdx.x == 0) s_item = atomicAdd(queue, 1);
+    __syncthreads();
+    const int it = s_item;
+    __syncthreads();
+    if (it >= n_items) break;
+    if (it < n_long) {
+      combine_segment(pl, epi, pl.longs[it], s_grp);
+      if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(pl.long_flag + it), "r"(gen)
+                     : "memory");
       }
-#pragma unroll
-      for (int v = 0; v < PV; ++v) {
-        const int c4 = threadIdx.x + v * CMB_NT;
-        if (c4 >= D4) continue;
-        float4 acc;
-        if (ng > 1) {
-          acc = make_float4(0.f, 0.f, 0.f, 0.f);
-          for (int g = 0; g < ng; ++g) acc = f4_add(acc, s_grp[g * D4 + c4]);
-        } else {
-          acc = seq_sum_rows(Pp + c4, n, D4);
-        }
-        if (d.z >= 0) epi.store(d.z, c4, acc, pre[v]);
-      }
-      __syncthreads();
       continue;
     }
-#pragma unroll 1
-    while (n > HP_CHUNK) {
-      const int ng = (n + HP_CHUNK - 1) / HP_CHUNK;
-      const int units = ng * D4;
-#pragma unroll 1
-      for (int ub = 0; ub < units; ub += blockDim.x) {
-        const int unit = ub + threadIdx.x;
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        int g = 0, c4 = 0;
-        if (unit < units) {
-          g = unit / D4;
-          c4 = unit - g * D4;
-          const int e = min(HP_CHUNK, n - g * HP_CHUNK);
-          acc = seq_sum_rows(Pp + (int64_t)g * HP_CHUNK * D4 + c4, e, D4);
-        }
-        __syncthreads();
-        if (unit < units) Pp[(int64_t)g * D4 + c4] = acc;
-        __syncthreads();
-      }
-      n = ng;
-    }
-#pragma unroll 1
-    for (int c4 = threadIdx.x; c4 < D4; c4 += blockDim.x) {
-      typename Epi::Pre p{};
-      if (d.z >= 0) p = epi.load(d.z, c4);
-      const float4 acc = seq_sum_rows(Pp + c4, n, D4);
-      if (d.z >= 0) epi.store(d.z, c4, acc, p);
+    const int4 c = pl.part_desc[it - n_long];  // {first sorted row, rows, dst, long index}
+    if (threadIdx.x == 0 && c.z >= 0) {
+      int v;
+      do {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(pl.long_flag + c.w)
+                     : "memory");
+      } while (v != gen);
+      __threadfence();
     }
     __syncthreads();
+    // column q of rows r0, r0 + rs, ... (one row per CMB_NT / D4 thread slice)
+    if (D4 <= CMB_NT) {
+      const int q = threadIdx.x % D4, r0 = threadIdx.x / D4, rs = CMB_NT / D4;
+      if (r0 < rs) {
+        const float4 row =
+            c.z >= 0 ? epi.w[(int64_t)c.z * D4 + q] : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int r = r0; r < c.y; r += rs)
+          epi.out[(int64_t)pl.sorted_pos[c.x + r] * D4 + q] = row;
+      }
+    } else {
+      for (int r = 0; r < c.y; ++r) {
+        const int64_t pos = pl.sorted_pos[c.x + r];
+        for (int cc = threadIdx.x; cc < D4; cc += CMB_NT)
+          epi.out[pos * D4 + cc] =
+              c.z >= 0 ? epi.w[(int64_t)c.z * D4 + cc] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&pl.counters[C_DONE], 1) == (int)gridDim.x - 1) {
+      pl.counters[C_QUEUE] = 0;
+      pl.counters[C_DONE] = 0;
+      pl.counters[C_GEN] = gen;
+    }
   }
   HP_SPAN_END(SP_COMBINE);
 }
@@ -757,6 +839,20 @@ int launch_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaSt
     HP_CUDA(cudaFuncSetAttribute(k_combine<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)((size_t)HP_CHUNK * CMB_D4 * sizeof(float4))));
     cconf = true;
+  }
+  if constexpr (Epi::kOut && !Epi::kRemote) {
+    if (pl.part == 1 && pl.cbcast) {  // roots + the pull of their rows, one work queue
+      static bool bconf = false;
+      if (!bconf) {
+        HP_CUDA(cudaFuncSetAttribute(k_combine_bcast<Epi>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)((size_t)HP_CHUNK * CMB_D4 * sizeof(float4))));
+        bconf = true;
+      }
+      launch_k(k_combine_bcast<Epi>, dim3(sm_count()), dim3(CMB_NT), csmem, st, pl, epi);
+      HP_LAUNCHED(1, "k_combine_bcast");
+      return HP_OK;
+    }
   }
   launch_k(k_combine<Epi>, dim3(cblocks), dim3(CMB_NT), csmem, st, pl, epi);
   HP_LAUNCHED(1, "k_combine");

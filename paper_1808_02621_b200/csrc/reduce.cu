@@ -173,10 +173,13 @@ int hp_apply_plan_pull(const float* rows, int64_t R, hp_slab slab, hp_optim opt,
     DedupPlan ps = pl, pg = pl;
     ps.part = 2;
     pg.part = 1;
+    pg.cbcast = g_cbcast;  // the long rows' pull inside the roots' kernel (k_combine_bcast)
     if ((rc = apply_plan(ps, rows, slab, opt, ss, out))) return rc;
     HP_CUDA(cudaEventRecord(join, ss));
     if ((rc = apply_plan(pg, rows, slab, opt, st, out))) return rc;
-    if ((rc = plan_stitch(ws, ws_bytes, R, slab.D, slab.V, slab.P, slab.w, out, st, 1))) return rc;
+    if (!pg.cbcast &&
+        (rc = plan_stitch(ws, ws_bytes, R, slab.D, slab.V, slab.P, slab.w, out, st, 1)))
+      return rc;
     HP_CUDA(cudaStreamWaitEvent(st, join, 0));
     return HP_OK;
   }
