@@ -133,8 +133,11 @@ void hp_debug_set_split_long(int on);
  * (38 -> 50 us): the long chain then reaches its TMA broadcast while the short
  * items and the next plan's cluster sort still hold the SMs. */
 void hp_debug_set_long_b8(int on);
-/* A/B: 1 (default) = the split apply's long roots and the pull of their rows
- * run as one work-queue kernel (k_combine_bcast); 0 = k_combine + k_bcast_rows. */
+/* A/B: >= 1 = the split apply's long roots and the pull of their rows run as
+ * one work-queue kernel (k_combine_bcast; > 1: that many CTAs, 1: a third of
+ * the SMs); 0 (default) = k_combine + k_bcast_rows. Measured at LM1B N = 1:
+ * 148 CTAs 38.4 us per step (they hold every SM's registers, the short items
+ * wait), 96 34.7-36.4, 49 40.5-41.0, 16 69.1 vs 36.1-36.4: off. */
 void hp_debug_set_cbcast(int on);
 /* A/B: k_reduce (local epilogues) grid cap in blocks per SM (default 16: one
  * group per item, many waves; 4 = one resident wave, groups loop over items). */

@@ -186,7 +186,7 @@ void hp_debug_set_reduce_b(int b) { hp::g_reduce_b = b; }
 void hp_debug_set_wait_timeout(long long cycles) { hp::g_wait_cycles = cycles; }
 void hp_debug_set_fuse_tree(int on) { hp::g_fuse_tree = on ? 1 : 0; }
 void hp_debug_set_reduce_bps(int n) { hp::g_reduce_bps = n < 1 ? 1 : n; }
-void hp_debug_set_cbcast(int on) { hp::g_cbcast = on ? 1 : 0; }
+void hp_debug_set_cbcast(int on) { hp::g_cbcast = on < 0 ? 0 : on; }
 void hp_debug_set_long_b8(int on) { hp::g_long_b8 = on < 0 ? 0 : on; }
 void hp_debug_set_split_long(int on) { hp::g_split_long = on ? 1 : 0; }
 void hp_debug_set_launch_prio(int on) { hp::g_launch_prio = on ? 1 : 0; }

@@ -849,7 +849,10 @@ int launch_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaSt
                                      (int)((size_t)HP_CHUNK * CMB_D4 * sizeof(float4))));
         bconf = true;
       }
-      launch_k(k_combine_bcast<Epi>, dim3(sm_count()), dim3(CMB_NT), csmem, st, pl, epi);
+      // a fraction of the SMs (one 512-thread CTA fills an SM's registers): the
+      // short items' k_reduce runs beside it on the rest
+      const int g = pl.cbcast > 1 ? pl.cbcast : std::max(1, sm_count() / 3);
+      launch_k(k_combine_bcast<Epi>, dim3(g), dim3(CMB_NT), csmem, st, pl, epi);
       HP_LAUNCHED(1, "k_combine_bcast");
       return HP_OK;
     }
