@@ -203,7 +203,7 @@ def test_apply_plan_pull_split_bit_exact(cuda, opt, mode):
     segments on a side stream beside the long chain (default; also with the
     8-rows-in-flight long-chunk reduce, and with the long roots + their pull in
     one work-queue kernel), on one stream, and with plans in build order
-    (hp_debug_set_split_long(0)) == oracle. Two steps per plan slot reuse."""
+    (hp_debug_set_split_long(0)) == oracle."""
     from paper_1808_02621_b200 import _lib, ops
     from paper_1808_02621_b200.synth import log_uniform_ids, zipf_ids
 
