@@ -776,6 +776,44 @@ void launch_k_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cud
     launch_k_reduce_b<TPI, VPT, B>(pl, vals, epi, st, blocks);
 }
 
+// The long segments' chunks alone on TMA (pl.part == 1, hp_debug_set_long_tma):
+// one CTA per chunk at a time, its <= 16 gradient rows bulk-copied into shared
+// memory (cta_stage_sum: batches of stage_rows(D) rows, one elected lane per
+// row) and summed per column in row order from +0.0 -> the chunk's partial
+// slot. Two DRAM round trips per 16-row chunk at D = 512 instead of eight.
+template <int CPT>
+__global__ void __launch_bounds__(256)
+k_reduce_long_tma(DedupPlan pl, const float* __restrict__ vals_f) {
+  __shared__ __align__(128) float4 s_stage[STAGE_F4];
+  __shared__ uint64_t s_bar;
+  HP_ENTRY(SP_REDUCE);
+  const float4* vals = reinterpret_cast<const float4*>(vals_f);
+  float4* partials = reinterpret_cast<float4*>(pl.partials);
+  const int D4 = pl.D >> 2, SR = stage_rows(pl.D);
+  const int n_part = pl.counters[C_PARTIALS];
+  if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+  __syncthreads();
+  uint32_t parity = 0;
+#pragma unroll 1
+  for (int it = blockIdx.x; it < n_part; it += gridDim.x) {  // long-first: [0, n_part) are chunks
+    const int4 item = pl.items[it];
+    parity = cta_stage_sum<CPT>(
+        s_stage, &s_bar, parity, item.y, D4, SR,
+        [&](int j) { return vals + (int64_t)pl.sorted_pos[item.x + j] * D4; },
+        [&](int, int c4, float4 a) { partials[(int64_t)item.z * D4 + c4] = a; }, false);
+    __syncthreads();  // s_stage is reused by the next chunk
+  }
+  HP_SPAN_END(SP_REDUCE);
+}
+
+inline void launch_k_reduce_long_tma(const DedupPlan& pl, const float* vals, cudaStream_t st) {
+  const int D4 = pl.D >> 2;
+  const int g = grid_for(2 * pl.T / HP_CHUNK + 2, 1, sm_count() * std::max(1, g_long_tma));
+  if (D4 <= 256) launch_k(k_reduce_long_tma<1>, dim3(g), dim3(256), 0, st, pl, vals);
+  else if (D4 <= 512) launch_k(k_reduce_long_tma<2>, dim3(g), dim3(256), 0, st, pl, vals);
+  else launch_k(k_reduce_long_tma<4>, dim3(g), dim3(256), 0, st, pl, vals);
+}
+
 // The long segments' chunks alone (pl.part == 1, hp_debug_set_long_b8 > 0;
 // A/B, off by default: faster alone, slower in the step, see the header):
 // every item is a full 16-row chunk, so each group keeps 8 rows in flight (2
@@ -807,6 +845,9 @@ int launch_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaSt
       default: launch_rowstream<8>(pl, vals, epi, st); break;
     }
     HP_LAUNCHED(1, "k_rowstream");
+  } else if (pl.part == 1 && g_long_tma && pl.reorder && pl.D <= 4 * 4096) {
+    launch_k_reduce_long_tma(pl, vals, st);
+    HP_LAUNCHED(1, "k_reduce_long_tma");
   } else if (pl.part == 1 && g_long_b8) {
     launch_k_reduce_long(pl, vals, st);
     HP_LAUNCHED(1, "k_reduce (long chunks)");
