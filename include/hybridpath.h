@@ -140,7 +140,9 @@ void hp_debug_set_long_b8(int on);
  * wait), 96 34.7-36.4, 49 40.5-41.0, 16 69.1 vs 36.1-36.4: off. */
 void hp_debug_set_cbcast(int on);
 /* A/B: b > 0 = the split apply's long chunks reduced on TMA (k_reduce_long_tma,
- * one CTA per chunk, up to b CTAs per SM); 0 = k_reduce. */
+ * one CTA per chunk, up to b CTAs per SM); 0 (default) = k_reduce. Measured:
+ * K4+K5 alone 34.9 -> 31.0 us, the LM1B step 36.1 -> 48-51 us (see
+ * profiles/r2_n1_chain_studies.txt): off. */
 void hp_debug_set_long_tma(int n);
 /* A/B: k_reduce (local epilogues) grid cap in blocks per SM (default 16: one
  * group per item, many waves; 4 = one resident wave, groups loop over items). */
