@@ -144,6 +144,9 @@ void hp_debug_set_cbcast(int on);
  * K4+K5 alone 34.9 -> 31.0 us, the LM1B step 36.1 -> 48-51 us (see
  * profiles/r2_n1_chain_studies.txt): off. */
 void hp_debug_set_long_tma(int n);
+/* A/B: 1 = k_combine capped at 64 registers per thread (8 partial rows in
+ * flight instead of 16; two 512-thread CTAs per SM); 0 (default) = 1 per SM. */
+void hp_debug_set_comb_lite(int on);
 /* A/B: k_reduce (local epilogues) grid cap in blocks per SM (default 16: one
  * group per item, many waves; 4 = one resident wave, groups loop over items). */
 void hp_debug_set_reduce_bps(int n);

@@ -110,6 +110,7 @@ SIGNATURES = {
     "hp_debug_set_long_b8": (None, [C.c_int]),
     "hp_debug_set_cbcast": (None, [C.c_int]),
     "hp_debug_set_long_tma": (None, [C.c_int]),
+    "hp_debug_set_comb_lite": (None, [C.c_int]),
     "hp_debug_set_reduce_bps": (None, [C.c_int]),
     "hp_debug_set_launch_prio": (None, [C.c_int]),
     "hp_debug_set_bcast_tma": (None, [C.c_int]),

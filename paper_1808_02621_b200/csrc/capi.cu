@@ -30,6 +30,7 @@ extern int g_split_long;
 extern int g_long_b8;
 extern int g_cbcast;
 extern int g_long_tma;
+extern int g_comb_lite;
 extern int g_reduce_bps;
 extern int g_bcast_tma;
 int g_launch_prio = 1;
@@ -187,6 +188,7 @@ void hp_debug_set_reduce_b(int b) { hp::g_reduce_b = b; }
 void hp_debug_set_wait_timeout(long long cycles) { hp::g_wait_cycles = cycles; }
 void hp_debug_set_fuse_tree(int on) { hp::g_fuse_tree = on ? 1 : 0; }
 void hp_debug_set_reduce_bps(int n) { hp::g_reduce_bps = n < 1 ? 1 : n; }
+void hp_debug_set_comb_lite(int on) { hp::g_comb_lite = on ? 1 : 0; }
 void hp_debug_set_long_tma(int n) { hp::g_long_tma = n < 0 ? 0 : n; }
 void hp_debug_set_cbcast(int on) { hp::g_cbcast = on < 0 ? 0 : on; }
 void hp_debug_set_long_b8(int on) { hp::g_long_b8 = on < 0 ? 0 : on; }

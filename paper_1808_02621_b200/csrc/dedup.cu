@@ -884,6 +884,7 @@ int g_reduce_b = 2;
 int g_split_long = 1;
 int g_reduce_bps = 16;  // k_reduce grid cap in blocks per SM (hp_debug_set_reduce_bps)
 int g_cbcast = 0;  // hp_debug_set_cbcast (A/B; measured slower in the step, see the header)
+int g_comb_lite = 0;  // hp_debug_set_comb_lite (A/B)
 int g_long_tma = 0;  // hp_debug_set_long_tma (A/B)
 int g_long_b8 = 0;  // long-chunk reduce with 8 rows in flight (hp_debug_set_long_b8; A/B)
 int g_fuse_tree = 0;

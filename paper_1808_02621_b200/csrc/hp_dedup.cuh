@@ -83,6 +83,7 @@ extern int g_owner_waves;     // peer-store kernels: many waves (1) or one resid
 extern int g_reduce_b;        // k_reduce rows in flight at VPT=2 (2, 4, 8)
 extern int g_reduce_bps;      // k_reduce grid cap, blocks per SM (local epilogues; default 16)
 extern int g_cbcast;          // >= 1: the split apply's long roots + their pull in one kernel (A/B)
+extern int g_comb_lite;       // 1: k_combine capped at 64 registers (two CTAs per SM)
 extern int g_long_tma;        // > 0: long chunks reduced on TMA (k_reduce_long_tma), g per SM
 extern int g_long_b8;         // > 0: long chunks reduced with 8 rows in flight (A/B; default 0)
 extern int g_split_long;      // 1 (default): long-first items; the split apply / push runs the short

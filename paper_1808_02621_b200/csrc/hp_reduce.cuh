@@ -399,6 +399,30 @@ static __device__ __noinline__ float4 seq_sum_rows(const float4* src, int n, int
   return acc;
 }
 
+// The same sum with HP_CHUNK / 2 loads in flight (two round trips), for the
+// register-capped k_combine variant (hp_debug_set_comb_lite).
+static __device__ __noinline__ float4 seq_sum_rows_half(const float4* src, int n, int D4) {
+  constexpr int H = HP_CHUNK / 2;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+  for (int j0 = 0; j0 < n; j0 += H) {
+    float4 x[H];
+#pragma unroll
+    for (int j = 0; j < H; ++j)
+      if (j0 + j < n) x[j] = src[(int64_t)(j0 + j) * D4];
+#pragma unroll
+    for (int j = 0; j < H; ++j)
+      if (j0 + j < n) acc = f4_add(acc, x[j]);
+  }
+  return acc;
+}
+
+template <bool LITE>
+__device__ __forceinline__ float4 comb_sum(const float4* src, int n, int D4) {
+  if constexpr (LITE) return seq_sum_rows_half(src, n, D4);
+  else return seq_sum_rows(src, n, D4);
+}
+
 // Upper levels for segments longer than HP_CHUNK: one CTA per long segment
 // {partial slot, n0, dst, u}. Latency-bound (a chain per hot id), so:
 //  * the CTA's first descriptor is loaded with the segment count (capacity
@@ -413,7 +437,7 @@ constexpr int CMB_NT = 512;  // threads per long segment: one pass over <= 4 gro
 // One long segment, by the whole CTA: its partial rows (k_reduce's level-0
 // chunk sums) summed up the tree in order, then the epilogue (apply) stores
 // the result. Ends with a __syncthreads.
-template <class Epi>
+template <class Epi, bool LITE = false>
 __device__ __forceinline__ void combine_segment(const DedupPlan& pl, const Epi& epi, int4 d,
                                                 float4* s_grp) {
   const int D4 = pl.D >> 2;
@@ -435,7 +459,7 @@ __device__ __forceinline__ void combine_segment(const DedupPlan& pl, const Epi& 
       for (int unit = threadIdx.x; unit < ng * D4; unit += blockDim.x) {
         const int g = unit / D4, c4 = unit - g * D4;
         const int e = min(HP_CHUNK, n - g * HP_CHUNK);
-        s_grp[g * D4 + c4] = seq_sum_rows(Pp + (int64_t)g * HP_CHUNK * D4 + c4, e, D4);
+        s_grp[g * D4 + c4] = comb_sum<LITE>(Pp + (int64_t)g * HP_CHUNK * D4 + c4, e, D4);
       }
       __syncthreads();
     }
@@ -448,7 +472,7 @@ __device__ __forceinline__ void combine_segment(const DedupPlan& pl, const Epi& 
         acc = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int g = 0; g < ng; ++g) acc = f4_add(acc, s_grp[g * D4 + c4]);
       } else {
-        acc = seq_sum_rows(Pp + c4, n, D4);
+        acc = comb_sum<LITE>(Pp + c4, n, D4);
       }
       if (d.z >= 0) epi.store(d.z, c4, acc, pre[v]);
     }
@@ -468,7 +492,7 @@ __device__ __forceinline__ void combine_segment(const DedupPlan& pl, const Epi& 
         g = unit / D4;
         c4 = unit - g * D4;
         const int e = min(HP_CHUNK, n - g * HP_CHUNK);
-        acc = seq_sum_rows(Pp + (int64_t)g * HP_CHUNK * D4 + c4, e, D4);
+        acc = comb_sum<LITE>(Pp + (int64_t)g * HP_CHUNK * D4 + c4, e, D4);
       }
       __syncthreads();
       if (unit < units) Pp[(int64_t)g * D4 + c4] = acc;
@@ -480,14 +504,14 @@ __device__ __forceinline__ void combine_segment(const DedupPlan& pl, const Epi& 
   for (int c4 = threadIdx.x; c4 < D4; c4 += blockDim.x) {
     typename Epi::Pre p{};
     if (d.z >= 0) p = epi.load(d.z, c4);
-    const float4 acc = seq_sum_rows(Pp + c4, n, D4);
+    const float4 acc = comb_sum<LITE>(Pp + c4, n, D4);
     if (d.z >= 0) epi.store(d.z, c4, acc, p);
   }
   __syncthreads();
 }
 
-template <class Epi>
-__global__ void __launch_bounds__(CMB_NT) k_combine(DedupPlan pl, Epi epi) {
+template <class Epi, bool LITE = false>
+__global__ void __launch_bounds__(CMB_NT, LITE ? 2 : 1) k_combine(DedupPlan pl, Epi epi) {
   extern __shared__ __align__(16) float4 s_grp[];  // [HP_CHUNK][D4] group sums
   HP_ENTRY(SP_COMBINE);
   const int n_long = pl.counters[C_LONG];
@@ -496,7 +520,7 @@ __global__ void __launch_bounds__(CMB_NT) k_combine(DedupPlan pl, Epi epi) {
                                                                    : make_int4(0, 0, 0, 0);
 #pragma unroll 1
   for (int li = blockIdx.x; li < n_long; li += gridDim.x)
-    combine_segment(pl, epi, li == (int)blockIdx.x ? d_first : pl.longs[li], s_grp);
+    combine_segment<Epi, LITE>(pl, epi, li == (int)blockIdx.x ? d_first : pl.longs[li], s_grp);
   HP_SPAN_END(SP_COMBINE);
 }
 
@@ -898,7 +922,17 @@ int launch_reduce(const DedupPlan& pl, const float* vals, const Epi& epi, cudaSt
       return HP_OK;
     }
   }
-  launch_k(k_combine<Epi>, dim3(cblocks), dim3(CMB_NT), csmem, st, pl, epi);
+  if (g_comb_lite) {  // A/B: 64 registers, two CTAs per SM
+    static bool lconf = false;
+    if (!lconf) {
+      HP_CUDA(cudaFuncSetAttribute(k_combine<Epi, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)((size_t)HP_CHUNK * CMB_D4 * sizeof(float4))));
+      lconf = true;
+    }
+    launch_k(k_combine<Epi, true>, dim3(cblocks), dim3(CMB_NT), csmem, st, pl, epi);
+  } else {
+    launch_k(k_combine<Epi>, dim3(cblocks), dim3(CMB_NT), csmem, st, pl, epi);
+  }
   HP_LAUNCHED(1, "k_combine");
   if (pl.part == 1) return HP_OK;  // split push: the caller publishes after the join
   if constexpr (Epi::kRemote) {
