@@ -197,8 +197,8 @@ def test_local_apply_and_gather(cuda, level0, opt):
 
 
 @pytest.mark.parametrize("opt", ["adagrad", "adam"])
-@pytest.mark.parametrize("mode", ["side", "side_b8", "side_tma", "side_cbcast", "one_stream",
-                                  "build_order"])
+@pytest.mark.parametrize("mode", ["side", "side_b8", "side_tma", "side_cbcast", "side_lite",
+                                  "one_stream", "build_order"])
 def test_apply_plan_pull_split_bit_exact(cuda, opt, mode):
     """K4 + K5 fused (hp_apply_plan_pull) at the LM1B softmax shape: the short
     segments on a side stream beside the long chain (default; also with the
@@ -218,6 +218,7 @@ def test_apply_plan_pull_split_bit_exact(cuda, opt, mode):
     _lib.load().hp_debug_set_long_b8(1 if mode == "side_b8" else 0)
     _lib.load().hp_debug_set_cbcast(24 if mode == "side_cbcast" else 0)
     _lib.load().hp_debug_set_long_tma(2 if mode == "side_tma" else 0)
+    _lib.load().hp_debug_set_comb_lite(1 if mode == "side_lite" else 0)
     try:
         for step in (1, 2):
             ids = np.concatenate([zipf_ids(rng, V, T), log_uniform_ids(rng, V, 8192)])
@@ -237,6 +238,7 @@ def test_apply_plan_pull_split_bit_exact(cuda, opt, mode):
         _lib.load().hp_debug_set_long_b8(0)
         _lib.load().hp_debug_set_cbcast(0)
         _lib.load().hp_debug_set_long_tma(0)
+        _lib.load().hp_debug_set_comb_lite(0)
 
 
 def test_init_rows_bit_exact(cuda):
