@@ -111,6 +111,9 @@ void hp_debug_set_dar_rg_blocks(int n);
 /* HP_DAR_SM: buckets per step (pieces of every chunk; the phases of one bucket
  * overlap the waits of the others), 1..16, default 1. */
 void hp_debug_set_dar_buckets(int n);
+/* A/B: 1 = the SM-store K7 kernels keep 16 (scatter) / 8 (reduce-gather)
+ * vectors in flight per thread, so fewer CTAs saturate NVLink (fp32 in/out). */
+void hp_debug_set_dar_deep(int on);
 /* Instrumentation: grids of the peer-store kernels (push reduce, owner rows):
  * 1 (default) = one group per item, many waves; 0 = one resident wave. */
 void hp_debug_set_owner_waves(int on);

@@ -1221,7 +1221,7 @@ template <> struct Vec4<__nv_bfloat16> {
 // my contribution straight from grad); 4 vectors in flight per thread. bf16
 // gradients travel as bf16 (slot s of a rank holds them at the same byte
 // offset as fp32 would, half of it used).
-template <typename InT>
+template <typename InT, int U = 4>
 __global__ void __launch_bounds__(256)
 k_ar_scatter(PeerTable peers, ArLayout A, const void* __restrict__ grad_v, int bk, int nb) {
   using V = Vec4<InT>;
@@ -1235,15 +1235,15 @@ k_ar_scatter(PeerTable peers, ArLayout A, const void* __restrict__ grad_v, int b
                                   (int64_t)A.me * A.sstride4 * 16);
   const int64_t lim = min(p1, max((int64_t)0, real4 - b4));  // real elements here
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t j0 = p0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < p1; j0 += 4 * stride) {
-    VT v[4];
+  for (int64_t j0 = p0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < p1; j0 += U * stride) {
+    VT v[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t j = j0 + u * stride;
       v[u] = j < lim ? V::ld(src + j) : V::zero();
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t j = j0 + u * stride;
       if (j < p1) dst[j] = v[u];
     }
@@ -1268,7 +1268,7 @@ __device__ __forceinline__ void put4<__nv_bfloat16>(void* base, int64_t i4, floa
   reinterpret_cast<uint2*>(base)[i4] = u;
 }
 
-template <typename OutT, typename InT>
+template <typename OutT, typename InT, int U = 2>
 __global__ void __launch_bounds__(256)
 k_ar_reduce_gather(PeerTable peers, void* my_win, ArLayout A, const void* __restrict__ grad_v,
                    float scale, int bk, int nb) {
@@ -1281,10 +1281,10 @@ k_ar_reduce_gather(PeerTable peers, void* my_win, ArLayout A, const void* __rest
   const char* slots = static_cast<const char*>(my_win) + A.slots_off;
   const VT* mine = static_cast<const VT*>(grad_v) + b4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t j0 = p0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < p1; j0 += 2 * stride) {
-    float4 acc[2];
+  for (int64_t j0 = p0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < p1; j0 += U * stride) {
+    float4 acc[U];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t j = j0 + u * stride;
       acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (j < p1)
@@ -1296,7 +1296,7 @@ k_ar_reduce_gather(PeerTable peers, void* my_win, ArLayout A, const void* __rest
         }
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t j = j0 + u * stride;
       if (j >= p1) continue;
       float4 v = acc[u];
@@ -1850,6 +1850,8 @@ int hp_dar_allreduce(hp_dar_t d, const void* grad_v, float scale, void* stream) 
     if (np > 0) {
       if (bf_in)
         launch_k(k_ar_scatter<__nv_bfloat16>, dim3(bx, np), dim3(256), 0, st, d->peers, d->A, g, b, nb);
+      else if (g_dar_deep)  // A/B: 16 vectors in flight per thread (fewer CTAs saturate the link)
+        launch_k(k_ar_scatter<float, 16>, dim3(bx, np), dim3(256), 0, st, d->peers, d->A, g, b, nb);
       else
         launch_k(k_ar_scatter<float>, dim3(bx, np), dim3(256), 0, st, d->peers, d->A, g, b, nb);
     }
@@ -1859,7 +1861,10 @@ int hp_dar_allreduce(hp_dar_t d, const void* grad_v, float scale, void* stream) 
     const int lag = nb - 1 - b;
     launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 0, d->A.n, wait_budget(), SP_AR_WAIT0, lag);
     const dim3 G(brg), Bk(256);
-    if (d->A.out_bytes == 4 && !bf_in)
+    if (d->A.out_bytes == 4 && !bf_in && g_dar_deep)
+      launch_k(k_ar_reduce_gather<float, float, 8>, G, Bk, 0, st, d->peers, d->win, d->A, g, scale, b,
+               nb);
+    else if (d->A.out_bytes == 4 && !bf_in)
       launch_k(k_ar_reduce_gather<float, float>, G, Bk, 0, st, d->peers, d->win, d->A, g, scale, b, nb);
     else if (d->A.out_bytes == 4)
       launch_k(k_ar_reduce_gather<float, __nv_bfloat16>, G, Bk, 0, st, d->peers, d->win, d->A, g,
