@@ -114,6 +114,9 @@ void hp_debug_set_dar_buckets(int n);
 /* A/B: 1 = the SM-store K7 kernels keep 16 (scatter) / 8 (reduce-gather)
  * vectors in flight per thread, so fewer CTAs saturate NVLink (fp32 in/out). */
 void hp_debug_set_dar_deep(int on);
+/* A/B: b > 0 = the SM-store K7 scatter moves 32 KB pieces by TMA bulk copies
+ * (global -> shared -> peer slot), b CTAs of one warp per peer chunk (fp32). */
+void hp_debug_set_dar_tma(int n);
 /* Instrumentation: grids of the peer-store kernels (push reduce, owner rows):
  * 1 (default) = one group per item, many waves; 0 = one resident wave. */
 void hp_debug_set_owner_waves(int on);

@@ -1253,6 +1253,46 @@ k_ar_scatter(PeerTable peers, ArLayout A, const void* __restrict__ grad_v, int b
   HP_SPAN_END(SP_AR_SCATTER);
 }
 
+// TMA variant of the scatter (fp32; hp_debug_set_dar_tma): each CTA moves its
+// pieces of the peer chunk global -> shared -> peer slot with bulk copies
+// (double-buffered, one elected thread), so a few CTAs saturate NVLink and the
+// rest of the SMs stay with the sparse tables. The slot padding past S_real is
+// never written (zero since the window's creation).
+constexpr int AR_TMA_F4 = 2048;  // 32 KB per piece
+__global__ void __launch_bounds__(32)
+k_ar_scatter_tma(PeerTable peers, ArLayout A, const float4* __restrict__ grad) {
+  extern __shared__ __align__(128) float4 s_buf[];  // [2][AR_TMA_F4]
+  __shared__ uint64_t s_bar[2];
+  HP_ENTRY(SP_AR_SCATTER);
+  const int c = (int)blockIdx.y < A.me ? (int)blockIdx.y : (int)blockIdx.y + 1;
+  const int64_t b4 = A.off4[c], c4 = A.off4[c + 1] - b4, real4 = A.S_real >> 2;
+  const int64_t lim = min(c4, max((int64_t)0, real4 - b4));
+  float4* dst = reinterpret_cast<float4*>(static_cast<char*>(peers.base[c]) + A.slots_off) +
+                (int64_t)A.me * A.sstride4;
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    uint32_t ph[2] = {0u, 0u};
+    int k = 0;
+    for (int64_t lo = (int64_t)blockIdx.x * AR_TMA_F4; lo < lim;
+         lo += (int64_t)gridDim.x * AR_TMA_F4, ++k) {
+      const int b = k & 1;
+      const uint32_t bytes = (uint32_t)min((int64_t)AR_TMA_F4, lim - lo) * 16u;
+      bulk_wait_read1();  // the store that last read buffer b (two pieces ago) is done reading
+      mbar_expect_tx(&s_bar[b], bytes);
+      bulk_g2s(s_buf + b * AR_TMA_F4, grad + b4 + lo, bytes, &s_bar[b]);
+      mbar_wait(&s_bar[b], ph[b]);
+      ph[b] ^= 1u;
+      bulk_s2g(dst + lo, s_buf + b * AR_TMA_F4, bytes);
+      bulk_commit();
+    }
+    bulk_wait0();  // every piece written before the kernel ends (k_signal publishes next)
+    fence_proxy_async_global();
+  }
+  HP_SPAN_END(SP_AR_SCATTER);
+}
+
 template <typename OutT>
 __device__ __forceinline__ void put4(void* base, int64_t i4, float4 v);
 template <>
@@ -1850,7 +1890,16 @@ int hp_dar_allreduce(hp_dar_t d, const void* grad_v, float scale, void* stream) 
     if (np > 0) {
       if (bf_in)
         launch_k(k_ar_scatter<__nv_bfloat16>, dim3(bx, np), dim3(256), 0, st, d->peers, d->A, g, b, nb);
-      else if (g_dar_deep)  // A/B: 16 vectors in flight per thread (fewer CTAs saturate the link)
+      else if (g_dar_tma) {  // A/B: TMA bulk copies, g_dar_tma CTAs per peer chunk
+        static bool tconf = false;
+        if (!tconf) {
+          HP_CUDA(cudaFuncSetAttribute(k_ar_scatter_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       2 * AR_TMA_F4 * 16));
+          tconf = true;
+        }
+        launch_k(k_ar_scatter_tma, dim3(g_dar_tma, np), dim3(32), 2 * AR_TMA_F4 * 16, st, d->peers,
+                 d->A, static_cast<const float4*>(g));
+      } else if (g_dar_deep)  // A/B: 16 vectors in flight per thread (fewer CTAs saturate the link)
         launch_k(k_ar_scatter<float, 16>, dim3(bx, np), dim3(256), 0, st, d->peers, d->A, g, b, nb);
       else
         launch_k(k_ar_scatter<float>, dim3(bx, np), dim3(256), 0, st, d->peers, d->A, g, b, nb);

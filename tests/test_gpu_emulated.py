@@ -37,7 +37,7 @@ def knobs(cuda):
     from paper_1808_02621_b200 import _lib
 
     lib = _lib.load()
-    defaults = {"owner_stream": 2, "dar_blocks": 0, "dar_buckets": 1, "dar_rg_blocks": 0, "wait_timeout": 0}
+    defaults = {"owner_stream": 2, "dar_blocks": 0, "dar_buckets": 1, "dar_rg_blocks": 0, "dar_tma": 0, "wait_timeout": 0}
 
     def set_(name, v):
         getattr(lib, f"hp_debug_set_{name}")(v)
@@ -199,6 +199,17 @@ def _eager_pipelined(emu, seeds, empty=()):
         emu.check_outputs(emu.oracle_step(data[i][0]))
     emu.check_tables()
     emu.errors()
+
+
+@pytest.mark.parametrize("n,ctas", [(2, 3), (4, 1)])
+def test_emulated_dense_tma_scatter_bit_exact(cuda, knobs, n, ctas):
+    """The SM-store dense exchange with its scatter on TMA bulk copies."""
+    knobs("dar_tma", ctas)
+    emu = Emu(cuda, n, _small_tables(), {"lstm": 100_000}, "adagrad", "p2p-sm")
+    try:
+        _eager_pipelined(emu, [1, 2, 3])
+    finally:
+        emu.close()
 
 
 @pytest.mark.parametrize("n,out_dtype", [(2, torch.float32), (3, torch.bfloat16)])
