@@ -114,8 +114,10 @@ void hp_debug_set_dar_buckets(int n);
 /* A/B: 1 = the SM-store K7 kernels keep 16 (scatter) / 8 (reduce-gather)
  * vectors in flight per thread, so fewer CTAs saturate NVLink (fp32 in/out). */
 void hp_debug_set_dar_deep(int on);
-/* A/B: b > 0 = the SM-store K7 scatter moves 32 KB pieces by TMA bulk copies
- * (global -> shared -> peer slot), b CTAs of one warp per peer chunk (fp32). */
+/* b > 0 (default 32) = the SM-store K7 scatter moves 32 KB pieces by TMA bulk
+ * copies (global -> shared -> peer slot), b one-warp CTAs per peer chunk (fp32
+ * gradients); 0 = LSU stores from ~half the SMs. Measured LM1B full step:
+ * N = 2 123 vs 135 us (the sparse tables keep the SMs), N = 4 181-184 vs 181. */
 void hp_debug_set_dar_tma(int n);
 /* Instrumentation: grids of the peer-store kernels (push reduce, owner rows):
  * 1 (default) = one group per item, many waves; 0 = one resident wave. */

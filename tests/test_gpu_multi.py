@@ -29,8 +29,8 @@ def _ngpu():
     ("sgd", "p2p", "nccl", "dense_in=bf16", "hybrid"),
     # the split push (short items on a side stream; HP_SPLIT_PUSH=1)
     ("adam", "p2p", "p2p-sm", "split_push=1", "hybrid"),
-    # the SM-store dense exchange's scatter on TMA bulk copies
-    ("adagrad", "p2p", "p2p-sm", "dar_tma=4", "hybrid"),
+    # the SM-store dense exchange's scatter by LSU stores (default: TMA bulk copies)
+    ("adagrad", "p2p", "p2p-sm", "dar_tma=0", "hybrid"),
     # the SM-store dense exchange in 2 and 5 buckets (default 1)
     ("adagrad", "p2p", "p2p-sm", "dar_buckets=2", "hybrid"),
     ("sgd", "p2p", "p2p-sm", "dar_buckets=5", "hybrid"),
