@@ -119,6 +119,9 @@ void hp_debug_set_dar_deep(int on);
  * gradients); 0 = LSU stores from ~half the SMs. Measured LM1B full step:
  * N = 2 123 vs 135 us (the sparse tables keep the SMs), N = 4 181-184 vs 181. */
 void hp_debug_set_dar_tma(int n);
+/* A/B: b > 0 = the SM-store K7 reduce/gather on TMA bulk copies (b CTAs of 128
+ * threads; fp32 in and out); 0 (default) = LSU loads and peer stores. */
+void hp_debug_set_dar_rg_tma(int n);
 /* Instrumentation: grids of the peer-store kernels (push reduce, owner rows):
  * 1 (default) = one group per item, many waves; 0 = one resident wave. */
 void hp_debug_set_owner_waves(int on);

@@ -52,6 +52,7 @@ SIGNATURES = {
     "hp_debug_set_dar_buckets": (None, [C.c_int]),
     "hp_debug_set_dar_deep": (None, [C.c_int]),
     "hp_debug_set_dar_tma": (None, [C.c_int]),
+    "hp_debug_set_dar_rg_tma": (None, [C.c_int]),
     "hp_debug_set_dar_rg_blocks": (None, [C.c_int]),
     "hp_debug_set_owner_waves": (None, [C.c_int]),
     "hp_debug_set_spans": (None, [vp]),

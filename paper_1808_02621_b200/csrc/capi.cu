@@ -23,6 +23,7 @@ extern int g_dar_blocks;
 extern int g_dar_buckets;
 extern int g_dar_deep;
 extern int g_dar_tma;
+extern int g_dar_rg_tma;
 extern int g_dar_rg_blocks;
 extern int g_owner_waves;
 extern int g_reduce_b;
@@ -184,6 +185,7 @@ void hp_debug_set_owner_stream(int on) { hp::g_owner_stream = on < 0 ? 0 : (on >
 void hp_debug_set_combine_blocks(int n) { hp::g_combine_blocks = n < 0 ? 0 : n; }
 void hp_debug_set_dar_blocks(int n) { hp::g_dar_blocks = n < 0 ? 0 : n; }
 void hp_debug_set_dar_rg_blocks(int n) { hp::g_dar_rg_blocks = n < 0 ? 0 : n; }
+void hp_debug_set_dar_rg_tma(int n) { hp::g_dar_rg_tma = n < 0 ? 0 : n; }
 void hp_debug_set_dar_tma(int n) { hp::g_dar_tma = n < 0 ? 0 : n; }
 void hp_debug_set_dar_deep(int on) { hp::g_dar_deep = on ? 1 : 0; }
 void hp_debug_set_dar_buckets(int n) { hp::g_dar_buckets = n < 1 ? 1 : (n > 16 ? 16 : n); }

@@ -79,6 +79,7 @@ extern int g_combine_blocks;  // k_combine grid cap for peer-store epilogues (0:
 extern int g_dar_blocks;      // HP_DAR_PIPE grid (0: one block per SM)
 extern int g_dar_rg_blocks;   // HP_DAR_SM reduce/gather grid (0: 2 per SM)
 extern int g_dar_tma;         // > 0: K7 scatter by TMA bulk copies, that many CTAs per peer chunk
+extern int g_dar_rg_tma;      // > 0: K7 reduce/gather by TMA bulk copies, that many CTAs
 extern int g_dar_deep;        // SM-store K7: 16 / 8 vectors in flight per thread (A/B)
 extern int g_dar_buckets;     // HP_DAR_SM buckets per step
 extern int g_owner_waves;     // peer-store kernels: many waves (1) or one resident wave (0)

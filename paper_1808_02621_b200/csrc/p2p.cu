@@ -1293,6 +1293,97 @@ k_ar_scatter_tma(PeerTable peers, ArLayout A, const float4* __restrict__ grad) {
   HP_SPAN_END(SP_AR_SCATTER);
 }
 
+// TMA variant of the reduce/gather (fp32 in and out; hp_debug_set_dar_rg_tma):
+// per 16 KB piece of my chunk, the n contributions are bulk-loaded into shared
+// memory in source-rank order (double-buffered: contribution s+1 lands while
+// s is added), summed per column by 128 threads from +0.0 in rank order,
+// scaled, staged in shared memory and bulk-stored into every rank's output.
+constexpr int AR_RG_F4 = 1024;  // 16 KB per piece
+__global__ void __launch_bounds__(128)
+k_ar_rg_tma(PeerTable peers, void* my_win, ArLayout A, const float4* __restrict__ grad, float scale) {
+  extern __shared__ __align__(128) float4 s_rg[];  // [2][AR_RG_F4] loads, [AR_RG_F4] result
+  __shared__ uint64_t s_bar[2];
+  HP_ENTRY(SP_AR_RG);
+  const int64_t b4 = A.off4[A.me], c4 = A.off4[A.me + 1] - b4;
+  const int64_t own_lim = min(c4, max((int64_t)0, (A.S_real >> 2) - b4));
+  const char* slots = static_cast<const char*>(my_win) + A.slots_off;
+  float4* res = s_rg + 2 * AR_RG_F4;
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+  }
+  __syncthreads();
+  uint32_t ph[2] = {0u, 0u};
+  int ld = 0;  // loads issued (buffer = ld & 1)
+  constexpr int PER = AR_RG_F4 / 128;
+#pragma unroll 1
+  for (int64_t lo = (int64_t)blockIdx.x * AR_RG_F4; lo < c4; lo += (int64_t)gridDim.x * AR_RG_F4) {
+    const int64_t len = min((int64_t)AR_RG_F4, c4 - lo);
+    // source s's piece: own gradient (real part; zeros past S_real) or slot s
+    auto issue = [&](int s, int b) {
+      if (threadIdx.x != 0) return;
+      const float4* src;
+      int64_t nbytes;
+      if (s == A.me) {
+        src = grad + b4 + lo;
+        nbytes = max((int64_t)0, min(len, own_lim - lo)) * 16;
+      } else {
+        src = reinterpret_cast<const float4*>(slots + (int64_t)s * A.sstride4 * 16) + lo;
+        nbytes = len * 16;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the generic reads of b
+      mbar_expect_tx(&s_bar[b], (uint32_t)nbytes);
+      if (nbytes > 0) bulk_g2s(s_rg + b * AR_RG_F4, src, (uint32_t)nbytes, &s_bar[b]);
+    };
+    float4 acc[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    issue(0, ld & 1);
+#pragma unroll 1
+    for (int s = 0; s < A.n; ++s) {
+      const int b = (ld + s) & 1;
+      if (s + 1 < A.n) issue(s + 1, (ld + s + 1) & 1);
+      mbar_wait(&s_bar[b], ph[b]);
+      ph[b] ^= 1u;
+      const int64_t have = s == A.me ? max((int64_t)0, min(len, own_lim - lo)) : len;
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int j = threadIdx.x + k * 128;
+        if (j < len) acc[k] = f4_add(acc[k], j < have ? s_rg[b * AR_RG_F4 + j] : make_float4(0.f, 0.f, 0.f, 0.f));
+      }
+      __syncthreads();  // buffer b is consumed before it is reloaded (contribution s+2)
+    }
+    ld += A.n;
+    if (threadIdx.x == 0) bulk_wait_read0();  // the previous piece's stores have read `res`
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int j = threadIdx.x + k * 128;
+      if (j < len) {
+        float4 v = acc[k];
+        v.x = __fmul_rn(v.x, scale);
+        v.y = __fmul_rn(v.y, scale);
+        v.z = __fmul_rn(v.z, scale);
+        v.w = __fmul_rn(v.w, scale);
+        res[j] = v;
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int r = 0; r < A.n; ++r)
+        bulk_s2g(reinterpret_cast<float4*>(static_cast<char*>(peers.base[r]) + A.out_off) + b4 + lo,
+                 res, (uint32_t)(len * 16));
+      bulk_commit();
+    }
+  }
+  if (threadIdx.x == 0) {
+    bulk_wait0();
+    fence_proxy_async_global();
+  }
+  HP_SPAN_END(SP_AR_RG);
+}
+
 template <typename OutT>
 __device__ __forceinline__ void put4(void* base, int64_t i4, float4 v);
 template <>
@@ -1910,7 +2001,16 @@ int hp_dar_allreduce(hp_dar_t d, const void* grad_v, float scale, void* stream) 
     const int lag = nb - 1 - b;
     launch_k(k_wait, dim3(1), dim3(64), 0, st, d->win, 0, d->A.n, wait_budget(), SP_AR_WAIT0, lag);
     const dim3 G(brg), Bk(256);
-    if (d->A.out_bytes == 4 && !bf_in && g_dar_deep)
+    if (d->A.out_bytes == 4 && !bf_in && g_dar_rg_tma > 0 && nb == 1) {  // TMA reduce/gather
+      static bool rconf = false;
+      if (!rconf) {
+        HP_CUDA(cudaFuncSetAttribute(k_ar_rg_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     3 * AR_RG_F4 * 16));
+        rconf = true;
+      }
+      launch_k(k_ar_rg_tma, dim3(g_dar_rg_tma), dim3(128), 3 * AR_RG_F4 * 16, st, d->peers, d->win,
+               d->A, static_cast<const float4*>(g), scale);
+    } else if (d->A.out_bytes == 4 && !bf_in && g_dar_deep)
       launch_k(k_ar_reduce_gather<float, float, 8>, G, Bk, 0, st, d->peers, d->win, d->A, g, scale, b,
                nb);
     else if (d->A.out_bytes == 4 && !bf_in)

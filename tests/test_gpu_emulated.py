@@ -37,7 +37,7 @@ def knobs(cuda):
     from paper_1808_02621_b200 import _lib
 
     lib = _lib.load()
-    defaults = {"owner_stream": 2, "dar_blocks": 0, "dar_buckets": 1, "dar_rg_blocks": 0, "dar_tma": 32, "wait_timeout": 0}
+    defaults = {"owner_stream": 2, "dar_blocks": 0, "dar_buckets": 1, "dar_rg_blocks": 0, "dar_tma": 32, "dar_rg_tma": 0, "wait_timeout": 0}
 
     def set_(name, v):
         getattr(lib, f"hp_debug_set_{name}")(v)
@@ -201,11 +201,12 @@ def _eager_pipelined(emu, seeds, empty=()):
     emu.errors()
 
 
-@pytest.mark.parametrize("n,ctas", [(2, 3), (4, 1), (3, 0)])
-def test_emulated_dense_tma_scatter_bit_exact(cuda, knobs, n, ctas):
+@pytest.mark.parametrize("n,ctas,rg", [(2, 3, 0), (4, 1, 0), (3, 0, 0), (2, 32, 5), (3, 32, 2)])
+def test_emulated_dense_tma_scatter_bit_exact(cuda, knobs, n, ctas, rg):
     """The SM-store dense exchange with its scatter on TMA bulk copies (few
-    CTAs), and by LSU stores (0)."""
+    CTAs), by LSU stores (0), and with the reduce/gather on TMA (rg CTAs)."""
     knobs("dar_tma", ctas)
+    knobs("dar_rg_tma", rg)
     emu = Emu(cuda, n, _small_tables(), {"lstm": 100_000}, "adagrad", "p2p-sm")
     try:
         _eager_pipelined(emu, [1, 2, 3])

@@ -31,6 +31,7 @@ def _ngpu():
     ("adam", "p2p", "p2p-sm", "split_push=1", "hybrid"),
     # the SM-store dense exchange's scatter by LSU stores (default: TMA bulk copies)
     ("adagrad", "p2p", "p2p-sm", "dar_tma=0", "hybrid"),
+    ("sgd", "p2p", "p2p-sm", "dar_rg_tma=24", "hybrid"),
     # the SM-store dense exchange in 2 and 5 buckets (default 1)
     ("adagrad", "p2p", "p2p-sm", "dar_buckets=2", "hybrid"),
     ("sgd", "p2p", "p2p-sm", "dar_buckets=5", "hybrid"),
