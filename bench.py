@@ -491,8 +491,9 @@ def main():
             algo += T * 4 * big.D
         us = kern[f"k4:{big.name}"]
         achieved = algo / (us * 1e-6) / 1e9
-        roof = {"kernel": (f"K4+K5 merge+apply+pull ({big.name}: k_reduce with the fused tree and "
-                           "pull, k_bcast_rows for the long segments)" if fused_pull else
+        roof = {"kernel": (f"K4+K5 merge+apply+pull ({big.name}: split apply - k_reduce short items "
+                           "with the pull on a side stream; long chunks -> k_combine -> k_bcast_rows)"
+                           if fused_pull else
                            f"K4 merge+apply ({big.name})"), "bound": "hbm",
                 "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"], "traffic": k4_traffic(wl.name, big.name),
