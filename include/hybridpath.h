@@ -114,10 +114,11 @@ void hp_debug_set_dar_buckets(int n);
 /* A/B: 1 = the SM-store K7 kernels keep 16 (scatter) / 8 (reduce-gather)
  * vectors in flight per thread, so fewer CTAs saturate NVLink (fp32 in/out). */
 void hp_debug_set_dar_deep(int on);
-/* b > 0 (default 32) = the SM-store K7 scatter moves 32 KB pieces by TMA bulk
+/* b > 0 (default 36) = the SM-store K7 scatter moves 32 KB pieces by TMA bulk
  * copies (global -> shared -> peer slot), b one-warp CTAs per peer chunk (fp32
- * gradients); 0 = LSU stores from ~half the SMs. Measured LM1B full step:
- * N = 2 123 vs 135 us (the sparse tables keep the SMs), N = 4 181-184 vs 181. */
+ * gradients); 0 = LSU stores from ~half the SMs. Measured LM1B full step at
+ * N = 2: 122 us (36 CTAs), 125 (32), 150 (28), 135 with LSU stores (the sparse
+ * tables keep the SMs); N = 4: 181-184 vs 181. */
 void hp_debug_set_dar_tma(int n);
 /* A/B: b > 0 = the SM-store K7 reduce/gather on TMA bulk copies (b CTAs of 128
  * threads; fp32 in and out); 0 (default) = LSU loads and peer stores. */

@@ -874,7 +874,7 @@ int g_owner_stream = 2;  // 0: k_owner_apply, 1: k_owner_stream, 2: k_owner_scan
 int g_combine_blocks = 0;  // 0: one CTA per long segment up to the SM count
 int g_dar_blocks = 0;     // HP_DAR_PIPE grid (0 = one block per SM)
 int g_dar_rg_blocks = 0;  // HP_DAR_SM reduce/gather grid (0: 2 per SM)
-int g_dar_tma = 32;  // K7 scatter on TMA, one-warp CTAs per peer chunk (hp_debug_set_dar_tma; 0: LSU stores)
+int g_dar_tma = 36;  // K7 scatter on TMA, one-warp CTAs per peer chunk (hp_debug_set_dar_tma; 0: LSU stores)
 int g_dar_rg_tma = 0;  // K7 reduce/gather on TMA, CTAs (hp_debug_set_dar_rg_tma, A/B)
 int g_dar_deep = 0;  // SM-store K7 with deep unrolls (hp_debug_set_dar_deep, A/B)
 int g_dar_buckets = 1;    // HP_DAR_SM buckets per step (hp_debug_set_dar_buckets)

@@ -37,7 +37,7 @@ def knobs(cuda):
     from paper_1808_02621_b200 import _lib
 
     lib = _lib.load()
-    defaults = {"owner_stream": 2, "dar_blocks": 0, "dar_buckets": 1, "dar_rg_blocks": 0, "dar_tma": 32, "dar_rg_tma": 0, "wait_timeout": 0}
+    defaults = {"owner_stream": 2, "dar_blocks": 0, "dar_buckets": 1, "dar_rg_blocks": 0, "dar_tma": 36, "dar_rg_tma": 0, "wait_timeout": 0}
 
     def set_(name, v):
         getattr(lib, f"hp_debug_set_{name}")(v)
